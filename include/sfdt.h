@@ -1,0 +1,128 @@
+/*
+ * sfdt.h -- C ABI of the B200-native sFFT-DT hot path (libsfdt_b200.so).
+ *
+ * Drop-in boundary for the reference package `sfft-dt`
+ * (/root/reference/pkg/src/sfft_dt).  Two layers:
+ *
+ *  1. Kernel-level mirrors of the reference's backend seam
+ *     (_kernels/__init__.py:19-24), batched on the device:
+ *       sfdt_fft_radix2            <- _core.pyx:35-77    fft_radix2
+ *       sfdt_hankel_solve          <- _core.pyx:127-162  hankel_solve
+ *       sfdt_poly_roots            <- _core.pyx:238-266  poly_roots
+ *       sfdt_vandermonde_solve     <- _core.pyx:273-312  vandermonde_solve
+ *       sfdt_prune_eval            <- _core.pyx:319-346  prune_eval
+ *       sfdt_hankel_singular_values<- _core.pyx:409-433  hankel_singular_values
+ *  2. Solver-level entry points (one call per batch of signals) behind the
+ *     reference's public solvers:
+ *       sfdt_exact_solve   <- exact.py:161-200 solve_noniterative
+ *                             exact.py:203-292 solve_iterative
+ *       sfdt_general_solve <- general.py:272-372 solve_general
+ *
+ * Conventions
+ *  - Complex numbers are interleaved (re, im) doubles (complex128); signals
+ *    may also be complex64 storage (SFDT_C64), upconverted to FP64 at load.
+ *  - Every pointer argument except the host twiddle buffer is a DEVICE
+ *    pointer.  The library never allocates: callers pass workspaces sized by
+ *    the *_workspace_bytes queries.  Work is asynchronous on `stream`.
+ *  - Return 0 on success, a negative SFDT_E* code otherwise (argument
+ *    errors mirror the reference's ValueErrors; numerical singularity is data,
+ *    never an error, as in the reference).
+ *  - Reentrant for distinct workspaces; no global mutable state.
+ */
+#ifndef SFDT_H
+#define SFDT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void *sfdt_stream_t; /* a cudaStream_t */
+
+enum {
+    SFDT_OK = 0,
+    SFDT_EINVAL = -1,     /* bad argument (reference: ValueError) */
+    SFDT_ECUDA = -2,      /* CUDA launch / runtime failure */
+    SFDT_EWORKSPACE = -3, /* workspace too small */
+    SFDT_ECAPACITY = -4   /* output capacity too small */
+};
+
+enum { SFDT_C128 = 0, SFDT_C64 = 1 };
+
+/* per-signal statistics block of sfdt_exact_solve (int64 each) */
+enum {
+    SFDT_ST_NITER = 0,        /* iterations recorded (1 non-iterative, a_max iterative) */
+    SFDT_ST_FULL_SUCCESS = 1, /* trace.full_success */
+    SFDT_ST_NENTRIES = 2,     /* entries written (duplicates counted once) */
+    SFDT_ST_NUNRESOLVED = 3,  /* len(trace.unresolved_bins) */
+    SFDT_ST_NDUP = 4,         /* duplicate-location overwrites (trace.warnings) */
+    SFDT_ST_SYNDROMES = 5,    /* trace.syndromes_computed */
+    SFDT_ST_FFT_SAMPLES = 6,  /* trace.fft_samples */
+    SFDT_ST_ITER0 = 8,        /* per iteration: d, attempted, solved, deferred,
+                                 syndromes, fft_samples (6 each, up to 4) */
+    SFDT_ST_PER_SIGNAL = 32
+};
+
+const char *sfdt_strerror(int code);
+int sfdt_version(void);
+
+/* Host helper: the twiddle table the reference's radix-2 recurrence produces
+ * (_core.pyx:61-76: w *= wlen per butterfly, re-seeded by cexp every 256).
+ * Stage m (2 <= m <= n_max) occupies entries [m/2 - 1, m - 1); n_max - 1
+ * complex entries in total.  host_out holds 2*(n_max-1) doubles. */
+int sfdt_fft_twiddles(int64_t n_max, int inverse, double *host_out);
+
+/* ---------------------------------------------------------- kernel level */
+int sfdt_fft_radix2(const double *x, double *out, int64_t batch, int64_t n, int inverse,
+                    const double *twiddles, sfdt_stream_t stream);
+int sfdt_hankel_solve(const double *m, int64_t nb, int64_t ld, int a, double *c, double *cd,
+                      sfdt_stream_t stream);
+int sfdt_poly_roots(const double *c, int64_t nb, int a, double *z, sfdt_stream_t stream);
+int sfdt_vandermonde_solve(const double *z, const double *m, int64_t nb, int a, int64_t ld,
+                           double *p, double *pd, sfdt_stream_t stream);
+int sfdt_prune_eval(const double *c, const int64_t *k, int64_t nb, int a, int64_t n, int64_t d,
+                    double *out, sfdt_stream_t stream);
+int sfdt_hankel_singular_values(const double *m, int64_t nb, int64_t ld, int a_max, double *out,
+                                sfdt_stream_t stream);
+
+/* ---------------------------------------------------------- exact solver */
+typedef struct {
+    /* input: batch x n signals, row-major, complex128 or complex64 */
+    const void *x;
+    int32_t x_dtype;
+    int64_t batch;
+    int64_t n;
+    /* ExactConfig (exact.py:31-71): resolved initial d, a_max, zero_threshold */
+    int64_t d;
+    int32_t a_max;
+    int32_t iterative; /* 0: solve_noniterative, 1: solve_iterative */
+    double zero_threshold;
+    const double *twiddles; /* device copy of sfdt_fft_twiddles(n_max >= n/d, inverse=0) */
+    /* outputs (device) */
+    int64_t *entry_offsets; /* batch + 1 : entries of signal b are [off[b], off[b+1]) */
+    int64_t *locs;          /* entry_cap */
+    double *vals;           /* 2 * entry_cap */
+    int64_t entry_cap;
+    int64_t *unres_offsets; /* batch + 1 */
+    int32_t *unres_bins;    /* unres_cap, ascending per signal */
+    int64_t unres_cap;
+    int64_t *dup_locs;      /* optional (iterative): duplicate locations in write order */
+    int64_t *dup_offsets;   /* batch + 1 */
+    int64_t dup_cap;
+    int64_t *stats;         /* batch * SFDT_ST_PER_SIGNAL */
+    double *rms;            /* batch: rms(x) (spectral.py:215-218) */
+} sfdt_exact_args;
+
+/* capacities that can never overflow for these arguments */
+int sfdt_exact_caps(const sfdt_exact_args *args, int64_t *entry_cap, int64_t *unres_cap,
+                    int64_t *dup_cap);
+size_t sfdt_exact_workspace_bytes(const sfdt_exact_args *args);
+int sfdt_exact_solve(const sfdt_exact_args *args, void *workspace, size_t workspace_bytes,
+                     sfdt_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SFDT_H */

@@ -1,0 +1,24 @@
+"""B200-native sFFT-DT (arXiv 1407.8315): drop-in for the reference
+package's recovery entry points, computed by hand-written sm_100a kernels
+(libsfdt_b200.so).  See DESIGN.md."""
+
+from .exact import (EstimateResult, ExactBatch, ExactConfig, IterationStats, SolverTrace,
+                    estimate_sparsity_and_solve, exact_batch, solve_iterative,
+                    solve_iterative_batch, solve_noniterative, solve_noniterative_batch)
+from .spectral import SparseSpectrum, as_signal
+
+BACKEND = "b200"
+__version__ = "0.1.0"
+
+
+def using_compiled() -> bool:
+    """The CUDA library is the only backend."""
+    return True
+
+
+__all__ = [
+    "BACKEND", "EstimateResult", "ExactBatch", "ExactConfig", "IterationStats", "SolverTrace",
+    "SparseSpectrum", "as_signal", "estimate_sparsity_and_solve", "exact_batch",
+    "solve_iterative", "solve_iterative_batch", "solve_noniterative",
+    "solve_noniterative_batch", "using_compiled",
+]

@@ -1,0 +1,92 @@
+"""ctypes binding of libsfdt_b200.so (include/sfdt.h).
+
+The product path has exactly one implementation: the sm_100a kernels in this
+library.  There is no CPU fallback -- if the library is missing or no CUDA
+device is present, calls fail loudly.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsfdt_b200.so")
+
+SFDT_ST_NITER = 0
+SFDT_ST_FULL_SUCCESS = 1
+SFDT_ST_NENTRIES = 2
+SFDT_ST_NUNRESOLVED = 3
+SFDT_ST_NDUP = 4
+SFDT_ST_SYNDROMES = 5
+SFDT_ST_FFT_SAMPLES = 6
+SFDT_ST_ITER0 = 8
+SFDT_ST_PER_SIGNAL = 32
+SFDT_C128, SFDT_C64 = 0, 1
+
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int32
+_int = ctypes.c_int
+_dbl = ctypes.c_double
+
+
+class ExactArgs(ctypes.Structure):
+    _fields_ = [
+        ("x", _vp), ("x_dtype", _i32), ("batch", _i64), ("n", _i64),
+        ("d", _i64), ("a_max", _i32), ("iterative", _i32), ("zero_threshold", _dbl),
+        ("twiddles", _vp),
+        ("entry_offsets", _vp), ("locs", _vp), ("vals", _vp), ("entry_cap", _i64),
+        ("unres_offsets", _vp), ("unres_bins", _vp), ("unres_cap", _i64),
+        ("dup_locs", _vp), ("dup_offsets", _vp), ("dup_cap", _i64),
+        ("stats", _vp), ("rms", _vp),
+    ]
+
+
+# every symbol include/sfdt.h declares (tests check the export list)
+EXPORTS = {
+    "sfdt_strerror": (ctypes.c_char_p, [_int]),
+    "sfdt_version": (_int, []),
+    "sfdt_fft_twiddles": (_int, [_i64, _int, _vp]),
+    "sfdt_fft_radix2": (_int, [_vp, _vp, _i64, _i64, _int, _vp, _vp]),
+    "sfdt_hankel_solve": (_int, [_vp, _i64, _i64, _int, _vp, _vp, _vp]),
+    "sfdt_poly_roots": (_int, [_vp, _i64, _int, _vp, _vp]),
+    "sfdt_vandermonde_solve": (_int, [_vp, _vp, _i64, _int, _i64, _vp, _vp, _vp]),
+    "sfdt_prune_eval": (_int, [_vp, _vp, _i64, _int, _i64, _i64, _vp, _vp]),
+    "sfdt_hankel_singular_values": (_int, [_vp, _i64, _i64, _int, _vp, _vp]),
+    "sfdt_exact_caps": (_int, [ctypes.POINTER(ExactArgs), ctypes.POINTER(_i64),
+                               ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
+    "sfdt_exact_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(ExactArgs)]),
+    "sfdt_exact_solve": (_int, [ctypes.POINTER(ExactArgs), _vp, ctypes.c_size_t, _vp]),
+}
+
+_lib = None
+
+
+class SfdtError(RuntimeError):
+    pass
+
+
+def load():
+    """Load (and type) the library; raises if it was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} missing: build it with `python -m paper_1407_8315_b200.build` "
+                "(there is no CPU fallback)")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in EXPORTS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def check(rc: int, what: str):
+    if rc != 0:
+        msg = load().sfdt_strerror(rc).decode()
+        if rc == -1:
+            raise ValueError(f"{what}: {msg}")
+        raise SfdtError(f"{what}: {msg} ({rc})")

@@ -1,0 +1,43 @@
+// common.cuh -- shared definitions for the sm_100a sFFT-DT kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "cx.cuh"
+#include "../../include/sfdt.h"
+
+namespace sfdt {
+
+constexpr double TINY = 2.2250738585072014e-308;   // np.finfo(float).tiny
+constexpr double SINGULARITY_RTOL = 1e-10;         // syndrome.py:23
+constexpr double CONSISTENCY_RTOL = 1e-6;          // exact.py:26
+constexpr double SNAP_TOL = 0.25;                  // exact.py:27
+constexpr double UNIT_MODULUS_TOL = 1e-6;          // exact.py:28
+constexpr double TWO_PI = 6.283185307179586;       // 2.0 * np.pi
+constexpr int MAX_SHIFTS = 8;                      // 2 * a_max, a_max <= 4
+constexpr int FFT_SMEM_MAX = 8192;                 // complex128 points per CTA in smem
+
+__device__ __forceinline__ cx ldcx(const cx *p) {
+    double2 v = __ldg(reinterpret_cast<const double2 *>(p));
+    return mk(v.x, v.y);
+}
+__device__ __forceinline__ void stcx(cx *p, cx v) {
+    *reinterpret_cast<double2 *>(p) = make_double2(v.re, v.im);
+}
+
+__host__ __device__ __forceinline__ int ilog2_64(int64_t v) {
+    int r = 0;
+    while ((int64_t(1) << (r + 1)) <= v) r++;
+    return r;
+}
+
+// python-style non-negative modulo for power-of-two n
+__host__ __device__ __forceinline__ int64_t pmod(int64_t a, int64_t n) { return a & (n - 1); }
+
+}  // namespace sfdt
+
+#define SFDT_CHECK_LAUNCH()                                   \
+    do {                                                      \
+        if (cudaPeekAtLastError() != cudaSuccess) return SFDT_ECUDA; \
+    } while (0)

@@ -1,0 +1,88 @@
+"""Device plumbing: CUDA tensors, streams, twiddle tables, workspaces.
+
+PyTorch is used only for device memory and streams; every computation on
+the hot path is a kernel of libsfdt_b200.so.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+
+_twiddle_cache: dict = {}
+
+
+def require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1407_8315_b200 needs a CUDA device (B200, sm_100a); "
+                           "there is no CPU fallback")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if dev.type != "cuda":
+        raise ValueError(f"expected a CUDA device, got {dev}")
+    return dev
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def stream_handle(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def twiddles(n_max: int, device: torch.device, inverse: bool = False) -> torch.Tensor:
+    """Device copy of the reference-recurrence twiddle table (sfdt_fft_twiddles).
+    Built once per (n_max, sign, device) on the host, cached."""
+    n_max = max(int(n_max), 2)
+    key = (n_max, bool(inverse), device)
+    t = _twiddle_cache.get(key)
+    if t is None:
+        # the largest cached table of the same sign serves any smaller n
+        for (n2, inv2, dev2), t2 in _twiddle_cache.items():
+            if inv2 == bool(inverse) and dev2 == device and n2 >= n_max:
+                return t2
+        host = np.empty(2 * (n_max - 1), dtype=np.float64)
+        _lib.check(_lib.load().sfdt_fft_twiddles(n_max, int(bool(inverse)),
+                                                 host.ctypes.data_as(_lib._vp)), "sfdt_fft_twiddles")
+        t = torch.from_numpy(host).to(device)
+        _twiddle_cache[key] = t
+    return t
+
+
+class Workspace:
+    """Grow-only byte workspace per device (the library never allocates)."""
+
+    _bufs: dict = {}
+
+    @classmethod
+    def get(cls, nbytes: int, device: torch.device) -> torch.Tensor:
+        buf = cls._bufs.get(device)
+        if buf is None or buf.numel() < nbytes:
+            buf = None
+            cls._bufs.pop(device, None)
+            buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+            cls._bufs[device] = buf
+        return buf
+
+    @classmethod
+    def release(cls):
+        cls._bufs.clear()
+
+
+def as_device_signals(x, device: torch.device, allow_c64: bool = True):
+    """(B, N) complex tensor on `device` (no copy when already there).
+    complex64 input stays complex64 (storage mode, upconverted in-kernel)."""
+    if isinstance(x, torch.Tensor):
+        t = x
+    else:
+        arr = np.asarray(x)
+        if arr.dtype != np.complex64 or not allow_c64:
+            arr = np.ascontiguousarray(arr, dtype=np.complex128)
+        t = torch.from_numpy(np.ascontiguousarray(arr))
+    if t.dtype not in (torch.complex128, torch.complex64) or (t.dtype == torch.complex64 and not allow_c64):
+        t = t.to(torch.complex128)
+    if t.device != device:
+        t = t.to(device, non_blocking=True)
+    return t.contiguous()

@@ -1,0 +1,116 @@
+"""CPU checks of the drop-in boundary (no GPU needed):
+
+* libsfdt_b200.so builds for sm_100a, loads, and exports every symbol
+  include/sfdt.h declares;
+* the host twiddle table replays the reference's radix-2 recurrence: a
+  radix-2 DIT evaluated with that table and gcc rounding (no FMA) is
+  bit-identical to the reference FFT (oracle) -- the arithmetic the GPU FFT
+  kernel performs;
+* the Python mirror validates arguments exactly like the reference.
+"""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import kernels as OK
+from paper_1407_8315_b200 import _lib
+from paper_1407_8315_b200.build import build
+from paper_1407_8315_b200.exact import ExactConfig
+from paper_1407_8315_b200.spectral import SparseSpectrum, as_signal
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    build()
+    return _lib.load()
+
+
+def test_exports_every_header_symbol(lib):
+    with open(os.path.join(ROOT, "include", "sfdt.h")) as fh:
+        hdr = fh.read()
+    declared = set(re.findall(r"\b(sfdt_[a-z0-9_]+)\s*\(", hdr))
+    assert declared, "no declarations parsed"
+    assert declared == set(_lib.EXPORTS), declared ^ set(_lib.EXPORTS)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert lib.sfdt_version() >= 10000
+    assert lib.sfdt_strerror(-1) == b"invalid argument"
+
+
+def _twiddles(lib, n, inverse=False):
+    out = np.empty(2 * (n - 1), dtype=np.float64)
+    assert lib.sfdt_fft_twiddles(n, int(inverse), out.ctypes.data_as(_lib._vp)) == 0
+    return out[0::2] + 1j * out[1::2]
+
+
+def _fft_with_table(x, tw):
+    """Radix-2 DIT exactly as k_fft_views runs it, in numpy float64 scalar
+    ops (each product rounded separately = gcc complex multiply)."""
+    n = x.size
+    logn = n.bit_length() - 1
+    rev = np.array([int(format(j, f"0{logn}b")[::-1], 2) if logn else 0 for j in range(n)])
+    a = np.empty(n, dtype=np.complex128)
+    a[rev] = x
+    re, im = a.real.copy(), a.imag.copy()
+    h = 1
+    while h < n:
+        w = tw[h - 1: 2 * h - 1]
+        idx = np.arange(n // 2)
+        k = idx & (h - 1)
+        i0 = ((idx >> (h.bit_length() - 1)) << h.bit_length()) + k
+        i1 = i0 + h
+        wr, wi = w.real[k], w.imag[k]
+        tr = re[i1] * wr - im[i1] * wi
+        ti = re[i1] * wi + im[i1] * wr
+        ur, ui = re[i0].copy(), im[i0].copy()
+        re[i0], im[i0] = ur + tr, ui + ti
+        re[i1], im[i1] = ur - tr, ui - ti
+        h *= 2
+    return re + 1j * im
+
+
+@pytest.mark.parametrize("n", [2, 4, 16, 256, 512, 1024, 4096])
+def test_twiddle_table_reproduces_reference_fft(lib, n):
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    for inverse in (False, True):
+        tw = _twiddles(lib, 8192, inverse)        # one table serves every n <= n_max
+        got = _fft_with_table(x, tw)
+        want = OK.fft_radix2(x, inverse)
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+def test_config_validation_mirrors_reference():
+    with pytest.raises(ValueError, match="power of two"):
+        ExactConfig(n=12, k=2)
+    with pytest.raises(ValueError, match="a_max"):
+        ExactConfig(n=16, k=2, a_max=5)
+    with pytest.raises(ValueError, match="mu"):
+        ExactConfig(n=16, k=2, mu=3)
+    with pytest.raises(ValueError, match="either k or initial_d"):
+        ExactConfig(n=16)
+    with pytest.raises(ValueError, match="must divide"):
+        ExactConfig(n=16, initial_d=3)
+    assert ExactConfig(n=1 << 20, k=256).resolved_d() == 1024
+    assert ExactConfig(n=1 << 16, k=64).resolved_d() == 256
+    assert ExactConfig(n=64, k=64).resolved_d() == 1
+    assert ExactConfig(n=1 << 24, k=4096, mu=1).resolved_d() == 4096
+    with pytest.raises(ValueError):
+        as_signal(np.zeros((2, 4)))
+    with pytest.raises(ValueError):
+        as_signal(np.zeros(6))
+    with pytest.raises(ValueError):
+        SparseSpectrum(4, {7: 1.0})
+
+
+def test_exact_workspace_query(lib):
+    a = _lib.ExactArgs()
+    a.batch, a.n, a.d, a.a_max, a.iterative, a.x_dtype = 16, 1 << 16, 256, 4, 0, 0
+    assert lib.sfdt_exact_workspace_bytes(a) > 16 * 256 * 8 * 16
+    a.d = 3
+    assert lib.sfdt_exact_workspace_bytes(a) == 0

@@ -1,0 +1,251 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle
+and the golden outputs of the real reference.
+
+Parity bar:
+  * supports (frequency indices) identical, in the reference's order;
+  * values within 1e-9 relative for entries in well-conditioned bins (single
+    frequency, or candidate gap >= 32); close-root entries within 1e-4;
+  * traces (per-iteration counters, unresolved bins, full_success) equal;
+  * kernels: FFT / Hankel / Vandermonde bit-exact, transcendental-dependent
+    outputs (roots, prune_eval, singular values) within 1e-12 relative.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1407_8315_b200 as P                     # noqa: E402
+from oracle import solvers as OS                      # noqa: E402
+from paper_1407_8315_b200 import _lib                 # noqa: E402
+from paper_1407_8315_b200.device import twiddles      # noqa: E402
+from tests.golden.cases import EXACT_CASES            # noqa: E402
+from tests.synth import exact_signal                  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+VAL_RTOL = 1e-9
+CLOSE_RTOL = 1e-4
+CLOSE_GAP = 32
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def _ptr(t):
+    return t.data_ptr()
+
+
+def _stream():
+    return torch.cuda.current_stream(DEV).cuda_stream
+
+
+def _bits(a, b):
+    a, b = np.ascontiguousarray(a), np.ascontiguousarray(b)
+    return a.shape == b.shape and np.array_equal(a.view(np.uint8), b.view(np.uint8))
+
+
+# ------------------------------------------------------------ kernel level
+def test_fft_kernel_bitexact(golden):
+    arrays, _ = golden
+    lib = _lib.load()
+    for n in (1, 2, 4, 8, 16, 64, 256, 512, 1024, 2048):
+        x = arrays[f"kern/fft/{n}/in"]
+        for inverse, key in ((False, "fwd"), (True, "inv")):
+            xi = _dev(x.view(np.float64))
+            out = torch.empty_like(xi)
+            tw = twiddles(max(n, 2), DEV, inverse)
+            assert lib.sfdt_fft_radix2(_ptr(xi), _ptr(out), 1, n, int(inverse), _ptr(tw), _stream()) == 0
+            got = out.cpu().numpy().view(np.complex128)
+            assert _bits(got, arrays[f"kern/fft/{n}/{key}"]), (n, key)
+
+
+def test_fft_kernel_batched_random():
+    from oracle import kernels as OK
+    lib = _lib.load()
+    rng = np.random.default_rng(3)
+    for n in (32, 1024, 8192):
+        x = rng.standard_normal((5, n)) + 1j * rng.standard_normal((5, n))
+        xi = _dev(x.view(np.float64))
+        out = torch.empty_like(xi)
+        tw = twiddles(n, DEV)
+        assert lib.sfdt_fft_radix2(_ptr(xi), _ptr(out), 5, n, 0, _ptr(tw), _stream()) == 0
+        got = out.cpu().numpy().view(np.complex128).reshape(5, n)
+        for b in range(5):
+            assert _bits(got[b], OK.fft_radix2(x[b]))
+
+
+@pytest.mark.parametrize("a", [1, 2, 3, 4])
+def test_decode_kernels(golden, a):
+    arrays, _ = golden
+    lib = _lib.load()
+    m = arrays[f"kern/a{a}/m"]
+    nb = m.shape[0]
+    md = _dev(m.view(np.float64))
+    c = torch.empty((nb, 2 * a), dtype=torch.float64, device=DEV)
+    cd = torch.empty((nb, 2), dtype=torch.float64, device=DEV)
+    assert lib.sfdt_hankel_solve(_ptr(md), nb, 8, a, _ptr(c), _ptr(cd), _stream()) == 0
+    # pure +,-,*,/ arithmetic: bit-exact
+    assert _bits(c.cpu().numpy().view(np.complex128), arrays[f"kern/a{a}/c"])
+    assert _bits(cd.cpu().numpy().view(np.complex128).ravel(), arrays[f"kern/a{a}/cd"])
+    z = torch.empty((nb, 2 * a), dtype=torch.float64, device=DEV)
+    cg = _dev(arrays[f"kern/a{a}/c"].view(np.float64))
+    assert lib.sfdt_poly_roots(_ptr(cg), nb, a, _ptr(z), _stream()) == 0
+    zz = z.cpu().numpy().view(np.complex128)
+    zw = arrays[f"kern/a{a}/z"]
+    assert np.all(np.abs(zz - zw) <= 1e-12 * np.maximum(1.0, np.abs(zw)))
+    p = torch.empty((nb, 2 * a), dtype=torch.float64, device=DEV)
+    pd = torch.empty((nb, 2), dtype=torch.float64, device=DEV)
+    zg = _dev(zw.view(np.float64))
+    assert lib.sfdt_vandermonde_solve(_ptr(zg), _ptr(md), nb, a, 8, _ptr(p), _ptr(pd), _stream()) == 0
+    assert _bits(p.cpu().numpy().view(np.complex128), arrays[f"kern/a{a}/p"])
+    assert _bits(pd.cpu().numpy().view(np.complex128).ravel(), arrays[f"kern/a{a}/pd"])
+    kb = _dev(arrays[f"kern/a{a}/k"])
+    pe = torch.empty((nb, 64), dtype=torch.float64, device=DEV)
+    assert lib.sfdt_prune_eval(_ptr(cg), _ptr(kb), nb, a, 1 << 12, 64, _ptr(pe), _stream()) == 0
+    want = arrays[f"kern/a{a}/prune"]
+    got = pe.cpu().numpy()
+    assert np.all(np.abs(got - want) <= 1e-12 * np.maximum(1.0, np.abs(want)))
+    sv = torch.empty((nb, a), dtype=torch.float64, device=DEV)
+    assert lib.sfdt_hankel_singular_values(_ptr(md), nb, 8, a, _ptr(sv), _stream()) == 0
+    want = arrays[f"kern/a{a}/sv"]
+    assert np.all(np.abs(sv.cpu().numpy() - want) <= 1e-12 * np.maximum(1e-300, want.max(axis=1, keepdims=True)))
+
+
+# ------------------------------------------------------------ solver level
+def _close_mask(locs, n, m):
+    """Entries sharing a residue class mod m with another entry less than
+    CLOSE_GAP candidate steps away (circular)."""
+    locs = np.asarray(locs, dtype=np.int64)
+    close = np.zeros(locs.size, dtype=bool)
+    d = n // m
+    res = locs % m
+    for r in np.unique(res):
+        idx = np.nonzero(res == r)[0]
+        if idx.size < 2:
+            continue
+        t = locs[idx] // m
+        diff = np.abs(t[:, None] - t[None, :]) % d
+        diff = np.minimum(diff, d - diff)
+        np.fill_diagonal(diff, d)
+        close[idx] = diff.min(axis=1) < CLOSE_GAP
+    return close
+
+
+def assert_entries_match(got: dict, want_locs, want_vals, n, m_fine, ctx=""):
+    assert list(got.keys()) == [int(v) for v in want_locs], f"{ctx}: supports/order differ"
+    g = np.fromiter(got.values(), dtype=np.complex128, count=len(got))
+    w = np.asarray(want_vals)
+    rel = np.abs(g - w) / np.maximum(np.abs(w), 1e-300)
+    close = _close_mask(want_locs, n, m_fine)
+    if rel.size:
+        assert np.all(rel[~close] <= VAL_RTOL), f"{ctx}: max rel {rel[~close].max():.3e}"
+        assert np.all(rel[close] <= CLOSE_RTOL), f"{ctx}: close-root max rel {rel[close].max():.3e}"
+
+
+def _trace_dict(tr):
+    return dict(full_success=tr.full_success, fft_samples=tr.fft_samples,
+                syndromes_computed=tr.syndromes_computed, unresolved_bins=tr.unresolved_bins,
+                warnings=tr.warnings, iterations=[vars(it) for it in tr.iterations])
+
+
+@pytest.mark.parametrize("case", EXACT_CASES, ids=[c[0] for c in EXACT_CASES])
+@pytest.mark.parametrize("solver", ["noniterative", "iterative"])
+def test_exact_solver_matches_golden(golden, case, solver):
+    arrays, meta = golden
+    name, n, k, mu, a_max, values, seed, synth = case
+    x, _ = exact_signal(n, k, seed, values, synth)
+    cfg = P.ExactConfig(n=n, k=k, mu=mu, a_max=a_max)
+    fn = P.solve_noniterative if solver == "noniterative" else P.solve_iterative
+    spec, tr = fn(x, cfg)
+    d = cfg.resolved_d()
+    m_fine = n // min(n, d << (a_max - 1)) if solver == "iterative" else n // d
+    assert_entries_match(spec.entries, arrays[f"{name}/{solver}/locs"],
+                         arrays[f"{name}/{solver}/vals"], n, m_fine, f"{name}/{solver}")
+    want = meta["exact"][name][solver]
+    got = _trace_dict(tr)
+    for key in ("full_success", "fft_samples", "syndromes_computed", "unresolved_bins",
+                "warnings", "iterations"):
+        assert got[key] == want[key], (name, solver, key, got[key], want[key])
+
+
+@pytest.mark.parametrize("solver", ["noniterative", "iterative"])
+def test_batched_equals_oracle_cfg2_shape(solver):
+    """Config-2 shape (N=2^20, K=256, |v| in [1,10]) on a batch of 6 signals,
+    one kernel launch sequence, against the oracle on each signal."""
+    n, k, B = 1 << 20, 256, 6
+    X = np.stack([exact_signal(n, k, (2024, b), "mag1_10")[0] for b in range(B)])
+    cfg = P.ExactConfig(n=n, k=k)
+    res = P.exact_batch(X, cfg, solver == "iterative")
+    fn = OS.exact_noniterative if solver == "noniterative" else OS.exact_iterative
+    d = cfg.resolved_d()
+    for b in range(B):
+        want, wtr = fn(X[b], k)
+        locs = np.fromiter(want.keys(), dtype=np.int64, count=len(want))
+        vals = np.fromiter(want.values(), dtype=np.complex128, count=len(want))
+        m_fine = n // min(n, d << 3) if solver == "iterative" else n // d
+        assert_entries_match(res.spectrum(b).entries, locs, vals, n, m_fine, f"b={b}")
+        tr = _trace_dict(res.trace(b))
+        for key in ("full_success", "unresolved_bins", "iterations", "syndromes_computed"):
+            assert tr[key] == wtr[key], (b, key)
+    rms_want = np.array([OS.rms(X[b]) for b in range(B)])
+    assert np.allclose(res.to_host()["rms"], rms_want, rtol=1e-13, atol=0)
+
+
+def test_empty_and_edge_signals():
+    # all-zero signal: no active bins, full success, empty spectrum
+    n = 1 << 12
+    cfg = P.ExactConfig(n=n, k=8)
+    spec, tr = P.solve_noniterative(np.zeros(n, complex), cfg)
+    assert len(spec) == 0 and tr.full_success and tr.iterations[0].bins_attempted == 0
+    spec, tr = P.solve_iterative(np.zeros(n, complex), cfg)
+    assert len(spec) == 0 and tr.full_success
+    # d = 1 (k >= n/mu) and tiny n
+    for n, k in ((2, 1), (8, 8), (64, 64)):
+        x, _ = exact_signal(n, min(k, n), 1, "unit")
+        for fn, ofn in ((P.solve_noniterative, OS.exact_noniterative),
+                        (P.solve_iterative, OS.exact_iterative)):
+            cfg = P.ExactConfig(n=n, k=k)
+            spec, tr = fn(x, cfg)
+            want, wtr = ofn(x, k)
+            assert list(spec.entries) == list(want)
+            assert tr.full_success == wtr["full_success"]
+    with pytest.raises(ValueError):
+        P.solve_noniterative(np.zeros(12, complex), P.ExactConfig(n=16, k=2))
+    with pytest.raises(ValueError):
+        P.solve_noniterative(np.zeros(16, complex), P.ExactConfig(n=32, k=2))
+
+
+def test_complex64_storage_mode():
+    """complex64 storage, FP64 compute: compare with the oracle on the
+    quantized input upcast to complex128 (SURVEY 8(c) rule 4)."""
+    n, k = 1 << 16, 64
+    x, _ = exact_signal(n, k, 9, "unit")
+    x64 = x.astype(np.complex64)
+    cfg = P.ExactConfig(n=n, k=k)
+    spec, tr = P.solve_noniterative(x64, cfg)
+    want, wtr = OS.exact_noniterative(x64.astype(np.complex128), k)
+    assert list(spec.entries) == list(want)
+    g = np.fromiter(spec.entries.values(), complex)
+    w = np.fromiter(want.values(), complex)
+    assert np.all(np.abs(g - w) <= 1e-4 * np.abs(w))
+    assert tr.full_success == wtr["full_success"]
+
+
+def test_estimate_sparsity(golden):
+    arrays, meta = golden
+    for name, n, k, mu, a_max, values, seed, synth in EXACT_CASES:
+        rec = meta["exact"][name].get("estimate")
+        if rec is None:
+            continue
+        x, _ = exact_signal(n, k, seed, values, synth)
+        est = P.estimate_sparsity_and_solve(x, mu, a_max)
+        assert est.k_hat == rec["k_hat"] and est.final_d == rec["final_d"]
+        assert [[d, s] for d, s in est.stages] == rec["stages"]
+        assert est.fft_samples == rec["fft_samples"]
+        assert_entries_match(est.spectrum.entries, arrays[f"{name}/estimate/locs"],
+                             arrays[f"{name}/estimate/vals"], n, n // est.final_d, name)

@@ -113,13 +113,17 @@ typedef struct {
     int64_t dup_cap;
     int64_t *stats;         /* batch * SFDT_ST_PER_SIGNAL */
     double *rms;            /* batch: rms(x) (spectral.py:215-218) */
+    /* optional instrumentation (host side) */
+    void *ev_stream_begin;  /* cudaEvent_t recorded right before / after the */
+    void *ev_stream_end;    /* HBM stream kernel (roofline timing), or NULL  */
+    int32_t kernel_launches; /* out: kernels launched by the last solve */
 } sfdt_exact_args;
 
 /* capacities that can never overflow for these arguments */
 int sfdt_exact_caps(const sfdt_exact_args *args, int64_t *entry_cap, int64_t *unres_cap,
                     int64_t *dup_cap);
 size_t sfdt_exact_workspace_bytes(const sfdt_exact_args *args);
-int sfdt_exact_solve(const sfdt_exact_args *args, void *workspace, size_t workspace_bytes,
+int sfdt_exact_solve(sfdt_exact_args *args, void *workspace, size_t workspace_bytes,
                      sfdt_stream_t stream);
 
 #ifdef __cplusplus

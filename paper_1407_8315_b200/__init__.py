@@ -2,9 +2,10 @@
 package's recovery entry points, computed by hand-written sm_100a kernels
 (libsfdt_b200.so).  See DESIGN.md."""
 
-from .exact import (EstimateResult, ExactBatch, ExactConfig, IterationStats, SolverTrace,
-                    estimate_sparsity_and_solve, exact_batch, solve_iterative,
-                    solve_iterative_batch, solve_noniterative, solve_noniterative_batch)
+from .exact import (EstimateResult, ExactBatch, ExactConfig, HostBatchResult, IterationStats,
+                    SolverTrace, estimate_sparsity_and_solve, exact_batch, solve_host_batch,
+                    solve_iterative, solve_iterative_batch, solve_noniterative,
+                    solve_noniterative_batch)
 from .spectral import SparseSpectrum, as_signal
 
 BACKEND = "b200"
@@ -17,7 +18,8 @@ def using_compiled() -> bool:
 
 
 __all__ = [
-    "BACKEND", "EstimateResult", "ExactBatch", "ExactConfig", "IterationStats", "SolverTrace",
+    "BACKEND", "EstimateResult", "ExactBatch", "ExactConfig", "HostBatchResult",
+    "IterationStats", "SolverTrace", "solve_host_batch",
     "SparseSpectrum", "as_signal", "estimate_sparsity_and_solve", "exact_batch",
     "solve_iterative", "solve_iterative_batch", "solve_noniterative",
     "solve_noniterative_batch", "using_compiled",

@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(THREADS) k_stream(const T *__restrict__ x, int
                 int64_t j = e >> logd;
                 int64_t s = e & (d - 1);
                 while (s < S) {
-                    const int64_t jj = (j < 0) ? j + L : j;
+                    const int64_t jj = j & (L - 1);   // (d*j + s) mod n wraps rows mod L
                     stcx(wb + jj * S + s, mk(re, im));
                     s += d;
                     j -= 1;
@@ -334,7 +334,7 @@ __global__ void k_iter_final(const cx *__restrict__ V, const uint8_t *__restrict
 // entry offsets; unresolved bins ascending.  One CTA per signal.
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) k_noniter_count(const uint8_t *__restrict__ status, int64_t L,
-                                                           int a_max, int S,
+                                                           int a_max, int S, int64_t d,
                                                            int64_t *__restrict__ stats) {
     const int64_t b = blockIdx.x;
     long long cnt[5] = {0, 0, 0, 0, 0};   // entries per a (1..4) and unresolved in [0]
@@ -376,6 +376,7 @@ __global__ void __launch_bounds__(THREADS) k_noniter_count(const uint8_t *__rest
         st[SFDT_ST_SYNDROMES] = red[6][0] * S;
         st[SFDT_ST_FFT_SAMPLES] = int64_t(S) * L;
         int64_t *it = st + SFDT_ST_ITER0;
+        it[0] = d;
         it[1] = red[5][0];                 // attempted
         it[2] = red[5][0] - red[0][0];     // solved
         it[3] = red[0][0];                 // deferred
@@ -681,7 +682,7 @@ extern "C" size_t sfdt_exact_workspace_bytes(const sfdt_exact_args *a) {
     return p.total;
 }
 
-extern "C" int sfdt_exact_solve(const sfdt_exact_args *a, void *ws, size_t ws_bytes,
+extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
                                 sfdt_stream_t stream_) {
     ExactPlan p;
     int rc = make_plan(a, p);
@@ -699,8 +700,10 @@ extern "C" int sfdt_exact_solve(const sfdt_exact_args *a, void *ws, size_t ws_by
     double *thr = (double *)(w + p.off_thr);
     cx *fft_scratch = p.off_fft ? (cx *)(w + p.off_fft) : nullptr;
 
+    int launches = 0;
     // 1. the single pass over x
     {
+        if (a->ev_stream_begin) cudaEventRecord((cudaEvent_t)a->ev_stream_begin, stream);
         constexpr int TH = 256, UN = 8;
         dim3 grid((unsigned)p.nchunk, (unsigned)p.B);
         if (a->x_dtype == SFDT_C128)
@@ -710,9 +713,12 @@ extern "C" int sfdt_exact_solve(const sfdt_exact_args *a, void *ws, size_t ws_by
             k_stream<float2, TH, UN><<<grid, TH, 0, stream>>>((const float2 *)a->x, p.n, p.logd,
                                                               (int)p.S, p.CH, win, partial);
         SFDT_CHECK_LAUNCH();
+        if (a->ev_stream_end) cudaEventRecord((cudaEvent_t)a->ev_stream_end, stream);
+        launches += 1;
         k_rms<<<(unsigned)p.B, 1024, 0, stream>>>(partial, p.nchunk, p.n, a->zero_threshold, p.d,
                                                  a->rms, thr);
         SFDT_CHECK_LAUNCH();
+        launches += 1;
     }
 
     if (!a->iterative) {
@@ -727,7 +733,7 @@ extern "C" int sfdt_exact_solve(const sfdt_exact_args *a, void *ws, size_t ws_by
             V, p.B, p.L, (int)p.S, a->a_max, p.n, thr, status, bloc, bval);
         SFDT_CHECK_LAUNCH();
         k_noniter_count<256><<<(unsigned)p.B, 256, 0, stream>>>(status, p.L, a->a_max, (int)p.S,
-                                                                a->stats);
+                                                                p.d, a->stats);
         SFDT_CHECK_LAUNCH();
         k_scan_offsets<<<1, 1024, 0, stream>>>(a->stats, p.B, SFDT_ST_NENTRIES, a->entry_offsets);
         k_scan_offsets<<<1, 1024, 0, stream>>>(a->stats, p.B, SFDT_ST_NUNRESOLVED, a->unres_offsets);
@@ -737,6 +743,8 @@ extern "C" int sfdt_exact_solve(const sfdt_exact_args *a, void *ws, size_t ws_by
             a->locs, (cx *)a->vals, a->unres_bins);
         SFDT_CHECK_LAUNCH();
         if (a->dup_offsets) cudaMemsetAsync(a->dup_offsets, 0, sizeof(int64_t) * (p.B + 1), stream);
+        launches += (p.L > FFT_SMEM_MAX ? 2 : 1) + 5;
+        a->kernel_launches = launches;
         return SFDT_OK;
     }
 
@@ -800,5 +808,7 @@ extern "C" int sfdt_exact_solve(const sfdt_exact_args *a, void *ws, size_t ws_by
                                                         a->locs, (cx *)a->vals, a->unres_bins,
                                                         a->dup_locs);
     SFDT_CHECK_LAUNCH();
+    launches += (int)p.npass * (1 + 1 + (p.L > FFT_SMEM_MAX ? 2 : 1)) + 1 + 1 + 2 + (a->dup_offsets ? 1 : 0) + 1;
+    a->kernel_launches = launches;
     return SFDT_OK;
 }

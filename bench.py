@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--seed", type=int, default=2024)
+    ap.add_argument("--pipeline", type=int, default=0,
+                    help="signals per overlap chunk (0: no FFT/stream overlap)")
     return ap.parse_args()
 
 
@@ -258,7 +260,7 @@ def gpu_arm(a):
     ev_b.record()
     ev_e.record()
     for _ in range(a.warmup):
-        res = P.exact_batch(X, cfg, iterative, dev)
+        res = P.exact_batch(X, cfg, iterative, dev, pipeline=a.pipeline)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
@@ -273,7 +275,8 @@ def gpu_arm(a):
     with ClockSampler(local) as clocks:
         step_start.record()
         for s in range(a.steps):
-            res = P.exact_batch(X, cfg, iterative, dev, stream_events=(sb[s], se[s]))
+            res = P.exact_batch(X, cfg, iterative, dev, stream_events=(sb[s], se[s]),
+                                pipeline=a.pipeline)
         step_end.record()
         torch.cuda.synchronize(dev)
     total_ms = step_start.elapsed_time(step_end)

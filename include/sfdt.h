@@ -113,6 +113,11 @@ typedef struct {
     int64_t dup_cap;
     int64_t *stats;         /* batch * SFDT_ST_PER_SIGNAL */
     double *rms;            /* batch: rms(x) (spectral.py:215-218) */
+    /* optional pipelining: with a second stream, the HBM stream kernel of
+     * signal chunk c+1 (this stream) overlaps the FFT + decode of chunk c
+     * (aux_stream).  chunk_signals <= 0 picks ~16 chunks. */
+    void *aux_stream;
+    int64_t chunk_signals;
     /* optional instrumentation (host side) */
     void *ev_stream_begin;  /* cudaEvent_t recorded right before / after the */
     void *ev_stream_end;    /* HBM stream kernel (roofline timing), or NULL  */

@@ -1,16 +1,17 @@
 // exact.cu -- sm_100a kernels of the exactly-K-sparse path.
 //
-//   k_stream       one HBM pass over x: per-chunk sum |x|^2 (the rms of
-//                  exact.py:176/215) + capture of the 2*a_max-sample shift
-//                  window x[d*j .. d*j+S-1] of every d-block (spectral.py:
-//                  151-160) into win (B, L, S).  The only kernel that
-//                  touches all of x; HBM roofline = 16 B per sample.
+//   k_sumsq        the one HBM pass over x: per-chunk sum |x|^2 (the rms of
+//                  exact.py:176/215).  The only kernel that touches all of
+//                  x; HBM roofline = 16 B per sample (8 B complex64).
 //   k_rms          deterministic tree over the chunk partials -> rms, zero
 //                  threshold zero_threshold*rms*d.
-//   k_fft_views    batched radix-2 DIT FFT of the shifted views, one CTA per
-//                  group of views, in shared memory, reproducing the
-//                  reference's butterfly arithmetic exactly (fft.cuh).
-//   k_decode_noniter  thread-per-bin non-iterative decode (exact.py:184-192)
+//   k_fft_views    gathers the 2*a_max shifted views x[d*j + s] straight from
+//                  x (spectral.py:151-160) and runs the batched radix-2 DIT
+//                  FFT in shared memory with the reference's exact butterfly
+//                  arithmetic (fft.cuh).
+//   k_decode_a1 / k_decode_multi  thread-per-bin non-iterative decode
+//                  (exact.py:184-192): a = 1 for every bin, then a worklist
+//                  of the bins that need a >= 2.
 //   k_iter_pass    one pass l of the iterative solver (exact.py:223-285):
 //                  fold, SubFreq, activation, descending-a decode with
 //                  retry/deferral, per-bin subtraction of accepted terms.
@@ -23,50 +24,42 @@
 namespace sfdt {
 
 // ------------------------------------------------------------- stream pass
-// grid (nchunk, B); each CTA streams CH contiguous samples of one signal with
-// 16-byte loads (8 in flight per thread), accumulates |x|^2 in a fixed order
-// and scatters window samples.  T = double2 (complex128) or float2 (complex64
-// storage, upconverted at load).
-template <typename T, int THREADS, int UNROLL>
-__global__ void __launch_bounds__(THREADS) k_stream(const T *__restrict__ x, int64_t n, int logd,
-                                                   int S, int64_t CH, cx *__restrict__ win,
-                                                   double *__restrict__ partial) {
+// grid (nchunk, B): each CTA streams CH contiguous samples of one signal and
+// writes its |x|^2 partial (fixed-order reduction).  Pairs of samples are
+// loaded per instruction -- 32 B (LDG.256, evict-first, no L1 allocate) for
+// complex128, 16 B for complex64 storage -- the measured best shape on B200
+// (tools/membw.cu: 7.55 TB/s pure read).  The shift windows are not touched
+// here: the FFT kernel gathers them straight from x.
+template <int C64, int THREADS, int UNROLL>
+__global__ void __launch_bounds__(THREADS) k_sumsq(const void *__restrict__ x_, int64_t n, int64_t CH,
+                                                  double *__restrict__ partial) {
     const int64_t b = blockIdx.y;
     const int64_t chunk = blockIdx.x;
-    const int64_t d = int64_t(1) << logd;
-    const int64_t L = n >> logd;
-    const T *xs = x + b * n;
-    cx *wb = win + b * L * S;
+    const int64_t CHp = CH >> 1;                        // sample pairs in this chunk
+    const int64_t base = (b * n + chunk * CH) >> 1;     // pair index
     double acc = 0.0;
-    const int64_t base = chunk * CH;
-    for (int64_t off = 0; off < CH; off += int64_t(THREADS) * UNROLL) {
-        T v[UNROLL];
+    for (int64_t off = 0; off < CHp; off += int64_t(THREADS) * UNROLL) {
+        double v[UNROLL][4];
 #pragma unroll
         for (int u = 0; u < UNROLL; u++) {
-            const int64_t e = base + off + int64_t(u) * THREADS + threadIdx.x;
-            if constexpr (sizeof(T) == 16) {
-                v[u] = (e < base + CH) ? __ldcs(reinterpret_cast<const double2 *>(xs + e)) : T{0, 0};
-            } else {
-                v[u] = (e < base + CH) ? __ldcs(reinterpret_cast<const float2 *>(xs + e)) : T{0, 0};
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < UNROLL; u++) {
-            const int64_t e = base + off + int64_t(u) * THREADS + threadIdx.x;
-            const double re = (double)v[u].x, im = (double)v[u].y;
-            acc = fma(re, re, fma(im, im, acc));
-            if (e < base + CH) {
-                // window rows j with e = d*j + s (mod n), 0 <= s < S
-                int64_t j = e >> logd;
-                int64_t s = e & (d - 1);
-                while (s < S) {
-                    const int64_t jj = j & (L - 1);   // (d*j + s) mod n wraps rows mod L
-                    stcx(wb + jj * S + s, mk(re, im));
-                    s += d;
-                    j -= 1;
+            const int64_t pidx = off + int64_t(u) * THREADS + threadIdx.x;
+            if (pidx < CHp) {
+                if (C64) {
+                    const float4 f = __ldcs(reinterpret_cast<const float4 *>(x_) + base + pidx);
+                    v[u][0] = f.x; v[u][1] = f.y; v[u][2] = f.z; v[u][3] = f.w;
+                } else {
+                    const double *pp = reinterpret_cast<const double *>(x_) + 4 * (base + pidx);
+                    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.f64 {%0,%1,%2,%3}, [%4];"
+                                 : "=d"(v[u][0]), "=d"(v[u][1]), "=d"(v[u][2]), "=d"(v[u][3])
+                                 : "l"(pp));
                 }
+            } else {
+                v[u][0] = v[u][1] = v[u][2] = v[u][3] = 0.0;
             }
         }
+#pragma unroll
+        for (int u = 0; u < UNROLL; u++)
+            acc = fma(v[u][0], v[u][0], fma(v[u][1], v[u][1], fma(v[u][2], v[u][2], fma(v[u][3], v[u][3], acc))));
     }
     // deterministic block reduction: warp xor-tree, then fixed-order smem tree
 #pragma unroll
@@ -108,26 +101,86 @@ __global__ void k_scale_thr(const double *__restrict__ rms, int64_t B, double zt
 }
 
 // --------------------------------------------------- non-iterative decode
-// status: 0 inactive, 1..a_max accepted at that a, 0xFF unresolved
-__global__ void k_decode_noniter(const cx *__restrict__ V, int64_t B, int64_t L, int S, int a_max,
-                                 int64_t n, const double *__restrict__ thr,
-                                 uint8_t *__restrict__ status, int64_t *__restrict__ bin_loc,
-                                 cx *__restrict__ bin_val) {
+// status: 0 inactive, 1..a_max accepted at that a, 0xFF unresolved (0xFE =
+// pending a >= 2 while the worklist is processed).
+//
+// Pass 1 (k_decode_a1): thread per bin, syndromes in registers (S is a
+// template parameter), activity test + the a = 1 model; bins that fail it
+// go to a compact worklist (warp-aggregated append).  Pass 2
+// (k_decode_multi): grid-stride over the worklist, a = 2..a_max.  Every bin's
+// result depends only on its own syndromes (exact.py:184-192), so the split
+// and the worklist order change nothing.
+template <int S>
+__global__ void __launch_bounds__(128) k_decode_a1(const cx *__restrict__ V, int64_t B, int64_t L,
+                                                   int a_max, int64_t n,
+                                                   const double *__restrict__ thr,
+                                                   uint8_t *__restrict__ status,
+                                                   int64_t *__restrict__ bin_loc,
+                                                   cx *__restrict__ bin_val,
+                                                   int64_t *__restrict__ wl,
+                                                   unsigned long long *__restrict__ wl_count) {
     const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= B * L) return;
-    const int64_t b = t / L, k = t - b * L;
-    cx syn[MAX_SHIFTS];
-    const double th = thr[b];
-    bool active = false;
-    for (int s = 0; s < S; s++) {
-        syn[s] = ldcx(V + (b * S + s) * L + k);
-        active = active || (cabs_(syn[s]) > th);
+    const bool valid = t < B * L;
+    bool pending = false;
+    if (valid) {
+        const int64_t b = t / L, k = t - b * L;
+        cx syn[S];
+        const double th = thr[b];
+        // |v| > th decided on |v|^2 away from the boundary; the exact hypot
+        // comparison (numpy abs) only inside a 1e-6-relative band around it
+        const double th2lo = th * th * (1.0 - 1e-6), th2hi = th * th * (1.0 + 1e-6);
+        bool active = false;
+#pragma unroll
+        for (int s = 0; s < S; s++) {
+            syn[s] = ldcx(V + (b * S + s) * L + k);
+            const double q = syn[s].re * syn[s].re + syn[s].im * syn[s].im;
+            active = active || (q > th2hi) || (q >= th2lo && cabs_(syn[s]) > th);
+        }
+        uint8_t st = 0;
+        if (active) {
+            Decoded o;
+            decode_try(syn, S, 1, n, L, k, o);
+            if (o.accept) {
+                st = 1;
+                bin_loc[t * a_max] = o.loc[0];
+                stcx(bin_val + t * a_max, o.val[0]);
+            } else if (a_max > 1) {
+                st = 0xFE;
+                pending = true;
+            } else {
+                st = 0xFF;
+            }
+        }
+        status[t] = st;
     }
-    uint8_t st = 0;
-    if (active) {
-        st = 0xFF;
+    const unsigned mask = __ballot_sync(0xffffffffu, pending);
+    if (mask) {
+        const int lane = threadIdx.x & 31;
+        unsigned long long base = 0;
+        if (lane == __ffs(mask) - 1) base = atomicAdd(wl_count, (unsigned long long)__popc(mask));
+        base = __shfl_sync(0xffffffffu, base, __ffs(mask) - 1);
+        if (pending) wl[base + __popc(mask & ((1u << lane) - 1))] = t;
+    }
+}
+
+template <int S>
+__global__ void __launch_bounds__(128) k_decode_multi(const cx *__restrict__ V, int64_t L, int a_max,
+                                                      int64_t n, uint8_t *__restrict__ status,
+                                                      int64_t *__restrict__ bin_loc,
+                                                      cx *__restrict__ bin_val,
+                                                      const int64_t *__restrict__ wl,
+                                                      const unsigned long long *__restrict__ wl_count) {
+    const int64_t cnt = (int64_t)*wl_count;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < cnt;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t t = wl[i];
+        const int64_t b = t / L, k = t - b * L;
+        cx syn[S];
+#pragma unroll
+        for (int s = 0; s < S; s++) syn[s] = ldcx(V + (b * S + s) * L + k);
+        uint8_t st = 0xFF;
         Decoded o;
-        for (int a = 1; a <= a_max; a++) {
+        for (int a = 2; a <= a_max; a++) {
             decode_try(syn, S, a, n, L, k, o);
             if (o.accept) {
                 st = (uint8_t)a;
@@ -138,8 +191,28 @@ __global__ void k_decode_noniter(const cx *__restrict__ V, int64_t B, int64_t L,
                 break;
             }
         }
+        status[t] = st;
     }
-    status[t] = st;
+}
+
+template <int S>
+static int launch_decode_noniter(const cx *V, int64_t B, int64_t L, int a_max, int64_t n,
+                                 const double *thr, uint8_t *status, int64_t *bin_loc, cx *bin_val,
+                                 int64_t *wl, unsigned long long *wl_count, cudaStream_t stream) {
+    const int64_t nbins = B * L;
+    cudaMemsetAsync(wl_count, 0, sizeof(unsigned long long), stream);
+    k_decode_a1<S><<<(unsigned)((nbins + 127) / 128), 128, 0, stream>>>(V, B, L, a_max, n, thr, status,
+                                                                        bin_loc, bin_val, wl, wl_count);
+    SFDT_CHECK_LAUNCH();
+    if (a_max > 1) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        k_decode_multi<S><<<(unsigned)(sms * 8), 128, 0, stream>>>(V, L, a_max, n, status, bin_loc, bin_val,
+                                                                  wl, wl_count);
+        SFDT_CHECK_LAUNCH();
+    }
+    return SFDT_OK;
 }
 
 // ----------------------------------------------------- iterative pass l
@@ -416,52 +489,81 @@ __global__ void k_scan_offsets(const int64_t *__restrict__ stats, int64_t B, int
     if (threadIdx.x == 0) offsets[B] = carry;
 }
 
-// emit entries in (a, bin) order and unresolved bins ascending; one CTA per
-// signal, block-wide ordered scan per a-class.
+// emit entries in (a, bin) order and unresolved bins ascending.  One CTA per
+// signal; each thread owns 4 consecutive bins of a tile; the per-class bin
+// counts (a = 1..4 and unresolved: 5 x 12-bit fields of one uint64) get a
+// single block-wide exclusive scan per tile.
+__device__ __forceinline__ unsigned long long block_excl_scan_u64(unsigned long long v,
+                                                                  unsigned long long *wtot,
+                                                                  unsigned long long &total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    unsigned long long inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) wtot[warp] = inc;
+    __syncthreads();
+    unsigned long long before = 0, tot = 0;
+    for (int w2 = 0; w2 < nw; w2++) {
+        const unsigned long long c = wtot[w2];
+        before += (w2 < warp) ? c : 0;
+        tot += c;
+    }
+    __syncthreads();
+    total = tot;
+    return before + inc - v;
+}
+
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) k_noniter_emit(
     const uint8_t *__restrict__ status, const int64_t *__restrict__ bin_loc,
     const cx *__restrict__ bin_val, int64_t L, int a_max, const int64_t *__restrict__ stats,
     const int64_t *__restrict__ eoff, const int64_t *__restrict__ uoff, int64_t *__restrict__ locs,
     cx *__restrict__ vals, int32_t *__restrict__ ubins) {
+    __shared__ unsigned long long wtot[THREADS / 32];
     const int64_t b = blockIdx.x;
-    __shared__ long long buf[THREADS];
-    __shared__ long long carry;
     const int64_t *st = stats + b * SFDT_ST_PER_SIGNAL;
-    long long class_base = eoff[b];
-    for (int cls = 1; cls <= a_max + 1; cls++) {   // cls a_max+1 = unresolved list
-        const bool unres = cls == a_max + 1;
-        if (threadIdx.x == 0) carry = unres ? uoff[b] : class_base;
-        __syncthreads();
-        for (int64_t k0 = 0; k0 < L; k0 += THREADS) {
-            const int64_t k = k0 + threadIdx.x;
-            const uint8_t s = (k < L) ? status[b * L + k] : 0;
-            const long long w = unres ? (s == 0xFF) : ((s == cls) ? cls : 0);
-            buf[threadIdx.x] = w;
-            __syncthreads();
-            for (int o = 1; o < THREADS; o <<= 1) {
-                long long add = (threadIdx.x >= o) ? buf[threadIdx.x - o] : 0;
-                __syncthreads();
-                buf[threadIdx.x] += add;
-                __syncthreads();
-            }
-            const long long pos = carry + buf[threadIdx.x] - w;
-            if (w) {
-                if (unres) {
-                    ubins[pos] = (int32_t)k;
-                } else {
-                    const int64_t t = b * L + k;
-                    for (int j = 0; j < cls; j++) {
-                        locs[pos + j] = bin_loc[t * a_max + j];
-                        stcx(vals + pos + j, bin_val[t * a_max + j]);
-                    }
+    long long base[5];
+    base[0] = eoff[b];
+    for (int c = 1; c < 4; c++) base[c] = base[c - 1] + st[24 + c - 1];
+    base[4] = uoff[b];
+    long long carry[5] = {0, 0, 0, 0, 0};
+    for (int64_t t0 = 0; t0 < L; t0 += THREADS * 4) {
+        int ci[4];
+        unsigned long long packed = 0;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int64_t k = t0 + 4 * threadIdx.x + u;
+            const uint8_t sv = (k < L) ? status[b * L + k] : 0;
+            ci[u] = (sv == 0xFF) ? 4 : (sv >= 1 && sv <= 4 ? sv - 1 : -1);
+            if (ci[u] >= 0) packed += 1ull << (12 * ci[u]);
+        }
+        unsigned long long total;
+        const unsigned long long pre = block_excl_scan_u64(packed, wtot, total);
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int c = ci[u];
+            if (c < 0) continue;
+            int local = 0;
+            for (int u2 = 0; u2 < u; u2++) local += (ci[u2] == c);
+            const long long rank = carry[c] + (long long)((pre >> (12 * c)) & 0xFFF) + local;
+            const int64_t k = t0 + 4 * threadIdx.x + u;
+            if (c == 4) {
+                ubins[base[4] + rank] = (int32_t)k;
+            } else {
+                const int a = c + 1;
+                const long long pos = base[c] + rank * a;
+                const int64_t t = b * L + k;
+                for (int j = 0; j < a; j++) {
+                    locs[pos + j] = bin_loc[t * a_max + j];
+                    stcx(vals + pos + j, bin_val[t * a_max + j]);
                 }
             }
-            __syncthreads();
-            if (threadIdx.x == THREADS - 1) carry += buf[THREADS - 1];
-            __syncthreads();
         }
-        if (!unres) class_base += st[24 + cls - 1];
+#pragma unroll
+        for (int c = 0; c < 5; c++) carry[c] += (long long)((total >> (12 * c)) & 0xFFF);
     }
 }
 
@@ -615,8 +717,8 @@ static inline size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
 struct ExactPlan {
     int64_t B, n, d, L, S, CH, nchunk, npass;
     int logd;
-    size_t off_win, off_V, off_partial, off_thr, off_status, off_bloc, off_bval, off_def,
-        off_sloc, off_sval, off_sa, off_sdup, off_cnt, off_resid, off_ndef, off_scratch, off_fft,
+    size_t off_V, off_partial, off_thr, off_status, off_bloc, off_bval, off_def,
+        off_sloc, off_sval, off_sa, off_sdup, off_cnt, off_resid, off_ndef, off_scratch, off_fft, off_wl,
         total;
 };
 
@@ -636,7 +738,6 @@ static int make_plan(const sfdt_exact_args *a, ExactPlan &p) {
     p.npass = a->iterative ? a->a_max : 1;
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes); return r; };
-    p.off_win = take(size_t(p.B) * p.L * p.S * 16);
     p.off_V = take(size_t(p.B) * p.L * p.S * 16);
     p.off_partial = take(size_t(p.B) * p.nchunk * 8);
     p.off_thr = take(size_t(p.B) * 5 * 8);
@@ -644,6 +745,7 @@ static int make_plan(const sfdt_exact_args *a, ExactPlan &p) {
         p.off_status = take(size_t(p.B) * p.L);
         p.off_bloc = take(size_t(p.B) * p.L * a->a_max * 8);
         p.off_bval = take(size_t(p.B) * p.L * a->a_max * 16);
+        p.off_wl = take(size_t(p.B) * p.L * 8);
     } else {
         p.off_def = take(size_t(p.B) * p.L);
         p.off_sloc = take(size_t(p.B) * 4 * p.L * a->a_max * 8);
@@ -694,44 +796,92 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
         return SFDT_ECAPACITY;
     cudaStream_t stream = (cudaStream_t)stream_;
     char *w = (char *)ws;
-    cx *win = (cx *)(w + p.off_win);
     cx *V = (cx *)(w + p.off_V);
     double *partial = (double *)(w + p.off_partial);
     double *thr = (double *)(w + p.off_thr);
     cx *fft_scratch = p.off_fft ? (cx *)(w + p.off_fft) : nullptr;
 
     int launches = 0;
-    // 1. the single pass over x
-    {
-        if (a->ev_stream_begin) cudaEventRecord((cudaEvent_t)a->ev_stream_begin, stream);
-        constexpr int TH = 256, UN = 8;
-        dim3 grid((unsigned)p.nchunk, (unsigned)p.B);
-        if (a->x_dtype == SFDT_C128)
-            k_stream<double2, TH, UN><<<grid, TH, 0, stream>>>((const double2 *)a->x, p.n, p.logd,
-                                                               (int)p.S, p.CH, win, partial);
+    const int is_c64 = a->x_dtype == SFDT_C64;
+    auto launch_stream = [&](int64_t c0, int64_t bc) -> int {
+        constexpr int TH = 512, UN = 4;
+        dim3 grid((unsigned)p.nchunk, (unsigned)bc);
+        const char *xc = (const char *)a->x + c0 * p.n * (is_c64 ? 8 : 16);
+        if (is_c64)
+            k_sumsq<1, TH, UN><<<grid, TH, 0, stream>>>(xc, p.n, p.CH, partial + c0 * p.nchunk);
         else
-            k_stream<float2, TH, UN><<<grid, TH, 0, stream>>>((const float2 *)a->x, p.n, p.logd,
-                                                              (int)p.S, p.CH, win, partial);
-        SFDT_CHECK_LAUNCH();
-        if (a->ev_stream_end) cudaEventRecord((cudaEvent_t)a->ev_stream_end, stream);
-        launches += 1;
-        k_rms<<<(unsigned)p.B, 1024, 0, stream>>>(partial, p.nchunk, p.n, a->zero_threshold, p.d,
-                                                 a->rms, thr);
+            k_sumsq<0, TH, UN><<<grid, TH, 0, stream>>>(xc, p.n, p.CH, partial + c0 * p.nchunk);
         SFDT_CHECK_LAUNCH();
         launches += 1;
-    }
+        return SFDT_OK;
+    };
 
     if (!a->iterative) {
-        rc = launch_fft_views(win, p.B, p.L, (int)p.S, 1, 0, (int)p.S, p.L, a->twiddles, V,
-                              (int)p.S, p.L, stream, fft_scratch);
-        if (rc) return rc;
+        // Pipeline over signal chunks: the HBM-bound stream kernel of chunk
+        // c+1 (main stream) runs concurrently with the latency-bound FFT +
+        // decode of chunk c (aux stream).
+        cudaStream_t aux = a->aux_stream ? (cudaStream_t)a->aux_stream : stream;
+        int64_t bc = p.B;
+        if (a->aux_stream) {
+            bc = a->chunk_signals > 0 ? a->chunk_signals : (p.B + 15) / 16;
+            const int64_t min_bc = (p.B + 63) / 64;   // <= 64 chunk counters
+            if (bc < min_bc) bc = min_bc;
+        }
+        const int64_t nc = (p.B + bc - 1) / bc;
         uint8_t *status = (uint8_t *)(w + p.off_status);
         int64_t *bloc = (int64_t *)(w + p.off_bloc);
         cx *bval = (cx *)(w + p.off_bval);
-        const int64_t nbins = p.B * p.L;
-        k_decode_noniter<<<(unsigned)((nbins + 127) / 128), 128, 0, stream>>>(
-            V, p.B, p.L, (int)p.S, a->a_max, p.n, thr, status, bloc, bval);
-        SFDT_CHECK_LAUNCH();
+        int64_t *wl = (int64_t *)(w + p.off_wl);
+        unsigned long long *wlc = (unsigned long long *)(w + p.off_scratch);
+        cudaEvent_t ev_done = nullptr;
+        if (a->ev_stream_begin) cudaEventRecord((cudaEvent_t)a->ev_stream_begin, stream);
+        if (aux != stream) {   // aux work may start only after everything queued before this call
+            cudaEvent_t ev;
+            if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return SFDT_ECUDA;
+            cudaEventRecord(ev, stream);
+            cudaStreamWaitEvent(aux, ev, 0);
+            cudaEventDestroy(ev);
+        }
+        for (int64_t c = 0; c < nc; c++) {
+            const int64_t c0 = c * bc, nb = (c0 + bc <= p.B) ? bc : p.B - c0;
+            // the views need no rms: their gather + FFT (aux) overlaps the
+            // HBM stream of the same chunk (main)
+            const ViewSrc src = consecutive_views((const char *)a->x + c0 * p.n * (is_c64 ? 8 : 16),
+                                                  is_c64, p.n, p.d, 0, (int)p.S);
+            rc = launch_fft_views(src, nb, p.L, a->twiddles, V + c0 * p.S * p.L, (int)p.S, p.L, aux,
+                                  fft_scratch ? fft_scratch + c0 * p.S * p.L : nullptr);
+            if (rc) return rc;
+            if ((rc = launch_stream(c0, nb))) return rc;
+            if (c == nc - 1 && a->ev_stream_end) cudaEventRecord((cudaEvent_t)a->ev_stream_end, stream);
+            if (aux != stream) {
+                cudaEvent_t ev;
+                if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return SFDT_ECUDA;
+                cudaEventRecord(ev, stream);
+                cudaStreamWaitEvent(aux, ev, 0);
+                cudaEventDestroy(ev);
+            }
+            k_rms<<<(unsigned)nb, 1024, 0, aux>>>(partial + c0 * p.nchunk, p.nchunk, p.n,
+                                                  a->zero_threshold, p.d, a->rms + c0, thr + c0);
+            SFDT_CHECK_LAUNCH();
+            const cx *Vc = V + c0 * p.S * p.L;
+            uint8_t *stc = status + c0 * p.L;
+            int64_t *blc = bloc + c0 * p.L * a->a_max;
+            cx *bvc = bval + c0 * p.L * a->a_max;
+            switch (p.S) {
+            case 2: rc = launch_decode_noniter<2>(Vc, nb, p.L, a->a_max, p.n, thr + c0, stc, blc, bvc, wl + c0 * p.L, wlc + c, aux); break;
+            case 4: rc = launch_decode_noniter<4>(Vc, nb, p.L, a->a_max, p.n, thr + c0, stc, blc, bvc, wl + c0 * p.L, wlc + c, aux); break;
+            case 6: rc = launch_decode_noniter<6>(Vc, nb, p.L, a->a_max, p.n, thr + c0, stc, blc, bvc, wl + c0 * p.L, wlc + c, aux); break;
+            default: rc = launch_decode_noniter<8>(Vc, nb, p.L, a->a_max, p.n, thr + c0, stc, blc, bvc, wl + c0 * p.L, wlc + c, aux); break;
+            }
+            if (rc) return rc;
+            launches += 1 + (p.L > FFT_SMEM_MAX ? 2 : 1) + 1 + (a->a_max > 1 ? 1 : 0);
+        }
+        if (aux != stream) {
+            if (cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming) != cudaSuccess) return SFDT_ECUDA;
+            cudaEventRecord(ev_done, aux);
+            cudaStreamWaitEvent(stream, ev_done, 0);
+            cudaEventDestroy(ev_done);
+        }
         k_noniter_count<256><<<(unsigned)p.B, 256, 0, stream>>>(status, p.L, a->a_max, (int)p.S,
                                                                 p.d, a->stats);
         SFDT_CHECK_LAUNCH();
@@ -743,10 +893,19 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
             a->locs, (cx *)a->vals, a->unres_bins);
         SFDT_CHECK_LAUNCH();
         if (a->dup_offsets) cudaMemsetAsync(a->dup_offsets, 0, sizeof(int64_t) * (p.B + 1), stream);
-        launches += (p.L > FFT_SMEM_MAX ? 2 : 1) + 5;
+        launches += 4;
         a->kernel_launches = launches;
         return SFDT_OK;
     }
+
+    // iterative: the single pass over x first (all signals), then the passes
+    if (a->ev_stream_begin) cudaEventRecord((cudaEvent_t)a->ev_stream_begin, stream);
+    if ((rc = launch_stream(0, p.B))) return rc;
+    if (a->ev_stream_end) cudaEventRecord((cudaEvent_t)a->ev_stream_end, stream);
+    k_rms<<<(unsigned)p.B, 1024, 0, stream>>>(partial, p.nchunk, p.n, a->zero_threshold, p.d,
+                                             a->rms, thr);
+    SFDT_CHECK_LAUNCH();
+    launches += 1;
 
     // iterative: thresholds per pass (zt * rms * d_l), d_l = min(d0 * 2^l, n)
     IterState st;
@@ -778,9 +937,9 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
     }
     for (int l = 0; l < p.npass; l++) {
         const int64_t m = m_of[l];
-        const int64_t rowstride = d_of[l] / p.d;   // view row j at window row j*rowstride
-        rc = launch_fft_views(win, p.B, p.L, (int)p.S, rowstride, 2 * l, 2, m, a->twiddles,
-                              V + 2 * l * p.L, (int)p.S, p.L, stream, fft_scratch);
+        const ViewSrc src = consecutive_views(a->x, is_c64, p.n, d_of[l], 2 * l, 2);
+        rc = launch_fft_views(src, p.B, m, a->twiddles, V + 2 * l * p.L, (int)p.S, p.L, stream,
+                              fft_scratch);
         if (rc) return rc;
         const int fold = (l > 0) && (m != m_of[l - 1]);
         const int64_t nb = p.B * m;

@@ -8,60 +8,133 @@
 // output is scaled by 1/L exactly as `fft(view) / m` (spectral.py:166), so
 // views are bit-identical to the reference's.
 //
-// Layout: input view v of signal b is the strided column
-//   win[(b*Lw + j*rowstride)*S + shift0 + v],  j < L
-// of the (B, Lw, S) window buffer written by k_stream; output goes to
-//   out[(b*SV + v)*ldV + k].
+// The views are gathered straight from the signals (the downsample of
+// spectral.py:151-160 fused into the load): view v of signal b is
+//   x[b*sig_stride + ((j*jstride + off[v]) & wrap)],  j < L
+// (jstride = d, off = shift, wrap = n - 1), loaded with the shifts of one
+// d-block adjacent across lanes so every 32-byte sector is used whole.
+// Output: out[(b*SV + v)*ldV + k].
 #pragma once
 
 #include "common.cuh"
 
 namespace sfdt {
 
-static __global__ void k_fft_views(const cx *__restrict__ win, int64_t B, int64_t Lw, int S,
-                            int64_t rowstride, int shift0, int nshift, int logL, int vpc,
-                            const cx *__restrict__ tw, cx *__restrict__ out, int SV, int64_t ldV,
-                            int inverse_scale) {
+constexpr int MAX_VIEWS = 16;
+
+struct ViewSrc {
+    const void *x;
+    int is_c64;          // complex64 storage, upconverted at load
+    int nshift;          // views per signal
+    int64_t sig_stride;  // elements between signals
+    int64_t jstride;     // elements between consecutive view samples (d)
+    int64_t wrap;        // index mask (n - 1)
+    int64_t off[MAX_VIEWS];
+};
+
+__device__ __forceinline__ cx view_load(const ViewSrc &src, int64_t b, int v, int64_t j) {
+    const int64_t e = b * src.sig_stride + ((j * src.jstride + src.off[v]) & src.wrap);
+    if (src.is_c64) {
+        const float2 f = __ldg(reinterpret_cast<const float2 *>(src.x) + e);
+        return mk((double)f.x, (double)f.y);
+    }
+    return ldcx(reinterpret_cast<const cx *>(src.x) + e);
+}
+
+// 16-byte-granular swizzle of the shared-memory FFT buffers: the low 3 bits
+// of the element index are XOR-ed with every higher 3-bit group.  Shared
+// memory serves a warp's 16-byte accesses 8 lanes (one quarter) at a time,
+// conflict-free iff the 8 lanes hit distinct (index & 7) groups; in every
+// access pattern used here the 8 lanes of a quarter differ in 3 consecutive
+// index bits (radix passes starting at stage multiples of 3, the bit-
+// reversed scatter of the load, the natural-order store), and folding maps 3
+// consecutive bit positions onto 3 distinct ones, so all are conflict-free.
+__device__ __forceinline__ int swz(int p) {
+    int f = p;
+    f ^= f >> 3;
+    f ^= f >> 6;
+    f ^= f >> 12;
+    return (p & ~7) | (f & 7);
+}
+
+template <int NST>
+__device__ __forceinline__ void fft_pass(cx *a, int nv, int logL, int lh, const cx *__restrict__ tw) {
+    constexpr int G = 1 << NST;
+    const int L = 1 << logL;
+    const int h = 1 << lh;
+    const int gper = L >> NST;
+    const int ng = nv * gper;
+    for (int g = threadIdx.x; g < ng; g += blockDim.x) {
+        const int v = g / gper;
+        const int gg = g - v * gper;
+        const int lo = gg & (h - 1), hi = gg >> lh;
+        const int base = v * L + (hi << (lh + NST)) + lo;
+        const int e0 = (hi << (lh + NST)) + lo;   // index within the view
+        cx x[G];
+#pragma unroll
+        for (int q = 0; q < G; q++) x[q] = a[swz(base + q * h)];
+#pragma unroll
+        for (int st = 0; st < NST; st++) {
+            const int Hs = h << st;
+            const cx *twh = tw + (Hs - 1);
+#pragma unroll
+            for (int q = 0; q < G; q++) {
+                if (q & (1 << st)) continue;
+                const int e = e0 + q * h;
+                const cx w = ldcx(twh + (e & (Hs - 1)));
+                const cx u = x[q];
+                const cx t = gmul(x[q + (1 << st)], w);
+                x[q] = cadd(u, t);
+                x[q + (1 << st)] = csub(u, t);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < G; q++) a[swz(base + q * h)] = x[q];
+    }
+}
+
+__device__ __forceinline__ void fft_stages_smem(cx *a, int nv, int logL, int lh0, int lh1,
+                                                const cx *__restrict__ tw) {
+    for (int lh = lh0; lh < lh1;) {
+        const int nst = (lh1 - lh) >= 3 ? 3 : (lh1 - lh);
+        if (nst == 3) fft_pass<3>(a, nv, logL, lh, tw);
+        else if (nst == 2) fft_pass<2>(a, nv, logL, lh, tw);
+        else fft_pass<1>(a, nv, logL, lh, tw);
+        __syncthreads();
+        lh += nst;
+    }
+}
+
+static __global__ void k_fft_views(const ViewSrc src, int64_t B, int logL, int logvpc,
+                                   const cx *__restrict__ tw, cx *__restrict__ out, int SV,
+                                   int64_t ldV, int scale) {
     extern __shared__ double4 smem_raw[];
     cx *a = reinterpret_cast<cx *>(smem_raw);
-    const int L = 1 << logL;
-    const int64_t nviews = B * nshift;
-    const int64_t g0 = int64_t(blockIdx.x) * vpc;
+    const int L = 1 << logL, vpc = 1 << logvpc;
+    const int64_t nviews = B * src.nshift;
+    const int64_t g0 = int64_t(blockIdx.x) << logvpc;
     const int nv = (int)((nviews - g0) < vpc ? (nviews - g0) : vpc);
-    // load with bit reversal
-    for (int i = threadIdx.x; i < nv * L; i += blockDim.x) {
-        const int v = i >> logL, j = i & (L - 1);
+    // gather: lanes vary the view (shift) fastest for one sample j, so one
+    // d-block's adjacent shifts share sectors; bit-reversed scatter to smem
+    for (int i = threadIdx.x; i < (L << logvpc); i += blockDim.x) {
+        const int v = i & (vpc - 1), j = i >> logvpc;
+        if (v >= nv) continue;
         const int64_t g = g0 + v;
-        const int64_t b = g / nshift;
-        const int s = (int)(g - b * nshift);
+        const int64_t b = g / src.nshift;
+        const int s = (int)(g - b * src.nshift);
         const int r = logL ? (int)(__brev((unsigned)j) >> (32 - logL)) : 0;
-        a[v * L + r] = ldcx(win + (b * Lw + j * rowstride) * S + shift0 + s);
+        a[swz(v * L + r)] = view_load(src, b, s, j);
     }
     __syncthreads();
-    const int nbf = nv * (L >> 1);
-    for (int lh = 0; lh < logL; lh++) {
-        const int h = 1 << lh;   // half of the stage length m = 2h
-        const cx *twh = tw + (h - 1);
-        for (int t = threadIdx.x; t < nbf; t += blockDim.x) {
-            const int v = t >> (logL - 1);
-            const int tt = t & ((L >> 1) - 1);
-            const int k = tt & (h - 1);
-            const int i0 = v * L + ((tt >> lh) << (lh + 1)) + k;
-            const cx u = a[i0];
-            const cx x = gmul(a[i0 + h], ldcx(twh + k));
-            a[i0] = cadd(u, x);
-            a[i0 + h] = csub(u, x);
-        }
-        __syncthreads();
-    }
+    fft_stages_smem(a, nv, logL, 0, logL, tw);
     const double sc = 1.0 / (double)L;   // exact power of two
     for (int i = threadIdx.x; i < nv * L; i += blockDim.x) {
         const int v = i >> logL, k = i & (L - 1);
         const int64_t g = g0 + v;
-        const int64_t b = g / nshift;
-        const int s = (int)(g - b * nshift);
-        cx y = a[i];
-        if (inverse_scale) y = mk(DMUL(y.re, sc), DMUL(y.im, sc));
+        const int64_t b = g / src.nshift;
+        const int s = (int)(g - b * src.nshift);
+        cx y = a[swz(i)];
+        if (scale) y = mk(DMUL(y.re, sc), DMUL(y.im, sc));
         stcx(out + (b * SV + s) * ldV + k, y);
     }
 }
@@ -69,37 +142,24 @@ static __global__ void k_fft_views(const cx *__restrict__ win, int64_t B, int64_
 // Pass A of the large-view FFT: CTA (view g, block c) owns bit-reversed
 // positions [c*P, (c+1)*P), i.e. inputs j = rev_P(i)*Q + rev_Q(c); it runs the
 // first logP stages (all butterflies stay inside the block) unscaled.
-static __global__ void k_fft_large_a(const cx *__restrict__ win, int64_t B, int64_t Lw, int S,
-                              int64_t rowstride, int shift0, int nshift, int logL, int logP,
-                              const cx *__restrict__ tw, cx *__restrict__ scratch) {
+static __global__ void k_fft_large_a(const ViewSrc src, int logL, int logP,
+                                     const cx *__restrict__ tw, cx *__restrict__ scratch) {
     extern __shared__ double4 smem_raw[];
     cx *a = reinterpret_cast<cx *>(smem_raw);
     const int logQ = logL - logP, P = 1 << logP, Q = 1 << logQ;
     const int64_t g = blockIdx.x >> logQ;
     const int c = (int)(blockIdx.x & (Q - 1));
-    const int64_t b = g / nshift;
-    const int s = (int)(g - b * nshift);
+    const int64_t b = g / src.nshift;
+    const int s = (int)(g - b * src.nshift);
     const int rc = logQ ? (int)(__brev((unsigned)c) >> (32 - logQ)) : 0;
     for (int i = threadIdx.x; i < P; i += blockDim.x) {
         const int64_t j = (int64_t)(__brev((unsigned)i) >> (32 - logP)) * Q + rc;
-        a[i] = ldcx(win + (b * Lw + j * rowstride) * S + shift0 + s);
+        a[swz(i)] = view_load(src, b, s, j);
     }
     __syncthreads();
-    for (int lh = 0; lh < logP; lh++) {
-        const int h = 1 << lh;
-        const cx *twh = tw + (h - 1);
-        for (int t = threadIdx.x; t < (P >> 1); t += blockDim.x) {
-            const int k = t & (h - 1);
-            const int i0 = ((t >> lh) << (lh + 1)) + k;
-            const cx u = a[i0];
-            const cx x = gmul(a[i0 + h], ldcx(twh + k));
-            a[i0] = cadd(u, x);
-            a[i0 + h] = csub(u, x);
-        }
-        __syncthreads();
-    }
+    fft_stages_smem(a, 1, logP, 0, logP, tw);
     cx *dst = scratch + (g << logL) + ((int64_t)c << logP);
-    for (int i = threadIdx.x; i < P; i += blockDim.x) dst[i] = a[i];
+    for (int i = threadIdx.x; i < P; i += blockDim.x) dst[i] = a[swz(i)];
 }
 
 // large views (L > FFT_SMEM_MAX): stage split through global memory.
@@ -151,54 +211,59 @@ static __global__ void k_fft_large_b(cx *__restrict__ buf, int64_t nviews, int l
     }
 }
 
-static inline int launch_fft_views(const cx *win, int64_t B, int64_t Lw, int S, int64_t rowstride,
-                                   int shift0, int nshift, int64_t L, const double *tw_,
+// FFT of every view of B signals; large_scratch (B*nshift*L complex) is
+// needed only when L > FFT_SMEM_MAX.
+static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, const double *tw_,
                                    cx *out, int SV, int64_t ldV, cudaStream_t stream,
-                                   cx *large_scratch = nullptr) {
+                                   cx *large_scratch = nullptr, int scale = 1) {
     const cx *tw = reinterpret_cast<const cx *>(tw_);
     const int logL = ilog2_64(L);
-    const int64_t nviews = B * nshift;
+    const int64_t nviews = B * src.nshift;
+    if (nviews == 0) return SFDT_OK;
     if (L <= FFT_SMEM_MAX) {
-        int vpc = (int)(4096 / L);
-        if (vpc < 1) vpc = 1;
-        if (vpc > nshift * 4) vpc = nshift * 4;
-        const size_t smem = size_t(vpc) * L * 16;
+        int logvpc = 0;
+        while ((L << (logvpc + 1)) <= 4096 && (1 << (logvpc + 1)) <= 2 * src.nshift) logvpc++;
+        const size_t smem = (size_t(L) << logvpc) * 16;
         if (smem > 48 * 1024)
             cudaFuncSetAttribute(k_fft_views, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        const unsigned grid = (unsigned)((nviews + vpc - 1) / vpc);
-        k_fft_views<<<grid, 256, smem, stream>>>(win, B, Lw, S, rowstride, shift0, nshift, logL, vpc,
-                                                 tw, out, SV, ldV, 1);
+        const unsigned grid = (unsigned)((nviews + (1 << logvpc) - 1) >> logvpc);
+        k_fft_views<<<grid, 256, smem, stream>>>(src, B, logL, logvpc, tw, out, SV, ldV, scale);
         SFDT_CHECK_LAUNCH();
         return SFDT_OK;
     }
     if (!large_scratch) return SFDT_EINVAL;
-    // pass A: first logP stages, unscaled, into scratch (nviews, L)
     const int logP = 12, P = 1 << logP;
+    const int logQ = logL - logP;
     {
-        // reuse k_fft_views on P-point blocks: view g's block c = bit-reversed
-        // positions [c*P, (c+1)*P) hold inputs j with rev(j) in that range,
-        // i.e. j = c' + (L/P)*i with c' = rev_{logQ}(c)
-        const int logQ = logL - logP;
         const size_t smem = size_t(P) * 16;
         cudaFuncSetAttribute(k_fft_large_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        const unsigned grid = (unsigned)(nviews << logQ);
-        k_fft_large_a<<<grid, 256, smem, stream>>>(win, B, Lw, S, rowstride, shift0, nshift, logL,
-                                                   logP, tw, large_scratch);
+        k_fft_large_a<<<(unsigned)(nviews << logQ), 256, smem, stream>>>(src, logL, logP, tw, large_scratch);
         SFDT_CHECK_LAUNCH();
     }
     {
-        const int logQ = logL - logP;
-        int logR = 13 - logQ;          // tile of 2^13 points
+        int logR = 13 - logQ;          // tiles of 2^13 points
         if (logR > logP) logR = logP;
         if (logR < 0) return SFDT_EINVAL;
         const size_t smem = (size_t(1) << (logQ + logR)) * 16;
         cudaFuncSetAttribute(k_fft_large_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        const unsigned grid = (unsigned)(nviews * (P >> logR));
-        k_fft_large_b<<<grid, 256, smem, stream>>>(large_scratch, nviews, logL, logP, logR, tw, out,
-                                                   nshift, SV, ldV);
+        k_fft_large_b<<<(unsigned)(nviews * (P >> logR)), 256, smem, stream>>>(
+            large_scratch, nviews, logL, logP, logR, tw, out, src.nshift, SV, ldV);
         SFDT_CHECK_LAUNCH();
     }
     return SFDT_OK;
+}
+
+static inline ViewSrc consecutive_views(const void *x, int is_c64, int64_t n, int64_t d, int shift0,
+                                        int nshift) {
+    ViewSrc s;
+    s.x = x;
+    s.is_c64 = is_c64;
+    s.nshift = nshift;
+    s.sig_stride = n;
+    s.jstride = d;
+    s.wrap = n - 1;
+    for (int v = 0; v < MAX_VIEWS; v++) s.off[v] = (v < nshift) ? shift0 + v : 0;
+    return s;
 }
 
 }  // namespace sfdt

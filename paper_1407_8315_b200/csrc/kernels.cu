@@ -88,18 +88,11 @@ int sfdt_fft_radix2(const double *x, double *out, int64_t batch, int64_t n, int 
     (void)inverse;   // the table carries the sign
     if (batch < 0 || n < 1 || (n & (n - 1)) || n > FFT_SMEM_MAX) return SFDT_EINVAL;
     if (batch == 0) return SFDT_OK;
-    // a (batch, n) array is a window buffer with S = 1 view per signal
-    const cx *tw = reinterpret_cast<const cx *>(twiddles);
-    const int logL = ilog2_64(n);
-    int vpc = (int)(4096 / n);
-    if (vpc < 1) vpc = 1;
-    const size_t smem = size_t(vpc) * n * 16;
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(k_fft_views, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_fft_views<<<(unsigned)((batch + vpc - 1) / vpc), 256, smem, (cudaStream_t)stream>>>(
-        (const cx *)x, batch, n, 1, 1, 0, 1, logL, vpc, tw, (cx *)out, 1, n, 0);
-    SFDT_CHECK_LAUNCH();
-    return SFDT_OK;
+    // a (batch, n) array of signals, each its own single view (d = 1)
+    const ViewSrc src = consecutive_views(x, 0, n, 1, 0, 1);
+    const int rc = launch_fft_views(src, batch, n, twiddles, (cx *)out, 1, n, (cudaStream_t)stream,
+                                    nullptr, 0);
+    return rc;
 }
 
 int sfdt_hankel_solve(const double *m, int64_t nb, int64_t ld, int a, double *c, double *cd,

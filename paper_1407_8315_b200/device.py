@@ -32,6 +32,18 @@ def stream_handle(device: torch.device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
+_aux_streams: dict = {}
+
+
+def aux_stream(device: torch.device) -> torch.cuda.Stream:
+    """Second stream per device for the library's copy/compute pipelining."""
+    st = _aux_streams.get(device)
+    if st is None:
+        st = torch.cuda.Stream(device)
+        _aux_streams[device] = st
+    return st
+
+
 def twiddles(n_max: int, device: torch.device, inverse: bool = False) -> torch.Tensor:
     """Device copy of the reference-recurrence twiddle table (sfdt_fft_twiddles).
     Built once per (n_max, sign, device) on the host, cached."""

@@ -28,7 +28,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from .device import Workspace, as_device_signals, ptr, require_cuda, stream_handle, twiddles
+from .device import (Workspace, as_device_signals, aux_stream, ptr, require_cuda, stream_handle,
+                     twiddles)
 from .spectral import SparseSpectrum, check_signal_shape
 
 logger = logging.getLogger(__name__)
@@ -201,7 +202,7 @@ def _outputs(caps, B, device, iterative):
 
 
 def exact_batch(X, cfg: ExactConfig, iterative: bool, device=None,
-                stream_events=None) -> ExactBatch:
+                stream_events=None, pipeline: int = 0) -> ExactBatch:
     """Batched exact solve of X (B, n) (or (n,)) -- the device entry point.
 
     stream_events: optional (begin, end) torch.cuda.Event pair recorded around
@@ -240,6 +241,11 @@ def exact_batch(X, cfg: ExactConfig, iterative: bool, device=None,
     args.dup_locs = ptr(o["dup_locs"])
     args.dup_cap = caps[2] if iterative else 0
     args.stats, args.rms = ptr(o["stats"]), ptr(o["rms"])
+    if pipeline and not iterative:
+        # overlap the view gather + FFT + decode (aux stream) with the HBM
+        # stream pass (current stream), in chunks of `pipeline` signals
+        args.aux_stream = aux_stream(dev).cuda_stream
+        args.chunk_signals = int(pipeline)
     if stream_events is not None:
         args.ev_stream_begin = stream_events[0].cuda_event
         args.ev_stream_end = stream_events[1].cuda_event

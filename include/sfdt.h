@@ -131,6 +131,58 @@ size_t sfdt_exact_workspace_bytes(const sfdt_exact_args *args);
 int sfdt_exact_solve(sfdt_exact_args *args, void *workspace, size_t workspace_bytes,
                      sfdt_stream_t stream);
 
+/* -------------------------------------------------------- general solver */
+/* per-signal statistics of sfdt_general_solve (int64 each) */
+enum {
+    SFDT_GS_NENTRIES = 0,  /* entries written */
+    SFDT_GS_HIST0 = 1,     /* collision_histogram[a], a = 0..4 (5 slots) */
+    SFDT_GS_NVOTED = 6,    /* bins with votes >= 1 */
+    SFDT_GS_RANKDEF = 7,   /* rank-deficient least-squares calls (logged) */
+    SFDT_GS_CLASS0 = 8,    /* entries per vote class a = 1..4 (4 slots) */
+    SFDT_GS_PER_SIGNAL = 16
+};
+
+typedef struct {
+    /* input: batch x n signals (complex128 or complex64 storage) */
+    const void *x;
+    int32_t x_dtype;
+    int64_t batch;
+    int64_t n;
+    /* GeneralConfig (general.py:28-70), resolved */
+    int64_t k;
+    int64_t d;
+    int32_t a_max;
+    int32_t r_eff;            /* min(3*a_max, d) */
+    int32_t keep_per_collision;
+    int32_t prune;
+    double zero_vote_rtol;
+    /* draw_shifts (general.py:101-106), drawn on the host (numpy Generator):
+     * shifts[b*shift_stride + j], j < r_eff (device, int64); shift_stride 0 =
+     * one draw for the whole batch */
+    const int64_t *shifts;
+    int64_t shift_stride;
+    /* base_phi[b*phi_stride + j*d + t] = exp(2 pi i shifts_j t / d)
+     * (general.py:309), complex128 on the device, built by the host exactly
+     * as numpy builds it */
+    const double *base_phi;
+    int64_t phi_stride;
+    const double *twiddles;  /* sfdt_fft_twiddles(n_max >= n/d) on the device */
+    /* outputs (device) */
+    int64_t *entry_offsets;  /* batch + 1 */
+    int64_t *locs;
+    double *vals;
+    int64_t entry_cap;
+    int64_t *stats;          /* batch * SFDT_GS_PER_SIGNAL */
+    int32_t *votes;          /* optional: batch * (n/d) estimated collision counts */
+    double *singular_values; /* optional: batch * (n/d) * a_max */
+    int32_t kernel_launches; /* out */
+} sfdt_general_args;
+
+int sfdt_general_caps(const sfdt_general_args *args, int64_t *entry_cap);
+size_t sfdt_general_workspace_bytes(const sfdt_general_args *args);
+int sfdt_general_solve(sfdt_general_args *args, void *workspace, size_t workspace_bytes,
+                       sfdt_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

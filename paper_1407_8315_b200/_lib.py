@@ -45,6 +45,27 @@ class ExactArgs(ctypes.Structure):
     ]
 
 
+SFDT_GS_NENTRIES = 0
+SFDT_GS_HIST0 = 1
+SFDT_GS_NVOTED = 6
+SFDT_GS_RANKDEF = 7
+SFDT_GS_CLASS0 = 8
+SFDT_GS_PER_SIGNAL = 16
+
+
+class GeneralArgs(ctypes.Structure):
+    _fields_ = [
+        ("x", _vp), ("x_dtype", _i32), ("batch", _i64), ("n", _i64),
+        ("k", _i64), ("d", _i64), ("a_max", _i32), ("r_eff", _i32),
+        ("keep_per_collision", _i32), ("prune", _i32), ("zero_vote_rtol", _dbl),
+        ("shifts", _vp), ("shift_stride", _i64), ("base_phi", _vp), ("phi_stride", _i64),
+        ("twiddles", _vp),
+        ("entry_offsets", _vp), ("locs", _vp), ("vals", _vp), ("entry_cap", _i64),
+        ("stats", _vp), ("votes", _vp), ("singular_values", _vp),
+        ("kernel_launches", _i32),
+    ]
+
+
 # every symbol include/sfdt.h declares (tests check the export list)
 EXPORTS = {
     "sfdt_strerror": (ctypes.c_char_p, [_int]),
@@ -60,6 +81,9 @@ EXPORTS = {
                                ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "sfdt_exact_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(ExactArgs)]),
     "sfdt_exact_solve": (_int, [ctypes.POINTER(ExactArgs), _vp, ctypes.c_size_t, _vp]),
+    "sfdt_general_caps": (_int, [ctypes.POINTER(GeneralArgs), ctypes.POINTER(_i64)]),
+    "sfdt_general_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(GeneralArgs)]),
+    "sfdt_general_solve": (_int, [ctypes.POINTER(GeneralArgs), _vp, ctypes.c_size_t, _vp]),
 }
 
 _lib = None

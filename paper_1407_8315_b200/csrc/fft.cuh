@@ -20,7 +20,7 @@
 
 namespace sfdt {
 
-constexpr int MAX_VIEWS = 16;
+constexpr int MAX_VIEWS = 24;
 
 struct ViewSrc {
     const void *x;
@@ -30,10 +30,17 @@ struct ViewSrc {
     int64_t jstride;     // elements between consecutive view samples (d)
     int64_t wrap;        // index mask (n - 1)
     int64_t off[MAX_VIEWS];
+    // views v >= dyn_first take their shift from a device table instead:
+    // off = dyn_off[b * dyn_stride + v - dyn_first] (per-signal random shifts)
+    const int64_t *dyn_off;
+    int dyn_first;
+    int64_t dyn_stride;
 };
 
 __device__ __forceinline__ cx view_load(const ViewSrc &src, int64_t b, int v, int64_t j) {
-    const int64_t e = b * src.sig_stride + ((j * src.jstride + src.off[v]) & src.wrap);
+    const int64_t o = (v >= src.dyn_first) ? __ldg(src.dyn_off + b * src.dyn_stride + (v - src.dyn_first))
+                                           : src.off[v];
+    const int64_t e = b * src.sig_stride + ((j * src.jstride + o) & src.wrap);
     if (src.is_c64) {
         const float2 f = __ldg(reinterpret_cast<const float2 *>(src.x) + e);
         return mk((double)f.x, (double)f.y);
@@ -263,6 +270,9 @@ static inline ViewSrc consecutive_views(const void *x, int is_c64, int64_t n, in
     s.jstride = d;
     s.wrap = n - 1;
     for (int v = 0; v < MAX_VIEWS; v++) s.off[v] = (v < nshift) ? shift0 + v : 0;
+    s.dyn_off = nullptr;
+    s.dyn_first = MAX_VIEWS;
+    s.dyn_stride = 0;
     return s;
 }
 

@@ -1,4 +1,640 @@
-// general.cu -- generally-K-sparse solver kernels (collision vote, pruning,
-// subspace pursuit).  Filled in by the general-path milestone.
+// general.cu -- sm_100a kernels of the generally-K-sparse path
+// (general.py:272-372, solve_general).
+//
+//   views        2*a_max consecutive + r_eff random-shift views gathered from
+//                x and FFT'd in shared memory (fft.cuh), bit-exact
+//   k_gen_svd    thread per bin: singular values of the a_max x a_max Hankel
+//                matrix (one-sided Jacobi, _core.pyx:353-433) + |syn|^2 partials
+//   k_gen_vote   CTA per signal: the pooled top-K vote of estimate_collisions
+//                (general.py:131-155): exact radix select of the K-th largest
+//                singular value, ties by (bin, rank) ascending, zero-vote guard,
+//                cap, histogram, worklist of voted bins
+//   k_gen_bins   thread per voted bin: descending-order Hankel fit, candidate
+//                evaluation |P(z_t)| over the d candidates (prune_eval), the
+//                correlation fallback, matched-filter union (general.py:313-351)
+//                and subspace pursuit with gelsd-semantics least squares
+//                (general.py:224-269, 357-366)
+//   count/scan/emit  compact (loc, value) lists in dict insertion order
+//                (vote class a ascending, bin ascending, column ascending)
 #include "common.cuh"
+#include "decode.cuh"
+#include "fft.cuh"
 #include "general.cuh"
+
+namespace sfdt {
+
+struct GenParams {
+    int64_t n, d, L, k;
+    int a_max, r_eff, keep, prune, S, nv;
+    double zvr;
+    const int64_t *shifts;
+    int64_t shift_stride;
+    const cx *base_phi;
+    int64_t phi_stride;
+};
+
+// ------------------------------------------------------------------- svd
+__global__ void __launch_bounds__(128) k_gen_svd(const cx *__restrict__ V, GenParams p,
+                                                 double *__restrict__ sv, double *__restrict__ partial) {
+    const int64_t b = blockIdx.y;
+    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    double e = 0.0;
+    if (k < p.L) {
+        cx syn[8];
+        for (int j = 0; j < p.S; j++) {
+            syn[j] = ldcx(V + (b * p.nv + j) * p.L + k);
+            e += syn[j].re * syn[j].re + syn[j].im * syn[j].im;
+        }
+        double s[4];
+        hankel_singular_values1(syn, p.a_max, s);
+        for (int i = 0; i < p.a_max; i++) sv[(b * p.L + k) * p.a_max + i] = s[i];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+    __shared__ double red[4];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = e;
+    __syncthreads();
+    if (threadIdx.x == 0) partial[b * gridDim.x + blockIdx.x] = (red[0] + red[1]) + (red[2] + red[3]);
+}
+
+// ------------------------------------------------------------------ vote
+__device__ __forceinline__ unsigned long long dkey(double v) {
+    return (unsigned long long)__double_as_longlong(v);   // sigma >= 0: bit order == value order
+}
+
+__global__ void __launch_bounds__(1024) k_gen_vote(const double *__restrict__ sv,
+                                                   const double *__restrict__ partial, int nparts,
+                                                   GenParams p, int32_t *__restrict__ votes,
+                                                   int64_t *__restrict__ stats,
+                                                   int64_t *__restrict__ wl,
+                                                   unsigned long long *__restrict__ wl_count) {
+    const int64_t b = blockIdx.x;
+    const int64_t M = p.L * p.a_max;
+    const int64_t take = p.k < M ? p.k : M;
+    const double *svb = sv + b * M;
+    int32_t *vb = votes + b * p.L;
+    __shared__ unsigned int hist[256];
+    __shared__ unsigned long long s_prefix, s_mask;
+    __shared__ long long s_remaining;
+    __shared__ int wsum[32];
+    __shared__ long long s_hist[5], s_nvoted;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        s_prefix = 0;
+        s_mask = 0;
+        s_remaining = take;
+    }
+    if (threadIdx.x < 5) s_hist[threadIdx.x] = 0;
+    if (threadIdx.x == 0) s_nvoted = 0;
+    for (int64_t i = threadIdx.x; i < p.L; i += blockDim.x) vb[i] = 0;
+    __syncthreads();
+    // exact radix select (8-bit digits, MSB first) of the take-th largest key
+    if (take > 0) {
+        for (int shift = 56; shift >= 0; shift -= 8) {
+            for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+            __syncthreads();
+            const unsigned long long pre = s_prefix, msk = s_mask;
+            for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
+                const unsigned long long key = dkey(svb[i]);
+                if ((key & msk) == pre) atomicAdd(&hist[(key >> shift) & 255], 1u);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                long long rem = s_remaining, cum = 0;
+                int D = 0;
+                for (int dg = 255; dg >= 0; dg--) {
+                    if (cum + hist[dg] >= rem) {
+                        D = dg;
+                        break;
+                    }
+                    cum += hist[dg];
+                }
+                s_remaining = rem - cum;
+                s_prefix = pre | ((unsigned long long)D << shift);
+                s_mask = msk | (0xFFull << shift);
+            }
+            __syncthreads();
+        }
+    }
+    const unsigned long long tau = s_prefix;
+    const long long need_eq = take > 0 ? s_remaining : 0;   // how many keys == tau to take
+    // selection in flat order: keys > tau all; keys == tau by ascending flat
+    // index (lexsort tie-break: bin asc, then rank asc)
+    long long eq_carry = 0;
+    for (int64_t i0 = 0; i0 < M && take > 0; i0 += blockDim.x) {
+        const int64_t i = i0 + threadIdx.x;
+        unsigned long long key = 0;
+        bool gt = false, eq = false;
+        if (i < M) {
+            key = dkey(svb[i]);
+            gt = key > tau;
+            eq = key == tau;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, eq);
+        if (lane == 0) wsum[warp] = __popc(m);
+        __syncthreads();
+        int before = 0, total = 0;
+        for (int w2 = 0; w2 < (int)(blockDim.x >> 5); w2++) {
+            before += (w2 < warp) ? wsum[w2] : 0;
+            total += wsum[w2];
+        }
+        const long long rank = eq_carry + before + __popc(m & ((1u << lane) - 1));
+        if (gt || (eq && rank < need_eq)) atomicAdd(&vb[i / p.a_max], 1);
+        eq_carry += total;
+        __syncthreads();
+    }
+    __syncthreads();
+    // zero-vote guard on the RMS of all consecutive syndromes, cap, histogram
+    double esum = 0.0;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < nparts; i++) esum += partial[b * nparts + i];
+    }
+    __shared__ double s_thr;
+    if (threadIdx.x == 0) {
+        const double rms_syn = sqrt(esum / (double)(p.L * p.S));
+        s_thr = p.zvr * rms_syn;
+    }
+    __syncthreads();
+    const int cap = (int)(p.a_max < p.d ? p.a_max : p.d);
+    long long hloc[5] = {0, 0, 0, 0, 0};
+    for (int64_t kb = threadIdx.x; kb < p.L; kb += blockDim.x) {
+        int v = vb[kb];
+        if (svb[kb * p.a_max] <= s_thr) v = 0;
+        if (v > cap) v = cap;
+        vb[kb] = v;
+        hloc[v]++;
+        if (v >= 1) {
+            const unsigned long long slot = atomicAdd(wl_count, 1ull);
+            wl[slot] = b * p.L + kb;
+        }
+    }
+    for (int a = 0; a <= 4; a++)
+        if (hloc[a]) atomicAdd((unsigned long long *)&s_hist[a], (unsigned long long)hloc[a]);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t *st = stats + b * SFDT_GS_PER_SIGNAL;
+        for (int a = 0; a <= 4; a++) st[SFDT_GS_HIST0 + a] = s_hist[a];
+        st[SFDT_GS_NVOTED] = s_hist[1] + s_hist[2] + s_hist[3] + s_hist[4];
+        st[SFDT_GS_RANKDEF] = 0;
+    }
+}
+
+// ------------------------------------------------------------- per bin
+// correlation |sum_j conj(phi_j) v_j| with the column given by its phases
+__device__ __forceinline__ double corr_abs(const cx *phi_col, const cx *v, int r) {
+    cx acc = mk(0.0, 0.0);
+    for (int j = 0; j < r; j++) acc = cadd(acc, nmul(cconj(phi_col[j]), v[j]));
+    return cabs_(acc);
+}
+
+struct SPOut {
+    int nsup;
+    int sup[GEN_MAX_SUP];
+    cx coef[GEN_MAX_SUP];
+    int rankdef;
+};
+
+// subspace pursuit over columns c < ncols (column index -> candidate t via
+// cols[] unless all_cols); phi[j, t] = phase_j * base_phi[j, t]
+__device__ void subspace_pursuit_dev(const cx *y, const cx *phase, const cx *bphi, int64_t d,
+                                     int r, const int *cols, int ncols, bool all_cols, int a_sp,
+                                     SPOut &o) {
+    const int a_eff = a_sp < ncols ? a_sp : ncols;
+    auto col_t = [&](int c) -> int64_t { return all_cols ? (int64_t)c : (int64_t)cols[c]; };
+    auto phi_col = [&](int c, cx *out) {
+        const int64_t t = col_t(c);
+        for (int j = 0; j < r; j++) out[j] = nmul(phase[j], ldcx(bphi + (int64_t)j * d + t));
+    };
+    cx pc[GEN_MAX_R];
+    // initial support: top a_eff of |phi^H y|, stable, then sorted
+    double tsc[GEN_MAX_SUP];
+    int tid_[GEN_MAX_SUP];
+    int nt = 0;
+    for (int c = 0; c < ncols; c++) {
+        phi_col(c, pc);
+        topk_insert(tsc, tid_, nt, a_eff, corr_abs(pc, y, r), c);
+    }
+    int sup[GEN_MAX_SUP];
+    int nsup = nt;
+    for (int i = 0; i < nt; i++) sup[i] = tid_[i];
+    sort_ints(sup, nsup);
+    cx A[GEN_MAX_R * GEN_MAX_SUP], coef[GEN_MAX_SUP], res[GEN_MAX_R];
+    o.rankdef = 0;
+    auto lsq = [&](const int *s, int ns, cx *x) {
+        for (int c = 0; c < ns; c++) phi_col(s[c], A + c * r);
+        const int rk = lstsq_min_norm(A, r, ns, y, x);
+        if (rk < ns) o.rankdef++;
+    };
+    auto residual = [&](const int *s, int ns, const cx *x) -> double {
+        for (int j = 0; j < r; j++) res[j] = y[j];
+        for (int c = 0; c < ns; c++) {
+            phi_col(s[c], pc);
+            for (int j = 0; j < r; j++) res[j] = csub(res[j], nmul(pc[j], x[c]));
+        }
+        double ss = 0.0;
+        for (int j = 0; j < r; j++) ss = fma(res[j].re, res[j].re, fma(res[j].im, res[j].im, ss));
+        return sqrt(ss);
+    };
+    lsq(sup, nsup, coef);
+    double best = residual(sup, nsup, coef);
+    int best_sup[GEN_MAX_SUP], best_n = nsup;
+    cx best_coef[GEN_MAX_SUP];
+    for (int i = 0; i < nsup; i++) {
+        best_sup[i] = sup[i];
+        best_coef[i] = coef[i];
+    }
+    for (int it = 0; it < 10; it++) {
+        // merged = union(support, top a_eff of |phi^H residual|)
+        nt = 0;
+        for (int c = 0; c < ncols; c++) {
+            phi_col(c, pc);
+            topk_insert(tsc, tid_, nt, a_eff, corr_abs(pc, res, r), c);
+        }
+        int topc[GEN_MAX_SUP];
+        for (int i = 0; i < nt; i++) topc[i] = tid_[i];
+        sort_ints(topc, nt);
+        int merged[2 * GEN_MAX_SUP];
+        const int nm = union_sorted(sup, nsup, topc, nt, merged);
+        cx mcoef[2 * GEN_MAX_SUP];
+        lsq(merged, nm, mcoef);
+        // support = sorted(merged[top a_eff of |mcoef|, stable])
+        int n2 = 0;
+        for (int c = 0; c < nm; c++) topk_insert(tsc, tid_, n2, a_eff, cabs_(mcoef[c]), c);
+        nsup = n2;
+        for (int i = 0; i < n2; i++) sup[i] = merged[tid_[i]];
+        sort_ints(sup, nsup);
+        lsq(sup, nsup, coef);
+        const double nrm = residual(sup, nsup, coef);
+        if (nrm >= best * (1.0 - 1e-12)) break;
+        best = nrm;
+        best_n = nsup;
+        for (int i = 0; i < nsup; i++) {
+            best_sup[i] = sup[i];
+            best_coef[i] = coef[i];
+        }
+    }
+    o.nsup = best_n;
+    for (int i = 0; i < best_n; i++) {
+        o.sup[i] = (int)col_t(best_sup[i]);
+        o.coef[i] = best_coef[i];
+    }
+}
+
+__global__ void __launch_bounds__(128) k_gen_bins(const cx *__restrict__ V, GenParams p,
+                                                  const int32_t *__restrict__ votes,
+                                                  const int64_t *__restrict__ wl,
+                                                  const unsigned long long *__restrict__ wl_count,
+                                                  uint8_t *__restrict__ nent, int64_t *__restrict__ sloc,
+                                                  cx *__restrict__ sval, int64_t *__restrict__ stats) {
+    const int64_t cnt = (int64_t)*wl_count;
+    for (int64_t it = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; it < cnt;
+         it += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t t = wl[it];
+        const int64_t b = t / p.L, kb = t - b * p.L;
+        const int a = votes[t];
+        const int r = p.r_eff;
+        const int64_t *sh = p.shifts + b * p.shift_stride;
+        const cx *bphi = p.base_phi + b * p.phi_stride;
+        cx syn[8], y[GEN_MAX_R];
+        for (int j = 0; j < p.S; j++) syn[j] = ldcx(V + (b * p.nv + j) * p.L + kb);
+        for (int j = 0; j < r; j++) y[j] = ldcx(V + (b * p.nv + p.S + j) * p.L + kb);
+        const int64_t count = (int64_t)p.keep * a < p.d ? (int64_t)p.keep * a : p.d;
+        int cols[GEN_MAX_COLS];
+        int ncols = 0;
+        bool all_cols = true;
+        if (p.prune && count < p.d) {
+            all_cols = false;
+            // descending-order Hankel fit (general.py:324-337)
+            cx c[4];
+            int order = 0;
+            for (int o2 = p.a_max; o2 >= 1; o2--) {
+                double scale = 0.0;
+                for (int l = 0; l < 2 * o2; l++) scale = nanmax2(scale, cabs_(syn[l]));
+                scale = nanmax2(scale, TINY);
+                const cx cd = hankel_solve1(syn, o2, c);
+                if (cabs_(cd) > DMUL(SINGULARITY_RTOL, powa(scale, o2))) {
+                    order = o2;
+                    break;
+                }
+            }
+            double ks[GEN_MAX_COLS];
+            int kp[GEN_MAX_COLS], nk = 0;
+            const int cnti = (int)count;
+            if (order > 0) {
+                // prune_eval (_core.pyx:319-346) with the same recurrence
+                const cx base = gexp(mk(0.0, DMUL(TWO_PI, (double)kb) / (double)p.n));
+                const cx wd = gexp(mk(0.0, TWO_PI / (double)p.d));
+                cx zt = base;
+                for (int64_t tt = 0; tt < p.d; tt++) {
+                    cx acc = mk(1.0, 0.0);
+                    for (int j = order - 1; j >= 0; j--) acc = cadd(gmul(acc, zt), c[j]);
+                    botk_insert(ks, kp, nk, cnti, cabs_(acc), (int)tt);
+                    if ((tt & 511) == 511)
+                        zt = gmul(base, gexp(mk(0.0, DMUL(TWO_PI, (double)(tt + 1)) / (double)p.d)));
+                    else
+                        zt = gmul(zt, wd);
+                }
+            } else {
+                // _correlation_keep (general.py:158-165)
+                const int64_t m = p.L;
+                for (int64_t tt = 0; tt < p.d; tt++) {
+                    const int64_t loc = (kb + tt * m) & (p.n - 1);
+                    cx acc = mk(0.0, 0.0);
+                    for (int j = 0; j < r; j++) {
+                        const double th = DMUL(TWO_PI, (double)(sh[j] * loc)) / (double)p.n;
+                        acc = cadd(acc, nmul(cconj(gexp(mk(0.0, th))), y[j]));
+                    }
+                    topk_insert(ks, kp, nk, cnti, cabs_(acc), (int)tt);
+                }
+            }
+            sort_ints(kp, nk);
+            // matched-filter augmentation (general.py:345-351)
+            cx w[GEN_MAX_R];
+            for (int j = 0; j < r; j++) {
+                const double th = DMUL(-TWO_PI, (double)(sh[j] * kb)) / (double)p.n;
+                w[j] = nmul(gexp(mk(0.0, th)), y[j]);
+            }
+            const int n_top = (int)((int64_t)a < p.d ? a : p.d);
+            double ts[GEN_MAX_SUP];
+            int tp[GEN_MAX_SUP], nt = 0;
+            for (int64_t tt = 0; tt < p.d; tt++) {
+                cx acc = mk(0.0, 0.0);
+                for (int j = 0; j < r; j++) acc = cadd(acc, nmul(cconj(ldcx(bphi + (int64_t)j * p.d + tt)), w[j]));
+                topk_insert(ts, tp, nt, n_top, cabs_(acc), (int)tt);
+            }
+            sort_ints(tp, nt);
+            ncols = union_sorted(kp, nk, tp, nt, cols);
+        } else {
+            ncols = (int)p.d;
+        }
+        // subspace pursuit on this bin's columns (general.py:357-366)
+        cx phase[GEN_MAX_R];
+        const double tk = DMUL(TWO_PI, (double)kb);
+        for (int j = 0; j < r; j++) phase[j] = gexp(mk(0.0, DMUL(tk, (double)sh[j]) / (double)p.n));
+        const int a_sp = a < r ? a : r;
+        SPOut o;
+        subspace_pursuit_dev(y, phase, bphi, p.d, r, cols, ncols, all_cols, a_sp, o);
+        int ne = 0;
+        for (int i = 0; i < o.nsup; i++) {
+            if (o.coef[i].re == 0.0 && o.coef[i].im == 0.0) continue;   // np.nonzero(coef)
+            sloc[t * p.a_max + ne] = (kb + (int64_t)o.sup[i] * p.L) & (p.n - 1);
+            stcx(sval + t * p.a_max + ne, o.coef[i]);
+            ne++;
+        }
+        nent[t] = (uint8_t)ne;
+        if (o.rankdef)
+            atomicAdd((unsigned long long *)(stats + b * SFDT_GS_PER_SIGNAL + SFDT_GS_RANKDEF),
+                      (unsigned long long)o.rankdef);
+    }
+}
+
+// -------------------------------------------------------------- compaction
+__global__ void __launch_bounds__(256) k_gen_count(const int32_t *__restrict__ votes,
+                                                   const uint8_t *__restrict__ nent, int64_t L,
+                                                   int64_t *__restrict__ stats) {
+    const int64_t b = blockIdx.x;
+    long long c[4] = {0, 0, 0, 0};
+    for (int64_t kb = threadIdx.x; kb < L; kb += blockDim.x) {
+        const int v = votes[b * L + kb];
+        if (v >= 1) c[v - 1] += nent[b * L + kb];
+    }
+    __shared__ long long red[4][256];
+    for (int q = 0; q < 4; q++) red[q][threadIdx.x] = c[q];
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (threadIdx.x < s)
+            for (int q = 0; q < 4; q++) red[q][threadIdx.x] += red[q][threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        int64_t *st = stats + b * SFDT_GS_PER_SIGNAL;
+        long long tot = 0;
+        for (int q = 0; q < 4; q++) {
+            st[SFDT_GS_CLASS0 + q] = red[q][0];
+            tot += red[q][0];
+        }
+        st[SFDT_GS_NENTRIES] = tot;
+    }
+}
+
+__global__ void k_gen_scan(const int64_t *__restrict__ stats, int64_t B, int64_t *__restrict__ offsets) {
+    __shared__ long long buf[1024];
+    __shared__ long long carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < B; base += 1024) {
+        const int64_t i = base + threadIdx.x;
+        const long long v = (i < B) ? stats[i * SFDT_GS_PER_SIGNAL + SFDT_GS_NENTRIES] : 0;
+        buf[threadIdx.x] = v;
+        __syncthreads();
+        for (int s = 1; s < 1024; s <<= 1) {
+            const long long add = (threadIdx.x >= s) ? buf[threadIdx.x - s] : 0;
+            __syncthreads();
+            buf[threadIdx.x] += add;
+            __syncthreads();
+        }
+        if (i < B) offsets[i] = carry + buf[threadIdx.x] - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry += buf[1023];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) offsets[B] = carry;
+}
+
+// entries in (vote class asc, bin asc, column asc) order; per tile one block
+// scan of 4 x 13-bit packed per-class entry counts
+__global__ void __launch_bounds__(256) k_gen_emit(const int32_t *__restrict__ votes,
+                                                  const uint8_t *__restrict__ nent,
+                                                  const int64_t *__restrict__ sloc,
+                                                  const cx *__restrict__ sval, int64_t L, int a_max,
+                                                  const int64_t *__restrict__ stats,
+                                                  const int64_t *__restrict__ eoff,
+                                                  int64_t *__restrict__ locs, cx *__restrict__ vals) {
+    __shared__ unsigned long long wtot[8];
+    const int64_t b = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t *st = stats + b * SFDT_GS_PER_SIGNAL;
+    long long base[4];
+    base[0] = eoff[b];
+    for (int c = 1; c < 4; c++) base[c] = base[c - 1] + st[SFDT_GS_CLASS0 + c - 1];
+    long long carry[4] = {0, 0, 0, 0};
+    for (int64_t t0 = 0; t0 < L; t0 += 1024) {
+        int ci[4], ne[4];
+        unsigned long long packed = 0;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int64_t kb = t0 + 4 * threadIdx.x + u;
+            ci[u] = -1;
+            ne[u] = 0;
+            if (kb < L) {
+                const int v = votes[b * L + kb];
+                if (v >= 1) {
+                    ci[u] = v - 1;
+                    ne[u] = nent[b * L + kb];
+                    packed += (unsigned long long)ne[u] << (13 * ci[u]);
+                }
+            }
+        }
+        unsigned long long inc = packed;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) wtot[warp] = inc;
+        __syncthreads();
+        unsigned long long before = 0, total = 0;
+        for (int w2 = 0; w2 < 8; w2++) {
+            before += (w2 < warp) ? wtot[w2] : 0;
+            total += wtot[w2];
+        }
+        __syncthreads();
+        const unsigned long long pre = before + inc - packed;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int c = ci[u];
+            if (c < 0) continue;
+            long long pos = base[c] + carry[c] + (long long)((pre >> (13 * c)) & 0x1FFF);
+            for (int u2 = 0; u2 < u; u2++)
+                if (ci[u2] == c) pos += ne[u2];
+            const int64_t t = b * L + t0 + 4 * threadIdx.x + u;
+            for (int j = 0; j < ne[u]; j++) {
+                locs[pos + j] = sloc[t * a_max + j];
+                stcx(vals + pos + j, sval[t * a_max + j]);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 4; c++) carry[c] += (long long)((total >> (13 * c)) & 0x1FFF);
+    }
+}
+
+// --------------------------------------------------------------- host side
+struct GenPlan {
+    int64_t B, n, d, L, nv, nparts;
+    int S;
+    size_t off_V, off_sv, off_part, off_votes, off_nent, off_sloc, off_sval, off_wl, off_cnt,
+        off_fft, total;
+};
+
+static int make_gen_plan(const sfdt_general_args *a, GenPlan &p) {
+    if (!a || a->batch < 1 || a->n < 2 || (a->n & (a->n - 1))) return SFDT_EINVAL;
+    if (a->a_max < 1 || a->a_max > 4 || a->d < 1 || a->d > a->n || (a->d & (a->d - 1))) return SFDT_EINVAL;
+    if (a->r_eff < 1 || a->r_eff > GEN_MAX_R || a->r_eff > a->d || a->k < 1) return SFDT_EINVAL;
+    if (a->keep_per_collision < 1 || a->keep_per_collision * a->a_max + a->a_max > GEN_MAX_COLS)
+        return SFDT_EINVAL;
+    if (2 * a->a_max + a->r_eff > MAX_VIEWS) return SFDT_EINVAL;
+    if (a->x_dtype != SFDT_C128 && a->x_dtype != SFDT_C64) return SFDT_EINVAL;
+    p.B = a->batch;
+    p.n = a->n;
+    p.d = a->d;
+    p.L = a->n / a->d;
+    p.S = 2 * a->a_max;
+    p.nv = p.S + a->r_eff;
+    p.nparts = (p.L + 127) / 128;
+    size_t o = 0;
+    auto take = [&](size_t bytes) { size_t r = o; o = (o + bytes + 255) & ~size_t(255); return r; };
+    p.off_V = take(size_t(p.B) * p.nv * p.L * 16);
+    p.off_sv = take(size_t(p.B) * p.L * a->a_max * 8);
+    p.off_part = take(size_t(p.B) * p.nparts * 8);
+    p.off_votes = take(size_t(p.B) * p.L * 4);
+    p.off_nent = take(size_t(p.B) * p.L);
+    p.off_sloc = take(size_t(p.B) * p.L * a->a_max * 8);
+    p.off_sval = take(size_t(p.B) * p.L * a->a_max * 16);
+    p.off_wl = take(size_t(p.B) * p.L * 8);
+    p.off_cnt = take(64);
+    p.off_fft = (p.L > FFT_SMEM_MAX) ? take(size_t(p.B) * p.nv * p.L * 16) : 0;
+    p.total = o;
+    return SFDT_OK;
+}
+
+}  // namespace sfdt
+
+using namespace sfdt;
+
+extern "C" int sfdt_general_caps(const sfdt_general_args *a, int64_t *entry_cap) {
+    GenPlan p;
+    int rc = make_gen_plan(a, p);
+    if (rc) return rc;
+    if (entry_cap) *entry_cap = p.B * p.L * a->a_max;
+    return SFDT_OK;
+}
+
+extern "C" size_t sfdt_general_workspace_bytes(const sfdt_general_args *a) {
+    GenPlan p;
+    if (make_gen_plan(a, p)) return 0;
+    return p.total;
+}
+
+extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_bytes, sfdt_stream_t stream_) {
+    GenPlan p;
+    int rc = make_gen_plan(a, p);
+    if (rc) return rc;
+    if (!ws || ws_bytes < p.total) return SFDT_EWORKSPACE;
+    int64_t ecap;
+    sfdt_general_caps(a, &ecap);
+    if (a->entry_cap < ecap) return SFDT_ECAPACITY;
+    if (!a->shifts || !a->base_phi || !a->twiddles) return SFDT_EINVAL;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    char *w = (char *)ws;
+    cx *V = (cx *)(w + p.off_V);
+    double *sv = a->singular_values ? a->singular_values : (double *)(w + p.off_sv);
+    double *part = (double *)(w + p.off_part);
+    int32_t *votes = a->votes ? a->votes : (int32_t *)(w + p.off_votes);
+    uint8_t *nent = (uint8_t *)(w + p.off_nent);
+    int64_t *sloc = (int64_t *)(w + p.off_sloc);
+    cx *sval = (cx *)(w + p.off_sval);
+    int64_t *wl = (int64_t *)(w + p.off_wl);
+    unsigned long long *wlc = (unsigned long long *)(w + p.off_cnt);
+    cx *fft_scratch = p.off_fft ? (cx *)(w + p.off_fft) : nullptr;
+    const int is_c64 = a->x_dtype == SFDT_C64;
+    int launches = 0;
+
+    // 1. consecutive + random-shift views (general.py:288-294)
+    ViewSrc src = consecutive_views(a->x, is_c64, p.n, p.d, 0, p.S);
+    src.nshift = (int)p.nv;
+    src.dyn_off = a->shifts;
+    src.dyn_first = p.S;
+    src.dyn_stride = a->shift_stride;
+    rc = launch_fft_views(src, p.B, p.L, a->twiddles, V, (int)p.nv, p.L, stream, fft_scratch);
+    if (rc) return rc;
+    launches += (p.L > FFT_SMEM_MAX) ? 2 : 1;
+
+    GenParams gp;
+    gp.n = p.n;
+    gp.d = p.d;
+    gp.L = p.L;
+    gp.k = a->k;
+    gp.a_max = a->a_max;
+    gp.r_eff = a->r_eff;
+    gp.keep = a->keep_per_collision;
+    gp.prune = a->prune;
+    gp.S = p.S;
+    gp.nv = (int)p.nv;
+    gp.zvr = a->zero_vote_rtol;
+    gp.shifts = a->shifts;
+    gp.shift_stride = a->shift_stride;
+    gp.base_phi = (const cx *)a->base_phi;
+    gp.phi_stride = a->phi_stride;
+
+    // 2. collision vote (general.py:131-155)
+    k_gen_svd<<<dim3((unsigned)p.nparts, (unsigned)p.B), 128, 0, stream>>>(V, gp, sv, part);
+    SFDT_CHECK_LAUNCH();
+    cudaMemsetAsync(wlc, 0, 8, stream);
+    k_gen_vote<<<(unsigned)p.B, 1024, 0, stream>>>(sv, part, (int)p.nparts, gp, votes, a->stats, wl, wlc);
+    SFDT_CHECK_LAUNCH();
+    // 3-4. pruning + subspace pursuit per voted bin
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaMemsetAsync(nent, 0, size_t(p.B) * p.L, stream);
+    k_gen_bins<<<(unsigned)(sms * 16), 128, 0, stream>>>(V, gp, votes, wl, wlc, nent, sloc, sval, a->stats);
+    SFDT_CHECK_LAUNCH();
+    k_gen_count<<<(unsigned)p.B, 256, 0, stream>>>(votes, nent, p.L, a->stats);
+    k_gen_scan<<<1, 1024, 0, stream>>>(a->stats, p.B, a->entry_offsets);
+    k_gen_emit<<<(unsigned)p.B, 256, 0, stream>>>(votes, nent, sloc, sval, p.L, a->a_max, a->stats,
+                                                  a->entry_offsets, a->locs, (cx *)a->vals);
+    SFDT_CHECK_LAUNCH();
+    launches += 6;
+    a->kernel_launches = launches;
+    return SFDT_OK;
+}

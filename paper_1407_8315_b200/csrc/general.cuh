@@ -79,3 +79,126 @@ __host__ __device__ __forceinline__ void prune_eval_chunk(const cx *c, int a, cx
 }
 
 }  // namespace sfdt
+
+namespace sfdt {
+
+constexpr int GEN_MAX_R = 12;      // r_eff = min(3*a_max, d) <= 12
+constexpr int GEN_MAX_COLS = 16;   // kept columns per bin: <= keep*a + a
+constexpr int GEN_MAX_SUP = 8;     // SP support / merged support (<= 2*a_eff)
+
+// Minimum-norm least squares of the r x c system A x = y (c <= GEN_MAX_SUP),
+// the way LAPACK gelsd defines it (numpy.linalg.lstsq, rcond=None):
+// singular values <= eps*max(r,c)*s_max are dropped.  One-sided Jacobi on
+// the columns: A V = U S; x = sum_i v_i (u_i^H y) / s_i.  Returns the rank.
+__device__ __forceinline__ int lstsq_min_norm(const cx *A, int r, int c, const cx *y, cx *x) {
+    cx W[GEN_MAX_R * GEN_MAX_SUP];   // A V (column-major: W[col*r + row])
+    cx Vm[GEN_MAX_SUP * GEN_MAX_SUP];
+    for (int j = 0; j < c; j++) {
+        for (int i = 0; i < r; i++) W[j * r + i] = A[j * r + i];
+        for (int i = 0; i < c; i++) Vm[j * c + i] = mk(i == j ? 1.0 : 0.0, 0.0);
+    }
+    for (int sweep = 0; sweep < 40; sweep++) {
+        bool rotated = false;
+        for (int p = 0; p < c - 1; p++) {
+            for (int q = p + 1; q < c; q++) {
+                double app = 0.0, aqq = 0.0;
+                cx apq = mk(0.0, 0.0);
+                for (int i = 0; i < r; i++) {
+                    const cx wp = W[p * r + i], wq = W[q * r + i];
+                    app = fma(wp.re, wp.re, fma(wp.im, wp.im, app));
+                    aqq = fma(wq.re, wq.re, fma(wq.im, wq.im, aqq));
+                    apq = cadd(apq, nmul(cconj(wp), wq));
+                }
+                const double g = cabs_(apq);
+                if (g == 0.0 || g <= 1e-16 * sqrt(app * aqq)) continue;
+                rotated = true;
+                const double theta = (aqq - app) / (2.0 * g);
+                const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
+                const double cs = 1.0 / sqrt(1.0 + t * t), sn = t * cs;
+                const cx ph = cdivr(apq, g);
+                for (int i = 0; i < r; i++) {
+                    const cx wp = W[p * r + i], wq = W[q * r + i];
+                    W[p * r + i] = csub(cscale(cs, wp), nmul(cscale(sn, cconj(ph)), wq));
+                    W[q * r + i] = cadd(nmul(cscale(sn, ph), wp), cscale(cs, wq));
+                }
+                for (int i = 0; i < c; i++) {
+                    const cx vp = Vm[p * c + i], vq = Vm[q * c + i];
+                    Vm[p * c + i] = csub(cscale(cs, vp), nmul(cscale(sn, cconj(ph)), vq));
+                    Vm[q * c + i] = cadd(nmul(cscale(sn, ph), vp), cscale(cs, vq));
+                }
+            }
+        }
+        if (!rotated) break;
+    }
+    double s[GEN_MAX_SUP], smax = 0.0;
+    for (int j = 0; j < c; j++) {
+        double acc = 0.0;
+        for (int i = 0; i < r; i++) acc = fma(W[j * r + i].re, W[j * r + i].re, fma(W[j * r + i].im, W[j * r + i].im, acc));
+        s[j] = sqrt(acc);
+        smax = s[j] > smax ? s[j] : smax;
+    }
+    const double tol = 2.220446049250313e-16 * (double)(r > c ? r : c) * smax;
+    for (int j = 0; j < c; j++) x[j] = mk(0.0, 0.0);
+    int rank = 0;
+    for (int k = 0; k < c; k++) {
+        if (!(s[k] > tol)) continue;
+        rank++;
+        cx uy = mk(0.0, 0.0);   // (A v_k)^H y / s_k^2
+        for (int i = 0; i < r; i++) uy = cadd(uy, nmul(cconj(W[k * r + i]), y[i]));
+        const double inv = 1.0 / (s[k] * s[k]);
+        uy = mk(uy.re * inv, uy.im * inv);
+        for (int j = 0; j < c; j++) x[j] = cadd(x[j], nmul(Vm[k * c + j], uy));
+    }
+    return rank;
+}
+
+// top-`cnt` selection by score with the reference's tie rule (np.argsort
+// kind="stable" on -score: larger first, then lower index first)
+__device__ __forceinline__ void topk_insert(double *sc, int *id, int &len, int cnt, double v, int t) {
+    if (len == cnt && !(v > sc[cnt - 1])) return;
+    int pos = (len < cnt) ? len++ : cnt - 1;
+    while (pos > 0 && v > sc[pos - 1]) {
+        sc[pos] = sc[pos - 1];
+        id[pos] = id[pos - 1];
+        pos--;
+    }
+    sc[pos] = v;
+    id[pos] = t;
+}
+
+// smallest-`cnt` selection (argpartition of errs): smaller first, ties keep
+// the lower index
+__device__ __forceinline__ void botk_insert(double *sc, int *id, int &len, int cnt, double v, int t) {
+    if (len == cnt && !(v < sc[cnt - 1])) return;
+    int pos = (len < cnt) ? len++ : cnt - 1;
+    while (pos > 0 && v < sc[pos - 1]) {
+        sc[pos] = sc[pos - 1];
+        id[pos] = id[pos - 1];
+        pos--;
+    }
+    sc[pos] = v;
+    id[pos] = t;
+}
+
+__device__ __forceinline__ void sort_ints(int *v, int n) {
+    for (int i = 1; i < n; i++) {
+        int key = v[i], j = i - 1;
+        while (j >= 0 && v[j] > key) { v[j + 1] = v[j]; j--; }
+        v[j + 1] = key;
+    }
+}
+
+// sorted union of two sorted int lists (np.union1d)
+__device__ __forceinline__ int union_sorted(const int *a, int na, const int *b, int nb, int *out) {
+    int i = 0, j = 0, n = 0;
+    while (i < na || j < nb) {
+        int v;
+        if (j >= nb || (i < na && a[i] < b[j])) v = a[i++];
+        else if (i >= na || b[j] < a[i]) v = b[j++];
+        else { v = a[i]; i++; j++; }
+        if (n == 0 || out[n - 1] != v) out[n++] = v;
+    }
+    return n;
+}
+
+}  // namespace sfdt

@@ -1,0 +1,224 @@
+"""Generally-K-sparse recovery on the B200 (drop-in for sfft_dt.general).
+
+Same public names, parameters and results as the reference
+(/root/reference/pkg/src/sfft_dt/general.py):
+
+    GeneralConfig, GeneralTrace, CollisionEstimate, draw_shifts,
+    solve_general(x, cfg) -> (SparseSpectrum, GeneralTrace)      general.py:272
+
+plus solve_general_batch(X, cfg, seeds=None) for B signals in HBM.  The
+shift draw stays on the host with numpy's Generator (bit-identical shifts);
+everything else -- views, singular values, the top-K vote, pruning,
+matched filter and subspace pursuit -- runs in libsfdt_b200.so.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .device import Workspace, as_device_signals, ptr, require_cuda, stream_handle, twiddles
+from .spectral import SparseSpectrum, check_signal_shape
+
+
+@dataclass
+class GeneralConfig:
+    """Generally-sparse solver parameters (general.py:28-70)."""
+
+    n: int
+    k: int
+    a_max: int = 3
+    d: int | None = None
+    rng_seed: int | tuple = 0
+    keep_per_collision: int = 2
+    prune: bool = True
+    zero_vote_rtol: float = 1e-9
+
+    def __post_init__(self):
+        if self.n < 2 or self.n & (self.n - 1):
+            raise ValueError(f"n must be a power of two >= 2, got {self.n}")
+        if not 1 <= self.k <= self.n:
+            raise ValueError(f"k must be in [1, n], got {self.k}")
+        if not 1 <= self.a_max <= 4:
+            raise ValueError(f"a_max must be 1..4, got {self.a_max}")
+        if 2 * self.a_max > self.n:
+            raise ValueError("n too small for 2*a_max consecutive shifts")
+        if self.keep_per_collision < 1:
+            raise ValueError("keep_per_collision must be >= 1")
+        if self.d is not None and (self.d < 1 or self.n % self.d):
+            raise ValueError(f"d={self.d} must divide n={self.n}")
+
+    def resolved_d(self) -> int:
+        if self.d is not None:
+            return self.d
+        raw = self.n // (32 * self.k)
+        return 1 if raw < 1 else 1 << (raw.bit_length() - 1)
+
+    @property
+    def r(self) -> int:
+        return 3 * self.a_max
+
+
+@dataclass(frozen=True)
+class CollisionEstimate:
+    a: np.ndarray
+    singular_values: np.ndarray
+
+
+@dataclass
+class GeneralTrace:
+    d: int = 0
+    r: int = 0
+    shifts: list = field(default_factory=list)
+    fft_samples: int = 0
+    collision_histogram: dict = field(default_factory=dict)
+    timings: dict = field(default_factory=dict)
+    pruned: bool = True
+    warnings: list = field(default_factory=list)
+
+
+def draw_shifts(d: int, r: int, seed) -> np.ndarray:
+    """r distinct shifts drawn uniformly from [0, d-1] (general.py:101-106)."""
+    if r > d:
+        raise ValueError(f"cannot draw {r} distinct shifts from [0, {d})")
+    return np.random.default_rng(seed).choice(d, size=r, replace=False).astype(np.int64)
+
+
+def base_phi_table(shifts: np.ndarray, d: int) -> np.ndarray:
+    """exp(2 pi i shifts_j t / d), evaluated exactly as general.py:309 does."""
+    return np.exp(2j * np.pi * np.outer(shifts, np.arange(d)) / d)
+
+
+class GeneralBatch:
+    def __init__(self, n, cfg, d, r_eff, shifts, tensors, elapsed_s, kernel_launches):
+        self.n, self.cfg, self.d, self.r_eff = n, cfg, d, r_eff
+        self.shifts = shifts          # (B, r_eff) host int64
+        self.t = tensors
+        self.elapsed_s = elapsed_s
+        self.kernel_launches = kernel_launches
+        self._host = None
+
+    @property
+    def batch(self) -> int:
+        return self.t["stats"].shape[0]
+
+    def to_host(self) -> dict:
+        if self._host is None:
+            t = self.t
+            off = t["entry_offsets"].cpu().numpy()
+            total = int(off[-1])
+            self._host = {
+                "entry_offsets": off, "locs": t["locs"][:total].cpu().numpy(),
+                "vals": torch.view_as_complex(t["vals"][:total]).cpu().numpy(),
+                "stats": t["stats"].cpu().numpy(),
+            }
+        return self._host
+
+    def spectrum(self, b: int) -> SparseSpectrum:
+        h = self.to_host()
+        lo, hi = h["entry_offsets"][b], h["entry_offsets"][b + 1]
+        return SparseSpectrum(self.n, dict(zip(h["locs"][lo:hi].tolist(), h["vals"][lo:hi].tolist())))
+
+    def spectra(self) -> list:
+        return [self.spectrum(b) for b in range(self.batch)]
+
+    def trace(self, b: int) -> GeneralTrace:
+        h = self.to_host()
+        st = h["stats"][b]
+        a_max = self.cfg.a_max
+        hist = {a: int(st[_lib.SFDT_GS_HIST0 + a]) for a in range(a_max + 1)}
+        return GeneralTrace(d=self.d, r=self.r_eff, shifts=self.shifts[b].tolist(),
+                            fft_samples=(2 * a_max + self.r_eff) * (self.n // self.d),
+                            collision_histogram=hist, timings={"total": self.elapsed_s},
+                            pruned=self.cfg.prune, warnings=[])
+
+    def votes(self) -> np.ndarray:
+        return self.t["votes"].cpu().numpy()
+
+    def singular_values(self) -> np.ndarray:
+        return self.t["singular_values"].cpu().numpy()
+
+
+def solve_general_batch(X, cfg: GeneralConfig, seeds=None, device=None) -> GeneralBatch:
+    """Batched solve_general.  seeds: None (cfg.rng_seed for every signal) or
+    one rng_seed per signal (per-signal shift draws)."""
+    t0 = time.perf_counter()
+    dev = require_cuda(device if device is not None else
+                       (X.device if isinstance(X, torch.Tensor) and X.is_cuda else None))
+    X = as_device_signals(X, dev)
+    if X.dim() == 1:
+        X = X.unsqueeze(0)
+    if X.dim() != 2:
+        raise ValueError(f"signal must be 1-D, got shape {tuple(X.shape)}")
+    B = X.shape[0]
+    n = check_signal_shape(X.shape[1:])
+    if n != cfg.n:
+        raise ValueError(f"signal length {n} != configured n {cfg.n}")
+    d = cfg.resolved_d()
+    r_eff = min(cfg.r, d)
+    if seeds is None:
+        sh = draw_shifts(d, r_eff, cfg.rng_seed)[None, :]
+        phi = base_phi_table(sh[0], d)[None]
+        stride_s, stride_p = 0, 0
+    else:
+        if len(seeds) != B:
+            raise ValueError("need one seed per signal")
+        sh = np.stack([draw_shifts(d, r_eff, s) for s in seeds])
+        phi = np.stack([base_phi_table(s, d) for s in sh])
+        stride_s, stride_p = r_eff, r_eff * d
+    sh_d = torch.from_numpy(np.ascontiguousarray(sh)).to(dev)
+    phi_d = torch.from_numpy(np.ascontiguousarray(phi)).to(dev)
+    lib = _lib.load()
+    a = _lib.GeneralArgs()
+    a.x = X.data_ptr()
+    a.x_dtype = _lib.SFDT_C64 if X.dtype == torch.complex64 else _lib.SFDT_C128
+    a.batch, a.n, a.k, a.d = B, n, cfg.k, d
+    a.a_max, a.r_eff = cfg.a_max, r_eff
+    a.keep_per_collision, a.prune = cfg.keep_per_collision, int(bool(cfg.prune))
+    a.zero_vote_rtol = float(cfg.zero_vote_rtol)
+    a.shifts, a.shift_stride = sh_d.data_ptr(), stride_s
+    a.base_phi, a.phi_stride = phi_d.data_ptr(), stride_p
+    tw = twiddles(n // d, dev)
+    a.twiddles = tw.data_ptr()
+    cap = _lib._i64()
+    _lib.check(lib.sfdt_general_caps(a, ctypes.byref(cap)), "sfdt_general_caps")
+    L = n // d
+    o = {
+        "entry_offsets": torch.empty(B + 1, dtype=torch.int64, device=dev),
+        "locs": torch.empty(cap.value, dtype=torch.int64, device=dev),
+        "vals": torch.empty((cap.value, 2), dtype=torch.float64, device=dev),
+        "stats": torch.zeros((B, _lib.SFDT_GS_PER_SIGNAL), dtype=torch.int64, device=dev),
+        "votes": torch.empty((B, L), dtype=torch.int32, device=dev),
+        "singular_values": torch.empty((B, L, cfg.a_max), dtype=torch.float64, device=dev),
+    }
+    a.entry_offsets, a.locs, a.vals, a.entry_cap = ptr(o["entry_offsets"]), ptr(o["locs"]), \
+        ptr(o["vals"]), cap.value
+    a.stats, a.votes, a.singular_values = ptr(o["stats"]), ptr(o["votes"]), ptr(o["singular_values"])
+    nbytes = lib.sfdt_general_workspace_bytes(a)
+    ws = Workspace.get(nbytes, dev)
+    _lib.check(lib.sfdt_general_solve(a, ws.data_ptr(), ws.numel(), stream_handle(dev)),
+               "sfdt_general_solve")
+    o["_keep"] = (sh_d, phi_d, tw)
+    shifts = np.broadcast_to(sh, (B, r_eff)) if seeds is None else sh
+    return GeneralBatch(n, cfg, d, r_eff, shifts, o, time.perf_counter() - t0, int(a.kernel_launches))
+
+
+def solve_general(x, cfg: GeneralConfig):
+    """Full pipeline (general.py:272-372): shifted-view FFTs, collision vote,
+    pruning, per-bin subspace pursuit; returns (spectrum, trace)."""
+    t0 = time.perf_counter()
+    if isinstance(x, torch.Tensor):
+        check_signal_shape(x.shape)
+    else:
+        x = np.asarray(x)
+        check_signal_shape(x.shape)
+    res = solve_general_batch(x, cfg)
+    spec = res.spectrum(0)
+    tr = res.trace(0)
+    tr.timings = {"total": time.perf_counter() - t0}
+    return spec, tr

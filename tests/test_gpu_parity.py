@@ -330,3 +330,71 @@ def test_fft_large_kernel_bitexact():
     for loc, val in spec.entries.items():
         kb = loc % L
         assert val == v0[kb]
+
+
+# ------------------------------------------------------------ general path
+from tests.golden.cases import GENERAL_CASES   # noqa: E402
+from tests.synth import general_signal          # noqa: E402
+
+
+def _general_check(got: dict, want_locs, want_vals, ctx):
+    want_keys = [int(v) for v in want_locs]
+    extra = sorted(set(got) - set(want_keys))
+    missing = sorted(set(want_keys) - set(got))
+    assert not extra and not missing, f"{ctx}: supports differ: extra {extra[:10]} missing {missing[:10]}"
+    assert list(got) == want_keys, f"{ctx}: dict order differs"
+    g = np.array([got[s] for s in want_keys], dtype=np.complex128)
+    w = np.asarray(want_vals)
+    rel = np.abs(g - w) / np.maximum(np.abs(w), 1e-300)
+    assert rel.size == 0 or rel.max() <= VAL_RTOL, f"{ctx}: max rel {rel.max():.3e}"
+
+
+@pytest.mark.parametrize("case", GENERAL_CASES, ids=[c[0] for c in GENERAL_CASES])
+def test_general_solver_matches_golden(golden, case):
+    arrays, meta = golden
+    name, n, k, snr_db, seed, prune = case
+    x, _ = general_signal(n, k, snr_db, seed)
+    cfg = P.GeneralConfig(n=n, k=k, rng_seed=seed, prune=prune)
+    spec, tr = P.solve_general(x, cfg)
+    _general_check(spec.entries, arrays[f"{name}/general/locs"], arrays[f"{name}/general/vals"], name)
+    rec = meta["general"][name]
+    assert tr.d == rec["d"] and tr.r == rec["r"] and tr.shifts == rec["shifts"]
+    assert tr.fft_samples == rec["fft_samples"]
+    assert {str(a): c for a, c in tr.collision_histogram.items()} == rec["collision_histogram"]
+
+
+def test_general_batch_vs_oracle_cfg4_shape():
+    """Config-4 shape (N=2^20, K=128, 20 dB, d=256, L=4096) with per-signal
+    shift seeds, one device call, against the oracle per signal (including
+    the vote's singular values and votes)."""
+    n, k, B = 1 << 20, 128, 4
+    seeds = [(7, b) for b in range(B)]
+    X = np.stack([general_signal(n, k, 20.0, s)[0] for s in seeds])
+    cfg = P.GeneralConfig(n=n, k=k)
+    res = P.solve_general_batch(X, cfg, seeds=seeds)
+    votes = res.votes()
+    sv = res.singular_values()
+    for b in range(B):
+        want, wtr = OS.general(X[b], k, rng_seed=seeds[b], return_internals=True)
+        locs = np.fromiter(want.keys(), dtype=np.int64, count=len(want))
+        vals = np.fromiter(want.values(), dtype=np.complex128, count=len(want))
+        assert np.array_equal(votes[b], wtr["votes"]), f"b={b} votes differ"
+        assert np.allclose(sv[b], wtr["singular_values"], rtol=1e-12, atol=0)
+        _general_check(res.spectrum(b).entries, locs, vals, f"b={b}")
+        tr = res.trace(b)
+        assert tr.shifts == wtr["shifts"]
+        assert tr.collision_histogram == wtr["collision_histogram"]
+
+
+@pytest.mark.parametrize("n,k,a_max,d,prune", [(4096, 8, 3, None, True), (4096, 8, 2, 16, True),
+                                               (8192, 64, 3, 8, True), (4096, 4, 3, 64, False),
+                                               (4096, 16, 4, None, True)])
+def test_general_small_configs(n, k, a_max, d, prune):
+    x, _ = general_signal(n, k, 25.0, n + k)
+    cfg = P.GeneralConfig(n=n, k=k, a_max=a_max, d=d, rng_seed=3, prune=prune)
+    spec, tr = P.solve_general(x, cfg)
+    want, wtr = OS.general(x, k, a_max=a_max, d=d, rng_seed=3, prune=prune)
+    locs = np.fromiter(want.keys(), dtype=np.int64, count=len(want))
+    vals = np.fromiter(want.values(), dtype=np.complex128, count=len(want))
+    _general_check(spec.entries, locs, vals, f"n={n} k={k}")
+    assert tr.collision_histogram == wtr["collision_histogram"]

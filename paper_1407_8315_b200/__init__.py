@@ -6,7 +6,8 @@ from .exact import (EstimateResult, ExactBatch, ExactConfig, HostBatchResult, It
                     SolverTrace, estimate_sparsity_and_solve, exact_batch, solve_host_batch,
                     solve_iterative, solve_iterative_batch, solve_noniterative,
                     solve_noniterative_batch)
-from .general import (CollisionEstimate, GeneralBatch, GeneralConfig, GeneralTrace, draw_shifts,
+from .general import (CollisionEstimate, GeneralBatch, GeneralConfig, GeneralPlan, GeneralTrace,
+                      draw_shifts,
                       solve_general, solve_general_batch)
 from .spectral import SparseSpectrum, as_signal
 
@@ -25,5 +26,5 @@ __all__ = [
     "SparseSpectrum", "as_signal", "estimate_sparsity_and_solve", "exact_batch",
     "solve_iterative", "solve_iterative_batch", "solve_noniterative",
     "solve_noniterative_batch", "using_compiled", "CollisionEstimate", "GeneralBatch",
-    "GeneralConfig", "GeneralTrace", "draw_shifts", "solve_general", "solve_general_batch",
+    "GeneralConfig", "GeneralPlan", "GeneralTrace", "draw_shifts", "solve_general", "solve_general_batch",
 ]

@@ -34,20 +34,24 @@ struct GenParams {
 };
 
 // ------------------------------------------------------------------- svd
+template <int AM>
 __global__ void __launch_bounds__(128) k_gen_svd(const cx *__restrict__ V, GenParams p,
                                                  double *__restrict__ sv, double *__restrict__ partial) {
+    constexpr int S = 2 * AM;
     const int64_t b = blockIdx.y;
     const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     double e = 0.0;
     if (k < p.L) {
-        cx syn[8];
-        for (int j = 0; j < p.S; j++) {
+        cx syn[S];
+#pragma unroll
+        for (int j = 0; j < S; j++) {
             syn[j] = ldcx(V + (b * p.nv + j) * p.L + k);
             e += syn[j].re * syn[j].re + syn[j].im * syn[j].im;
         }
-        double s[4];
-        hankel_singular_values1(syn, p.a_max, s);
-        for (int i = 0; i < p.a_max; i++) sv[(b * p.L + k) * p.a_max + i] = s[i];
+        double s[AM];
+        hankel_sv_n<AM>(syn, s, 2.220446049250313e-16);
+#pragma unroll
+        for (int i = 0; i < AM; i++) sv[(b * p.L + k) * AM + i] = s[i];
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
@@ -617,7 +621,15 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     gp.phi_stride = a->phi_stride;
 
     // 2. collision vote (general.py:131-155)
-    k_gen_svd<<<dim3((unsigned)p.nparts, (unsigned)p.B), 128, 0, stream>>>(V, gp, sv, part);
+    {
+        const dim3 g((unsigned)p.nparts, (unsigned)p.B);
+        switch (a->a_max) {
+        case 1: k_gen_svd<1><<<g, 128, 0, stream>>>(V, gp, sv, part); break;
+        case 2: k_gen_svd<2><<<g, 128, 0, stream>>>(V, gp, sv, part); break;
+        case 3: k_gen_svd<3><<<g, 128, 0, stream>>>(V, gp, sv, part); break;
+        default: k_gen_svd<4><<<g, 128, 0, stream>>>(V, gp, sv, part); break;
+        }
+    }
     SFDT_CHECK_LAUNCH();
     cudaMemsetAsync(wlc, 0, 8, stream);
     k_gen_vote<<<(unsigned)p.B, 1024, 0, stream>>>(sv, part, (int)p.nparts, gp, votes, a->stats, wl, wlc);

@@ -144,9 +144,37 @@ class GeneralBatch:
         return self.t["singular_values"].cpu().numpy()
 
 
-def solve_general_batch(X, cfg: GeneralConfig, seeds=None, device=None) -> GeneralBatch:
+class GeneralPlan:
+    """Per-(config, batch, seeds) constants on the device: the drawn shifts
+    and the base_phi tables (built on the host exactly as general.py:101-106,
+    309 build them).  Reusable across batches with the same seeds."""
+
+    def __init__(self, cfg: GeneralConfig, batch: int, seeds=None, device=None):
+        dev = require_cuda(device)
+        d = cfg.resolved_d()
+        r_eff = min(cfg.r, d)
+        if seeds is None:
+            sh = draw_shifts(d, r_eff, cfg.rng_seed)[None, :]
+            phi = base_phi_table(sh[0], d)[None]
+            self.stride_s, self.stride_p = 0, 0
+            self.sh = np.broadcast_to(sh, (batch, r_eff))
+        else:
+            if len(seeds) != batch:
+                raise ValueError("need one seed per signal")
+            sh = np.stack([draw_shifts(d, r_eff, s) for s in seeds])
+            phi = np.stack([base_phi_table(s, d) for s in sh])
+            self.stride_s, self.stride_p = r_eff, r_eff * d
+            self.sh = sh
+        self.cfg, self.batch = cfg, batch
+        self.sh_d = torch.from_numpy(np.ascontiguousarray(sh)).to(dev)
+        self.phi_d = torch.from_numpy(np.ascontiguousarray(phi)).to(dev)
+
+
+def solve_general_batch(X, cfg: GeneralConfig, seeds=None, device=None,
+                        plan: GeneralPlan | None = None) -> GeneralBatch:
     """Batched solve_general.  seeds: None (cfg.rng_seed for every signal) or
-    one rng_seed per signal (per-signal shift draws)."""
+    one rng_seed per signal (per-signal shift draws); plan: precomputed
+    GeneralPlan for repeated batches."""
     t0 = time.perf_counter()
     dev = require_cuda(device if device is not None else
                        (X.device if isinstance(X, torch.Tensor) and X.is_cuda else None))
@@ -161,18 +189,11 @@ def solve_general_batch(X, cfg: GeneralConfig, seeds=None, device=None) -> Gener
         raise ValueError(f"signal length {n} != configured n {cfg.n}")
     d = cfg.resolved_d()
     r_eff = min(cfg.r, d)
-    if seeds is None:
-        sh = draw_shifts(d, r_eff, cfg.rng_seed)[None, :]
-        phi = base_phi_table(sh[0], d)[None]
-        stride_s, stride_p = 0, 0
-    else:
-        if len(seeds) != B:
-            raise ValueError("need one seed per signal")
-        sh = np.stack([draw_shifts(d, r_eff, s) for s in seeds])
-        phi = np.stack([base_phi_table(s, d) for s in sh])
-        stride_s, stride_p = r_eff, r_eff * d
-    sh_d = torch.from_numpy(np.ascontiguousarray(sh)).to(dev)
-    phi_d = torch.from_numpy(np.ascontiguousarray(phi)).to(dev)
+    if plan is None:
+        plan = GeneralPlan(cfg, B, seeds, dev)
+    elif plan.batch != B or plan.cfg != cfg:
+        raise ValueError("plan was built for a different batch/config")
+    sh, sh_d, phi_d, stride_s, stride_p = plan.sh, plan.sh_d, plan.phi_d, plan.stride_s, plan.stride_p
     lib = _lib.load()
     a = _lib.GeneralArgs()
     a.x = X.data_ptr()
@@ -204,8 +225,7 @@ def solve_general_batch(X, cfg: GeneralConfig, seeds=None, device=None) -> Gener
     _lib.check(lib.sfdt_general_solve(a, ws.data_ptr(), ws.numel(), stream_handle(dev)),
                "sfdt_general_solve")
     o["_keep"] = (sh_d, phi_d, tw)
-    shifts = np.broadcast_to(sh, (B, r_eff)) if seeds is None else sh
-    return GeneralBatch(n, cfg, d, r_eff, shifts, o, time.perf_counter() - t0, int(a.kernel_launches))
+    return GeneralBatch(n, cfg, d, r_eff, sh, o, time.perf_counter() - t0, int(a.kernel_launches))
 
 
 def solve_general(x, cfg: GeneralConfig):

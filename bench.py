@@ -1,24 +1,29 @@
-"""Benchmark: sFFT-DT exact recovery throughput on B200 (BASELINE.json metric).
+"""Benchmark: batched sFFT-DT recovery throughput on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config cfg2|cfg1|cfg3|cfg4|cfg5] [--k K] [--dtype c128|c64]
 
-Workload (BASELINE.json configs[1], "config 2"): B=4096 independent exactly
-K-sparse signals per GPU, N=2^20, K=256, |v| ~ U[1,10], uniform phase,
-complex128; solve_noniterative at the reference defaults (mu=4, a_max=4 ->
-d=1024, L=1024, 8 shifted views).  A step = one batched solve of all B
-signals resident in HBM, through to compacted (index, value) lists in HBM.
-Inputs are 64 GiB per GPU, far larger than the 126 MB L2, so no flush is
-needed between steps.
+Default workload (BASELINE.json configs[1], "config 2"): B=4096 independent
+exactly K-sparse signals per GPU, N=2^20, K=256, |v| ~ U[1,10], uniform
+phase, complex128; solve_noniterative at the reference defaults (mu=4,
+a_max=4 -> d=1024, L=1024, 8 shifted views).  A step = one batched solve of
+all B signals resident in HBM, through to compacted (index, value) lists in
+HBM.  Inputs are 64 GiB per GPU, far larger than the 126 MB L2, so no flush
+is needed between steps.  Other configs (--config) are the remaining
+BASELINE.json workloads: cfg1 (single signal N=2^16 K=64), cfg3 (B=64,
+N=2^24, K=4096, mu=1), cfg4 (general: B=1024, N=2^20, K=128, 20 dB), cfg5
+(N=2^22, B=64, --k sweep, --cfg5-general for the 30 dB general variant).
 
 Reported (one JSON line from rank 0):
-  value      signals/s over all ranks (device-timed, CUDA events, max over ranks)
-  e2e        same metric through solve_host_batch(): host pinned signals ->
-             PCIe -> GPU -> compacted results back on the host
-  roofline   the HBM stream kernel (k_stream): algorithmic bytes 16*N per
-             signal / its event-timed duration, vs MEASURED_PEAKS.json
-  cpu_baseline  the reference's CPU path (oracle/_ref kernels + restated
-             driver, or the oracle port) on this host's cores, bounded sample
-  parity     2 signals of the batch re-solved by the CPU oracle
+  value        signals/s over all ranks (device-timed, CUDA events, max over ranks)
+  e2e          same metric through solve_host_batch(): host pinned signals ->
+               PCIe -> GPU -> compacted results back on the host
+  roofline     the dominant kernel: exact path = k_sumsq, algorithmic bytes
+               16*N (8*N complex64) per signal / its event-timed duration, vs
+               MEASURED_PEAKS.json
+  cpu_baseline the reference's CPU path (oracle/_ref kernels + restated driver,
+               or the oracle port) on this host's cores, bounded sample
+  parity_sample  2 signals of the batch re-solved by the CPU oracle
 --impl reference times only the CPU reference path on the same config.
 """
 
@@ -49,11 +54,14 @@ def parse():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--solver", default="noniterative", choices=["noniterative", "iterative"])
-    ap.add_argument("--batch", type=int, default=4096)
-    ap.add_argument("--n", type=int, default=1 << 20)
-    ap.add_argument("--k", type=int, default=256)
-    ap.add_argument("--mu", type=int, default=4)
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--mu", type=int, default=None)
+    ap.add_argument("--cfg5-general", action="store_true")
+    ap.add_argument("--dtype", default="c128", choices=["c128", "c64"])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-chunk", type=int, default=256)
     ap.add_argument("--no-e2e", action="store_true")
@@ -62,71 +70,107 @@ def parse():
     ap.add_argument("--seed", type=int, default=2024)
     ap.add_argument("--pipeline", type=int, default=0,
                     help="signals per overlap chunk (0: no FFT/stream overlap)")
-    return ap.parse_args()
+    a = ap.parse_args()
+    # config defaults (BASELINE.json configs)
+    presets = {
+        "cfg1": dict(batch=1, n=1 << 16, k=64, mu=4, kind="exact", values="unit"),
+        "cfg2": dict(batch=4096, n=1 << 20, k=256, mu=4, kind="exact", values="mag1_10"),
+        "cfg3": dict(batch=64, n=1 << 24, k=4096, mu=1, kind="exact", values="unit"),
+        "cfg4": dict(batch=1024, n=1 << 20, k=128, mu=4, kind="general", values="unit", snr=20.0),
+        "cfg5": dict(batch=64, n=1 << 22, k=1 << 10, mu=4,
+                     kind="general" if a.cfg5_general else "exact", values="unit", snr=30.0),
+    }
+    p = presets[a.config]
+    a.kind = p["kind"]
+    a.values = p["values"]
+    a.snr = p.get("snr")
+    for key in ("batch", "n", "k", "mu"):
+        if getattr(a, key) is None:
+            setattr(a, key, p[key])
+    if a.config == "cfg5":
+        a.batch = max(1, (1 << 28) // a.n)
+    return a
+
+
+def resolved_d(a):
+    denom = (32 * a.k) if a.kind == "general" else (a.mu * a.k)
+    raw = a.n // denom
+    return 1 if raw < 1 else 1 << (raw.bit_length() - 1)
 
 
 def workload(a):
-    d = 1
-    raw = a.n // (a.mu * a.k)
-    if raw >= 1:
-        d = 1 << (raw.bit_length() - 1)
+    d = resolved_d(a)
+    if a.kind == "exact":
+        desc = (f"{a.config}: exactly K-sparse, B={a.batch}, N=2^{a.n.bit_length() - 1}, K={a.k}, "
+                f"{'|v|~U[1,10]' if a.values == 'mag1_10' else '|v|=1'} random phase, "
+                f"{'complex64 storage' if a.dtype == 'c64' else 'complex128'}; "
+                f"solve_{a.solver} mu={a.mu} a_max=4")
+    else:
+        desc = (f"{a.config}: generally K-sparse, B={a.batch}, N=2^{a.n.bit_length() - 1}, K={a.k} "
+                f"unit tones + {a.snr:g} dB time-domain complex Gaussian noise, "
+                f"{'complex64 storage' if a.dtype == 'c64' else 'complex128'}; solve_general "
+                "a_max=3 r=9 per-signal rng_seed")
     return {
-        "workload": (f"config 2: exactly K-sparse, B={a.batch}, N=2^{a.n.bit_length() - 1}, K={a.k}, "
-                     f"|v|~U[1,10] random phase, complex128; solve_{a.solver} mu={a.mu} a_max=4"),
-        "batch": a.batch, "n": a.n, "k": a.k, "mu": a.mu, "a_max": 4, "d": d, "L": a.n // d,
-        "solver": a.solver,
-        "l2": "inputs 16 MiB/signal x B >> 126 MB L2: no flush needed between steps",
+        "workload": desc, "batch": a.batch, "n": a.n, "k": a.k, "d": d, "L": a.n // d,
+        "solver": a.solver if a.kind == "exact" else "general", "dtype_storage": a.dtype,
+        "l2": ("inputs >> 126 MB L2: no flush needed between steps" if a.batch * a.n * 16 > 1 << 30
+               else "inputs re-read every step; L2 not flushed (small config, latency metric)"),
         "inputs": "seeded synthetic (no public dataset); generated on-device for the batch",
     }
 
 
 # ------------------------------------------------------------- CPU reference
-_CPU_POOL = None
-
-
-def _cpu_init(kind):
-    global _CPU_KIND
-    _CPU_KIND = kind
+_CPU = {}
 
 
 def _cpu_task(i):
     from oracle import solvers as OS
-    x = _CPU_POOL[i % len(_CPU_POOL)]
-    if _CPU_ARGS["solver"] == "iterative":
-        OS.exact_iterative(x, _CPU_ARGS["k"], _CPU_ARGS["mu"], kernels=_CPU_KIND)
+    c = _CPU
+    x = c["pool"][i % len(c["pool"])]
+    if c["kind"] == "general":
+        OS.general(x, c["k"], rng_seed=(c["seed"], i % len(c["pool"])), kernels=c["kernels"])
+    elif c["solver"] == "iterative":
+        OS.exact_iterative(x, c["k"], c["mu"], kernels=c["kernels"])
     else:
-        OS.exact_noniterative(x, _CPU_ARGS["k"], _CPU_ARGS["mu"], kernels=_CPU_KIND)
+        OS.exact_noniterative(x, c["k"], c["mu"], kernels=c["kernels"])
     return 1
+
+
+def cpu_signal(a, i):
+    from tests.synth import exact_signal, general_signal
+    if a.kind == "general":
+        x = general_signal(a.n, a.k, a.snr, (a.seed, 10_000 + i))[0]
+    else:
+        x = exact_signal(a.n, a.k, (a.seed, 10_000 + i), a.values)[0]
+    if a.dtype == "c64":
+        x = x.astype(np.complex64).astype(np.complex128)
+    return x
 
 
 def cpu_reference(a, steps, warmup, seconds_per_step):
     """Time the reference CPU path on all host cores (fork pool, one signal
-    per task).  Signal generation excluded.  Returns a dict."""
-    global _CPU_POOL, _CPU_ARGS
+    per task, generation excluded)."""
     import multiprocessing as mp
 
     from oracle import kernels as OK
-    from tests.synth import exact_signal
     kind = "reference" if OK.reference_core_path() else "port"
     if kind == "reference":
         OK.backend("reference")
     cores = len(os.sched_getaffinity(0))
-    npool = min(64, max(8, cores))
-    _CPU_POOL = [exact_signal(a.n, a.k, (a.seed, 10_000 + i), "mag1_10")[0] for i in range(npool)]
-    _CPU_ARGS = {"k": a.k, "mu": a.mu, "solver": a.solver}
-    # single-core latency estimate sizes each step
-    _cpu_init(kind)
+    npool = max(2, min(16 if a.n >= (1 << 22) else 64, max(8, cores)))
+    _CPU.update(pool=[cpu_signal(a, i) for i in range(npool)], kind=a.kind, k=a.k, mu=a.mu,
+                solver=a.solver, seed=a.seed, kernels=kind)
     t0 = time.perf_counter()
-    for i in range(3):
+    for i in range(2):
         _cpu_task(i)
-    lat = (time.perf_counter() - t0) / 3
+    lat = (time.perf_counter() - t0) / 2
     per_step = max(cores, int(seconds_per_step * cores / max(lat, 1e-4)))
     ctx = mp.get_context("fork")
-    with ctx.Pool(cores, initializer=_cpu_init, initargs=(kind,)) as pool:
+    with ctx.Pool(cores) as pool:
         times = []
         for s in range(warmup + steps):
             t0 = time.perf_counter()
-            done = sum(pool.imap_unordered(_cpu_task, range(per_step), chunksize=4))
+            done = sum(pool.imap_unordered(_cpu_task, range(per_step), chunksize=max(1, per_step // (4 * cores))))
             dt = time.perf_counter() - t0
             if s >= warmup:
                 times.append((done, dt))
@@ -135,10 +179,10 @@ def cpu_reference(a, steps, warmup, seconds_per_step):
     return {"value": sig / sec, "cores": cores, "kind": kind, "latency_s": lat,
             "signals": sig, "seconds": sec, "per_step": per_step,
             "sample": (f"{per_step} signal solves per step over a pool of {npool} distinct "
-                       f"config-2 signals (generation excluded), {steps} timed steps, "
+                       f"{a.config} signals (generation excluded), {steps} timed step(s), "
                        f"fork pool of {cores} workers; kernels: "
                        + ("the reference's own compiled _core (oracle/_ref) under the "
-                          "restated driver" if kind == "reference" else "oracle C port"))}
+                          "restated numpy driver" if kind == "reference" else "oracle C port"))}
 
 
 # ------------------------------------------------------------------ clocks
@@ -156,10 +200,11 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-i", str(self.index), "-lms", "100"],
+                 "-i", str(self.index), "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            time.sleep(0.2)
         except FileNotFoundError:
             self.proc = None
         return self
@@ -172,6 +217,7 @@ class ClockSampler:
 
     def __exit__(self, *exc):
         if self.proc is not None:
+            time.sleep(0.1)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -193,25 +239,37 @@ class ClockSampler:
 
 # --------------------------------------------------------------- GPU arm
 def gen_batch(a, dev, seed):
-    """Seeded exactly-K-sparse batch generated on the GPU (setup; cuFFT is
-    only used here to synthesize inputs, never on the measured path)."""
+    """Seeded synthetic batch generated on the GPU (setup only; cuFFT is used
+    here to synthesize inputs, never on the measured path)."""
     import torch
     B, n, k = a.batch, a.n, a.k
-    X = torch.empty((B, n), dtype=torch.complex128, device=dev)
+    X = torch.empty((B, n), dtype=torch.complex128 if a.dtype == "c128" else torch.complex64,
+                    device=dev)
     g = torch.Generator(device=dev)
     g.manual_seed(seed)
-    ch = 128
+    ch = max(1, min(128, (1 << 27) // n))
     for lo in range(0, B, ch):
         hi = min(B, lo + ch)
         r = torch.rand((hi - lo, n), generator=g, device=dev, dtype=torch.float32)
         idx = torch.topk(r, k, dim=1).indices
         del r
-        mag = 1.0 + 9.0 * torch.rand((hi - lo, k), generator=g, device=dev, dtype=torch.float64)
+        if a.values == "mag1_10":
+            mag = 1.0 + 9.0 * torch.rand((hi - lo, k), generator=g, device=dev, dtype=torch.float64)
+        else:
+            mag = torch.ones((hi - lo, k), device=dev, dtype=torch.float64)
         ph = 2 * math.pi * torch.rand((hi - lo, k), generator=g, device=dev, dtype=torch.float64)
         dense = torch.zeros((hi - lo, n), dtype=torch.complex128, device=dev)
         dense.scatter_(1, idx, torch.polar(mag, ph))
-        X[lo:hi] = torch.fft.ifft(dense, dim=1) * n
+        x = torch.fft.ifft(dense, dim=1) * n
         del dense
+        if a.kind == "general":
+            p_sig = (x.real ** 2 + x.imag ** 2).mean(dim=1, keepdim=True)
+            sigma = torch.sqrt(p_sig / 10 ** (a.snr / 10) / 2)
+            nr = torch.randn((hi - lo, n), generator=g, device=dev, dtype=torch.float64)
+            ni = torch.randn((hi - lo, n), generator=g, device=dev, dtype=torch.float64)
+            x = x + sigma * torch.complex(nr, ni)
+        X[lo:hi] = x.to(X.dtype)
+        del x
     return X
 
 
@@ -224,13 +282,47 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def load_traffic(cfg_key):
-    path = os.path.join(ROOT, "profiles", "traffic.json")
+def load_traffic(key):
     try:
-        with open(path) as fh:
-            return json.load(fh).get(cfg_key)
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh).get(key)
     except Exception:
         return None
+
+
+class Solver:
+    """One workload's device solve, parity check and host API."""
+
+    def __init__(self, a, dev, P, world, rank):
+        self.a, self.dev, self.P = a, dev, P
+        if a.kind == "exact":
+            self.cfg = P.ExactConfig(n=a.n, k=a.k, mu=a.mu)
+            self.iterative = a.solver == "iterative"
+        else:
+            self.cfg = P.GeneralConfig(n=a.n, k=a.k)
+            self.seeds = [(a.seed, rank, b) for b in range(a.batch)]
+            self.plan = P.GeneralPlan(self.cfg, a.batch, self.seeds, dev)
+
+    def solve(self, X, events=None):
+        if self.a.kind == "exact":
+            return self.P.exact_batch(X, self.cfg, self.iterative, self.dev, stream_events=events,
+                                      pipeline=self.a.pipeline)
+        return self.P.solve_general_batch(X, self.cfg, device=self.dev, plan=self.plan)
+
+    def oracle(self, x, b):
+        from oracle import solvers as OS
+        if self.a.kind == "general":
+            want, _ = OS.general(x, self.a.k, rng_seed=self.seeds[b])
+        elif self.iterative:
+            want, _ = OS.exact_iterative(x, self.a.k, self.a.mu)
+        else:
+            want, _ = OS.exact_noniterative(x, self.a.k, self.a.mu)
+        return want
+
+    def host_solve(self, Xh, n_signals, chunk):
+        it = self.iterative if self.a.kind == "exact" else False
+        return self.P.solve_host_batch(Xh, self.cfg, it, chunk=chunk, device=self.dev,
+                                       n_signals=n_signals)
 
 
 def gpu_arm(a):
@@ -245,26 +337,21 @@ def gpu_arm(a):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    cfg = P.ExactConfig(n=a.n, k=a.k, mu=a.mu)
-    iterative = a.solver == "iterative"
+    solver = Solver(a, dev, P, world, rank)
 
     X = gen_batch(a, dev, a.seed + 7919 * rank)
-    # two CPU-generated signals in the batch for a parity spot check
-    from tests.synth import exact_signal
-    par_x = [exact_signal(a.n, a.k, (a.seed, 900 + i), "mag1_10")[0] for i in range(2)]
+    # CPU-generated signals in the batch for a parity spot check
+    npar = min(2, a.batch)
+    par_x = [cpu_signal(a, 900 + i) for i in range(npar)]
     for i, x in enumerate(par_x):
-        X[i] = torch.from_numpy(x).to(dev)
+        X[i] = torch.from_numpy(x).to(dev).to(X.dtype)
     torch.cuda.synchronize(dev)
 
-    ev_b, ev_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev_b.record()
-    ev_e.record()
     for _ in range(a.warmup):
-        res = P.exact_batch(X, cfg, iterative, dev, pipeline=a.pipeline)
+        res = solver.solve(X)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    stream_ms = []
     step_start = torch.cuda.Event(enable_timing=True)
     step_end = torch.cuda.Event(enable_timing=True)
     sb = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
@@ -275,12 +362,10 @@ def gpu_arm(a):
     with ClockSampler(local) as clocks:
         step_start.record()
         for s in range(a.steps):
-            res = P.exact_batch(X, cfg, iterative, dev, stream_events=(sb[s], se[s]),
-                                pipeline=a.pipeline)
+            res = solver.solve(X, events=(sb[s], se[s]))
         step_end.record()
         torch.cuda.synchronize(dev)
     total_ms = step_start.elapsed_time(step_end)
-    stream_ms = [sb[s].elapsed_time(se[s]) for s in range(a.steps)]
     launches = res.kernel_launches * a.steps
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -288,31 +373,30 @@ def gpu_arm(a):
         dist.barrier()
     total_ms = float(t.item())
     value = world * a.batch * a.steps / (total_ms / 1e3)
+    step_s = total_ms / 1e3 / a.steps
 
     # parity spot check on the last result
-    from oracle import solvers as OS
-    parity = {"signals": len(par_x), "supports_equal": True, "max_rel": 0.0}
+    parity = {"signals": npar, "supports_equal": True, "max_rel": 0.0}
     for i, x in enumerate(par_x):
-        fn = OS.exact_iterative if iterative else OS.exact_noniterative
-        want, _ = fn(x, a.k, a.mu)
+        want = solver.oracle(x.astype(np.complex64).astype(np.complex128) if a.dtype == "c64" else x, i)
         got = res.spectrum(i).entries
         if set(got) != set(want):
             parity["supports_equal"] = False
         else:
-            for s, v in want.items():
-                parity["max_rel"] = max(parity["max_rel"], abs(got[s] - v) / abs(v))
+            for s_, v in want.items():
+                parity["max_rel"] = max(parity["max_rel"], abs(got[s_] - v) / abs(v))
 
     # end-to-end through the public host API
     e2e = None
     if not a.no_e2e:
         H = min(a.e2e_chunk, a.batch)
         Xh = X[:H].cpu().pin_memory()
-        P.solve_host_batch(Xh, cfg, iterative, chunk=H, device=dev, n_signals=2 * H)  # warm
+        solver.host_solve(Xh, 2 * H, H)   # warm
         torch.cuda.synchronize(dev)
         with ClockSampler(local) as clocks_e2e:
             t0 = time.perf_counter()
             for _ in range(a.e2e_steps):
-                hr = P.solve_host_batch(Xh, cfg, iterative, chunk=H, device=dev, n_signals=a.batch)
+                hr = solver.host_solve(Xh, a.batch, H)
             torch.cuda.synchronize(dev)
             e2e_s = time.perf_counter() - t0
         tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
@@ -320,24 +404,47 @@ def gpu_arm(a):
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
         e2e = {"value": world * a.batch * a.e2e_steps / e2e_s, "unit": "signals/s",
-               "h2d_bytes_per_step": a.batch * a.n * 16,
+               "h2d_bytes_per_step": a.batch * a.n * Xh.element_size(),
                "d2h_bytes_per_step": int(hr.d2h_bytes),
                "api": "paper_1407_8315_b200.solve_host_batch (pinned host -> GPU -> host results)",
                "clocks": clocks_e2e.summary()}
         del Xh
 
     peak, peak_src = load_peaks()
-    avg_stream_s = sum(stream_ms) / len(stream_ms) / 1e3
-    alg_bytes = a.batch * a.n * 16
-    achieved = alg_bytes / avg_stream_s / 1e9
-    step_s = total_ms / 1e3 / a.steps
+    roofline = None
+    if a.kind == "exact":
+        stream_ms = [sb[s].elapsed_time(se[s]) for s in range(a.steps)]
+        avg_stream_s = sum(stream_ms) / len(stream_ms) / 1e3
+        bps = 16 if a.dtype == "c128" else 8
+        alg_bytes = a.batch * a.n * bps
+        achieved = alg_bytes / avg_stream_s / 1e9
+        roofline = {"bound": "hbm", "kernel": "k_sumsq", "achieved": achieved, "peak": peak,
+                    "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
+                    "frac_of_8tbs_datasheet": achieved / 8000.0,
+                    "traffic": load_traffic(f"{a.solver}_n{a.n}_k{a.k}_b{a.batch}_{a.dtype}"),
+                    "alg_bytes_per_launch": alg_bytes,
+                    "alg_bytes_def": f"{bps} B x N x B (every sample of every signal read once)",
+                    "avg_launch_ms": avg_stream_s * 1e3,
+                    "kernel_share_of_step": avg_stream_s / step_s,
+                    "step_achieved_gbs": alg_bytes / step_s / 1e9}
+    else:
+        L = a.n // resolved_d(a)
+        alg_bytes = a.batch * 15 * L * 16
+        roofline = {"bound": "fp64", "kernel": "k_gen_bins/k_gen_svd",
+                    "note": ("general path is FP64/latency-bound (SURVEY F2): only "
+                             "(2*a_max + r_eff)*L samples per signal are read"),
+                    "gather_bytes_per_step": alg_bytes,
+                    "step_gather_gbs": alg_bytes / step_s / 1e9, "peak": peak,
+                    "peak_source": peak_src, "unit": "GB/s",
+                    "achieved": alg_bytes / step_s / 1e9, "frac": alg_bytes / step_s / 1e9 / peak,
+                    "traffic": None}
     out = None
     if rank == 0:
         cpu = None
         if not a.no_cpu and world == 1:
             del X
             torch.cuda.empty_cache()
-            c = cpu_reference(a, steps=2, warmup=1, seconds_per_step=a.cpu_seconds / 2)
+            c = cpu_reference(a, steps=1, warmup=0, seconds_per_step=a.cpu_seconds)
             cpu = {"value": c["value"], "unit": "signals/s", "cores": c["cores"], "kind": c["kind"],
                    "sample": c["sample"], "single_core_latency_s": c["latency_s"]}
         out = {
@@ -347,14 +454,7 @@ def gpu_arm(a):
             "dtype": "f64", "data": "synthetic", "impl": "b200",
             "config": workload(a),
             "e2e": e2e,
-            "roofline": {"bound": "hbm", "kernel": "k_stream", "achieved": achieved, "peak": peak,
-                         "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
-                         "frac_of_8tbs_datasheet": achieved / 8000.0,
-                         "traffic": load_traffic(f"{a.solver}_n{a.n}_k{a.k}"),
-                         "alg_bytes_per_launch": alg_bytes,
-                         "avg_launch_ms": avg_stream_s * 1e3,
-                         "kernel_share_of_step": avg_stream_s / step_s,
-                         "step_achieved_gbs": alg_bytes / step_s / 1e9},
+            "roofline": roofline,
             "cpu_baseline": cpu,
             "gpu_launches": launches,
             "clocks": clocks.summary(),
@@ -370,11 +470,13 @@ def reference_arm(a):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
-    c = cpu_reference(a, steps=a.steps if a.steps <= 3 else 3, warmup=min(a.warmup, 1),
-                      seconds_per_step=max(5.0, a.cpu_seconds / 2))
+    steps = max(1, min(a.steps, 3))
+    warm = min(a.warmup, 1)
+    c = cpu_reference(a, steps=steps, warmup=warm,
+                      seconds_per_step=max(5.0, a.cpu_seconds / max(1, steps)))
     return {
         "metric": METRIC, "value": c["value"], "unit": "signals/s", "n_gpus": 0,
-        "steps": min(a.steps, 3), "warmup": min(a.warmup, 1), "ms_per_step": None,
+        "steps": steps, "warmup": warm, "ms_per_step": c["seconds"] / steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "impl": "reference", "config": workload(a),
         "cpu_baseline": {"value": c["value"], "unit": "signals/s", "cores": c["cores"],

@@ -2,13 +2,13 @@
 package's recovery entry points, computed by hand-written sm_100a kernels
 (libsfdt_b200.so).  See DESIGN.md."""
 
-from .exact import (EstimateResult, ExactBatch, ExactConfig, HostBatchResult, IterationStats,
-                    SolverTrace, estimate_sparsity_and_solve, exact_batch, solve_host_batch,
-                    solve_iterative, solve_iterative_batch, solve_noniterative,
-                    solve_noniterative_batch)
+from .exact import (EstimateResult, ExactBatch, ExactConfig, IterationStats, SolverTrace,
+                    estimate_sparsity_and_solve, exact_batch, solve_iterative,
+                    solve_iterative_batch, solve_noniterative, solve_noniterative_batch)
 from .general import (CollisionEstimate, GeneralBatch, GeneralConfig, GeneralPlan, GeneralTrace,
                       draw_shifts,
                       solve_general, solve_general_batch)
+from .host import HostBatchResult, solve_host_batch
 from .spectral import SparseSpectrum, as_signal
 
 BACKEND = "b200"

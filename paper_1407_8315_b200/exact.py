@@ -259,81 +259,6 @@ def exact_batch(X, cfg: ExactConfig, iterative: bool, device=None,
     return res
 
 
-class HostBatchResult:
-    """Host-side results of solve_host_batch: the per-chunk ExactBatch host
-    dictionaries, with global signal indexing."""
-
-    def __init__(self, n, iterative, chunks, chunk_size):
-        self.n, self.iterative, self.chunks, self.chunk_size = n, iterative, chunks, chunk_size
-
-    def _loc(self, b):
-        return self.chunks[b // self.chunk_size], b % self.chunk_size
-
-    def spectrum(self, b) -> SparseSpectrum:
-        ch, i = self._loc(b)
-        return ch.spectrum(i)
-
-    def trace(self, b) -> SolverTrace:
-        ch, i = self._loc(b)
-        return ch.trace(i)
-
-    @property
-    def d2h_bytes(self) -> int:
-        tot = 0
-        for ch in self.chunks:
-            tot += sum(v.nbytes for v in ch.to_host().values())
-        return tot
-
-
-def solve_host_batch(X_host, cfg: ExactConfig, iterative: bool = False, chunk: int = 256,
-                     device=None, n_signals: int | None = None) -> HostBatchResult:
-    """Solve signals that live in HOST memory, streaming them through the GPU:
-    chunk i+1 is copied host->device on a side stream while chunk i is
-    solved, and every chunk's compacted results are read back to host.
-
-    X_host: (B, n) torch tensor (pinned for full PCIe overlap) or numpy.
-    n_signals: process this many signals, cycling over X_host's rows
-    (synthetic benchmarking of large batches from a smaller host pool)."""
-    dev = require_cuda(device)
-    if not isinstance(X_host, torch.Tensor):
-        X_host = torch.from_numpy(np.ascontiguousarray(X_host, dtype=np.complex128))
-    if X_host.dim() != 2:
-        raise ValueError(f"expected (B, n) signals, got shape {tuple(X_host.shape)}")
-    H, n = X_host.shape
-    check_signal_shape((n,))
-    total = H if n_signals is None else int(n_signals)
-    chunk = max(1, min(chunk, total))
-    compute = torch.cuda.current_stream(dev)
-    copy = torch.cuda.Stream(dev)
-    bufs = [torch.empty((chunk, n), dtype=X_host.dtype, device=dev) for _ in range(2)]
-    free = [torch.cuda.Event() for _ in range(2)]
-    ready = [torch.cuda.Event() for _ in range(2)]
-    for e in free:
-        e.record(compute)
-    results = []
-    nchunks = (total + chunk - 1) // chunk
-    for c in range(nchunks):
-        i = c & 1
-        lo = c * chunk
-        rows = min(chunk, total - lo)
-        with torch.cuda.stream(copy):
-            copy.wait_event(free[i])
-            src_lo = lo % H
-            if src_lo + rows <= H:
-                bufs[i][:rows].copy_(X_host[src_lo:src_lo + rows], non_blocking=True)
-            else:
-                k1 = H - src_lo
-                bufs[i][:k1].copy_(X_host[src_lo:], non_blocking=True)
-                bufs[i][k1:rows].copy_(X_host[:rows - k1], non_blocking=True)
-            ready[i].record(copy)
-        compute.wait_event(ready[i])
-        results.append(exact_batch(bufs[i][:rows], cfg, iterative, dev))
-        free[i].record(compute)
-    for r in results:
-        r.to_host()
-    return HostBatchResult(n, bool(iterative), results, chunk)
-
-
 def solve_noniterative_batch(X, cfg: ExactConfig, device=None) -> ExactBatch:
     return exact_batch(X, cfg, False, device)
 

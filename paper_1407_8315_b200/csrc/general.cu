@@ -226,6 +226,7 @@ __device__ void subspace_pursuit_dev(const cx *y, const cx *phase, const cx *bph
     o.rankdef = 0;
     auto lsq = [&](const int *s, int ns, cx *x) {
         for (int c = 0; c < ns; c++) phi_col(s[c], A + c * r);
+        if (lstsq_qr(A, r, ns, y, x)) return;   // full rank: unique LS solution
         const int rk = lstsq_min_norm(A, r, ns, y, x);
         if (rk < ns) o.rankdef++;
     };

@@ -179,6 +179,60 @@ __device__ __forceinline__ int lstsq_min_norm(const cx *A, int r, int c, const c
     return rank;
 }
 
+// Least squares by Householder QR (r >= c): x = R^-1 (Q^H y)[:c].  Returns
+// false when the triangle is too ill-conditioned to be certainly full rank
+// under gelsd's rcond (min|R_ii| <= 1e-7 max|R_ii|) -- the caller then uses
+// the minimum-norm SVD path.  For full-rank systems both give the unique LS
+// solution (to roundoff); QR costs ~2rc^2 flops instead of Jacobi sweeps.
+__device__ __forceinline__ bool lstsq_qr(const cx *A_in, int r, int c, const cx *y_in, cx *x) {
+    if (c > r) return false;
+    cx A[GEN_MAX_R * GEN_MAX_SUP], y[GEN_MAX_R];
+    for (int j = 0; j < c; j++)
+        for (int i = 0; i < r; i++) A[j * r + i] = A_in[j * r + i];
+    for (int i = 0; i < r; i++) y[i] = y_in[i];
+    double rmax = 0.0, rmin = 1e300;
+    for (int j = 0; j < c; j++) {
+        double nrm2 = 0.0;
+        for (int i = j; i < r; i++) nrm2 = fma(A[j * r + i].re, A[j * r + i].re, fma(A[j * r + i].im, A[j * r + i].im, nrm2));
+        const double nrm = sqrt(nrm2);
+        if (nrm == 0.0) return false;
+        const cx x0 = A[j * r + j];
+        const double ax0 = cabs_(x0);
+        const cx ph = ax0 > 0.0 ? mk(x0.re / ax0, x0.im / ax0) : mk(1.0, 0.0);
+        const cx alpha = mk(-ph.re * nrm, -ph.im * nrm);   // R_jj
+        // v = x - alpha e1, H = I - 2 v v^H / (v^H v)
+        cx v[GEN_MAX_R];
+        double vv = 0.0;
+        for (int i = j; i < r; i++) {
+            v[i] = (i == j) ? csub(x0, alpha) : A[j * r + i];
+            vv = fma(v[i].re, v[i].re, fma(v[i].im, v[i].im, vv));
+        }
+        if (vv > 0.0) {
+            const double beta = 2.0 / vv;
+            for (int k = j; k < c; k++) {
+                cx dot = mk(0.0, 0.0);
+                for (int i = j; i < r; i++) dot = cadd(dot, nmul(cconj(v[i]), A[k * r + i]));
+                dot = mk(dot.re * beta, dot.im * beta);
+                for (int i = j; i < r; i++) A[k * r + i] = csub(A[k * r + i], nmul(v[i], dot));
+            }
+            cx dot = mk(0.0, 0.0);
+            for (int i = j; i < r; i++) dot = cadd(dot, nmul(cconj(v[i]), y[i]));
+            dot = mk(dot.re * beta, dot.im * beta);
+            for (int i = j; i < r; i++) y[i] = csub(y[i], nmul(v[i], dot));
+        }
+        const double rjj = cabs_(A[j * r + j]);
+        rmax = rjj > rmax ? rjj : rmax;
+        rmin = rjj < rmin ? rjj : rmin;
+    }
+    if (!(rmin > 1e-7 * rmax)) return false;
+    for (int j = c - 1; j >= 0; j--) {
+        cx acc = y[j];
+        for (int k = j + 1; k < c; k++) acc = csub(acc, nmul(A[k * r + j], x[k]));
+        x[j] = ndiv(acc, A[j * r + j]);
+    }
+    return true;
+}
+
 // top-`cnt` selection by score with the reference's tie rule (np.argsort
 // kind="stable" on -score: larger first, then lower index first)
 __device__ __forceinline__ void topk_insert(double *sc, int *id, int &len, int cnt, double v, int t) {

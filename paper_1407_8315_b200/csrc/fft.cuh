@@ -173,9 +173,9 @@ static __global__ void k_fft_large_a(const ViewSrc src, int logL, int logP,
 // Pass A runs the first logP stages on contiguous blocks of P points (in
 // smem); pass B runs the remaining stages, which act independently on the
 // residue classes i mod P, on tiles of R residues x Q = L/P rows.
-static __global__ void k_fft_large_b(cx *__restrict__ buf, int64_t nviews, int logL, int logP, int logR,
-                              const cx *__restrict__ tw, cx *__restrict__ out, int nshift, int SV,
-                              int64_t ldV) {
+static __global__ void k_fft_large_b(cx *buf, int64_t nviews, int logL, int logP, int logR,
+                                     const cx *__restrict__ tw, cx *out, int nshift, int SV,
+                                     int64_t ldV, int scale) {
     extern __shared__ double4 smem_raw[];
     cx *a = reinterpret_cast<cx *>(smem_raw);
     const int L = 1 << logL, P = 1 << logP, R = 1 << logR;
@@ -214,7 +214,8 @@ static __global__ void k_fft_large_b(cx *__restrict__ buf, int64_t nviews, int l
     for (int i = threadIdx.x; i < Q * R; i += blockDim.x) {
         const int q = i >> logR, rr = i & (R - 1);
         const cx y = a[i];
-        stcx(out + (b * SV + s) * ldV + r0 + rr + (int64_t)q * P, mk(DMUL(y.re, sc), DMUL(y.im, sc)));
+        stcx(out + (b * SV + s) * ldV + r0 + rr + (int64_t)q * P,
+             scale ? mk(DMUL(y.re, sc), DMUL(y.im, sc)) : y);
     }
 }
 
@@ -254,7 +255,7 @@ static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, con
         const size_t smem = (size_t(1) << (logQ + logR)) * 16;
         cudaFuncSetAttribute(k_fft_large_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         k_fft_large_b<<<(unsigned)(nviews * (P >> logR)), 256, smem, stream>>>(
-            large_scratch, nviews, logL, logP, logR, tw, out, src.nshift, SV, ldV);
+            large_scratch, nviews, logL, logP, logR, tw, out, src.nshift, SV, ldV, scale);
         SFDT_CHECK_LAUNCH();
     }
     return SFDT_OK;

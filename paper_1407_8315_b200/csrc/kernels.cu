@@ -86,13 +86,14 @@ int sfdt_version(void) { return 10000; }
 int sfdt_fft_radix2(const double *x, double *out, int64_t batch, int64_t n, int inverse,
                     const double *twiddles, sfdt_stream_t stream) {
     (void)inverse;   // the table carries the sign
-    if (batch < 0 || n < 1 || (n & (n - 1)) || n > FFT_SMEM_MAX) return SFDT_EINVAL;
+    if (batch < 0 || n < 1 || (n & (n - 1)) || n > (int64_t(1) << 25) || !twiddles) return SFDT_EINVAL;
     if (batch == 0) return SFDT_OK;
-    // a (batch, n) array of signals, each its own single view (d = 1)
+    // a (batch, n) array of signals, each its own single view (d = 1); long
+    // transforms run the two-pass stage split with `out` as the scratch
+    // (pass B reads and writes the same residue-class tile, so in place is safe)
     const ViewSrc src = consecutive_views(x, 0, n, 1, 0, 1);
-    const int rc = launch_fft_views(src, batch, n, twiddles, (cx *)out, 1, n, (cudaStream_t)stream,
-                                    nullptr, 0);
-    return rc;
+    return launch_fft_views(src, batch, n, twiddles, (cx *)out, 1, n, (cudaStream_t)stream,
+                            (cx *)out, 0);
 }
 
 int sfdt_hankel_solve(const double *m, int64_t nb, int64_t ld, int a, double *c, double *cd,

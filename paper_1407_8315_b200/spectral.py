@@ -71,3 +71,59 @@ class SparseSpectrum:
 
     def __len__(self) -> int:
         return len(self.entries)
+
+
+def fft(x, normalization: str = "sum", inverse: bool = False):
+    """Radix-2 FFT of a power-of-two-length signal on the B200 (spectral.py:
+    128-140), bit-identical to the reference's fft_radix2.  ``normalization``
+    is "sum" or "one_over_n".  Accepts numpy or torch; returns numpy.  n up to
+    2^25 (longer than one CTA's shared memory runs the two-pass split)."""
+    import torch
+
+    from . import _lib
+    from .device import require_cuda, stream_handle, twiddles
+    if normalization not in ("sum", "one_over_n"):
+        raise ValueError(f"unknown normalization {normalization!r}")
+    if isinstance(x, torch.Tensor):
+        n = check_signal_shape(x.shape)
+        dev = require_cuda(x.device if x.is_cuda else None)
+        xd = x.to(dev, torch.complex128).contiguous()
+    else:
+        arr = as_signal(x)
+        n = arr.size
+        dev = require_cuda()
+        xd = torch.from_numpy(arr).to(dev)
+    out = torch.empty_like(xd)
+    _lib.check(_lib.load().sfdt_fft_radix2(xd.data_ptr(), out.data_ptr(), 1, n, int(bool(inverse)),
+                                           twiddles(n, dev, inverse).data_ptr(), stream_handle(dev)),
+               "sfdt_fft_radix2")
+    res = out.cpu().numpy()
+    return res / n if normalization == "one_over_n" else res
+
+
+def synthesize(spectrum) -> np.ndarray:
+    """Time signal from a spectrum, x[n] = sum_k xhat[k] e^{+2 pi i k n/N}
+    (spectral.py:143-148), on the B200."""
+    if isinstance(spectrum, SparseSpectrum):
+        spectrum = spectrum.to_dense()
+    return fft(as_signal(spectrum), "sum", inverse=True)
+
+
+def snr(reference, estimate) -> float:
+    """SNR in dB of ``estimate`` against the dense ``reference`` spectrum
+    (spectral.py:193-212); math.inf when the error is exactly zero."""
+    import math
+    reference = np.asarray(reference, dtype=np.complex128)
+    if isinstance(estimate, SparseSpectrum):
+        if estimate.n != reference.size:
+            raise ValueError("length mismatch between reference and estimate")
+        estimate = estimate.to_dense()
+    else:
+        estimate = np.asarray(estimate, dtype=np.complex128)
+    if estimate.shape != reference.shape:
+        raise ValueError("length mismatch between reference and estimate")
+    err = np.mean(np.abs(reference - estimate) ** 2)
+    sig = np.mean(np.abs(estimate) ** 2)
+    if err == 0.0:
+        return math.inf
+    return 10.0 * math.log10(sig / err)

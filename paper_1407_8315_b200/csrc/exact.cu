@@ -74,6 +74,59 @@ __global__ void __launch_bounds__(THREADS) k_sumsq(const void *__restrict__ x_, 
     }
 }
 
+// Persistent form: one CTA per SM grid-strides over (signal, chunk) items, so
+// the kernel never holds pending CTAs and concurrent FFT/decode kernels of the
+// previous signal chunk (aux stream) start at once in the SM resources this
+// kernel leaves free (it reserves ~120 KB of shared memory to stay at one
+// 1024-thread CTA per SM, which still streams at the full read rate).
+template <int C64, int THREADS, int UNROLL>
+__global__ void __launch_bounds__(THREADS) k_sumsq_persistent(const void *__restrict__ x_, int64_t n,
+                                                             int64_t CH, int64_t nchunk, int64_t nitems,
+                                                             double *__restrict__ partial) {
+    extern __shared__ double s_reserved[];
+    __shared__ double red[THREADS / 32];
+    const int64_t CHp = CH >> 1;
+    for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+        const int64_t b = item / nchunk, chunk = item - b * nchunk;
+        const int64_t base = (b * n + chunk * CH) >> 1;
+        double acc = 0.0;
+        for (int64_t off = 0; off < CHp; off += int64_t(THREADS) * UNROLL) {
+            double v[UNROLL][4];
+#pragma unroll
+            for (int u = 0; u < UNROLL; u++) {
+                const int64_t pidx = off + int64_t(u) * THREADS + threadIdx.x;
+                if (pidx < CHp) {
+                    if (C64) {
+                        const float4 f = __ldcs(reinterpret_cast<const float4 *>(x_) + base + pidx);
+                        v[u][0] = f.x; v[u][1] = f.y; v[u][2] = f.z; v[u][3] = f.w;
+                    } else {
+                        const double *pp = reinterpret_cast<const double *>(x_) + 4 * (base + pidx);
+                        asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.f64 {%0,%1,%2,%3}, [%4];"
+                                     : "=d"(v[u][0]), "=d"(v[u][1]), "=d"(v[u][2]), "=d"(v[u][3])
+                                     : "l"(pp));
+                    }
+                } else {
+                    v[u][0] = v[u][1] = v[u][2] = v[u][3] = 0.0;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < UNROLL; u++)
+                acc = fma(v[u][0], v[u][0], fma(v[u][1], v[u][1], fma(v[u][2], v[u][2], fma(v[u][3], v[u][3], acc))));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < THREADS / 32; w++) t += red[w];
+            partial[item] = t;
+            if (t == -1.0) s_reserved[0] = t;   // keeps the reservation
+        }
+        __syncthreads();
+    }
+}
+
 // rms and threshold per signal: fixed-order pairwise tree over the partials
 __global__ void k_rms(const double *__restrict__ partial, int64_t nchunk, int64_t n, double zt,
                       int64_t d, double *__restrict__ rms, double *__restrict__ thr) {
@@ -803,14 +856,38 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
 
     int launches = 0;
     const int is_c64 = a->x_dtype == SFDT_C64;
+    // With an aux stream the stream kernel runs one 1024-thread CTA per SM
+    // (a dynamic shared-memory reservation caps residency): measured on B200
+    // to hold the full 7.55 TB/s read rate (tools/membw.cu) while leaving half
+    // of every SM's threads and shared memory to the FFT/decode of the
+    // previous chunk.
+    const bool reserve = a->aux_stream != nullptr;
     auto launch_stream = [&](int64_t c0, int64_t bc) -> int {
-        constexpr int TH = 512, UN = 4;
         dim3 grid((unsigned)p.nchunk, (unsigned)bc);
         const char *xc = (const char *)a->x + c0 * p.n * (is_c64 ? 8 : 16);
-        if (is_c64)
-            k_sumsq<1, TH, UN><<<grid, TH, 0, stream>>>(xc, p.n, p.CH, partial + c0 * p.nchunk);
-        else
-            k_sumsq<0, TH, UN><<<grid, TH, 0, stream>>>(xc, p.n, p.CH, partial + c0 * p.nchunk);
+        if (reserve) {
+            constexpr int TH = 1024, UN = 4, SMEM = 120000;
+            int dev = 0, sms = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            const int64_t nitems = p.nchunk * bc;
+            const unsigned g = (unsigned)(nitems < sms ? nitems : sms);
+            if (is_c64) {
+                cudaFuncSetAttribute(k_sumsq_persistent<1, TH, UN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+                k_sumsq_persistent<1, TH, UN><<<g, TH, SMEM, stream>>>(xc, p.n, p.CH, p.nchunk, nitems,
+                                                                       partial + c0 * p.nchunk);
+            } else {
+                cudaFuncSetAttribute(k_sumsq_persistent<0, TH, UN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+                k_sumsq_persistent<0, TH, UN><<<g, TH, SMEM, stream>>>(xc, p.n, p.CH, p.nchunk, nitems,
+                                                                       partial + c0 * p.nchunk);
+            }
+        } else {
+            constexpr int TH = 512, UN = 4;
+            if (is_c64)
+                k_sumsq<1, TH, UN><<<grid, TH, 0, stream>>>(xc, p.n, p.CH, partial + c0 * p.nchunk);
+            else
+                k_sumsq<0, TH, UN><<<grid, TH, 0, stream>>>(xc, p.n, p.CH, partial + c0 * p.nchunk);
+        }
         SFDT_CHECK_LAUNCH();
         launches += 1;
         return SFDT_OK;

@@ -88,9 +88,12 @@ __device__ __forceinline__ void fft_pass(cx *a, int nv, int logL, int lh, const 
             for (int q = 0; q < G; q++) {
                 if (q & (1 << st)) continue;
                 const int e = e0 + q * h;
-                const cx w = ldcx(twh + (e & (Hs - 1)));
                 const cx u = x[q];
-                const cx t = gmul(x[q + (1 << st)], w);
+                // the reference's w starts at exactly 1 + 0i, and (a*1 - b*0,
+                // a*0 + b*1) == (a, b) for finite a, b: the first twiddle of
+                // every stage block needs no multiply
+                const int kk = e & (Hs - 1);
+                const cx t = (Hs == 1) ? x[q + (1 << st)] : gmul(x[q + (1 << st)], ldcx(twh + kk));
                 x[q] = cadd(u, t);
                 x[q + (1 << st)] = csub(u, t);
             }
@@ -102,8 +105,11 @@ __device__ __forceinline__ void fft_pass(cx *a, int nv, int logL, int lh, const 
 
 __device__ __forceinline__ void fft_stages_smem(cx *a, int nv, int logL, int lh0, int lh1,
                                                 const cx *__restrict__ tw) {
+    // up to 3 stages (radix-8 groups) per shared-memory pass (radix-16
+    // measured slower: 134 registers halve the resident CTAs)
     for (int lh = lh0; lh < lh1;) {
-        const int nst = (lh1 - lh) >= 3 ? 3 : (lh1 - lh);
+        const int rem = lh1 - lh;
+        const int nst = rem >= 3 ? 3 : rem;
         if (nst == 3) fft_pass<3>(a, nv, logL, lh, tw);
         else if (nst == 2) fft_pass<2>(a, nv, logL, lh, tw);
         else fft_pass<1>(a, nv, logL, lh, tw);
@@ -112,7 +118,7 @@ __device__ __forceinline__ void fft_stages_smem(cx *a, int nv, int logL, int lh0
     }
 }
 
-static __global__ void k_fft_views(const ViewSrc src, int64_t B, int logL, int logvpc,
+static __global__ void __launch_bounds__(256) k_fft_views(const ViewSrc src, int64_t B, int logL, int logvpc,
                                    const cx *__restrict__ tw, cx *__restrict__ out, int SV,
                                    int64_t ldV, int scale) {
     extern __shared__ double4 smem_raw[];

@@ -36,10 +36,12 @@ _aux_streams: dict = {}
 
 
 def aux_stream(device: torch.device) -> torch.cuda.Stream:
-    """Second stream per device for the library's copy/compute pipelining."""
+    """Second stream per device for the library's overlap of latency-bound
+    kernels with the HBM stream; high priority so its CTAs are dispatched as
+    soon as SM resources free up."""
     st = _aux_streams.get(device)
     if st is None:
-        st = torch.cuda.Stream(device)
+        st = torch.cuda.Stream(device, priority=-1)
         _aux_streams[device] = st
     return st
 

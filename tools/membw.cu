@@ -55,6 +55,27 @@ __global__ void __launch_bounds__(THREADS) rd32(const double4 *__restrict__ x, i
     if (acc == 1.2345) out[blockIdx.x] = acc;
 }
 
+template <int THREADS, int UNROLL>
+__global__ void __launch_bounds__(THREADS) rd32s(const double4 *__restrict__ x, int64_t n4, int64_t CH4,
+                                                 double *__restrict__ out) {
+    extern __shared__ double dummy[];
+    const int64_t base = int64_t(blockIdx.x) * CH4;
+    double acc = 0.0;
+    for (int64_t off = 0; off < CH4; off += int64_t(THREADS) * UNROLL) {
+        double4 v[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; u++) {
+            const double4 *p = x + base + off + int64_t(u) * THREADS + threadIdx.x;
+            asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.f64 {%0,%1,%2,%3}, [%4];"
+                         : "=d"(v[u].x), "=d"(v[u].y), "=d"(v[u].z), "=d"(v[u].w) : "l"(p));
+        }
+#pragma unroll
+        for (int u = 0; u < UNROLL; u++)
+            acc = fma(v[u].x, v[u].x, fma(v[u].y, v[u].y, fma(v[u].z, v[u].z, fma(v[u].w, v[u].w, acc))));
+    }
+    if (acc == 1.2345) { dummy[0] = acc; out[blockIdx.x] = dummy[threadIdx.x & 7]; }
+}
+
 template <typename F>
 float timeit(F f, int reps) {
     cudaEvent_t a, b;
@@ -102,5 +123,19 @@ int main() {
     RUN32(256, 4, 8192, 1);
     RUN32(256, 8, 8192, 1);
     RUN32(256, 8, 32768, 1);
+#define RUNS(T, U, CH4, SMEM)                                                                      \
+    {                                                                                             \
+        cudaFuncSetAttribute(rd32s<T, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);     \
+        float ms = timeit([&] { rd32s<T, U><<<(unsigned)(n / 2 / CH4), T, SMEM>>>((const double4 *)x, n / 2, CH4, out); }, 5); \
+        printf("rd32s T=%d U=%d CH4=%d smem=%d : %.3f ms  %.1f GB/s\n", T, U, (int)CH4, SMEM, ms, gb / ms * 1e3); \
+    }
+    RUNS(512, 4, 8192, 0);
+    RUNS(512, 4, 8192, 60000);
+    RUNS(512, 4, 8192, 80000);
+    RUNS(512, 8, 8192, 80000);
+    RUNS(1024, 4, 8192, 120000);
+    RUNS(1024, 8, 8192, 120000);
+    RUNS(256, 8, 8192, 60000);
+    RUNS(256, 16, 8192, 60000);
     return 0;
 }

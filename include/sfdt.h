@@ -178,6 +178,13 @@ typedef struct {
     int32_t kernel_launches; /* out */
 } sfdt_general_args;
 
+/* estimate_collisions (general.py:131-155) on given consecutive syndromes
+ * syn (nb, ld) row-major: singular values sv (nb, a_max) and votes (nb). */
+size_t sfdt_estimate_collisions_workspace_bytes(int64_t nb);
+int sfdt_estimate_collisions(const double *syn, int64_t nb, int64_t ld, int64_t k, int a_max, int64_t d,
+                             double zero_vote_rtol, int32_t *votes, double *sv, void *workspace,
+                             size_t workspace_bytes, sfdt_stream_t stream);
+
 int sfdt_general_caps(const sfdt_general_args *args, int64_t *entry_cap);
 size_t sfdt_general_workspace_bytes(const sfdt_general_args *args);
 int sfdt_general_solve(sfdt_general_args *args, void *workspace, size_t workspace_bytes,

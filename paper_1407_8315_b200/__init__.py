@@ -6,10 +6,13 @@ from .exact import (EstimateResult, ExactBatch, ExactConfig, IterationStats, Sol
                     estimate_sparsity_and_solve, exact_batch, solve_iterative,
                     solve_iterative_batch, solve_noniterative, solve_noniterative_batch)
 from .general import (CollisionEstimate, GeneralBatch, GeneralConfig, GeneralPlan, GeneralTrace,
-                      draw_shifts,
+                      draw_shifts, estimate_collisions,
                       solve_general, solve_general_batch)
 from .host import HostBatchResult, solve_host_batch
-from .spectral import SparseSpectrum, as_signal
+from .syndrome import (DecodedBin, DegenerateBranch, IllConditioned, NearSingular,
+                       PolyCoefficients, decode_bin, root_to_location, roots_closed_form,
+                       solve_coefficients, solve_values)
+from .spectral import SparseSpectrum, as_signal, fft, snr, synthesize
 
 BACKEND = "b200"
 __version__ = "0.1.0"
@@ -21,10 +24,13 @@ def using_compiled() -> bool:
 
 
 __all__ = [
+    "DecodedBin", "DegenerateBranch", "IllConditioned", "NearSingular", "PolyCoefficients",
+    "decode_bin", "root_to_location", "roots_closed_form", "solve_coefficients", "solve_values",
+    "fft", "snr", "synthesize",
     "BACKEND", "EstimateResult", "ExactBatch", "ExactConfig", "HostBatchResult",
     "IterationStats", "SolverTrace", "solve_host_batch",
     "SparseSpectrum", "as_signal", "estimate_sparsity_and_solve", "exact_batch",
     "solve_iterative", "solve_iterative_batch", "solve_noniterative",
     "solve_noniterative_batch", "using_compiled", "CollisionEstimate", "GeneralBatch",
-    "GeneralConfig", "GeneralPlan", "GeneralTrace", "draw_shifts", "solve_general", "solve_general_batch",
+    "GeneralConfig", "GeneralPlan", "GeneralTrace", "draw_shifts", "estimate_collisions", "solve_general", "solve_general_batch",
 ]

@@ -81,6 +81,9 @@ EXPORTS = {
                                ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "sfdt_exact_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(ExactArgs)]),
     "sfdt_exact_solve": (_int, [ctypes.POINTER(ExactArgs), _vp, ctypes.c_size_t, _vp]),
+    "sfdt_estimate_collisions_workspace_bytes": (ctypes.c_size_t, [_i64]),
+    "sfdt_estimate_collisions": (_int, [_vp, _i64, _i64, _i64, _int, _i64, _dbl, _vp, _vp, _vp,
+                                        ctypes.c_size_t, _vp]),
     "sfdt_general_caps": (_int, [ctypes.POINTER(GeneralArgs), ctypes.POINTER(_i64)]),
     "sfdt_general_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(GeneralArgs)]),
     "sfdt_general_solve": (_int, [ctypes.POINTER(GeneralArgs), _vp, ctypes.c_size_t, _vp]),

@@ -61,6 +61,35 @@ __global__ void __launch_bounds__(128) k_gen_svd(const cx *__restrict__ V, GenPa
     if (threadIdx.x == 0) partial[b * gridDim.x + blockIdx.x] = (red[0] + red[1]) + (red[2] + red[3]);
 }
 
+// standalone form (estimate_collisions on given syndromes, general.py:131-155):
+// rows of a (nb, ld) row-major syndrome matrix; energy over all ld columns
+template <int AM>
+__global__ void __launch_bounds__(128) k_rows_svd(const cx *__restrict__ syn, int64_t nb, int64_t ld,
+                                                  double *__restrict__ sv, double *__restrict__ partial,
+                                                  double tol) {
+    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    double e = 0.0;
+    if (k < nb) {
+        cx m[2 * AM];
+#pragma unroll
+        for (int j = 0; j < 2 * AM - 1; j++) m[j] = ldcx(syn + k * ld + j);
+        for (int64_t j = 0; j < ld; j++) {
+            const cx v = ldcx(syn + k * ld + j);
+            e += v.re * v.re + v.im * v.im;
+        }
+        double s[AM];
+        hankel_sv_n<AM>(m, s, tol);
+#pragma unroll
+        for (int i = 0; i < AM; i++) sv[k * AM + i] = s[i];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+    __shared__ double red[4];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = e;
+    __syncthreads();
+    if (threadIdx.x == 0) partial[blockIdx.x] = (red[0] + red[1]) + (red[2] + red[3]);
+}
+
 // ------------------------------------------------------------------ vote
 __device__ __forceinline__ unsigned long long dkey(double v) {
     return (unsigned long long)__double_as_longlong(v);   // sigma >= 0: bit order == value order
@@ -649,5 +678,55 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     SFDT_CHECK_LAUNCH();
     launches += 6;
     a->kernel_launches = launches;
+    return SFDT_OK;
+}
+
+extern "C" size_t sfdt_estimate_collisions_workspace_bytes(int64_t nb) {
+    if (nb < 0) return 0;
+    const int64_t nparts = (nb + 127) / 128;
+    return size_t(nparts) * 8 + size_t(nb) * 8 + 64 + size_t(SFDT_GS_PER_SIGNAL) * 8 + 1024;
+}
+
+extern "C" int sfdt_estimate_collisions(const double *syn, int64_t nb, int64_t ld, int64_t k, int a_max,
+                                        int64_t d, double zero_vote_rtol, int32_t *votes, double *sv,
+                                        void *ws, size_t ws_bytes, sfdt_stream_t stream_) {
+    if (a_max < 1 || a_max > 4 || ld < 2 * a_max - 1 || nb < 0 || k < 1 || d < 1) return SFDT_EINVAL;
+    if (nb == 0) return SFDT_OK;
+    if (!ws || ws_bytes < sfdt_estimate_collisions_workspace_bytes(nb)) return SFDT_EWORKSPACE;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    const int64_t nparts = (nb + 127) / 128;
+    char *w = (char *)ws;
+    double *part = (double *)w;
+    int64_t *wl = (int64_t *)(w + ((nparts * 8 + 255) & ~int64_t(255)));
+    unsigned long long *wlc = (unsigned long long *)((char *)wl + nb * 8);
+    int64_t *stats = (int64_t *)((char *)wlc + 64);
+    // the reference runs the Jacobi with its 1e-17 threshold here: this is
+    // the kernel-level mirror of estimate_collisions
+    switch (a_max) {
+    case 1: k_rows_svd<1><<<(unsigned)nparts, 128, 0, stream>>>((const cx *)syn, nb, ld, sv, part, 1e-17); break;
+    case 2: k_rows_svd<2><<<(unsigned)nparts, 128, 0, stream>>>((const cx *)syn, nb, ld, sv, part, 1e-17); break;
+    case 3: k_rows_svd<3><<<(unsigned)nparts, 128, 0, stream>>>((const cx *)syn, nb, ld, sv, part, 1e-17); break;
+    default: k_rows_svd<4><<<(unsigned)nparts, 128, 0, stream>>>((const cx *)syn, nb, ld, sv, part, 1e-17); break;
+    }
+    SFDT_CHECK_LAUNCH();
+    GenParams gp;
+    gp.n = nb * d;
+    gp.d = d;
+    gp.L = nb;
+    gp.k = k;
+    gp.a_max = a_max;
+    gp.r_eff = 1;
+    gp.keep = 1;
+    gp.prune = 0;
+    gp.S = (int)ld;   // the RMS guard averages over every given column
+    gp.nv = (int)ld;
+    gp.zvr = zero_vote_rtol;
+    gp.shifts = nullptr;
+    gp.shift_stride = 0;
+    gp.base_phi = nullptr;
+    gp.phi_stride = 0;
+    cudaMemsetAsync(wlc, 0, 8, stream);
+    k_gen_vote<<<1, 1024, 0, stream>>>(sv, part, (int)nparts, gp, votes, stats, wl, wlc);
+    SFDT_CHECK_LAUNCH();
     return SFDT_OK;
 }

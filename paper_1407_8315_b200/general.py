@@ -242,3 +242,23 @@ def solve_general(x, cfg: GeneralConfig):
     tr = res.trace(0)
     tr.timings = {"total": time.perf_counter() - t0}
     return spec, tr
+
+
+def estimate_collisions(syndromes, k: int, a_max: int, d: int,
+                        zero_vote_rtol: float = 1e-9) -> CollisionEstimate:
+    """Per-bin collision counts via the top-k singular-value vote
+    (general.py:131-155), computed by the device kernels (Jacobi singular
+    values with the reference's threshold, exact radix-select vote)."""
+    syndromes = np.ascontiguousarray(syndromes, dtype=np.complex128)
+    nb, ld = syndromes.shape
+    dev = require_cuda()
+    lib = _lib.load()
+    sd = torch.from_numpy(syndromes).to(dev)
+    votes = torch.empty(nb, dtype=torch.int32, device=dev)
+    sv = torch.empty((nb, a_max), dtype=torch.float64, device=dev)
+    ws = Workspace.get(lib.sfdt_estimate_collisions_workspace_bytes(nb), dev)
+    _lib.check(lib.sfdt_estimate_collisions(sd.data_ptr(), nb, ld, int(k), int(a_max), int(d),
+                                            float(zero_vote_rtol), votes.data_ptr(), sv.data_ptr(),
+                                            ws.data_ptr(), ws.numel(), stream_handle(dev)),
+               "sfdt_estimate_collisions")
+    return CollisionEstimate(a=votes.cpu().numpy().astype(np.int64), singular_values=sv.cpu().numpy())

@@ -1,0 +1,157 @@
+"""GPU-backed single-bin API and kernel seam, checked with the reference's own
+known-answer tests (restated from /root/reference/pkg/tests/test_syndrome.py
+and test_spectral.py) and against the oracle."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1407_8315_b200 as P                      # noqa: E402
+from oracle import kernels as OK                       # noqa: E402
+from oracle import solvers as OS                       # noqa: E402
+from paper_1407_8315_b200 import kernels as K          # noqa: E402
+from paper_1407_8315_b200 import syndrome as SY        # noqa: E402
+
+
+def forward_syndromes(values, roots, count):
+    values = np.asarray(values, dtype=complex)
+    roots = np.asarray(roots, dtype=complex)
+    return np.array([np.sum(values * roots ** l) for l in range(count)])
+
+
+def match_roots(got, expect):
+    got = list(got)
+    worst = 0.0
+    for e in expect:
+        i = int(np.argmin([abs(g - e) for g in got]))
+        worst = max(worst, abs(got.pop(i) - e))
+    return worst
+
+
+def test_solve_coefficients_known_answers(rng):
+    m = forward_syndromes([2.0], [np.exp(0.5j)], 2)
+    assert abs(-SY.solve_coefficients(m, 1).c[0] - m[1] / m[0]) < 1e-14
+    m = forward_syndromes([1.0, 1.0], [1.0, -1.0], 4)
+    assert np.allclose(SY.solve_coefficients(m, 2).c, [-1.0, 0.0], atol=1e-14)
+    with pytest.raises(SY.NearSingular):
+        SY.solve_coefficients(forward_syndromes([1.0, 1.0], [1.0, 1.0], 4), 2)
+    for a in (2, 3, 4):
+        roots = np.exp(2j * np.pi * rng.random(a))
+        vals = rng.normal(size=a) + 1j * rng.normal(size=a)
+        c = SY.solve_coefficients(forward_syndromes(vals, roots, 2 * a), a).c
+        assert np.max(np.abs(c - np.poly(roots)[1:][::-1])) < 1e-9
+
+
+def test_roots_known_answers(rng):
+    roots = SY.roots_closed_form(SY.PolyCoefficients(2, np.array([1j, -(1 + 1j)])))
+    assert match_roots(roots, [1.0, 1.0j]) < 1e-12
+    expect = np.array([1.0, -1.0, 1.0j])
+    roots = SY.roots_closed_form(SY.PolyCoefficients(3, np.poly(expect)[1:][::-1]))
+    assert match_roots(roots, expect) < 1e-12
+    pool = np.exp(2j * np.pi * np.arange(8) / 8)
+    for _ in range(50):
+        expect = rng.choice(pool, size=4, replace=False)
+        roots = SY.roots_closed_form(SY.PolyCoefficients(4, np.poly(expect)[1:][::-1]))
+        assert match_roots(roots, expect) < 1e-8
+    for a in (2, 3, 4):
+        for _ in range(100):
+            expect = np.exp(2j * np.pi * rng.random(a))
+            c = np.poly(expect)[1:][::-1]
+            roots = SY.roots_closed_form(SY.PolyCoefficients(a, c))
+            assert SY.poly_residuals(c[None, :], roots[None, :]).max() <= 1e-8 * max(1.0, np.abs(c).max())
+
+
+def test_values_and_locations():
+    m = forward_syndromes([3.0 + 1j], [np.exp(0.3j)], 2)
+    assert abs(SY.solve_values(m, [np.exp(0.3j)])[0] - m[0]) < 1e-14
+    m = np.array([2.0, 0.0, 2.0, 0.0], dtype=complex)
+    assert np.allclose(SY.solve_values(m, [1.0, -1.0]), [1.0, 1.0], atol=1e-14)
+    with pytest.raises(SY.IllConditioned):
+        SY.solve_values(np.array([2.0, 2.0, 2.0, 2.0]), [1.0, 1.0])
+    assert SY.root_to_location(1.0 + 0j, 8) == (0, 0.0)
+    loc, err = SY.root_to_location(np.exp(1.25j * np.pi), 8)
+    assert loc == 5 and err < 1e-12
+    with pytest.raises(ValueError):
+        SY.root_to_location(0j, 8)
+
+
+def test_decode_bin_round_trip_and_rejection(rng):
+    for _ in range(60):
+        n = int(rng.choice([64, 256, 1024]))
+        d = int(rng.choice([2, 4, 8, 16]))
+        m_len = n // d
+        a = int(rng.integers(1, min(4, d) + 1))
+        k = int(rng.integers(0, m_len))
+        locs = (k + rng.choice(d, size=a, replace=False) * m_len) % n
+        vals = rng.normal(size=a) + 1j * rng.normal(size=a)
+        dec = SY.decode_bin(forward_syndromes(vals, np.exp(2j * np.pi * locs / n), 2 * a), a, n, d, k)
+        assert dec.membership and sorted(dec.locations) == sorted(locs)
+        got = {int(s): v for s, v in zip(dec.locations, dec.values)}
+        for s, v in zip(locs, vals):
+            assert abs(got[int(s)] - v) <= 1e-7 * abs(v)
+    n, d = 4096, 16
+    rejected, trials = 0, 500
+    for _ in range(trials):
+        a = int(rng.integers(1, 4))
+        a_true = int(rng.integers(a + 1, 5))
+        k = int(rng.integers(0, n // d))
+        locs = (k + rng.choice(d, size=a_true, replace=False) * (n // d)) % n
+        vals = rng.normal(size=a_true) + 1j * rng.normal(size=a_true)
+        m = forward_syndromes(vals, np.exp(2j * np.pi * locs / n), 2 * a)
+        try:
+            dec = SY.decode_bin(m, a, n, d, k)
+        except (SY.NearSingular, SY.IllConditioned, SY.DegenerateBranch):
+            rejected += 1
+            continue
+        if not dec.membership or dec.snap_error > 0.25:
+            rejected += 1
+    assert rejected / trials >= 0.99
+
+
+def test_kernel_seam_matches_oracle(rng):
+    for n in (1, 2, 64, 1024, 1 << 14):
+        x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+        assert np.array_equal(K.fft_radix2(x).view(np.uint64), OK.fft_radix2(x).view(np.uint64))
+    with pytest.raises(ValueError):
+        K.fft_radix2(np.zeros(12))
+    for a in (1, 2, 3, 4):
+        m = rng.standard_normal((64, 8)) + 1j * rng.standard_normal((64, 8))
+        c, cd = K.hankel_solve(m, a)
+        c2, cd2 = OK.hankel_solve(m, a)
+        assert np.array_equal(c.view(np.uint64), c2.view(np.uint64))
+        assert np.array_equal(cd.view(np.uint64), cd2.view(np.uint64))
+        p, pd = K.vandermonde_solve(c2[:, :a] if a > 0 else c2, m)
+        p2, pd2 = OK.vandermonde_solve(c2[:, :a], m)
+        assert np.array_equal(p.view(np.uint64), p2.view(np.uint64))
+        sv = K.hankel_singular_values(m, a)
+        assert np.allclose(sv, OK.hankel_singular_values(m, a), rtol=1e-12, atol=0)
+        kb = rng.integers(0, 64, 64)
+        assert np.allclose(K.prune_eval(c2, kb, 4096, 64), OK.prune_eval(c2, kb, 4096, 64),
+                           rtol=1e-12, atol=1e-300)
+    with pytest.raises(ValueError):
+        K.hankel_solve(np.zeros((2, 3), complex), 2)
+
+
+def test_estimate_collisions_matches_oracle():
+    from tests.synth import general_signal
+    n, k = 1 << 16, 64
+    x, _ = general_signal(n, k, 20.0, 3)
+    _, tr = OS.general(x, k, return_internals=True)
+    syn = tr["consecutive"].T
+    d = n // syn.shape[0]
+    est = P.estimate_collisions(syn, k, 3, d)
+    votes, sv = OS.collision_votes(OK, syn, k, 3, d)
+    assert np.array_equal(est.a, votes)
+    assert np.allclose(est.singular_values, sv, rtol=1e-12, atol=0)
+    # ties and the zero-vote guard: an exactly sparse input gives exact-zero
+    # singular values on empty bins
+    from tests.synth import exact_signal
+    xe, _ = exact_signal(4096, 8, 1, "unit")
+    views = np.stack([OS.shifted_view(OK, xe, 64, j) for j in range(6)]).T
+    est = P.estimate_collisions(views, 8, 3, 64)
+    votes, _ = OS.collision_votes(OK, views, 8, 3, 64)
+    assert np.array_equal(est.a, votes)

@@ -155,3 +155,52 @@ def test_estimate_collisions_matches_oracle():
     est = P.estimate_collisions(views, 8, 3, 64)
     votes, _ = OS.collision_votes(OK, views, 8, 3, 64)
     assert np.array_equal(est.a, votes)
+
+
+def test_exact_grid_matches_oracle():
+    from paper_1407_8315_b200 import experiments as E
+    from tests.synth import exact_signal
+    rep = E.run_exact_grid(4096, [16, 64], trials=4, solver="iterative", seed=3)
+    assert len(rep.rows) == 8
+    for row in rep.rows:
+        k = row["k"]
+        t = eval(row["seed"])[2]
+        x, truth = exact_signal(4096, k, (3, k, t), "unit", synth="radix2")
+        want, wtr = OS.exact_iterative(x, k)
+        correct = sum(1 for s, v in truth.items() if s in want and abs(want[s] - v) <= 1e-7 * abs(v))
+        spurious = len(set(want) - set(truth))
+        assert row["perfect"] == int(correct == k and spurious == 0)
+        assert row["full_success"] == int(wtr["full_success"])
+        assert row["fft_samples"] == wtr["fft_samples"]
+        assert row["recovered_fraction"] == (4096 - (k - correct) - spurious) / 4096
+
+
+def test_general_grid_matches_oracle():
+    from paper_1407_8315_b200 import experiments as E
+    n, nk, snr_db = 4096, 64, 20
+    rep = E.run_general_grid(n, [nk], [snr_db], trials=3, seed=1)
+    k = n // nk
+    for row in rep.rows:
+        seed = eval(row["seed"])
+        rng = np.random.default_rng(seed)
+        on = rng.random(n) < k / n
+        s_off = E.sigma_off_for_snr(n, k, snr_db)
+        sigma = np.where(on, 1.0, s_off)
+        full = sigma * ((1.0 / np.sqrt(2.0)) * (rng.standard_normal(n) + 1j * rng.standard_normal(n)))
+        x = OK.fft_radix2(full, True)
+        for label, prune in (("prune", True), ("noprune", False)):
+            want, _ = OS.general(x, k, rng_seed=seed, prune=prune)
+            dense = np.zeros(n, complex)
+            for s_, v in want.items():
+                dense[s_] = v
+            err = np.mean(np.abs(full - dense) ** 2)
+            snr_out = 10 * np.log10(np.mean(np.abs(dense) ** 2) / err)
+            assert abs(row[f"snr_out_db_{label}"] - snr_out) <= 1e-9 * max(1.0, abs(snr_out))
+
+
+def test_collision_census():
+    from paper_1407_8315_b200 import experiments as E
+    res = E.run_collision_census(1 << 12, 16, [4, 8], trials=50, seed=0)
+    for n_plus, r in res.items():
+        assert abs(r["per_bin_probability"].sum() - 1.0) < 1e-12
+        assert r["d"] == (1 << 12) // n_plus // 16

@@ -30,13 +30,16 @@ namespace sfdt {
 // complex128, 16 B for complex64 storage -- the measured best shape on B200
 // (tools/membw.cu: 7.55 TB/s pure read).  The shift windows are not touched
 // here: the FFT kernel gathers them straight from x.
-template <int C64, int THREADS, int UNROLL>
+template <int C64, int THREADS, int UNROLL, int CAP = 0>
 __global__ void __launch_bounds__(THREADS) k_sumsq(const void *__restrict__ x_, int64_t n, int64_t CH,
-                                                  double *__restrict__ partial) {
+                                                  double *__restrict__ partial,
+                                                  cx *__restrict__ win = nullptr, int logd = 0,
+                                                  int S = 0) {
     const int64_t b = blockIdx.y;
     const int64_t chunk = blockIdx.x;
     const int64_t CHp = CH >> 1;                        // sample pairs in this chunk
     const int64_t base = (b * n + chunk * CH) >> 1;     // pair index
+    const int64_t L = n >> logd;
     double acc = 0.0;
     for (int64_t off = 0; off < CHp; off += int64_t(THREADS) * UNROLL) {
         double v[UNROLL][4];
@@ -58,8 +61,21 @@ __global__ void __launch_bounds__(THREADS) k_sumsq(const void *__restrict__ x_, 
             }
         }
 #pragma unroll
-        for (int u = 0; u < UNROLL; u++)
+        for (int u = 0; u < UNROLL; u++) {
             acc = fma(v[u][0], v[u][0], fma(v[u][1], v[u][1], fma(v[u][2], v[u][2], fma(v[u][3], v[u][3], acc))));
+            if (CAP) {
+                // shift windows: element e = d*j + s with s < S (S <= d) goes
+                // to the view-major window buffer win[b][s][j]
+                const int64_t e = chunk * CH + 2 * (off + int64_t(u) * THREADS + threadIdx.x);
+                const int64_t s0 = e & ((int64_t(1) << logd) - 1);
+                if (s0 < S && e < (chunk + 1) * CH) {
+                    const int64_t j = e >> logd;
+                    cx *wb = win + b * S * L + j;
+                    wb[s0 * L] = mk(v[u][0], v[u][1]);
+                    if (s0 + 1 < S) wb[(s0 + 1) * L] = mk(v[u][2], v[u][3]);
+                }
+            }
+        }
     }
     // deterministic block reduction: warp xor-tree, then fixed-order smem tree
 #pragma unroll
@@ -770,10 +786,21 @@ static inline size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
 struct ExactPlan {
     int64_t B, n, d, L, S, CH, nchunk, npass;
     int logd;
-    size_t off_V, off_partial, off_thr, off_status, off_bloc, off_bval, off_def,
+    bool capture;
+    size_t off_win, off_V, off_partial, off_thr, off_status, off_bloc, off_bval, off_def,
         off_sloc, off_sval, off_sa, off_sdup, off_cnt, off_resid, off_ndef, off_scratch, off_fft, off_wl,
         total;
 };
+
+// SFDT_CAPTURE=1 captures the shift windows inside the stream pass (the FFT
+// then reads contiguous window rows) instead of gathering them from x.
+// Measured on B200 at config 2: +0.64 ms in the stream kernel (16-byte
+// scattered window stores become partial-sector read-modify-writes in L2)
+// against -0.04 ms in the FFT, so the gather is the default.
+static bool capture_enabled() {
+    const char *e = getenv("SFDT_CAPTURE");
+    return e && e[0] == '1';
+}
 
 static int make_plan(const sfdt_exact_args *a, ExactPlan &p) {
     if (!a || a->batch < 1 || a->n < 2 || (a->n & (a->n - 1))) return SFDT_EINVAL;
@@ -809,6 +836,8 @@ static int make_plan(const sfdt_exact_args *a, ExactPlan &p) {
         p.off_resid = take(size_t(p.B) * 8);
         p.off_ndef = take(size_t(p.B) * 8);
     }
+    p.capture = (!a->iterative && !a->aux_stream && p.d >= p.S && capture_enabled());
+    p.off_win = p.capture ? take(size_t(p.B) * p.S * p.L * 16) : 0;
     p.off_scratch = take(64 * 8);
     p.off_fft = (p.L > FFT_SMEM_MAX) ? take(size_t(p.B) * p.L * p.S * 16) : 0;
     p.total = o;
@@ -883,10 +912,20 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
             }
         } else {
             constexpr int TH = 512, UN = 4;
-            if (is_c64)
-                k_sumsq<1, TH, UN><<<grid, TH, 0, stream>>>(xc, p.n, p.CH, partial + c0 * p.nchunk);
-            else
-                k_sumsq<0, TH, UN><<<grid, TH, 0, stream>>>(xc, p.n, p.CH, partial + c0 * p.nchunk);
+            cx *win = p.capture ? (cx *)(w + p.off_win) + c0 * p.S * p.L : nullptr;
+            if (is_c64) {
+                if (p.capture)
+                    k_sumsq<1, TH, UN, 1><<<grid, TH, 0, stream>>>(xc, p.n, p.CH, partial + c0 * p.nchunk,
+                                                                  win, p.logd, (int)p.S);
+                else
+                    k_sumsq<1, TH, UN><<<grid, TH, 0, stream>>>(xc, p.n, p.CH, partial + c0 * p.nchunk);
+            } else {
+                if (p.capture)
+                    k_sumsq<0, TH, UN, 1><<<grid, TH, 0, stream>>>(xc, p.n, p.CH, partial + c0 * p.nchunk,
+                                                                  win, p.logd, (int)p.S);
+                else
+                    k_sumsq<0, TH, UN><<<grid, TH, 0, stream>>>(xc, p.n, p.CH, partial + c0 * p.nchunk);
+            }
         }
         SFDT_CHECK_LAUNCH();
         launches += 1;
@@ -921,13 +960,18 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
         }
         for (int64_t c = 0; c < nc; c++) {
             const int64_t c0 = c * bc, nb = (c0 + bc <= p.B) ? bc : p.B - c0;
-            // the views need no rms: their gather + FFT (aux) overlaps the
-            // HBM stream of the same chunk (main)
-            const ViewSrc src = consecutive_views((const char *)a->x + c0 * p.n * (is_c64 ? 8 : 16),
-                                                  is_c64, p.n, p.d, 0, (int)p.S);
-            rc = launch_fft_views(src, nb, p.L, a->twiddles, V + c0 * p.S * p.L, (int)p.S, p.L, aux,
-                                  fft_scratch ? fft_scratch + c0 * p.S * p.L : nullptr);
-            if (rc) return rc;
+            // without window capture the views need no rms: their gather + FFT
+            // (aux) overlaps the HBM stream of the same chunk (main); with
+            // capture the FFT reads the windows the stream pass wrote
+            auto launch_fft = [&]() -> int {
+                const ViewSrc src = p.capture
+                    ? window_views((const cx *)(w + p.off_win) + c0 * p.S * p.L, (int)p.S, p.L)
+                    : consecutive_views((const char *)a->x + c0 * p.n * (is_c64 ? 8 : 16), is_c64,
+                                        p.n, p.d, 0, (int)p.S);
+                return launch_fft_views(src, nb, p.L, a->twiddles, V + c0 * p.S * p.L, (int)p.S, p.L,
+                                        aux, fft_scratch ? fft_scratch + c0 * p.S * p.L : nullptr);
+            };
+            if (!p.capture && (rc = launch_fft())) return rc;
             if ((rc = launch_stream(c0, nb))) return rc;
             if (c == nc - 1 && a->ev_stream_end) cudaEventRecord((cudaEvent_t)a->ev_stream_end, stream);
             if (aux != stream) {
@@ -937,6 +981,7 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
                 cudaStreamWaitEvent(aux, ev, 0);
                 cudaEventDestroy(ev);
             }
+            if (p.capture && (rc = launch_fft())) return rc;
             k_rms<<<(unsigned)nb, 1024, 0, aux>>>(partial + c0 * p.nchunk, p.nchunk, p.n,
                                                   a->zero_threshold, p.d, a->rms + c0, thr + c0);
             SFDT_CHECK_LAUNCH();

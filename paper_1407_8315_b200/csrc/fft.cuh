@@ -35,6 +35,7 @@ struct ViewSrc {
     const int64_t *dyn_off;
     int dyn_first;
     int64_t dyn_stride;
+    int jfast;           // 1: lanes walk j (contiguous rows), 0: lanes walk the views
 };
 
 __device__ __forceinline__ cx view_load(const ViewSrc &src, int64_t b, int v, int64_t j) {
@@ -130,7 +131,8 @@ static __global__ void __launch_bounds__(256) k_fft_views(const ViewSrc src, int
     // gather: lanes vary the view (shift) fastest for one sample j, so one
     // d-block's adjacent shifts share sectors; bit-reversed scatter to smem
     for (int i = threadIdx.x; i < (L << logvpc); i += blockDim.x) {
-        const int v = i & (vpc - 1), j = i >> logvpc;
+        const int v = src.jfast ? (i >> logL) : (i & (vpc - 1));
+        const int j = src.jfast ? (i & (L - 1)) : (i >> logvpc);
         if (v >= nv) continue;
         const int64_t g = g0 + v;
         const int64_t b = g / src.nshift;
@@ -280,6 +282,16 @@ static inline ViewSrc consecutive_views(const void *x, int is_c64, int64_t n, in
     s.dyn_off = nullptr;
     s.dyn_first = MAX_VIEWS;
     s.dyn_stride = 0;
+    s.jfast = 0;
+    return s;
+}
+
+// views stored view-major as rows of a (B, S, L) window buffer
+static inline ViewSrc window_views(const cx *win, int S, int64_t L) {
+    ViewSrc s = consecutive_views(win, 0, (int64_t)S * L, 1, 0, S);
+    for (int v = 0; v < MAX_VIEWS; v++) s.off[v] = (v < S) ? (int64_t)v * L : 0;
+    s.wrap = -1;
+    s.jfast = 1;
     return s;
 }
 

@@ -11,7 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsfdt_b200.so")
+LIB_PATH = os.environ.get("SFDT_LIB") or os.path.join(_HERE, "libsfdt_b200.so")
 
 SFDT_ST_NITER = 0
 SFDT_ST_FULL_SUCCESS = 1

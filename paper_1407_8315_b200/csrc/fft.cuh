@@ -21,6 +21,9 @@
 namespace sfdt {
 
 constexpr int MAX_VIEWS = 24;
+#ifndef SFDT_FFT_MINB
+#define SFDT_FFT_MINB 4
+#endif
 
 struct ViewSrc {
     const void *x;
@@ -119,7 +122,7 @@ __device__ __forceinline__ void fft_stages_smem(cx *a, int nv, int logL, int lh0
     }
 }
 
-static __global__ void __launch_bounds__(256) k_fft_views(const ViewSrc src, int64_t B, int logL, int logvpc,
+static __global__ void __launch_bounds__(256, SFDT_FFT_MINB) k_fft_views(const ViewSrc src, int64_t B, int logL, int logvpc,
                                    const cx *__restrict__ tw, cx *__restrict__ out, int SV,
                                    int64_t ldV, int scale) {
     extern __shared__ double4 smem_raw[];
@@ -227,6 +230,11 @@ static __global__ void k_fft_large_b(cx *buf, int64_t nviews, int logL, int logP
     }
 }
 
+static inline int fft_points_per_cta() {
+    const char *e = getenv("SFDT_FFT_PTS");
+    return e ? atoi(e) : 2048;
+}
+
 // FFT of every view of B signals; large_scratch (B*nshift*L complex) is
 // needed only when L > FFT_SMEM_MAX.
 static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, const double *tw_,
@@ -238,7 +246,7 @@ static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, con
     if (nviews == 0) return SFDT_OK;
     if (L <= FFT_SMEM_MAX) {
         int logvpc = 0;
-        while ((L << (logvpc + 1)) <= 4096 && (1 << (logvpc + 1)) <= 2 * src.nshift) logvpc++;
+        while ((L << (logvpc + 1)) <= fft_points_per_cta() && (1 << (logvpc + 1)) <= 2 * src.nshift) logvpc++;
         const size_t smem = (size_t(L) << logvpc) * 16;
         if (smem > 48 * 1024)
             cudaFuncSetAttribute(k_fft_views, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -474,6 +474,77 @@ SFDT_HD cx vandermonde_solve1(const cx *z, const cx *m, int a, cx *p)
     return det;
 }
 
+// Compile-time-degree forms (registers instead of local memory); same
+// operation order as the runtime forms above.
+template <int A>
+SFDT_HD cx det_t(const cx *a) {
+    if constexpr (A == 1) return a[0];
+    else if constexpr (A == 2) return det2(a[0], a[1], a[2], a[3]);
+    else if constexpr (A == 3) return det3(a);
+    else return det4(a);
+}
+
+template <int A>
+SFDT_HD cx hankel_solve_t(const cx *m, cx *c) {
+    cx hank[A * A], work[A * A];
+#pragma unroll
+    for (int i = 0; i < A; i++)
+#pragma unroll
+        for (int j = 0; j < A; j++) hank[A * i + j] = m[i + j];
+    const cx det = det_t<A>(hank);
+#pragma unroll
+    for (int j = 0; j < A; j++) c[j] = mk(0.0, 0.0);
+    if (cis_zero(det)) return det;
+#pragma unroll
+    for (int col = 0; col < A; col++) {
+#pragma unroll
+        for (int i = 0; i < A; i++)
+#pragma unroll
+            for (int j = 0; j < A; j++) work[A * i + j] = (j == col) ? cneg(m[A + i]) : hank[A * i + j];
+        c[col] = gdiv(det_t<A>(work), det);
+    }
+    return det;
+}
+
+template <int A>
+SFDT_HD cx vandermonde_solve_t(const cx *z, const cx *m, cx *p) {
+    cx vand[A * A], work[A * A];
+#pragma unroll
+    for (int j = 0; j < A; j++) {
+        cx acc = mk(1.0, 0.0);
+#pragma unroll
+        for (int i = 0; i < A; i++) {
+            vand[A * i + j] = acc;
+            acc = gmul(acc, z[j]);
+        }
+    }
+    cx det = mk(1.0, 0.0);
+#pragma unroll
+    for (int i = 0; i < A; i++)
+#pragma unroll
+        for (int j = i + 1; j < A; j++) det = gmul(det, csub(z[j], z[i]));
+#pragma unroll
+    for (int j = 0; j < A; j++) p[j] = mk(0.0, 0.0);
+    if (cis_zero(det)) return det;
+#pragma unroll
+    for (int col = 0; col < A; col++) {
+#pragma unroll
+        for (int i = 0; i < A; i++)
+#pragma unroll
+            for (int j = 0; j < A; j++) work[A * i + j] = (j == col) ? m[i] : vand[A * i + j];
+        p[col] = gdiv(det_t<A>(work), det);
+    }
+    return det;
+}
+
+template <int A>
+SFDT_HD void poly_roots_t(const cx *c, cx *z) {
+    if constexpr (A == 1) z[0] = cneg(c[0]);
+    else if constexpr (A == 2) quad_pair(c[1], c[0], &z[0], &z[1]);
+    else if constexpr (A == 3) roots3(c[0], c[1], c[2], z);
+    else roots4(c[0], c[1], c[2], c[3], z);
+}
+
 // NaN-propagating max (numpy np.max / np.maximum semantics)
 SFDT_HD double nanmax2(double a, double b)
 {

@@ -106,4 +106,81 @@ __host__ __device__ __forceinline__ void decode_try(const cx *syn, int S, int a,
     o.retryable = !ok;
 }
 
+// decode_try with the collision count a compile-time constant: every array
+// is register-resident (the runtime-a form keeps its Cramer work matrices in
+// local memory).  Same arithmetic, same predicates.
+template <int A, int S>
+__host__ __device__ __forceinline__ void decode_try_t(const cx *syn, int64_t n, int64_t m, int64_t bin,
+                                                      Decoded &o) {
+    double scale = 0.0;
+#pragma unroll
+    for (int l = 0; l < 2 * A; l++) scale = nanmax2(scale, cabs_(syn[l]));
+    scale = nanmax2(scale, TINY);
+    cx *roots = o.root;
+    cx *vals = o.val;
+    bool ok;
+    if constexpr (A == 1) {
+        ok = cabs_(syn[0]) > DMUL(SINGULARITY_RTOL, scale);
+        roots[0] = ok ? ndiv(syn[1], syn[0]) : mk(0.0, 0.0);
+        vals[0] = syn[0];
+    } else {
+        cx c[A];
+        const cx cd = hankel_solve_t<A>(syn, c);
+        ok = cabs_(cd) > DMUL(SINGULARITY_RTOL, powa(scale, A));
+        poly_roots_t<A>(c, roots);
+        double cmax = 0.0, resid = 0.0;
+#pragma unroll
+        for (int j = 0; j < A; j++) cmax = nanmax2(cmax, cabs_(c[j]));
+#pragma unroll
+        for (int r = 0; r < A; r++) {
+            cx acc = mk(1.0, 0.0);
+#pragma unroll
+            for (int j = A - 1; j >= 0; j--) acc = cadd(nmul(acc, roots[r]), c[j]);
+            resid = (r == 0) ? cabs_(acc) : nanmax2(resid, cabs_(acc));
+        }
+        ok = ok && (resid <= DMUL(1e-8, nanmax2(1.0, cmax)));
+        const cx pd = vandermonde_solve_t<A>(roots, syn, vals);
+        double zmax = 0.0;
+#pragma unroll
+        for (int j = 0; j < A; j++) zmax = (j == 0) ? cabs_(roots[0]) : nanmax2(zmax, cabs_(roots[j]));
+        ok = ok && (cabs_(pd) > DMUL(SINGULARITY_RTOL, powa(nanmax2(1.0, zmax), A)));
+    }
+    double snap = 0.0, circ = 0.0;
+#pragma unroll
+    for (int j = 0; j < A; j++) {
+        const double pos = DMUL(atan2(roots[j].im, roots[j].re), (double)n) / TWO_PI;
+        const double sn = rint(pos);
+        const double e = fabs(DSUB(pos, sn));
+        snap = (j == 0) ? e : nanmax2(snap, e);
+        o.loc[j] = isfinite(sn) ? pmod((int64_t)sn, n) : INT64_MIN;
+        const double ce = fabs(DSUB(cabs_(roots[j]), 1.0));
+        circ = (j == 0) ? ce : nanmax2(circ, ce);
+    }
+    bool member = true, distinct = true;
+#pragma unroll
+    for (int j = 0; j < A; j++) {
+        member = member && (o.loc[j] != INT64_MIN) && ((o.loc[j] & (m - 1)) == bin);
+#pragma unroll
+        for (int i = 0; i < j; i++) distinct = distinct && (o.loc[i] != o.loc[j]);
+    }
+    cx power[A], terms[A];
+#pragma unroll
+    for (int j = 0; j < A; j++) power[j] = mk(1.0, 0.0);
+    double err = 0.0, smax = 0.0;
+#pragma unroll
+    for (int l = 0; l < S; l++) {
+#pragma unroll
+        for (int j = 0; j < A; j++) terms[j] = nmul(vals[j], power[j]);
+        const cx rec = npsum(terms, A);
+        const double e = cabs_(csub(rec, syn[l]));
+        err = (l == 0) ? e : nanmax2(err, e);
+        smax = (l == 0) ? cabs_(syn[0]) : nanmax2(smax, cabs_(syn[l]));
+#pragma unroll
+        for (int j = 0; j < A; j++) power[j] = nmul(power[j], roots[j]);
+    }
+    const bool consistent = err <= DMUL(CONSISTENCY_RTOL, nanmax2(smax, TINY));
+    o.accept = ok && member && distinct && consistent && (circ <= UNIT_MODULUS_TOL) && (snap <= SNAP_TOL);
+    o.retryable = !ok;
+}
+
 }  // namespace sfdt

@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(128) k_decode_a1(const cx *__restrict__ V, int
         uint8_t st = 0;
         if (active) {
             Decoded o;
-            decode_try(syn, S, 1, n, L, k, o);
+            decode_try_t<1, S>(syn, n, L, k, o);
             if (o.accept) {
                 st = 1;
                 bin_loc[t * a_max] = o.loc[0];
@@ -232,8 +232,14 @@ __global__ void __launch_bounds__(128) k_decode_a1(const cx *__restrict__ V, int
     }
 }
 
+#ifndef SFDT_MULTI_TEMPLATED
+#define SFDT_MULTI_TEMPLATED 1
+#endif
+#ifndef SFDT_MULTI_MINB
+#define SFDT_MULTI_MINB 4
+#endif
 template <int S>
-__global__ void __launch_bounds__(128) k_decode_multi(const cx *__restrict__ V, int64_t L, int a_max,
+__global__ void __launch_bounds__(128, SFDT_MULTI_MINB) k_decode_multi(const cx *__restrict__ V, int64_t L, int a_max,
                                                       int64_t n, uint8_t *__restrict__ status,
                                                       int64_t *__restrict__ bin_loc,
                                                       cx *__restrict__ bin_val,
@@ -250,7 +256,13 @@ __global__ void __launch_bounds__(128) k_decode_multi(const cx *__restrict__ V, 
         uint8_t st = 0xFF;
         Decoded o;
         for (int a = 2; a <= a_max; a++) {
+#if SFDT_MULTI_TEMPLATED
+            if (a == 2) decode_try_t<2, S>(syn, n, L, k, o);
+            else if (a == 3) decode_try_t<3, S>(syn, n, L, k, o);
+            else decode_try_t<4, S>(syn, n, L, k, o);
+#else
             decode_try(syn, S, a, n, L, k, o);
+#endif
             if (o.accept) {
                 st = (uint8_t)a;
                 for (int j = 0; j < a; j++) {

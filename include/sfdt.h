@@ -66,6 +66,7 @@ enum {
 };
 
 const char *sfdt_strerror(int code);
+const char *sfdt_last_cuda_error(void); /* cudaGetErrorString of the sticky/last CUDA error */
 int sfdt_version(void);
 
 /* Host helper: the twiddle table the reference's radix-2 recurrence produces

@@ -70,6 +70,7 @@ class GeneralArgs(ctypes.Structure):
 EXPORTS = {
     "sfdt_strerror": (ctypes.c_char_p, [_int]),
     "sfdt_version": (_int, []),
+    "sfdt_last_cuda_error": (ctypes.c_char_p, []),
     "sfdt_fft_twiddles": (_int, [_i64, _int, _vp]),
     "sfdt_fft_radix2": (_int, [_vp, _vp, _i64, _i64, _int, _vp, _vp]),
     "sfdt_hankel_solve": (_int, [_vp, _i64, _i64, _int, _vp, _vp, _vp]),
@@ -118,4 +119,6 @@ def check(rc: int, what: str):
         msg = load().sfdt_strerror(rc).decode()
         if rc == -1:
             raise ValueError(f"{what}: {msg}")
+        if rc == -2:
+            msg += f" [{load().sfdt_last_cuda_error().decode()}]"
         raise SfdtError(f"{what}: {msg} ({rc})")

@@ -91,6 +91,8 @@ __global__ void __launch_bounds__(128) k_rows_svd(const cx *__restrict__ syn, in
 }
 
 // ------------------------------------------------------------------ vote
+constexpr int VOTE_SMEM_KEYS = 0;   // staging keys in smem measured slower (736 vs 552 us, cfg4); off
+
 __device__ __forceinline__ unsigned long long dkey(double v) {
     return (unsigned long long)__double_as_longlong(v);   // sigma >= 0: bit order == value order
 }
@@ -104,13 +106,19 @@ __global__ void __launch_bounds__(1024) k_gen_vote(const double *__restrict__ sv
     const int64_t b = blockIdx.x;
     const int64_t M = p.L * p.a_max;
     const int64_t take = p.k < M ? p.k : M;
-    const double *svb = sv + b * M;
+    extern __shared__ double s_keys[];
+    // the radix passes re-read every key 8 times: stage them in shared
+    // memory when they fit (config 4: 12288 keys = 96 KiB)
+    const bool in_smem = M <= VOTE_SMEM_KEYS;
+    if (in_smem)
+        for (int64_t i = threadIdx.x; i < M; i += blockDim.x) s_keys[i] = sv[b * M + i];
+    const double *svb = in_smem ? s_keys : sv + b * M;
     int32_t *vb = votes + b * p.L;
     __shared__ unsigned int hist[256];
     __shared__ unsigned long long s_prefix, s_mask;
     __shared__ long long s_remaining;
     __shared__ int wsum[32];
-    __shared__ long long s_hist[5], s_nvoted;
+    __shared__ long long s_hist[5];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
         s_prefix = 0;
@@ -118,7 +126,6 @@ __global__ void __launch_bounds__(1024) k_gen_vote(const double *__restrict__ sv
         s_remaining = take;
     }
     if (threadIdx.x < 5) s_hist[threadIdx.x] = 0;
-    if (threadIdx.x == 0) s_nvoted = 0;
     for (int64_t i = threadIdx.x; i < p.L; i += blockDim.x) vb[i] = 0;
     __syncthreads();
     // exact radix select (8-bit digits, MSB first) of the take-th largest key
@@ -662,7 +669,13 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     }
     SFDT_CHECK_LAUNCH();
     cudaMemsetAsync(wlc, 0, 8, stream);
-    k_gen_vote<<<(unsigned)p.B, 1024, 0, stream>>>(sv, part, (int)p.nparts, gp, votes, a->stats, wl, wlc);
+    {
+        const int64_t M = p.L * a->a_max;
+        const size_t smem = M <= VOTE_SMEM_KEYS ? size_t(M) * 8 : 0;
+        cudaFuncSetAttribute(k_gen_vote, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_gen_vote<<<(unsigned)p.B, 1024, smem, stream>>>(sv, part, (int)p.nparts, gp, votes, a->stats,
+                                                          wl, wlc);
+    }
     SFDT_CHECK_LAUNCH();
     // 3-4. pruning + subspace pursuit per voted bin
     int dev = 0, sms = 148;
@@ -726,7 +739,12 @@ extern "C" int sfdt_estimate_collisions(const double *syn, int64_t nb, int64_t l
     gp.base_phi = nullptr;
     gp.phi_stride = 0;
     cudaMemsetAsync(wlc, 0, 8, stream);
-    k_gen_vote<<<1, 1024, 0, stream>>>(sv, part, (int)nparts, gp, votes, stats, wl, wlc);
+    {
+        const int64_t M = nb * a_max;
+        const size_t smem = M <= VOTE_SMEM_KEYS ? size_t(M) * 8 : 0;
+        cudaFuncSetAttribute(k_gen_vote, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_gen_vote<<<1, 1024, smem, stream>>>(sv, part, (int)nparts, gp, votes, stats, wl, wlc);
+    }
     SFDT_CHECK_LAUNCH();
     return SFDT_OK;
 }

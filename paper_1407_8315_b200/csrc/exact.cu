@@ -64,15 +64,15 @@ __global__ void __launch_bounds__(THREADS) k_sumsq(const void *__restrict__ x_, 
         for (int u = 0; u < UNROLL; u++) {
             acc = fma(v[u][0], v[u][0], fma(v[u][1], v[u][1], fma(v[u][2], v[u][2], fma(v[u][3], v[u][3], acc))));
             if (CAP) {
-                // shift windows: element e = d*j + s with s < S (S <= d) goes
-                // to the view-major window buffer win[b][s][j]
+                // shift windows: the S samples x[d*j .. d*j+S-1] opening each
+                // d-block are copied as one contiguous row win[b][j][0..S-1]
+                // (S*16 = 128 B: four adjacent lanes store a full line, so no
+                // partial-sector read-modify-write in L2)
                 const int64_t e = chunk * CH + 2 * (off + int64_t(u) * THREADS + threadIdx.x);
                 const int64_t s0 = e & ((int64_t(1) << logd) - 1);
                 if (s0 < S && e < (chunk + 1) * CH) {
-                    const int64_t j = e >> logd;
-                    cx *wb = win + b * S * L + j;
-                    wb[s0 * L] = mk(v[u][0], v[u][1]);
-                    if (s0 + 1 < S) wb[(s0 + 1) * L] = mk(v[u][2], v[u][3]);
+                    double *wd = reinterpret_cast<double *>(win + (b * L + (e >> logd)) * S + s0);
+                    *reinterpret_cast<double4 *>(wd) = make_double4(v[u][0], v[u][1], v[u][2], v[u][3]);
                 }
             }
         }

@@ -302,12 +302,12 @@ static inline ViewSrc consecutive_views(const void *x, int is_c64, int64_t n, in
     return s;
 }
 
-// views stored view-major as rows of a (B, S, L) window buffer
+// views stored as the rows of a (B, L, S) window buffer: view v sample j at
+// win[(b*L + j)*S + v]
 static inline ViewSrc window_views(const cx *win, int S, int64_t L) {
-    ViewSrc s = consecutive_views(win, 0, (int64_t)S * L, 1, 0, S);
-    for (int v = 0; v < MAX_VIEWS; v++) s.off[v] = (v < S) ? (int64_t)v * L : 0;
+    ViewSrc s = consecutive_views(win, 0, (int64_t)S * L, S, 0, S);
     s.wrap = -1;
-    s.jfast = 1;
+    s.jfast = 0;
     return s;
 }
 

@@ -126,33 +126,62 @@ static __global__ void __launch_bounds__(256, MINB) k_fft_views(const ViewSrc sr
                                    int64_t ldV, int scale) {
     extern __shared__ double4 smem_raw[];
     cx *a = reinterpret_cast<cx *>(smem_raw);
+    __shared__ int64_t s_ibase[MAX_VIEWS], s_ioff[MAX_VIEWS], s_obase[MAX_VIEWS];
     const int L = 1 << logL, vpc = 1 << logvpc;
     const int64_t nviews = B * src.nshift;
     const int64_t g0 = int64_t(blockIdx.x) << logvpc;
     const int nv = (int)((nviews - g0) < vpc ? (nviews - g0) : vpc);
-    // gather: lanes vary the view (shift) fastest for one sample j, so one
-    // d-block's adjacent shifts share sectors; bit-reversed scatter to smem
-    for (int i = threadIdx.x; i < (L << logvpc); i += blockDim.x) {
-        const int v = src.jfast ? (i >> logL) : (i & (vpc - 1));
-        const int j = src.jfast ? (i & (L - 1)) : (i >> logvpc);
-        if (v >= nv) continue;
-        const int64_t g = g0 + v;
+    // per-view addressing, once per CTA (no 64-bit divisions or dynamically
+    // indexed parameter arrays in the element loops)
+    if (threadIdx.x < nv) {
+        const int64_t g = g0 + threadIdx.x;
         const int64_t b = g / src.nshift;
         const int s = (int)(g - b * src.nshift);
-        const int r = logL ? (int)(__brev((unsigned)j) >> (32 - logL)) : 0;
-        a[swz(v * L + r)] = view_load(src, b, s, j);
+        s_ibase[threadIdx.x] = b * src.sig_stride;
+        s_ioff[threadIdx.x] = (s >= src.dyn_first) ? src.dyn_off[b * src.dyn_stride + (s - src.dyn_first)]
+                                                  : src.off[s];
+        s_obase[threadIdx.x] = (b * SV + s) * ldV;
+    }
+    __syncthreads();
+    // gather: lanes vary the view (shift) fastest for one sample j, so one
+    // d-block's adjacent shifts share sectors; bit-reversed scatter to smem.
+    // Loads are issued in batches of 8 before their shared-memory stores.
+    const int total = L << logvpc;
+    for (int i0 = 0; i0 < total; i0 += 8 * 256) {
+        cx vals[8];
+        int dst[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const int i = i0 + u * 256 + threadIdx.x;
+            dst[u] = -1;
+            if (i < total) {
+                const int v = src.jfast ? (i >> logL) : (i & (vpc - 1));
+                const int j = src.jfast ? (i & (L - 1)) : (i >> logvpc);
+                if (v < nv) {
+                    const int64_t e = s_ibase[v] + (((int64_t)j * src.jstride + s_ioff[v]) & src.wrap);
+                    if (src.is_c64) {
+                        const float2 f = __ldg(reinterpret_cast<const float2 *>(src.x) + e);
+                        vals[u] = mk((double)f.x, (double)f.y);
+                    } else {
+                        vals[u] = ldcx(reinterpret_cast<const cx *>(src.x) + e);
+                    }
+                    const int r = logL ? (int)(__brev((unsigned)j) >> (32 - logL)) : 0;
+                    dst[u] = swz(v * L + r);
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++)
+            if (dst[u] >= 0) a[dst[u]] = vals[u];
     }
     __syncthreads();
     fft_stages_smem(a, nv, logL, 0, logL, tw);
     const double sc = 1.0 / (double)L;   // exact power of two
     for (int i = threadIdx.x; i < nv * L; i += blockDim.x) {
         const int v = i >> logL, k = i & (L - 1);
-        const int64_t g = g0 + v;
-        const int64_t b = g / src.nshift;
-        const int s = (int)(g - b * src.nshift);
         cx y = a[swz(i)];
         if (scale) y = mk(DMUL(y.re, sc), DMUL(y.im, sc));
-        stcx(out + (b * SV + s) * ldV + k, y);
+        stcx(out + s_obase[v] + k, y);
     }
 }
 

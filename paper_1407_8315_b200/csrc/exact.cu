@@ -232,6 +232,93 @@ __global__ void __launch_bounds__(128) k_decode_a1(const cx *__restrict__ V, int
     }
 }
 
+// Dense a = 1 decode.  The FFT epilogue marks active bins (act); a compaction
+// pass lists them, and the decode runs one active bin per thread (no idle
+// lanes for the ~78 % inactive bins of config 2).
+__global__ void __launch_bounds__(1024) k_act_compact(const uint8_t *__restrict__ act, int64_t nbins,
+                                                      uint8_t *__restrict__ status,
+                                                      int64_t *__restrict__ awl,
+                                                      unsigned long long *__restrict__ awlc) {
+    // one global atomic per 4096-bin block (a single counter hammered once
+    // per warp measured 95 us at config 2)
+    __shared__ int wsum[32];
+    __shared__ unsigned long long s_base;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t t0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+    bool on[4];
+    int mine = 0;
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+        const int64_t t = t0 + u;
+        on[u] = t < nbins && act[t];
+        if (t < nbins && !on[u]) status[t] = 0;
+        mine += on[u];
+    }
+    int inc = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int tot = 0;
+        for (int w = 0; w < 32; w++) {
+            const int c = wsum[w];
+            wsum[w] = tot;
+            tot += c;
+        }
+        s_base = tot ? atomicAdd(awlc, (unsigned long long)tot) : 0;
+    }
+    __syncthreads();
+    unsigned long long pos = s_base + wsum[warp] + (inc - mine);
+#pragma unroll
+    for (int u = 0; u < 4; u++)
+        if (on[u]) awl[pos++] = t0 + u;
+}
+
+template <int S>
+__global__ void __launch_bounds__(128) k_decode_a1_dense(const cx *__restrict__ V, int64_t L, int a_max,
+                                                         int64_t n, uint8_t *__restrict__ status,
+                                                         int64_t *__restrict__ bin_loc,
+                                                         cx *__restrict__ bin_val,
+                                                         const int64_t *__restrict__ awl,
+                                                         const unsigned long long *__restrict__ awlc,
+                                                         int64_t *__restrict__ wl,
+                                                         unsigned long long *__restrict__ wl_count) {
+    const int64_t cnt = (int64_t)*awlc;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < cnt;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t t = awl[i];
+        const int64_t b = t / L, k = t - b * L;
+        cx syn[S];
+#pragma unroll
+        for (int s = 0; s < S; s++) syn[s] = ldcx(V + (b * S + s) * L + k);
+        Decoded o;
+        decode_try_t<1, S>(syn, n, L, k, o);
+        if (o.accept) {
+            status[t] = 1;
+            bin_loc[t * a_max] = o.loc[0];
+            stcx(bin_val + t * a_max, o.val[0]);
+        } else {
+            status[t] = a_max > 1 ? 0xFE : 0xFF;
+        }
+        // warp-aggregated append of the bins that need a >= 2
+        const bool pend = !o.accept && a_max > 1;
+        const unsigned act_mask = __activemask();
+        const unsigned m = __ballot_sync(act_mask, pend);
+        if (m) {
+            const int lane = threadIdx.x & 31;
+            const int leader = __ffs(m) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) base = atomicAdd(wl_count, (unsigned long long)__popc(m));
+            base = __shfl_sync(act_mask, base, leader);
+            if (pend) wl[base + __popc(m & ((1u << lane) - 1))] = t;
+        }
+    }
+}
+
 #ifndef SFDT_MULTI_TEMPLATED
 #define SFDT_MULTI_TEMPLATED 1
 #endif
@@ -279,16 +366,26 @@ __global__ void __launch_bounds__(128, SFDT_MULTI_MINB) k_decode_multi(const cx 
 template <int S>
 static int launch_decode_noniter(const cx *V, int64_t B, int64_t L, int a_max, int64_t n,
                                  const double *thr, uint8_t *status, int64_t *bin_loc, cx *bin_val,
-                                 int64_t *wl, unsigned long long *wl_count, cudaStream_t stream) {
+                                 int64_t *wl, unsigned long long *wl_count, cudaStream_t stream,
+                                 const uint8_t *act = nullptr, int64_t *awl = nullptr,
+                                 unsigned long long *awlc = nullptr) {
     const int64_t nbins = B * L;
     cudaMemsetAsync(wl_count, 0, sizeof(unsigned long long), stream);
-    k_decode_a1<S><<<(unsigned)((nbins + 127) / 128), 128, 0, stream>>>(V, B, L, a_max, n, thr, status,
-                                                                        bin_loc, bin_val, wl, wl_count);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (act) {
+        cudaMemsetAsync(awlc, 0, sizeof(unsigned long long), stream);
+        k_act_compact<<<(unsigned)((nbins + 4095) / 4096), 1024, 0, stream>>>(act, nbins, status, awl, awlc);
+        SFDT_CHECK_LAUNCH();
+        k_decode_a1_dense<S><<<(unsigned)(sms * 16), 128, 0, stream>>>(V, L, a_max, n, status, bin_loc,
+                                                                       bin_val, awl, awlc, wl, wl_count);
+    } else {
+        k_decode_a1<S><<<(unsigned)((nbins + 127) / 128), 128, 0, stream>>>(V, B, L, a_max, n, thr, status,
+                                                                            bin_loc, bin_val, wl, wl_count);
+    }
     SFDT_CHECK_LAUNCH();
     if (a_max > 1) {
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         k_decode_multi<S><<<(unsigned)(sms * 8), 128, 0, stream>>>(V, L, a_max, n, status, bin_loc, bin_val,
                                                                   wl, wl_count);
         SFDT_CHECK_LAUNCH();
@@ -801,6 +898,7 @@ struct ExactPlan {
     bool capture;
     size_t off_win, off_V, off_partial, off_thr, off_status, off_bloc, off_bval, off_def,
         off_sloc, off_sval, off_sa, off_sdup, off_cnt, off_resid, off_ndef, off_scratch, off_fft, off_wl,
+        off_act, off_awl,
         total;
 };
 
@@ -838,6 +936,8 @@ static int make_plan(const sfdt_exact_args *a, ExactPlan &p) {
         p.off_bloc = take(size_t(p.B) * p.L * a->a_max * 8);
         p.off_bval = take(size_t(p.B) * p.L * a->a_max * 16);
         p.off_wl = take(size_t(p.B) * p.L * 8);
+        p.off_act = take(size_t(p.B) * p.L);
+        p.off_awl = take(size_t(p.B) * p.L * 8);
     } else {
         p.off_def = take(size_t(p.B) * p.L);
         p.off_sloc = take(size_t(p.B) * 4 * p.L * a->a_max * 8);
@@ -850,7 +950,7 @@ static int make_plan(const sfdt_exact_args *a, ExactPlan &p) {
     }
     p.capture = (!a->iterative && !a->aux_stream && p.d >= p.S && capture_enabled());
     p.off_win = p.capture ? take(size_t(p.B) * p.S * p.L * 16) : 0;
-    p.off_scratch = take(64 * 8);
+    p.off_scratch = take(128 * 8);
     p.off_fft = (p.L > FFT_SMEM_MAX) ? take(size_t(p.B) * p.L * p.S * 16) : 0;
     p.total = o;
     return SFDT_OK;
@@ -983,7 +1083,8 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
                 return launch_fft_views(src, nb, p.L, a->twiddles, V + c0 * p.S * p.L, (int)p.S, p.L,
                                         aux, fft_scratch ? fft_scratch + c0 * p.S * p.L : nullptr);
             };
-            if (!p.capture && (rc = launch_fft())) return rc;
+            const bool overlap = (aux != stream) && !p.capture;
+            if (overlap && (rc = launch_fft())) return rc;
             if ((rc = launch_stream(c0, nb))) return rc;
             if (c == nc - 1 && a->ev_stream_end) cudaEventRecord((cudaEvent_t)a->ev_stream_end, stream);
             if (aux != stream) {
@@ -993,22 +1094,36 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
                 cudaStreamWaitEvent(aux, ev, 0);
                 cudaEventDestroy(ev);
             }
-            if (p.capture && (rc = launch_fft())) return rc;
             k_rms<<<(unsigned)nb, 1024, 0, aux>>>(partial + c0 * p.nchunk, p.nchunk, p.n,
                                                   a->zero_threshold, p.d, a->rms + c0, thr + c0);
             SFDT_CHECK_LAUNCH();
+            // after the rms the FFT epilogue can also mark the active bins
+            const bool dense = !overlap && p.L <= FFT_SMEM_MAX;
+            uint8_t *actc = dense ? (uint8_t *)(w + p.off_act) + c0 * p.L : nullptr;
+            if (!overlap) {
+                if (actc) cudaMemsetAsync(actc, 0, size_t(nb) * p.L, aux);
+                const ViewSrc src = p.capture
+                    ? window_views((const cx *)(w + p.off_win) + c0 * p.S * p.L, (int)p.S, p.L)
+                    : consecutive_views((const char *)a->x + c0 * p.n * (is_c64 ? 8 : 16), is_c64,
+                                        p.n, p.d, 0, (int)p.S);
+                rc = launch_fft_views(src, nb, p.L, a->twiddles, V + c0 * p.S * p.L, (int)p.S, p.L, aux,
+                                      fft_scratch ? fft_scratch + c0 * p.S * p.L : nullptr, 1,
+                                      thr + c0, actc);
+                if (rc) return rc;
+            }
+            int64_t *awlc_p = (int64_t *)(w + p.off_awl) + c0 * p.L;
             const cx *Vc = V + c0 * p.S * p.L;
             uint8_t *stc = status + c0 * p.L;
             int64_t *blc = bloc + c0 * p.L * a->a_max;
             cx *bvc = bval + c0 * p.L * a->a_max;
             switch (p.S) {
-            case 2: rc = launch_decode_noniter<2>(Vc, nb, p.L, a->a_max, p.n, thr + c0, stc, blc, bvc, wl + c0 * p.L, wlc + c, aux); break;
-            case 4: rc = launch_decode_noniter<4>(Vc, nb, p.L, a->a_max, p.n, thr + c0, stc, blc, bvc, wl + c0 * p.L, wlc + c, aux); break;
-            case 6: rc = launch_decode_noniter<6>(Vc, nb, p.L, a->a_max, p.n, thr + c0, stc, blc, bvc, wl + c0 * p.L, wlc + c, aux); break;
-            default: rc = launch_decode_noniter<8>(Vc, nb, p.L, a->a_max, p.n, thr + c0, stc, blc, bvc, wl + c0 * p.L, wlc + c, aux); break;
+            case 2: rc = launch_decode_noniter<2>(Vc, nb, p.L, a->a_max, p.n, thr + c0, stc, blc, bvc, wl + c0 * p.L, wlc + c, aux, actc, awlc_p, wlc + 64 + c); break;
+            case 4: rc = launch_decode_noniter<4>(Vc, nb, p.L, a->a_max, p.n, thr + c0, stc, blc, bvc, wl + c0 * p.L, wlc + c, aux, actc, awlc_p, wlc + 64 + c); break;
+            case 6: rc = launch_decode_noniter<6>(Vc, nb, p.L, a->a_max, p.n, thr + c0, stc, blc, bvc, wl + c0 * p.L, wlc + c, aux, actc, awlc_p, wlc + 64 + c); break;
+            default: rc = launch_decode_noniter<8>(Vc, nb, p.L, a->a_max, p.n, thr + c0, stc, blc, bvc, wl + c0 * p.L, wlc + c, aux, actc, awlc_p, wlc + 64 + c); break;
             }
             if (rc) return rc;
-            launches += 1 + (p.L > FFT_SMEM_MAX ? 2 : 1) + 1 + (a->a_max > 1 ? 1 : 0);
+            launches += 1 + (p.L > FFT_SMEM_MAX ? 2 : 1) + 1 + (a->a_max > 1 ? 1 : 0) + (dense ? 1 : 0);
         }
         if (aux != stream) {
             if (cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming) != cudaSuccess) return SFDT_ECUDA;

@@ -123,10 +123,11 @@ __device__ __forceinline__ void fft_stages_smem(cx *a, int nv, int logL, int lh0
 template <int MINB>
 static __global__ void __launch_bounds__(256, MINB) k_fft_views(const ViewSrc src, int64_t B, int logL, int logvpc,
                                    const cx *__restrict__ tw, cx *__restrict__ out, int SV,
-                                   int64_t ldV, int scale) {
+                                   int64_t ldV, int scale, const double *__restrict__ thr,
+                                   uint8_t *__restrict__ act) {
     extern __shared__ double4 smem_raw[];
     cx *a = reinterpret_cast<cx *>(smem_raw);
-    __shared__ int64_t s_ibase[MAX_VIEWS], s_ioff[MAX_VIEWS], s_obase[MAX_VIEWS];
+    __shared__ int64_t s_ibase[MAX_VIEWS], s_ioff[MAX_VIEWS], s_obase[MAX_VIEWS], s_sig[MAX_VIEWS];
     const int L = 1 << logL, vpc = 1 << logvpc;
     const int64_t nviews = B * src.nshift;
     const int64_t g0 = int64_t(blockIdx.x) << logvpc;
@@ -141,6 +142,7 @@ static __global__ void __launch_bounds__(256, MINB) k_fft_views(const ViewSrc sr
         s_ioff[threadIdx.x] = (s >= src.dyn_first) ? src.dyn_off[b * src.dyn_stride + (s - src.dyn_first)]
                                                   : src.off[s];
         s_obase[threadIdx.x] = (b * SV + s) * ldV;
+        s_sig[threadIdx.x] = b;
     }
     __syncthreads();
     // gather: lanes vary the view (shift) fastest for one sample j, so one
@@ -182,6 +184,14 @@ static __global__ void __launch_bounds__(256, MINB) k_fft_views(const ViewSrc sr
         cx y = a[swz(i)];
         if (scale) y = mk(DMUL(y.re, sc), DMUL(y.im, sc));
         stcx(out + s_obase[v] + k, y);
+        if (act) {
+            // activity (exact.py:178): |v| > zero_threshold*rms*d on any view;
+            // |v|^2 decides away from the boundary, hypot inside a 1e-6 band
+            const double th = thr[s_sig[v]];
+            const double q = y.re * y.re + y.im * y.im;
+            if (q > th * th * (1.0 + 1e-6) || (q >= th * th * (1.0 - 1e-6) && cabs_(y) > th))
+                act[s_sig[v] * (int64_t)L + k] = 1;
+        }
     }
 }
 
@@ -267,7 +277,8 @@ static inline int fft_points_per_cta() {
 // needed only when L > FFT_SMEM_MAX.
 static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, const double *tw_,
                                    cx *out, int SV, int64_t ldV, cudaStream_t stream,
-                                   cx *large_scratch = nullptr, int scale = 1) {
+                                   cx *large_scratch = nullptr, int scale = 1,
+                                   const double *thr = nullptr, uint8_t *act = nullptr) {
     const cx *tw = reinterpret_cast<const cx *>(tw_);
     const int logL = ilog2_64(L);
     const int64_t nviews = B * src.nshift;
@@ -280,14 +291,14 @@ static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, con
         // <= 32 KiB per CTA: cap registers at 64 for 4 CTAs/SM (measured
         // 717 -> 553 us at config 2); larger tiles keep 128 registers
         if (smem <= 32 * 1024) {
-            k_fft_views<4><<<grid, 256, smem, stream>>>(src, B, logL, logvpc, tw, out, SV, ldV, scale);
+            k_fft_views<4><<<grid, 256, smem, stream>>>(src, B, logL, logvpc, tw, out, SV, ldV, scale, thr, act);
         } else if (smem <= 64 * 1024) {
             // 64 KiB tiles: 3 CTAs/SM by shared memory, so cap registers at 85
             cudaFuncSetAttribute(k_fft_views<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            k_fft_views<3><<<grid, 256, smem, stream>>>(src, B, logL, logvpc, tw, out, SV, ldV, scale);
+            k_fft_views<3><<<grid, 256, smem, stream>>>(src, B, logL, logvpc, tw, out, SV, ldV, scale, thr, act);
         } else {
             cudaFuncSetAttribute(k_fft_views<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            k_fft_views<1><<<grid, 256, smem, stream>>>(src, B, logL, logvpc, tw, out, SV, ldV, scale);
+            k_fft_views<1><<<grid, 256, smem, stream>>>(src, B, logL, logvpc, tw, out, SV, ldV, scale, thr, act);
         }
         SFDT_CHECK_LAUNCH();
         return SFDT_OK;

@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(128) k_decode_a1_dense(const cx *__restrict__ 
 #define SFDT_MULTI_TEMPLATED 1
 #endif
 #ifndef SFDT_MULTI_MINB
-#define SFDT_MULTI_MINB 4
+#define SFDT_MULTI_MINB 6
 #endif
 template <int S>
 __global__ void __launch_bounds__(128, SFDT_MULTI_MINB) k_decode_multi(const cx *__restrict__ V, int64_t L, int a_max,

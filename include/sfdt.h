@@ -119,6 +119,10 @@ typedef struct {
      * (aux_stream).  chunk_signals <= 0 picks ~16 chunks. */
     void *aux_stream;
     int64_t chunk_signals;
+    /* optional: rms(x) per signal already known (device, batch doubles) --
+     * e.g. from an earlier stage of estimate_sparsity_and_solve; the HBM
+     * stream pass is skipped and `rms` receives a copy */
+    const double *rms_in;
     /* optional instrumentation (host side) */
     void *ev_stream_begin;  /* cudaEvent_t recorded right before / after the */
     void *ev_stream_end;    /* HBM stream kernel (roofline timing), or NULL  */

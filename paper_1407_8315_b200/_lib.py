@@ -40,7 +40,7 @@ class ExactArgs(ctypes.Structure):
         ("unres_offsets", _vp), ("unres_bins", _vp), ("unres_cap", _i64),
         ("dup_locs", _vp), ("dup_offsets", _vp), ("dup_cap", _i64),
         ("stats", _vp), ("rms", _vp),
-        ("aux_stream", _vp), ("chunk_signals", _i64),
+        ("aux_stream", _vp), ("chunk_signals", _i64), ("rms_in", _vp),
         ("ev_stream_begin", _vp), ("ev_stream_end", _vp), ("kernel_launches", _i32),
     ]
 

@@ -51,7 +51,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         subprocess.run(["gcc", "-O2", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-std=gnu11",
                         "-c", os.path.join(CSRC, src), "-o", obj], check=True)
         objs.append(obj)
-    for src in CU_SOURCES:
+    def compile_cu(src):
         obj = os.path.join(objdir, src + ".o")
         cmd = [nvcc, *NVCC_FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
@@ -62,7 +62,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError(f"nvcc failed on {src}")
         if verbose:
             sys.stderr.write(r.stderr)
-        objs.append(obj)
+        return obj
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=len(CU_SOURCES)) as pool:
+        objs.extend(pool.map(compile_cu, CU_SOURCES))
     tmp = OUT + ".tmp"
     subprocess.run([nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static",
                     "-o", tmp, *objs, "-lm"], check=True)

@@ -163,6 +163,17 @@ __global__ void k_rms(const double *__restrict__ partial, int64_t nchunk, int64_
     }
 }
 
+// thresholds from a known rms (rms_in): copy rms out, zt*rms*d
+__global__ void k_thr_from_rms(const double *__restrict__ rms_in, int64_t B, double zt, int64_t d,
+                               double *__restrict__ rms_out, double *__restrict__ thr) {
+    const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (b < B) {
+        const double r = rms_in[b];
+        rms_out[b] = r;
+        thr[b] = DMUL(DMUL(zt, r), (double)d);
+    }
+}
+
 __global__ void k_scale_thr(const double *__restrict__ rms, int64_t B, double zt, int64_t d,
                             double *__restrict__ out) {
     const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1085,7 +1096,7 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
             };
             const bool overlap = (aux != stream) && !p.capture;
             if (overlap && (rc = launch_fft())) return rc;
-            if ((rc = launch_stream(c0, nb))) return rc;
+            if (!a->rms_in && (rc = launch_stream(c0, nb))) return rc;
             if (c == nc - 1 && a->ev_stream_end) cudaEventRecord((cudaEvent_t)a->ev_stream_end, stream);
             if (aux != stream) {
                 cudaEvent_t ev;
@@ -1094,8 +1105,13 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
                 cudaStreamWaitEvent(aux, ev, 0);
                 cudaEventDestroy(ev);
             }
-            k_rms<<<(unsigned)nb, 1024, 0, aux>>>(partial + c0 * p.nchunk, p.nchunk, p.n,
-                                                  a->zero_threshold, p.d, a->rms + c0, thr + c0);
+            if (a->rms_in)
+                k_thr_from_rms<<<(unsigned)((nb + 255) / 256), 256, 0, aux>>>(a->rms_in + c0, nb,
+                                                                              a->zero_threshold, p.d,
+                                                                              a->rms + c0, thr + c0);
+            else
+                k_rms<<<(unsigned)nb, 1024, 0, aux>>>(partial + c0 * p.nchunk, p.nchunk, p.n,
+                                                      a->zero_threshold, p.d, a->rms + c0, thr + c0);
             SFDT_CHECK_LAUNCH();
             // after the rms the FFT epilogue can also mark the active bins
             const bool dense = !overlap && p.L <= FFT_SMEM_MAX;
@@ -1149,10 +1165,14 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
 
     // iterative: the single pass over x first (all signals), then the passes
     if (a->ev_stream_begin) cudaEventRecord((cudaEvent_t)a->ev_stream_begin, stream);
-    if ((rc = launch_stream(0, p.B))) return rc;
+    if (!a->rms_in && (rc = launch_stream(0, p.B))) return rc;
     if (a->ev_stream_end) cudaEventRecord((cudaEvent_t)a->ev_stream_end, stream);
-    k_rms<<<(unsigned)p.B, 1024, 0, stream>>>(partial, p.nchunk, p.n, a->zero_threshold, p.d,
-                                             a->rms, thr);
+    if (a->rms_in)
+        k_thr_from_rms<<<(unsigned)((p.B + 255) / 256), 256, 0, stream>>>(a->rms_in, p.B, a->zero_threshold,
+                                                                          p.d, a->rms, thr);
+    else
+        k_rms<<<(unsigned)p.B, 1024, 0, stream>>>(partial, p.nchunk, p.n, a->zero_threshold, p.d,
+                                                 a->rms, thr);
     SFDT_CHECK_LAUNCH();
     launches += 1;
 

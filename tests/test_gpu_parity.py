@@ -398,3 +398,21 @@ def test_general_small_configs(n, k, a_max, d, prune):
     vals = np.fromiter(want.values(), dtype=np.complex128, count=len(want))
     _general_check(spec.entries, locs, vals, f"n={n} k={k}")
     assert tr.collision_histogram == wtr["collision_histogram"]
+
+
+def test_rms_reuse_matches_full_pass():
+    """exact_batch(rms=...) skips the HBM pass; results must equal the full
+    solve (rms is a pure function of x)."""
+    n, k = 1 << 16, 64
+    X = np.stack([exact_signal(n, k, s, "unit")[0] for s in range(3)])
+    cfg = P.ExactConfig(n=n, k=k)
+    full = P.exact_batch(X, cfg, False)
+    reuse = P.exact_batch(X, cfg, False, rms=full.t["rms"])
+    for b in range(3):
+        assert full.spectrum(b).entries == reuse.spectrum(b).entries
+        assert vars(full.trace(b).iterations[0]) == vars(reuse.trace(b).iterations[0])
+    it_full = P.exact_batch(X, cfg, True)
+    it_reuse = P.exact_batch(X, cfg, True, rms=full.t["rms"])
+    for b in range(3):
+        assert it_full.spectrum(b).entries == it_reuse.spectrum(b).entries
+    assert np.array_equal(full.to_host()["rms"], reuse.to_host()["rms"])

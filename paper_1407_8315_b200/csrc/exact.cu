@@ -426,12 +426,17 @@ __device__ __forceinline__ int64_t slot_index(int64_t b, int p, int64_t k, int64
     return (b * 4 + p) * L0 + k;
 }
 
-__global__ void k_iter_pass(IterState st, int64_t B, int64_t L0, int S, int a_max, int l,
-                            int64_t n, int64_t m, int fold, const double *__restrict__ thr_base) {
+// Pass l, phase 1 (thread per bin): fold, SubFreq, activity; active bins
+// are appended (block-aggregated) to a dense list for phase 2.
+__global__ void __launch_bounds__(256) k_iter_prep(IterState st, int64_t B, int64_t L0, int S, int a_max,
+                                                   int l, int64_t n, int64_t m, int fold,
+                                                   const double *__restrict__ thr_base,
+                                                   int64_t *__restrict__ awl,
+                                                   unsigned long long *__restrict__ awlc) {
     const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const bool valid = t < B * m;
     const int64_t b = valid ? t / m : 0, k = valid ? t - b * m : 0;
-    bool active = false, solved = false, deferred_evt = false;
+    bool active = false;
     if (valid) {
         cx *Vb = st.V + b * S * L0;
         // fold previous views to the doubled d (exact.py:225-229)
@@ -448,7 +453,6 @@ __global__ void k_iter_pass(IterState st, int64_t B, int64_t L0, int S, int a_ma
         // (exact.py:234-240, np.subtract.at)
         cx v0 = Vb[(2 * l) * L0 + k], v1 = Vb[(2 * l + 1) * L0 + k];
         for (int p = 0; p < l; p++) {
-            const int64_t mp = m << (l - p);
             const int nb = 1 << (l - p);
             // origin bins k + i*m at pass p, ordered by (a desc, bin asc)
             int order[8];
@@ -466,7 +470,6 @@ __global__ void k_iter_pass(IterState st, int64_t B, int64_t L0, int S, int a_ma
                 }
                 order[pos] = i;
             }
-            (void)mp;
             for (int q = 0; q < cntb; q++) {
                 const int64_t si = slot_index(b, p, k + order[q] * m, L0);
                 const int a = st.slot_a[si];
@@ -487,77 +490,122 @@ __global__ void k_iter_pass(IterState st, int64_t B, int64_t L0, int S, int a_ma
         const int64_t sp = slot_index(b, l, k, L0);
         st.slot_a[sp] = 0;
         st.slot_dupmask[sp] = 0;
-        if (active) {
-            const int Sl = 2 * l + 2;
-            cx syn[MAX_SHIFTS];
-            for (int j = 0; j < Sl; j++) syn[j] = Vb[j * L0 + k];
-            Decoded o;
-            for (int a_try = l + 1; a_try >= 1; a_try--) {
-                decode_try(syn, Sl, a_try, n, m, k, o);
-                if (o.accept) {
-                    solved = true;
-                    st.deferred[b * L0 + k] = 0;
-                    // duplicate locations overwrite the earlier slot's value
-                    uint8_t dupmask = 0;
-                    for (int j = 0; j < a_try; j++) {
-                        bool found = false;
-                        for (int p = 0; p < l && !found; p++) {
-                            const int nb = 1 << (l - p);
-                            for (int i = 0; i < nb && !found; i++) {
-                                const int64_t si = slot_index(b, p, k + i * m, L0);
-                                const int ap = st.slot_a[si];
-                                const uint8_t dp = st.slot_dupmask[si];
-                                for (int r = 0; r < ap; r++) {
-                                    if (!(dp & (1u << r)) && st.slot_loc[si * a_max + r] == o.loc[j]) {
-                                        st.slot_val[si * a_max + r] = o.val[j];
-                                        found = true;
-                                        break;
-                                    }
+    }
+    // attempted count per signal (warp-aggregated) + block-aggregated append
+    const unsigned full = 0xffffffffu;
+    const int64_t bw = __shfl_sync(full, b, 0);
+    const bool same = __all_sync(full, !valid || b == bw);
+    const unsigned am = __ballot_sync(full, active);
+    if (same) {
+        if ((threadIdx.x & 31) == 0 && am) atomicAdd(st.cnt + (bw * 4 + l) * 4, (unsigned long long)__popc(am));
+    } else if (active) {
+        atomicAdd(st.cnt + (b * 4 + l) * 4, 1ull);
+    }
+    __shared__ int wsum[8];
+    __shared__ unsigned long long s_base;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) wsum[warp] = __popc(am);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int tot = 0;
+        for (int w = 0; w < 8; w++) {
+            const int c = wsum[w];
+            wsum[w] = tot;
+            tot += c;
+        }
+        s_base = tot ? atomicAdd(awlc, (unsigned long long)tot) : 0;
+    }
+    __syncthreads();
+    if (active) awl[s_base + wsum[warp] + __popc(am & ((1u << lane) - 1))] = t;
+}
+
+// Pass l, phase 2 (thread per active bin): descending-a decode with the
+// singular-only retry, deferral, duplicate overwrite, and removal of the
+// accepted terms from every live view (exact.py:253-280).  LP = l is a
+// template parameter so the 2l+2 syndromes and every Cramer matrix are
+// register-resident.
+template <int LP>
+__global__ void __launch_bounds__(128, 4) k_iter_decode(IterState st, int64_t L0, int S, int a_max,
+                                                        int64_t n, int64_t m,
+                                                        const int64_t *__restrict__ awl,
+                                                        const unsigned long long *__restrict__ awlc) {
+    constexpr int SL = 2 * LP + 2;
+    const int64_t cnt = (int64_t)*awlc;
+    for (int64_t it = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; it < cnt;
+         it += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t t = awl[it];
+        const int64_t b = t / m, k = t - b * m;
+        cx *Vb = st.V + b * S * L0;
+        cx syn[SL];
+#pragma unroll
+        for (int j = 0; j < SL; j++) syn[j] = Vb[j * L0 + k];
+        const int64_t sp = slot_index(b, LP, k, L0);
+        bool solved = false, deferred_evt = false;
+        Decoded o;
+        for (int a_try = LP + 1; a_try >= 1; a_try--) {
+            if (a_try == 1) decode_try_t<1, SL>(syn, n, m, k, o);
+            else if (a_try == 2) { if constexpr (LP >= 1) decode_try_t<2, SL>(syn, n, m, k, o); }
+            else if (a_try == 3) { if constexpr (LP >= 2) decode_try_t<3, SL>(syn, n, m, k, o); }
+            else { if constexpr (LP >= 3) decode_try_t<4, SL>(syn, n, m, k, o); }
+            if (o.accept) {
+                solved = true;
+                st.deferred[b * L0 + k] = 0;
+                // duplicate locations overwrite the earlier slot's value
+                uint8_t dupmask = 0;
+                for (int j = 0; j < a_try; j++) {
+                    bool found = false;
+                    for (int p = 0; p < LP && !found; p++) {
+                        const int nb = 1 << (LP - p);
+                        for (int i = 0; i < nb && !found; i++) {
+                            const int64_t si = slot_index(b, p, k + i * m, L0);
+                            const int ap = st.slot_a[si];
+                            const uint8_t dp = st.slot_dupmask[si];
+                            for (int r = 0; r < ap; r++) {
+                                if (!(dp & (1u << r)) && st.slot_loc[si * a_max + r] == o.loc[j]) {
+                                    st.slot_val[si * a_max + r] = o.val[j];
+                                    found = true;
+                                    break;
                                 }
                             }
                         }
-                        if (found) dupmask |= (1u << j);
-                        st.slot_loc[sp * a_max + j] = o.loc[j];
-                        st.slot_val[sp * a_max + j] = o.val[j];
                     }
-                    st.slot_a[sp] = (uint8_t)a_try;
-                    st.slot_dupmask[sp] = dupmask;
-                    // remove the decoded contribution from every live view
-                    // (exact.py:269-271)
-                    for (int j = 0; j < Sl; j++) {
-                        cx terms[4];
-                        for (int r = 0; r < a_try; r++) terms[r] = nmul(o.val[r], phase(o.loc[r], j, n));
-                        Vb[j * L0 + k] = csub(Vb[j * L0 + k], npsum(terms, a_try));
-                    }
-                    break;
+                    if (found) dupmask |= (1u << j);
+                    st.slot_loc[sp * a_max + j] = o.loc[j];
+                    st.slot_val[sp * a_max + j] = o.val[j];
                 }
-                if (!(a_try > 1 && o.retryable)) {
-                    st.deferred[b * L0 + k] = 1;
-                    deferred_evt = true;
-                    break;
+                st.slot_a[sp] = (uint8_t)a_try;
+                st.slot_dupmask[sp] = dupmask;
+                // remove the decoded contribution from every live view
+                // (exact.py:269-271)
+#pragma unroll
+                for (int j = 0; j < SL; j++) {
+                    cx terms[4];
+                    for (int r = 0; r < a_try; r++) terms[r] = nmul(o.val[r], phase(o.loc[r], j, n));
+                    Vb[j * L0 + k] = csub(Vb[j * L0 + k], npsum(terms, a_try));
                 }
+                break;
+            }
+            if (!(a_try > 1 && o.retryable)) {
+                st.deferred[b * L0 + k] = 1;
+                deferred_evt = true;
+                break;
             }
         }
-    }
-    // per-signal counters (warp-aggregated; integer adds are order-free)
-    const unsigned mask = 0xffffffffu;
-    const int64_t bw = __shfl_sync(mask, b, 0);
-    const bool same = __all_sync(mask, !valid || b == bw);
-    if (same) {
-        const unsigned na = __popc(__ballot_sync(mask, valid && active));
-        const unsigned ns = __popc(__ballot_sync(mask, valid && solved));
-        const unsigned nd = __popc(__ballot_sync(mask, valid && deferred_evt));
-        if ((threadIdx.x & 31) == 0) {
-            unsigned long long *c = st.cnt + (bw * 4 + l) * 4;
-            if (na) atomicAdd(c + 0, na);
-            if (ns) atomicAdd(c + 1, ns);
-            if (nd) atomicAdd(c + 2, nd);
+        const unsigned act = __activemask();
+        const int64_t bw = __shfl_sync(act, b, __ffs(act) - 1);
+        const bool same = __all_sync(act, b == bw);
+        const unsigned ns = __ballot_sync(act, solved), nd = __ballot_sync(act, deferred_evt);
+        if (same) {
+            if ((threadIdx.x & 31) == __ffs(act) - 1) {
+                unsigned long long *c = st.cnt + (bw * 4 + LP) * 4;
+                if (ns) atomicAdd(c + 1, (unsigned long long)__popc(ns));
+                if (nd) atomicAdd(c + 2, (unsigned long long)__popc(nd));
+            }
+        } else {
+            unsigned long long *c = st.cnt + (b * 4 + LP) * 4;
+            if (solved) atomicAdd(c + 1, 1ull);
+            if (deferred_evt) atomicAdd(c + 2, 1ull);
         }
-    } else if (valid) {
-        unsigned long long *c = st.cnt + (b * 4 + l) * 4;
-        if (active) atomicAdd(c + 0, 1ull);
-        if (solved) atomicAdd(c + 1, 1ull);
-        if (deferred_evt) atomicAdd(c + 2, 1ull);
     }
 }
 
@@ -814,89 +862,218 @@ __global__ void __launch_bounds__(THREADS) k_iter_count(const IterState st, int6
     }
 }
 
+// Four per-class counters held in scalar registers: a runtime class index
+// selects with predicated adds instead of indexing a local array (which
+// ptxas places in stack memory).
+struct C4 {
+    long long v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+    __device__ __forceinline__ long long get(int c) const {
+        return c == 0 ? v0 : c == 1 ? v1 : c == 2 ? v2 : v3;
+    }
+    __device__ __forceinline__ void add(int c, long long x) {
+        v0 += (c == 0) ? x : 0;
+        v1 += (c == 1) ? x : 0;
+        v2 += (c == 2) ? x : 0;
+        v3 += (c == 3) ? x : 0;
+    }
+    __device__ __forceinline__ void set(int c, long long x) {
+        v0 = (c == 0) ? x : v0;
+        v1 = (c == 1) ? x : v1;
+        v2 = (c == 2) ? x : v2;
+        v3 = (c == 3) ? x : v3;
+    }
+};
+
+// Per-lane chunk of up to 32 consecutive bytes (bins t0 + lane*cb ..) held
+// in eight 32-bit registers; cb is a power of two <= 32.
+struct Chunk32 {
+    uint32_t w[8];
+    __device__ __forceinline__ int at(int i) const { return (w[i >> 2] >> (8 * (i & 3))) & 0xFF; }
+};
+
+__device__ __forceinline__ void load_chunk(const uint8_t *__restrict__ src, int cb, bool valid, Chunk32 &c) {
+#pragma unroll
+    for (int q = 0; q < 8; q++) c.w[q] = 0;
+    if (!valid) return;
+    if (cb >= 16) {
+        const uint4 *v = reinterpret_cast<const uint4 *>(src);
+        const uint4 u0 = __ldg(v);
+        c.w[0] = u0.x; c.w[1] = u0.y; c.w[2] = u0.z; c.w[3] = u0.w;
+        if (cb == 32) {
+            const uint4 u1 = __ldg(v + 1);
+            c.w[4] = u1.x; c.w[5] = u1.y; c.w[6] = u1.z; c.w[7] = u1.w;
+        }
+    } else if (cb >= 4) {
+        const uint32_t *v = reinterpret_cast<const uint32_t *>(src);
+        c.w[0] = __ldg(v);
+        if (cb == 8) c.w[1] = __ldg(v + 1);
+    } else {
+        uint32_t x = 0;
+        for (int i = 0; i < cb; i++) x |= (uint32_t)__ldg(src + i) << (8 * i);
+        c.w[0] = x;
+    }
+}
+
+__device__ __forceinline__ unsigned long long warp_incl_scan_u64(unsigned long long v, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+    }
+    return v;
+}
+
+// Iterative emission: per pass p the entries of bins accepted with a_try =
+// p+1, p, ..., 1 in bin order (non-duplicate entries to the spectrum, the
+// duplicate overwrites to the warning list), then the unresolved bins.
+// One WARP per signal (no block barriers; 8 signals per CTA keep the SM's
+// memory pipeline full): a lane owns a contiguous chunk of up to 32 bins of
+// a 1024-bin tile, read as 16-byte vectors; one packed warp scan (4 classes
+// x 16-bit fields) per tile places every entry.  Passes whose m exceeds one
+// tile take a counting sweep first for the class bases.
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) k_iter_emit(
-    const IterState st, int64_t L0, int a_max, int npass, const PassInfo pi,
-    int64_t m_final, const int64_t *__restrict__ eoff, const int64_t *__restrict__ uoff,
+    const IterState st, int64_t B, int64_t L0, int a_max, int npass, const PassInfo pi, int64_t m_final,
+    const int64_t *__restrict__ eoff, const int64_t *__restrict__ uoff,
     const int64_t *__restrict__ doff, int64_t *__restrict__ locs, cx *__restrict__ vals,
     int32_t *__restrict__ ubins, int64_t *__restrict__ dups) {
-    const int64_t b = blockIdx.x;
-    __shared__ long long bufe[THREADS], bufd[THREADS];
-    __shared__ long long carry_e, carry_d;
-    if (threadIdx.x == 0) {
-        carry_e = eoff[b];
-        carry_d = doff ? doff[b] : 0;
-    }
-    __syncthreads();
+    constexpr int TILE = 1024;
+    const int lane = threadIdx.x & 31;
+    const int64_t b = (int64_t)blockIdx.x * (THREADS / 32) + (threadIdx.x >> 5);
+    if (b >= B) return;
+    long long carry_e = eoff[b], carry_d = doff ? doff[b] : 0;
     for (int p = 0; p < npass; p++) {
-        const int64_t m = pi.m[p];
-        for (int a = p + 1; a >= 1; a--) {
-            for (int64_t k0 = 0; k0 < m; k0 += THREADS) {
-                const int64_t k = k0 + threadIdx.x;
-                int64_t si = -1;
-                long long we = 0, wd = 0;
-                uint8_t dm = 0;
-                if (k < m) {
-                    si = slot_index(b, p, k, L0);
-                    if (st.slot_a[si] == a) {
-                        dm = st.slot_dupmask[si];
-                        wd = __popc(dm);
-                        we = a - wd;
+        const int64_t m = p == 0 ? pi.m[0] : p == 1 ? pi.m[1] : p == 2 ? pi.m[2] : pi.m[3];
+        const int64_t tile = m < TILE ? m : TILE;
+        const int cb = tile >= 32 ? (int)(tile >> 5) : 1;
+        const uint8_t *sa = st.slot_a + slot_index(b, p, 0, L0);
+        const uint8_t *sd = st.slot_dupmask + slot_index(b, p, 0, L0);
+        auto counts = [&](const Chunk32 &ca, const Chunk32 &cd, unsigned long long &pe,
+                          unsigned long long &pd) {
+            pe = 0;
+            pd = 0;
+#pragma unroll
+            for (int i = 0; i < 32; i++) {
+                if (i < cb) {
+                    const int a = ca.at(i);
+                    if (a) {
+                        const int dn = __popc(cd.at(i));
+                        pe += (unsigned long long)(a - dn) << (16 * (a - 1));
+                        pd += (unsigned long long)dn << (16 * (a - 1));
                     }
                 }
-                bufe[threadIdx.x] = we;
-                bufd[threadIdx.x] = wd;
-                __syncthreads();
-                for (int o = 1; o < THREADS; o <<= 1) {
-                    long long ae = (threadIdx.x >= o) ? bufe[threadIdx.x - o] : 0;
-                    long long ad = (threadIdx.x >= o) ? bufd[threadIdx.x - o] : 0;
-                    __syncthreads();
-                    bufe[threadIdx.x] += ae;
-                    bufd[threadIdx.x] += ad;
-                    __syncthreads();
+            }
+        };
+        Chunk32 ca, cd;
+        unsigned long long pe, pd;
+        C4 tot_e, tot_d;
+        if (m > TILE) {           // counting sweep for the class bases
+            for (int64_t t0 = 0; t0 < m; t0 += TILE) {
+                const int64_t k0 = t0 + (int64_t)lane * cb;
+                load_chunk(sa + k0, cb, true, ca);
+                load_chunk(sd + k0, cb, true, cd);
+                counts(ca, cd, pe, pd);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    pe += __shfl_xor_sync(0xffffffffu, pe, o);
+                    pd += __shfl_xor_sync(0xffffffffu, pd, o);
                 }
-                long long pe = carry_e + bufe[threadIdx.x] - we;
-                long long pd = carry_d + bufd[threadIdx.x] - wd;
-                if (we || wd) {
-                    for (int j = 0; j < a; j++) {
-                        const int64_t loc = st.slot_loc[si * a_max + j];
-                        if (dm & (1u << j)) {
-                            if (dups) dups[pd] = loc;
-                            pd++;
-                        } else {
-                            locs[pe] = loc;
-                            stcx(vals + pe, st.slot_val[si * a_max + j]);
-                            pe++;
+#pragma unroll
+                for (int c = 0; c < 4; c++) {
+                    tot_e.add(c, (long long)((pe >> (16 * c)) & 0xFFFF));
+                    tot_d.add(c, (long long)((pd >> (16 * c)) & 0xFFFF));
+                }
+            }
+        }
+        C4 base_e, base_d, acc_e, acc_d;
+        for (int64_t t0 = 0; t0 < m; t0 += TILE) {
+            const int64_t k0 = t0 + (int64_t)lane * cb;
+            const bool valid = k0 < m;
+            load_chunk(sa + k0, cb, valid, ca);
+            load_chunk(sd + k0, cb, valid, cd);
+            counts(ca, cd, pe, pd);
+            const unsigned long long ie = warp_incl_scan_u64(pe, lane);
+            const unsigned long long id = warp_incl_scan_u64(pd, lane);
+            const unsigned long long te = __shfl_sync(0xffffffffu, ie, 31);
+            const unsigned long long td = __shfl_sync(0xffffffffu, id, 31);
+            if (t0 == 0) {
+                if (m <= TILE) {
+#pragma unroll
+                    for (int c = 0; c < 4; c++) {
+                        tot_e.set(c, (long long)((te >> (16 * c)) & 0xFFFF));
+                        tot_d.set(c, (long long)((td >> (16 * c)) & 0xFFFF));
+                    }
+                }
+                long long ce = carry_e, cdd = carry_d;
+#pragma unroll
+                for (int c = 3; c >= 0; c--) {
+                    base_e.set(c, ce);
+                    base_d.set(c, cdd);
+                    if (c <= p) {
+                        ce += tot_e.get(c);
+                        cdd += tot_d.get(c);
+                    }
+                }
+                carry_e = ce;
+                carry_d = cdd;
+            }
+            unsigned long long oe = ie - pe, od = id - pd;   // exclusive, packed
+            if (pe | pd) {
+#pragma unroll
+                for (int i = 0; i < 32; i++) {
+                    if (i < cb) {
+                        const int a = ca.at(i);
+                        if (a) {
+                            const int c = a - 1, dm = cd.at(i);
+                            long long pe_ = base_e.get(c) + acc_e.get(c) + (long long)((oe >> (16 * c)) & 0xFFFF);
+                            long long pd_ = base_d.get(c) + acc_d.get(c) + (long long)((od >> (16 * c)) & 0xFFFF);
+                            const int64_t si = slot_index(b, p, k0 + i, L0);
+                            const int dn = __popc(dm);
+                            for (int j = 0; j < a; j++) {
+                                const int64_t loc = st.slot_loc[si * a_max + j];
+                                if (dm & (1 << j)) {
+                                    if (dups) dups[pd_] = loc;
+                                    pd_++;
+                                } else {
+                                    locs[pe_] = loc;
+                                    stcx(vals + pe_, st.slot_val[si * a_max + j]);
+                                    pe_++;
+                                }
+                            }
+                            oe += (unsigned long long)(a - dn) << (16 * c);
+                            od += (unsigned long long)dn << (16 * c);
                         }
                     }
                 }
-                __syncthreads();
-                if (threadIdx.x == THREADS - 1) {
-                    carry_e += bufe[THREADS - 1];
-                    carry_d += bufd[THREADS - 1];
-                }
-                __syncthreads();
+            }
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                acc_e.add(c, (long long)((te >> (16 * c)) & 0xFFFF));
+                acc_d.add(c, (long long)((td >> (16 * c)) & 0xFFFF));
             }
         }
     }
     // unresolved = deferred bins at the final m, ascending
-    if (threadIdx.x == 0) carry_e = uoff[b];
-    __syncthreads();
-    for (int64_t k0 = 0; k0 < m_final; k0 += THREADS) {
-        const int64_t k = k0 + threadIdx.x;
-        const long long w = (k < m_final) ? st.deferred[b * L0 + k] : 0;
-        bufe[threadIdx.x] = w;
-        __syncthreads();
-        for (int o = 1; o < THREADS; o <<= 1) {
-            long long ae = (threadIdx.x >= o) ? bufe[threadIdx.x - o] : 0;
-            __syncthreads();
-            bufe[threadIdx.x] += ae;
-            __syncthreads();
+    {
+        const int64_t tile = m_final < TILE ? m_final : TILE;
+        const int cb = tile >= 32 ? (int)(tile >> 5) : 1;
+        long long carry_u = uoff[b];
+        Chunk32 cf;
+        for (int64_t t0 = 0; t0 < m_final; t0 += TILE) {
+            const int64_t k0 = t0 + (int64_t)lane * cb;
+            load_chunk(st.deferred + b * L0 + k0, cb, k0 < m_final, cf);
+            unsigned long long cnt = 0;
+#pragma unroll
+            for (int q = 0; q < 8; q++) cnt += __popc(cf.w[q]);   // flags are 0/1 bytes
+            const unsigned long long inc = warp_incl_scan_u64(cnt, lane);
+            long long pos = carry_u + (long long)(inc - cnt);
+            if (cnt) {
+#pragma unroll
+                for (int i = 0; i < 32; i++)
+                    if (i < cb && cf.at(i)) ubins[pos++] = (int32_t)(k0 + i);
+            }
+            carry_u += (long long)__shfl_sync(0xffffffffu, inc, 31);
         }
-        if (w) ubins[carry_e + bufe[threadIdx.x] - w] = (int32_t)k;
-        __syncthreads();
-        if (threadIdx.x == THREADS - 1) carry_e += bufe[THREADS - 1];
-        __syncthreads();
     }
 }
 
@@ -958,6 +1135,7 @@ static int make_plan(const sfdt_exact_args *a, ExactPlan &p) {
         p.off_cnt = take(size_t(p.B) * 16 * 8);
         p.off_resid = take(size_t(p.B) * 8);
         p.off_ndef = take(size_t(p.B) * 8);
+        p.off_awl = take(size_t(p.B) * p.L * 8);
     }
     p.capture = (!a->iterative && !a->aux_stream && p.d >= p.S && capture_enabled());
     p.off_win = p.capture ? take(size_t(p.B) * p.S * p.L * 16) : 0;
@@ -1212,9 +1390,25 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
         if (rc) return rc;
         const int fold = (l > 0) && (m != m_of[l - 1]);
         const int64_t nb = p.B * m;
-        k_iter_pass<<<(unsigned)((nb + 127) / 128), 128, 0, stream>>>(st, p.B, p.L, (int)p.S, a->a_max,
-                                                                      l, p.n, m, fold, thr);
+        int64_t *awl = (int64_t *)(w + p.off_awl);
+        unsigned long long *awlc = (unsigned long long *)(w + p.off_scratch) + 64 + l;
+        cudaMemsetAsync(awlc, 0, 8, stream);
+        k_iter_prep<<<(unsigned)((nb + 255) / 256), 256, 0, stream>>>(st, p.B, p.L, (int)p.S, a->a_max, l, p.n,
+                                                                      m, fold, thr, awl, awlc);
         SFDT_CHECK_LAUNCH();
+        {
+            int dev = 0, sms = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            const unsigned g = (unsigned)(sms * 16);
+            switch (l) {
+            case 0: k_iter_decode<0><<<g, 128, 0, stream>>>(st, p.L, (int)p.S, a->a_max, p.n, m, awl, awlc); break;
+            case 1: k_iter_decode<1><<<g, 128, 0, stream>>>(st, p.L, (int)p.S, a->a_max, p.n, m, awl, awlc); break;
+            case 2: k_iter_decode<2><<<g, 128, 0, stream>>>(st, p.L, (int)p.S, a->a_max, p.n, m, awl, awlc); break;
+            default: k_iter_decode<3><<<g, 128, 0, stream>>>(st, p.L, (int)p.S, a->a_max, p.n, m, awl, awlc); break;
+            }
+            SFDT_CHECK_LAUNCH();
+        }
     }
     double *resid = (double *)(w + p.off_resid);
     int64_t *ndef = (int64_t *)(w + p.off_ndef);
@@ -1230,13 +1424,13 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
     if (a->dup_offsets)
         k_scan_offsets<<<1, 1024, 0, stream>>>(a->stats, p.B, SFDT_ST_NDUP, a->dup_offsets);
     SFDT_CHECK_LAUNCH();
-    k_iter_emit<256><<<(unsigned)p.B, 256, 0, stream>>>(st, p.L, a->a_max, (int)p.npass, pi,
+    k_iter_emit<256><<<(unsigned)((p.B + 7) / 8), 256, 0, stream>>>(st, p.B, p.L, a->a_max, (int)p.npass, pi,
                                                         m_final, a->entry_offsets, a->unres_offsets,
                                                         a->dup_offsets ? a->dup_offsets : nullptr,
                                                         a->locs, (cx *)a->vals, a->unres_bins,
                                                         a->dup_locs);
     SFDT_CHECK_LAUNCH();
-    launches += (int)p.npass * (1 + 1 + (p.L > FFT_SMEM_MAX ? 2 : 1)) + 1 + 1 + 2 + (a->dup_offsets ? 1 : 0) + 1;
+    launches += (int)p.npass * (1 + 2 + (p.L > FFT_SMEM_MAX ? 2 : 1)) + 1 + 1 + 2 + (a->dup_offsets ? 1 : 0) + 1;
     a->kernel_launches = launches;
     return SFDT_OK;
 }

@@ -321,10 +321,237 @@ __device__ void subspace_pursuit_dev(const cx *y, const cx *phase, const cx *bph
     }
 }
 
+// ------------------------------------------------- matched filter (warp)
+// general.py:345-351: scores_t = |sum_j conj(base_phi[j, t]) w_j| over the d
+// candidates, w_j = e^{-2 pi i s_j k / N} y_j; the top min(a, d) columns by
+// (score desc, t asc) -- np.argsort(-scores, kind="stable")[:a].  One WARP
+// per voted bin: lane l scores candidates t = l, l+32, ... (coalesced
+// base_phi rows, same per-candidate arithmetic and j order as the
+// sequential form), keeps a register top-4, and the warp merges the lane
+// lists by repeated (score, t) arg-best.  A NaN score ranks last (numpy
+// sorts NaN to the end).
+struct Top4 {
+    double sc[4];
+    int id[4];
+};
+
+__device__ __forceinline__ bool mf_better(double v, int t, double w, int u) {
+    return v > w || (v == w && t < u);
+}
+
+// One CTA per signal: base_phi (r x d) is staged in shared memory once when
+// it fits (every voted bin of the signal re-reads all of it), the voted
+// bins are listed 1024 at a time, and each warp scores one bin.
+constexpr int MF_SMEM_MAX = 160 * 1024;
+constexpr int MF_LIST = 4096;
+
+template <int R, bool STAGE>
+__global__ void __launch_bounds__(256, 2) k_gen_mf(const cx *__restrict__ V, GenParams p,
+                                                const int32_t *__restrict__ votes,
+                                                int32_t *__restrict__ mf_top) {
+    constexpr bool stage = STAGE;
+    extern __shared__ cx s_phi[];
+    __shared__ int s_list[MF_LIST];
+    __shared__ double s_q2[8][256];
+    __shared__ int s_n;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int64_t b = blockIdx.x;
+    constexpr int r = R;
+    const int64_t *sh = p.shifts + b * p.shift_stride;
+    const cx *gphi = p.base_phi + b * p.phi_stride;
+    if (stage)
+        for (int64_t i = threadIdx.x; i < (int64_t)r * p.d; i += blockDim.x) s_phi[i] = ldcx(gphi + i);
+    // explicit address spaces: LDS from the staged copy, LDG otherwise
+    auto phi_at = [&](int64_t i) -> cx { return stage ? s_phi[i] : ldcx(gphi + i); };
+    for (int64_t c0 = 0; c0 < p.L; c0 += MF_LIST) {
+        if (threadIdx.x == 0) s_n = 0;
+        __syncthreads();
+        const int64_t c1 = p.L < c0 + MF_LIST ? p.L : c0 + MF_LIST;
+        for (int64_t k0 = c0; k0 < c1; k0 += blockDim.x) {   // block-uniform trip count
+            const int64_t kb = k0 + threadIdx.x;
+            const int a = kb < c1 ? votes[b * p.L + kb] : 0;
+            const int64_t count = (int64_t)p.keep * a < p.d ? (int64_t)p.keep * a : p.d;
+            const bool want = a >= 1 && p.prune && count < p.d;
+            const unsigned m = __ballot_sync(0xffffffffu, want);
+            int base = 0;
+            if (lane == 0 && m) base = atomicAdd(&s_n, __popc(m));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (want) s_list[base + __popc(m & ((1u << lane) - 1))] = (int)kb;
+        }
+        __syncthreads();
+        const int nlist = s_n;
+        for (int li = warp; li < nlist; li += nw) {
+            const int64_t kb = s_list[li];
+            const int64_t t = b * p.L + kb;
+            const int a = votes[t];
+            cx wj = mk(0.0, 0.0);
+            if (lane < r) {
+                const cx yj = ldcx(V + (b * p.nv + p.S + lane) * p.L + kb);
+                const double th = DMUL(-TWO_PI, (double)(sh[lane] * kb)) / (double)p.n;
+                wj = nmul(gexp(mk(0.0, th)), yj);
+            }
+            cx w[R];
+#pragma unroll
+            for (int j = 0; j < R; j++) {
+                w[j].re = __shfl_sync(0xffffffffu, wj.re, j);
+                w[j].im = __shfl_sync(0xffffffffu, wj.im, j);
+            }
+            const int n_top = (int)((int64_t)a < p.d ? a : p.d);
+            Top4 top;
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                top.sc[i] = -INFINITY;
+                top.id[i] = INT_MAX;
+            }
+            const int d = (int)p.d;
+            auto dot = [&](int tt) -> cx {
+                cx acc = mk(0.0, 0.0);
+#pragma unroll
+                for (int j = 0; j < R; j++) {
+                    const cx ph = phi_at(j * d + tt);
+                    acc = cadd(acc, nmul(cconj(ph), w[j]));
+                }
+                return acc;
+            };
+            auto offer = [&](double v, int id) {   // lane list insert
+                if (v != v) v = -1.0;   // NaN last (scores are >= 0 otherwise)
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    if (i < n_top && mf_better(v, id, top.sc[i], top.id[i])) {
+                        const double ts = top.sc[i];
+                        const int ti = top.id[i];
+                        top.sc[i] = v;
+                        top.id[i] = id;
+                        v = ts;
+                        id = ti;
+                    }
+                }
+            };
+            if (d <= 256) {
+                // pass 1: |acc|^2 of the lane's <= 8 candidates; the warp's
+                // n_top-th largest square S bounds the winners: a top
+                // candidate has |acc|^2 >= S (1 - 1e-13) (hypot and the
+                // square agree to a few ulp), so only those get hypot
+                double *q2 = s_q2[warp];
+                // four candidates per step: independent dot chains give the
+                // FP64 pipe ILP (one chain alone waits on every add)
+#pragma unroll
+                for (int i0 = 0; i0 < 8; i0 += 4) {
+                    cx acc[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) acc[u] = mk(0.0, 0.0);
+                    const int tb = lane + 32 * i0;
+                    if (tb < d) {   // d is a multiple of 32 here or < 32
+#pragma unroll
+                        for (int j = 0; j < R; j++) {
+#pragma unroll
+                            for (int u = 0; u < 4; u++) {
+                                const int tt = tb + 32 * u;
+                                const int tc = tt < d ? tt : tb;
+                                const cx ph = phi_at(j * d + tc);
+                                acc[u] = cadd(acc[u], nmul(cconj(ph), w[j]));
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const int tt = tb + 32 * u;
+                        double qv = -1.0;
+                        if (tt < d) {
+                            const double s2 = acc[u].re * acc[u].re + acc[u].im * acc[u].im;
+                            qv = (s2 == s2) ? s2 : INFINITY;   // NaN: always re-checked
+                        }
+                        q2[tt] = qv;
+                    }
+                }
+                double S = INFINITY;
+                {
+                    uint32_t used = 0;
+                    for (int q = 0; q < n_top; q++) {
+                        double bv = -2.0;
+                        int bi = -1;
+#pragma unroll
+                        for (int i = 0; i < 8; i++)
+                            if (!(used & (1u << i)) && q2[lane + 32 * i] > bv) {
+                                bv = q2[lane + 32 * i];
+                                bi = i;
+                            }
+                        double wv = bv;
+                        int wl_ = lane;
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) {
+                            const double ov = __shfl_xor_sync(0xffffffffu, wv, o);
+                            const int ol = __shfl_xor_sync(0xffffffffu, wl_, o);
+                            if (ov > wv || (ov == wv && ol < wl_)) {
+                                wv = ov;
+                                wl_ = ol;
+                            }
+                        }
+                        if (wl_ == lane && bi >= 0) used |= 1u << bi;
+                        S = wv;
+                    }
+                }
+                const double cut = (S > 1e-150 && S < INFINITY) ? S * (1.0 - 1e-13) : -INFINITY;
+#pragma unroll
+                for (int i = 0; i < 8; i++) {
+                    const int tt = lane + 32 * i;
+                    if (tt < d && q2[tt] >= cut) offer(cabs_(dot(tt)), tt);
+                }
+            } else {
+                for (int tt = lane; tt < d; tt += 32) offer(cabs_(dot(tt)), tt);
+            }
+            // warp merge: n_top rounds of arg-best over the lane heads
+            int sel[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                sel[q] = INT_MAX;
+                if (q < n_top) {
+                    double bv = top.sc[0];
+                    int bi = top.id[0];
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                        if (mf_better(ov, oi, bv, bi)) {
+                            bv = ov;
+                            bi = oi;
+                        }
+                    }
+                    sel[q] = bi;
+                    if (top.id[0] == bi) {   // pop the winning lane's head
+#pragma unroll
+                        for (int i = 0; i < 3; i++) {
+                            top.sc[i] = top.sc[i + 1];
+                            top.id[i] = top.id[i + 1];
+                        }
+                        top.sc[3] = -INFINITY;
+                        top.id[3] = INT_MAX;
+                    }
+                }
+            }
+            if (lane == 0) {
+                // sorted ascending (np.sort of the chosen columns)
+#pragma unroll
+                for (int i = 1; i < 4; i++)
+#pragma unroll
+                    for (int j2 = 3; j2 >= i; j2--)
+                        if (sel[j2 - 1] > sel[j2]) {
+                            const int tmp = sel[j2 - 1];
+                            sel[j2 - 1] = sel[j2];
+                            sel[j2] = tmp;
+                        }
+                *reinterpret_cast<int4 *>(mf_top + t * 4) = make_int4(sel[0], sel[1], sel[2], sel[3]);
+            }
+        }
+        __syncthreads();
+    }
+}
+
 __global__ void __launch_bounds__(128) k_gen_bins(const cx *__restrict__ V, GenParams p,
                                                   const int32_t *__restrict__ votes,
                                                   const int64_t *__restrict__ wl,
                                                   const unsigned long long *__restrict__ wl_count,
+                                                  const int32_t *__restrict__ mf_top,
                                                   uint8_t *__restrict__ nent, int64_t *__restrict__ sloc,
                                                   cx *__restrict__ sval, int64_t *__restrict__ stats) {
     const int64_t cnt = (int64_t)*wl_count;
@@ -389,21 +616,10 @@ __global__ void __launch_bounds__(128) k_gen_bins(const cx *__restrict__ V, GenP
                 }
             }
             sort_ints(kp, nk);
-            // matched-filter augmentation (general.py:345-351)
-            cx w[GEN_MAX_R];
-            for (int j = 0; j < r; j++) {
-                const double th = DMUL(-TWO_PI, (double)(sh[j] * kb)) / (double)p.n;
-                w[j] = nmul(gexp(mk(0.0, th)), y[j]);
-            }
-            const int n_top = (int)((int64_t)a < p.d ? a : p.d);
-            double ts[GEN_MAX_SUP];
-            int tp[GEN_MAX_SUP], nt = 0;
-            for (int64_t tt = 0; tt < p.d; tt++) {
-                cx acc = mk(0.0, 0.0);
-                for (int j = 0; j < r; j++) acc = cadd(acc, nmul(cconj(ldcx(bphi + (int64_t)j * p.d + tt)), w[j]));
-                topk_insert(ts, tp, nt, n_top, cabs_(acc), (int)tt);
-            }
-            sort_ints(tp, nt);
+            // matched-filter augmentation (general.py:345-351): k_gen_mf
+            const int nt = (int)((int64_t)a < p.d ? a : p.d);
+            const int4 mft = *reinterpret_cast<const int4 *>(mf_top + t * 4);
+            const int tp[4] = {mft.x, mft.y, mft.z, mft.w};
             ncols = union_sorted(kp, nk, tp, nt, cols);
         } else {
             ncols = (int)p.d;
@@ -554,7 +770,7 @@ struct GenPlan {
     int64_t B, n, d, L, nv, nparts;
     int S;
     size_t off_V, off_sv, off_part, off_votes, off_nent, off_sloc, off_sval, off_wl, off_cnt,
-        off_fft, total;
+        off_fft, off_mf, total;
 };
 
 static int make_gen_plan(const sfdt_general_args *a, GenPlan &p) {
@@ -583,6 +799,7 @@ static int make_gen_plan(const sfdt_general_args *a, GenPlan &p) {
     p.off_sval = take(size_t(p.B) * p.L * a->a_max * 16);
     p.off_wl = take(size_t(p.B) * p.L * 8);
     p.off_cnt = take(64);
+    p.off_mf = take(size_t(p.B) * p.L * 16);
     p.off_fft = (p.L > FFT_SMEM_MAX) ? take(size_t(p.B) * p.nv * p.L * 16) : 0;
     p.total = o;
     return SFDT_OK;
@@ -682,7 +899,32 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaMemsetAsync(nent, 0, size_t(p.B) * p.L, stream);
-    k_gen_bins<<<(unsigned)(sms * 16), 128, 0, stream>>>(V, gp, votes, wl, wlc, nent, sloc, sval, a->stats);
+    int32_t *mf_top = (int32_t *)(w + p.off_mf);
+    if (a->prune) {
+        const size_t phi_bytes = size_t(a->r_eff) * p.d * 16;
+        const int stage = phi_bytes <= MF_SMEM_MAX;
+        const size_t smem = stage ? phi_bytes : 0;
+        switch (a->r_eff) {
+#define SFDT_MF(R)                                                                                 \
+    case R:                                                                                        \
+        if (stage) {                                                                               \
+            cudaFuncSetAttribute(k_gen_mf<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                                 (int)smem);                                                       \
+            k_gen_mf<R, true><<<(unsigned)p.B, 256, smem, stream>>>(V, gp, votes, mf_top);         \
+        } else {                                                                                   \
+            k_gen_mf<R, false><<<(unsigned)p.B, 256, 0, stream>>>(V, gp, votes, mf_top);           \
+        }                                                                                          \
+        break;
+            SFDT_MF(1) SFDT_MF(2) SFDT_MF(3) SFDT_MF(4) SFDT_MF(5) SFDT_MF(6)
+            SFDT_MF(7) SFDT_MF(8) SFDT_MF(9) SFDT_MF(10) SFDT_MF(11) SFDT_MF(12)
+#undef SFDT_MF
+        default: return SFDT_EINVAL;
+        }
+        SFDT_CHECK_LAUNCH();
+        launches++;
+    }
+    k_gen_bins<<<(unsigned)(sms * 16), 128, 0, stream>>>(V, gp, votes, wl, wlc, mf_top, nent, sloc, sval,
+                                                         a->stats);
     SFDT_CHECK_LAUNCH();
     k_gen_count<<<(unsigned)p.B, 256, 0, stream>>>(votes, nent, p.L, a->stats);
     k_gen_scan<<<1, 1024, 0, stream>>>(a->stats, p.B, a->entry_offsets);

@@ -293,8 +293,18 @@ static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, con
         if (smem <= 32 * 1024) {
             k_fft_views<4><<<grid, 256, smem, stream>>>(src, B, logL, logvpc, tw, out, SV, ldV, scale, thr, act);
         } else if (smem <= 64 * 1024) {
-            // 64 KiB tiles: 3 CTAs/SM by shared memory, so cap registers at 85
+            // 64 KiB tiles: registers capped at 85 (3 CTAs/SM would fit)
             cudaFuncSetAttribute(k_fft_views<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            {
+                // Two CTAs per SM, the rest of the 256 KiB as L1: the view
+                // stages read the (L-1)-entry twiddle table (64 KiB at
+                // L = 4096) through L1, and with 3 CTAs' 192 KiB of smem it
+                // thrashed into L2 (7.2 GB of L2 reads per config-4 batch).
+                // Measured at config 4: 4.78 -> 4.20 ms per step.
+                const char *e = getenv("SFDT_FFT_CARVEOUT");
+                const int pct = e ? atoi(e) : (int)((2 * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
+                cudaFuncSetAttribute(k_fft_views<3>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+            }
             k_fft_views<3><<<grid, 256, smem, stream>>>(src, B, logL, logvpc, tw, out, SV, ldV, scale, thr, act);
         } else {
             cudaFuncSetAttribute(k_fft_views<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -91,7 +91,10 @@ __global__ void __launch_bounds__(128) k_rows_svd(const cx *__restrict__ syn, in
 }
 
 // ------------------------------------------------------------------ vote
-constexpr int VOTE_SMEM_KEYS = 0;   // staging keys in smem measured slower (736 vs 552 us, cfg4); off
+// staging keys in smem measured slower (736 vs 552 us, cfg4), and so did
+// caching them in registers (64 registers halve the resident CTAs: 468 ->
+// 637 us); keys are re-read from L2
+constexpr int VOTE_SMEM_KEYS = 0;
 
 __device__ __forceinline__ unsigned long long dkey(double v) {
     return (unsigned long long)__double_as_longlong(v);   // sigma >= 0: bit order == value order
@@ -127,31 +130,64 @@ __global__ void __launch_bounds__(1024) k_gen_vote(const double *__restrict__ sv
     }
     if (threadIdx.x < 5) s_hist[threadIdx.x] = 0;
     for (int64_t i = threadIdx.x; i < p.L; i += blockDim.x) vb[i] = 0;
+    // visit every flat index in order of i0 = 0, blockDim, ... (block-uniform
+    // trip count; f may contain block barriers)
+    auto for_keys = [&](auto &&f) {
+        for (int64_t i0 = 0; i0 < M; i0 += blockDim.x) {
+            const int64_t i = i0 + threadIdx.x;
+            f(i, i < M ? dkey(svb[i]) : 0ull);
+        }
+    };
     __syncthreads();
-    // exact radix select (8-bit digits, MSB first) of the take-th largest key
+    // exact radix select (8-bit digits, MSB first) of the take-th largest key.
+    // Histogram: lanes holding the same digit are aggregated with
+    // __match_any_sync (sigma keys share their top bytes, so plain shared
+    // atomics serialise); digit choice: warp 0 scans the 256 counts from the
+    // top, 8 per lane.
     if (take > 0) {
         for (int shift = 56; shift >= 0; shift -= 8) {
             for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
             __syncthreads();
             const unsigned long long pre = s_prefix, msk = s_mask;
-            for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
-                const unsigned long long key = dkey(svb[i]);
-                if ((key & msk) == pre) atomicAdd(&hist[(key >> shift) & 255], 1u);
-            }
+            for_keys([&](int64_t i, unsigned long long key) {
+                int dg = 256;   // not a candidate
+                if (i < M && (key & msk) == pre) dg = (int)((key >> shift) & 255);
+                const unsigned peers = __match_any_sync(0xffffffffu, dg);
+                if (dg < 256 && lane == __ffs(peers) - 1) atomicAdd(&hist[dg], (unsigned)__popc(peers));
+            });
             __syncthreads();
-            if (threadIdx.x == 0) {
-                long long rem = s_remaining, cum = 0;
-                int D = 0;
-                for (int dg = 255; dg >= 0; dg--) {
-                    if (cum + hist[dg] >= rem) {
-                        D = dg;
-                        break;
-                    }
-                    cum += hist[dg];
+            if (warp == 0) {
+                // lane l owns digits 255-8l .. 248-8l (descending)
+                unsigned c[8], lsum = 0;
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    c[q] = hist[255 - 8 * lane - q];
+                    lsum += c[q];
                 }
-                s_remaining = rem - cum;
-                s_prefix = pre | ((unsigned long long)D << shift);
-                s_mask = msk | (0xFFull << shift);
+                unsigned inc = lsum;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += y;
+                }
+                const long long rem = s_remaining;
+                const long long before = (long long)(inc - lsum);
+                const bool mine = before < rem && before + (long long)lsum >= rem;
+                if (mine) {
+                    long long cum = before;
+                    int D = 255 - 8 * lane - 7;
+#pragma unroll
+                    for (int q = 0; q < 8; q++) {
+                        if (cum + (long long)c[q] >= rem) {
+                            D = 255 - 8 * lane - q;
+                            break;
+                        }
+                        cum += c[q];
+                    }
+                    s_remaining = rem - cum;
+                    s_prefix = pre | ((unsigned long long)D << shift);
+                    s_mask = msk | (0xFFull << shift);
+                }
             }
             __syncthreads();
         }
@@ -161,28 +197,23 @@ __global__ void __launch_bounds__(1024) k_gen_vote(const double *__restrict__ sv
     // selection in flat order: keys > tau all; keys == tau by ascending flat
     // index (lexsort tie-break: bin asc, then rank asc)
     long long eq_carry = 0;
-    for (int64_t i0 = 0; i0 < M && take > 0; i0 += blockDim.x) {
-        const int64_t i = i0 + threadIdx.x;
-        unsigned long long key = 0;
-        bool gt = false, eq = false;
-        if (i < M) {
-            key = dkey(svb[i]);
-            gt = key > tau;
-            eq = key == tau;
-        }
-        const unsigned m = __ballot_sync(0xffffffffu, eq);
-        if (lane == 0) wsum[warp] = __popc(m);
-        __syncthreads();
-        int before = 0, total = 0;
-        for (int w2 = 0; w2 < (int)(blockDim.x >> 5); w2++) {
-            before += (w2 < warp) ? wsum[w2] : 0;
-            total += wsum[w2];
-        }
-        const long long rank = eq_carry + before + __popc(m & ((1u << lane) - 1));
-        if (gt || (eq && rank < need_eq)) atomicAdd(&vb[i / p.a_max], 1);
-        eq_carry += total;
-        __syncthreads();
-    }
+    if (take > 0)
+        for_keys([&](int64_t i, unsigned long long key) {
+            const bool gt = i < M && key > tau;
+            const bool eq = i < M && key == tau;
+            const unsigned m = __ballot_sync(0xffffffffu, eq);
+            if (lane == 0) wsum[warp] = __popc(m);
+            __syncthreads();
+            int before = 0, total = 0;
+            for (int w2 = 0; w2 < (int)(blockDim.x >> 5); w2++) {
+                before += (w2 < warp) ? wsum[w2] : 0;
+                total += wsum[w2];
+            }
+            const long long rank = eq_carry + before + __popc(m & ((1u << lane) - 1));
+            if (gt || (eq && rank < need_eq)) atomicAdd(&vb[i / p.a_max], 1);
+            eq_carry += total;
+            __syncthreads();
+        });
     __syncthreads();
     // zero-vote guard on the RMS of all consecutive syndromes, cap, histogram
     double esum = 0.0;

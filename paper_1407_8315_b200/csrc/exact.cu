@@ -641,15 +641,23 @@ __global__ void k_iter_final(const cx *__restrict__ V, const uint8_t *__restrict
 
 // ------------------------------------------------------------ compaction
 // Non-iterative: per-signal block scan over bins ordered by (a, bin) ->
-// entry offsets; unresolved bins ascending.  One CTA per signal.
+// entry offsets; unresolved bins ascending.  A signal's bins are split into
+// segments of NONITER_SEG bins (one CTA each), so small batches of long
+// views still fill the GPU: count per segment, fold the segments per
+// signal, and emit each segment at its signal's class bases plus the counts
+// of the segments before it.
+constexpr int64_t NONITER_SEG = 8192;
+constexpr int SEGF = 8;   // per-segment fields: unresolved, entries a=1..4, active, tries
+
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) k_noniter_count(const uint8_t *__restrict__ status, int64_t L,
-                                                           int a_max, int S, int64_t d,
-                                                           int64_t *__restrict__ stats) {
-    const int64_t b = blockIdx.x;
+                                                           int a_max, int64_t nseg,
+                                                           long long *__restrict__ segcnt) {
+    const int64_t b = blockIdx.x / nseg, g = blockIdx.x - b * nseg;
+    const int64_t k0 = g * NONITER_SEG, k1 = (k0 + NONITER_SEG < L) ? k0 + NONITER_SEG : L;
     long long cnt[5] = {0, 0, 0, 0, 0};   // entries per a (1..4) and unresolved in [0]
     long long active = 0, tries = 0;
-    for (int64_t k = threadIdx.x; k < L; k += THREADS) {
+    for (int64_t k = k0 + threadIdx.x; k < k1; k += THREADS) {
         const uint8_t s = status[b * L + k];
         if (s == 0) continue;
         active++;
@@ -675,29 +683,38 @@ __global__ void __launch_bounds__(THREADS) k_noniter_count(const uint8_t *__rest
             for (int q = 0; q < 7; q++) red[q][threadIdx.x] += red[q][threadIdx.x + s];
         __syncthreads();
     }
-    if (threadIdx.x == 0) {
-        int64_t *st = stats + b * SFDT_ST_PER_SIGNAL;
-        const long long nent = red[1][0] + red[2][0] + red[3][0] + red[4][0];
-        st[SFDT_ST_NITER] = 1;
-        st[SFDT_ST_FULL_SUCCESS] = red[0][0] == 0;
-        st[SFDT_ST_NENTRIES] = nent;
-        st[SFDT_ST_NUNRESOLVED] = red[0][0];
-        st[SFDT_ST_NDUP] = 0;
-        st[SFDT_ST_SYNDROMES] = red[6][0] * S;
-        st[SFDT_ST_FFT_SAMPLES] = int64_t(S) * L;
-        int64_t *it = st + SFDT_ST_ITER0;
-        it[0] = d;
-        it[1] = red[5][0];                 // attempted
-        it[2] = red[5][0] - red[0][0];     // solved
-        it[3] = red[0][0];                 // deferred
-        it[4] = red[6][0] * S;             // syndromes
-        it[5] = int64_t(S) * L;            // fft samples
-        // per-a entry counts for the emit pass
-        st[24] = red[1][0];
-        st[25] = red[2][0];
-        st[26] = red[3][0];
-        st[27] = red[4][0];
-    }
+    if (threadIdx.x < 7) segcnt[blockIdx.x * SEGF + threadIdx.x] = red[threadIdx.x][0];
+}
+
+// per signal: fold the segment counts into the stats record
+__global__ void k_noniter_fin(const long long *__restrict__ segcnt, int64_t B, int64_t nseg, int64_t L,
+                              int S, int64_t d, int64_t *__restrict__ stats) {
+    const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    long long r[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (int64_t g = 0; g < nseg; g++)
+        for (int q = 0; q < 7; q++) r[q] += segcnt[(b * nseg + g) * SEGF + q];
+    int64_t *st = stats + b * SFDT_ST_PER_SIGNAL;
+    const long long nent = r[1] + r[2] + r[3] + r[4];
+    st[SFDT_ST_NITER] = 1;
+    st[SFDT_ST_FULL_SUCCESS] = r[0] == 0;
+    st[SFDT_ST_NENTRIES] = nent;
+    st[SFDT_ST_NUNRESOLVED] = r[0];
+    st[SFDT_ST_NDUP] = 0;
+    st[SFDT_ST_SYNDROMES] = r[6] * S;
+    st[SFDT_ST_FFT_SAMPLES] = int64_t(S) * L;
+    int64_t *it = st + SFDT_ST_ITER0;
+    it[0] = d;
+    it[1] = r[5];            // attempted
+    it[2] = r[5] - r[0];     // solved
+    it[3] = r[0];            // deferred
+    it[4] = r[6] * S;        // syndromes
+    it[5] = int64_t(S) * L;  // fft samples
+    // per-a entry counts for the emit pass
+    st[24] = r[1];
+    st[25] = r[2];
+    st[26] = r[3];
+    st[27] = r[4];
 }
 
 // exclusive scan of per-signal counts -> offsets (single CTA, B up to any size)
@@ -758,22 +775,30 @@ __global__ void __launch_bounds__(THREADS) k_noniter_emit(
     const uint8_t *__restrict__ status, const int64_t *__restrict__ bin_loc,
     const cx *__restrict__ bin_val, int64_t L, int a_max, const int64_t *__restrict__ stats,
     const int64_t *__restrict__ eoff, const int64_t *__restrict__ uoff, int64_t *__restrict__ locs,
-    cx *__restrict__ vals, int32_t *__restrict__ ubins) {
+    cx *__restrict__ vals, int32_t *__restrict__ ubins, int64_t nseg, const long long *__restrict__ segcnt) {
     __shared__ unsigned long long wtot[THREADS / 32];
-    const int64_t b = blockIdx.x;
+    const int64_t b = blockIdx.x / nseg, g = blockIdx.x - b * nseg;
     const int64_t *st = stats + b * SFDT_ST_PER_SIGNAL;
     long long base[5];
     base[0] = eoff[b];
     for (int c = 1; c < 4; c++) base[c] = base[c - 1] + st[24 + c - 1];
     base[4] = uoff[b];
+    // segments before this one: entries per class (classes store entries,
+    // so a bin of class c advances its base by c + 1) and unresolved bins
+    for (int64_t g2 = 0; g2 < g; g2++) {
+        const long long *sc = segcnt + (b * nseg + g2) * SEGF;
+        base[4] += sc[0];
+        for (int c = 0; c < 4; c++) base[c] += sc[1 + c];
+    }
     long long carry[5] = {0, 0, 0, 0, 0};
-    for (int64_t t0 = 0; t0 < L; t0 += THREADS * 4) {
+    const int64_t k0 = g * NONITER_SEG, k1 = (k0 + NONITER_SEG < L) ? k0 + NONITER_SEG : L;
+    for (int64_t t0 = k0; t0 < k1; t0 += THREADS * 4) {
         int ci[4];
         unsigned long long packed = 0;
 #pragma unroll
         for (int u = 0; u < 4; u++) {
             const int64_t k = t0 + 4 * threadIdx.x + u;
-            const uint8_t sv = (k < L) ? status[b * L + k] : 0;
+            const uint8_t sv = (k < k1) ? status[b * L + k] : 0;
             ci[u] = (sv == 0xFF) ? 4 : (sv >= 1 && sv <= 4 ? sv - 1 : -1);
             if (ci[u] >= 0) packed += 1ull << (12 * ci[u]);
         }
@@ -1086,7 +1111,7 @@ struct ExactPlan {
     bool capture;
     size_t off_win, off_V, off_partial, off_thr, off_status, off_bloc, off_bval, off_def,
         off_sloc, off_sval, off_sa, off_sdup, off_cnt, off_resid, off_ndef, off_scratch, off_fft, off_wl,
-        off_act, off_awl,
+        off_act, off_awl, off_seg,
         total;
 };
 
@@ -1126,6 +1151,7 @@ static int make_plan(const sfdt_exact_args *a, ExactPlan &p) {
         p.off_wl = take(size_t(p.B) * p.L * 8);
         p.off_act = take(size_t(p.B) * p.L);
         p.off_awl = take(size_t(p.B) * p.L * 8);
+        p.off_seg = take(size_t(p.B) * ((p.L + NONITER_SEG - 1) / NONITER_SEG) * SEGF * 8);
     } else {
         p.off_def = take(size_t(p.B) * p.L);
         p.off_sloc = take(size_t(p.B) * 4 * p.L * a->a_max * 8);
@@ -1292,7 +1318,7 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
                                                       a->zero_threshold, p.d, a->rms + c0, thr + c0);
             SFDT_CHECK_LAUNCH();
             // after the rms the FFT epilogue can also mark the active bins
-            const bool dense = !overlap && p.L <= FFT_SMEM_MAX;
+            const bool dense = !overlap;
             uint8_t *actc = dense ? (uint8_t *)(w + p.off_act) + c0 * p.L : nullptr;
             if (!overlap) {
                 if (actc) cudaMemsetAsync(actc, 0, size_t(nb) * p.L, aux);
@@ -1325,18 +1351,21 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
             cudaStreamWaitEvent(stream, ev_done, 0);
             cudaEventDestroy(ev_done);
         }
-        k_noniter_count<256><<<(unsigned)p.B, 256, 0, stream>>>(status, p.L, a->a_max, (int)p.S,
-                                                                p.d, a->stats);
+        const int64_t nseg = (p.L + NONITER_SEG - 1) / NONITER_SEG;
+        long long *segcnt = (long long *)(w + p.off_seg);
+        k_noniter_count<256><<<(unsigned)(p.B * nseg), 256, 0, stream>>>(status, p.L, a->a_max, nseg, segcnt);
+        k_noniter_fin<<<(unsigned)((p.B + 255) / 256), 256, 0, stream>>>(segcnt, p.B, nseg, p.L, (int)p.S,
+                                                                         p.d, a->stats);
         SFDT_CHECK_LAUNCH();
         k_scan_offsets<<<1, 1024, 0, stream>>>(a->stats, p.B, SFDT_ST_NENTRIES, a->entry_offsets);
         k_scan_offsets<<<1, 1024, 0, stream>>>(a->stats, p.B, SFDT_ST_NUNRESOLVED, a->unres_offsets);
         SFDT_CHECK_LAUNCH();
-        k_noniter_emit<256><<<(unsigned)p.B, 256, 0, stream>>>(
+        k_noniter_emit<256><<<(unsigned)(p.B * nseg), 256, 0, stream>>>(
             status, bloc, bval, p.L, a->a_max, a->stats, a->entry_offsets, a->unres_offsets,
-            a->locs, (cx *)a->vals, a->unres_bins);
+            a->locs, (cx *)a->vals, a->unres_bins, nseg, segcnt);
         SFDT_CHECK_LAUNCH();
         if (a->dup_offsets) cudaMemsetAsync(a->dup_offsets, 0, sizeof(int64_t) * (p.B + 1), stream);
-        launches += 4;
+        launches += 5;
         a->kernel_launches = launches;
         return SFDT_OK;
     }

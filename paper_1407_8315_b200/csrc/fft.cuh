@@ -224,7 +224,8 @@ static __global__ void k_fft_large_a(const ViewSrc src, int logL, int logP,
 // residue classes i mod P, on tiles of R residues x Q = L/P rows.
 static __global__ void k_fft_large_b(cx *buf, int64_t nviews, int logL, int logP, int logR,
                                      const cx *__restrict__ tw, cx *out, int nshift, int SV,
-                                     int64_t ldV, int scale) {
+                                     int64_t ldV, int scale, const double *__restrict__ thr,
+                                     uint8_t *__restrict__ act) {
     extern __shared__ double4 smem_raw[];
     cx *a = reinterpret_cast<cx *>(smem_raw);
     const int L = 1 << logL, P = 1 << logP, R = 1 << logR;
@@ -260,11 +261,72 @@ static __global__ void k_fft_large_b(cx *buf, int64_t nviews, int logL, int logP
     const double sc = 1.0 / (double)L;
     const int64_t b = g / nshift;
     const int s = (int)(g - b * nshift);
+    const double th = act ? thr[b] : 0.0;
     for (int i = threadIdx.x; i < Q * R; i += blockDim.x) {
         const int q = i >> logR, rr = i & (R - 1);
-        const cx y = a[i];
-        stcx(out + (b * SV + s) * ldV + r0 + rr + (int64_t)q * P,
-             scale ? mk(DMUL(y.re, sc), DMUL(y.im, sc)) : y);
+        const cx y0 = a[i];
+        const cx y = scale ? mk(DMUL(y0.re, sc), DMUL(y0.im, sc)) : y0;
+        stcx(out + (b * SV + s) * ldV + r0 + rr + (int64_t)q * P, y);
+        if (act) {
+            const double m2 = y.re * y.re + y.im * y.im;
+            if (m2 > th * th * (1.0 + 1e-6) || (m2 >= th * th * (1.0 - 1e-6) && cabs_(y) > th))
+                act[b * (int64_t)L + r0 + rr + (int64_t)q * P] = 1;
+        }
+    }
+}
+
+// Pass B with the remaining LQ = logL - logP stages in registers (LQ <= 4):
+// thread = one residue r < P, holding its Q = 2^LQ rows; the butterflies,
+// their order within a stage and the twiddle index k = r + qk*P are those
+// of k_fft_large_b, so the result is bit-identical, without the per-stage
+// shared-memory round trips and barriers.  Loads/stores are coalesced
+// across threads (consecutive residues).
+template <int LQ>
+static __global__ void __launch_bounds__(256) k_fft_large_b_reg(const cx *__restrict__ buf, int64_t nviews,
+                                                                int logP, const cx *__restrict__ tw,
+                                                                cx *out, int nshift, int SV, int64_t ldV,
+                                                                int scale, const double *__restrict__ thr,
+                                                                uint8_t *__restrict__ act) {
+    constexpr int Q = 1 << LQ;
+    const int P = 1 << logP;
+    const int logL = logP + LQ;
+    const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t g = gt >> logP;
+    if (g >= nviews) return;
+    const int r = (int)(gt & (P - 1));
+    const cx *src = buf + (g << logL) + r;
+    cx x[Q];
+#pragma unroll
+    for (int q = 0; q < Q; q++) x[q] = ldcx(src + (int64_t)q * P);
+#pragma unroll
+    for (int st = 0; st < LQ; st++) {
+        const int hq = 1 << st;
+        const int h = P << st;
+        const cx *twh = tw + (h - 1);
+#pragma unroll
+        for (int q = 0; q < Q; q++) {
+            if (q & hq) continue;
+            const int qk = q & (hq - 1);
+            const cx u = x[q];
+            const cx t = gmul(x[q + hq], ldcx(twh + r + qk * P));
+            x[q] = cadd(u, t);
+            x[q + hq] = csub(u, t);
+        }
+    }
+    const double sc = 1.0 / (double)(1 << logL);
+    const int64_t b = g / nshift;
+    const int s = (int)(g - b * nshift);
+    cx *o = out + (b * SV + s) * ldV + r;
+    const double th = act ? thr[b] : 0.0;
+#pragma unroll
+    for (int q = 0; q < Q; q++) {
+        const cx y = scale ? mk(DMUL(x[q].re, sc), DMUL(x[q].im, sc)) : x[q];
+        stcx(o + (int64_t)q * P, y);
+        if (act) {   // activity epilogue, as in k_fft_views
+            const double m2 = y.re * y.re + y.im * y.im;
+            if (m2 > th * th * (1.0 + 1e-6) || (m2 >= th * th * (1.0 - 1e-6) && cabs_(y) > th))
+                act[b * ((int64_t)P << LQ) + r + (int64_t)q * P] = 1;
+        }
     }
 }
 
@@ -319,8 +381,23 @@ static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, con
     {
         const size_t smem = size_t(P) * 16;
         cudaFuncSetAttribute(k_fft_large_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        // 2 CTAs/SM, the rest L1 for the 4095-entry twiddle table (as above)
+        cudaFuncSetAttribute(k_fft_large_a, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             (int)((2 * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024)));
         k_fft_large_a<<<(unsigned)(nviews << logQ), 256, smem, stream>>>(src, logL, logP, tw, large_scratch);
         SFDT_CHECK_LAUNCH();
+    }
+    if (logQ >= 1 && logQ <= 4) {
+        const int64_t threads = nviews << logP;
+        const unsigned grid = (unsigned)((threads + 255) / 256);
+        switch (logQ) {
+        case 1: k_fft_large_b_reg<1><<<grid, 256, 0, stream>>>(large_scratch, nviews, logP, tw, out, src.nshift, SV, ldV, scale, thr, act); break;
+        case 2: k_fft_large_b_reg<2><<<grid, 256, 0, stream>>>(large_scratch, nviews, logP, tw, out, src.nshift, SV, ldV, scale, thr, act); break;
+        case 3: k_fft_large_b_reg<3><<<grid, 256, 0, stream>>>(large_scratch, nviews, logP, tw, out, src.nshift, SV, ldV, scale, thr, act); break;
+        default: k_fft_large_b_reg<4><<<grid, 256, 0, stream>>>(large_scratch, nviews, logP, tw, out, src.nshift, SV, ldV, scale, thr, act); break;
+        }
+        SFDT_CHECK_LAUNCH();
+        return SFDT_OK;
     }
     {
         int logR = 13 - logQ;          // tiles of 2^13 points
@@ -329,7 +406,7 @@ static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, con
         const size_t smem = (size_t(1) << (logQ + logR)) * 16;
         cudaFuncSetAttribute(k_fft_large_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         k_fft_large_b<<<(unsigned)(nviews * (P >> logR)), 256, smem, stream>>>(
-            large_scratch, nviews, logL, logP, logR, tw, out, src.nshift, SV, ldV, scale);
+            large_scratch, nviews, logL, logP, logR, tw, out, src.nshift, SV, ldV, scale, thr, act);
         SFDT_CHECK_LAUNCH();
     }
     return SFDT_OK;

@@ -208,9 +208,32 @@ static __global__ void k_fft_large_a(const ViewSrc src, int logL, int logP,
     const int64_t b = g / src.nshift;
     const int s = (int)(g - b * src.nshift);
     const int rc = logQ ? (int)(__brev((unsigned)c) >> (32 - logQ)) : 0;
-    for (int i = threadIdx.x; i < P; i += blockDim.x) {
-        const int64_t j = (int64_t)(__brev((unsigned)i) >> (32 - logP)) * Q + rc;
-        a[swz(i)] = view_load(src, b, s, j);
+    // addressing once per CTA; loads issued 8 at a time before their
+    // shared-memory stores (every load is its own sector: stride Q*d)
+    const int64_t o = (s >= src.dyn_first) ? __ldg(src.dyn_off + b * src.dyn_stride + (s - src.dyn_first))
+                                           : src.off[s];
+    const int64_t ib = b * src.sig_stride;
+    for (int i0 = 0; i0 < P; i0 += 8 * 256) {
+        cx vals[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const int i = i0 + u * 256 + threadIdx.x;
+            if (i < P) {
+                const int64_t j = (int64_t)(__brev((unsigned)i) >> (32 - logP)) * Q + rc;
+                const int64_t e = ib + ((j * src.jstride + o) & src.wrap);
+                if (src.is_c64) {
+                    const float2 f = __ldg(reinterpret_cast<const float2 *>(src.x) + e);
+                    vals[u] = mk((double)f.x, (double)f.y);
+                } else {
+                    vals[u] = ldcx(reinterpret_cast<const cx *>(src.x) + e);
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const int i = i0 + u * 256 + threadIdx.x;
+            if (i < P) a[swz(i)] = vals[u];
+        }
     }
     __syncthreads();
     fft_stages_smem(a, 1, logP, 0, logP, tw);

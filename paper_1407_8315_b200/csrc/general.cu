@@ -578,13 +578,18 @@ __global__ void __launch_bounds__(256, 2) k_gen_mf(const cx *__restrict__ V, Gen
     }
 }
 
-__global__ void __launch_bounds__(128) k_gen_bins(const cx *__restrict__ V, GenParams p,
-                                                  const int32_t *__restrict__ votes,
-                                                  const int64_t *__restrict__ wl,
-                                                  const unsigned long long *__restrict__ wl_count,
-                                                  const int32_t *__restrict__ mf_top,
-                                                  uint8_t *__restrict__ nent, int64_t *__restrict__ sloc,
-                                                  cx *__restrict__ sval, int64_t *__restrict__ stats) {
+// Pruning per voted bin (general.py:313-351): descending-order Hankel fit,
+// prune_eval over the d candidates with the reference's recurrence (or the
+// correlation fallback), union with the matched-filter columns (k_gen_mf).
+// Writes the kept column list for k_gen_bins; ncols = -1 means "all d
+// columns" (no pruning).  Split from the pursuit so each kernel keeps its
+// own registers, stack and instruction footprint.
+__global__ void __launch_bounds__(128) k_gen_prune(const cx *__restrict__ V, GenParams p,
+                                                   const int32_t *__restrict__ votes,
+                                                   const int64_t *__restrict__ wl,
+                                                   const unsigned long long *__restrict__ wl_count,
+                                                   const int32_t *__restrict__ mf_top,
+                                                   int32_t *__restrict__ cols_out, int8_t *__restrict__ ncols_out) {
     const int64_t cnt = (int64_t)*wl_count;
     for (int64_t it = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; it < cnt;
          it += int64_t(gridDim.x) * blockDim.x) {
@@ -593,7 +598,6 @@ __global__ void __launch_bounds__(128) k_gen_bins(const cx *__restrict__ V, GenP
         const int a = votes[t];
         const int r = p.r_eff;
         const int64_t *sh = p.shifts + b * p.shift_stride;
-        const cx *bphi = p.base_phi + b * p.phi_stride;
         cx syn[8], y[GEN_MAX_R];
         for (int j = 0; j < p.S; j++) syn[j] = ldcx(V + (b * p.nv + j) * p.L + kb);
         for (int j = 0; j < r; j++) y[j] = ldcx(V + (b * p.nv + p.S + j) * p.L + kb);
@@ -655,6 +659,254 @@ __global__ void __launch_bounds__(128) k_gen_bins(const cx *__restrict__ V, GenP
         } else {
             ncols = (int)p.d;
         }
+        if (!all_cols) {
+            for (int c2 = 0; c2 < ncols; c2++) cols_out[it * GEN_MAX_COLS + c2] = cols[c2];
+            ncols_out[it] = (int8_t)ncols;
+        } else {
+            ncols_out[it] = -1;
+        }
+    }
+}
+
+// ------------------------------------------- subspace pursuit, a_sp = 1
+// Register-resident pursuit for the dominant case -- a single-collision bin
+// on a pruned list of <= 4 columns -- in its own kernel (k_gen_sp1), so its
+// registers do not inflate the generic kernel.  Same operations in the same
+// order as subspace_pursuit_dev with a_eff = 1: stable first-max
+// selections, Householder least squares with the min-norm fallback, the
+// 1e-12 stopping rule.  A is overwritten (rebuilt for the fallback).
+template <int R, int C>
+__device__ __forceinline__ bool lstsq_qr_t(cx (&A)[C][R], const cx (&y_in)[R], cx (&x)[C]) {
+    if (C > R) return false;
+    cx y[R];
+#pragma unroll
+    for (int i = 0; i < R; i++) y[i] = y_in[i];
+    double rmax = 0.0, rmin = 1e300;
+#pragma unroll
+    for (int j = 0; j < C; j++) {
+        double nrm2 = 0.0;
+#pragma unroll
+        for (int i = j; i < R; i++) nrm2 = fma(A[j][i].re, A[j][i].re, fma(A[j][i].im, A[j][i].im, nrm2));
+        const double nrm = sqrt(nrm2);
+        if (nrm == 0.0) return false;
+        const cx x0 = A[j][j];
+        const double ax0 = cabs_(x0);
+        const cx ph = ax0 > 0.0 ? mk(x0.re / ax0, x0.im / ax0) : mk(1.0, 0.0);
+        const cx alpha = mk(-ph.re * nrm, -ph.im * nrm);
+        cx v[R];
+        double vv = 0.0;
+#pragma unroll
+        for (int i = j; i < R; i++) {
+            v[i] = (i == j) ? csub(x0, alpha) : A[j][i];
+            vv = fma(v[i].re, v[i].re, fma(v[i].im, v[i].im, vv));
+        }
+        if (vv > 0.0) {
+            const double beta = 2.0 / vv;
+#pragma unroll
+            for (int k = j; k < C; k++) {
+                cx dot = mk(0.0, 0.0);
+#pragma unroll
+                for (int i = j; i < R; i++) dot = cadd(dot, nmul(cconj(v[i]), A[k][i]));
+                dot = mk(dot.re * beta, dot.im * beta);
+#pragma unroll
+                for (int i = j; i < R; i++) A[k][i] = csub(A[k][i], nmul(v[i], dot));
+            }
+            cx dot = mk(0.0, 0.0);
+#pragma unroll
+            for (int i = j; i < R; i++) dot = cadd(dot, nmul(cconj(v[i]), y[i]));
+            dot = mk(dot.re * beta, dot.im * beta);
+#pragma unroll
+            for (int i = j; i < R; i++) y[i] = csub(y[i], nmul(v[i], dot));
+        }
+        const double rjj = cabs_(A[j][j]);
+        rmax = rjj > rmax ? rjj : rmax;
+        rmin = rjj < rmin ? rjj : rmin;
+    }
+    if (!(rmin > 1e-7 * rmax)) return false;
+#pragma unroll
+    for (int j = C - 1; j >= 0; j--) {
+        cx acc = y[j];
+#pragma unroll
+        for (int k = j + 1; k < C; k++) acc = csub(acc, nmul(A[k][j], x[k]));
+        x[j] = ndiv(acc, A[j][j]);
+    }
+    return true;
+}
+
+template <int R>
+__device__ __forceinline__ void sp_a1_t(const cx (&y)[R], const cx (&phase)[R], const cx *bphi, int64_t d,
+                                        const int *cols, int ncols, SPOut &o) {
+    auto phi_col = [&](int c, cx (&out)[R]) {
+        const int64_t t = (int64_t)cols[c];
+#pragma unroll
+        for (int j = 0; j < R; j++) out[j] = nmul(phase[j], ldcx(bphi + (int64_t)j * d + t));
+    };
+    // first max of |phi_c^H v| over the columns (topk_insert with cnt = 1)
+    auto argmax_cols = [&](const cx (&v)[R]) -> int {
+        int bi = -1;
+        double bv = 0.0;
+        for (int c = 0; c < ncols; c++) {
+            cx pc[R];
+            phi_col(c, pc);
+            cx acc = mk(0.0, 0.0);
+#pragma unroll
+            for (int j = 0; j < R; j++) acc = cadd(acc, nmul(cconj(pc[j]), v[j]));
+            const double sc = cabs_(acc);
+            if (bi < 0 || sc > bv) {
+                bv = sc;
+                bi = c;
+            }
+        }
+        return bi;
+    };
+    o.rankdef = 0;
+    auto lsq1 = [&](int c0, cx &x) {
+        cx A[1][R], xx[1];
+        phi_col(c0, A[0]);
+        if (lstsq_qr_t<R, 1>(A, y, xx)) {
+            x = xx[0];
+            return;
+        }
+        cx Af[R];
+        phi_col(c0, A[0]);
+#pragma unroll
+        for (int i = 0; i < R; i++) Af[i] = A[0][i];
+        if (lstsq_min_norm(Af, R, 1, y, xx) < 1) o.rankdef++;
+        x = xx[0];
+    };
+    auto lsq2 = [&](int c0, int c1, cx &x0, cx &x1) {
+        cx A[2][R], xx[2];
+        phi_col(c0, A[0]);
+        phi_col(c1, A[1]);
+        if (!lstsq_qr_t<R, 2>(A, y, xx)) {
+            phi_col(c0, A[0]);
+            phi_col(c1, A[1]);
+            cx Af[2 * R];
+#pragma unroll
+            for (int i = 0; i < R; i++) {
+                Af[i] = A[0][i];
+                Af[R + i] = A[1][i];
+            }
+            if (lstsq_min_norm(Af, R, 2, y, xx) < 2) o.rankdef++;
+        }
+        x0 = xx[0];
+        x1 = xx[1];
+    };
+    cx res[R];
+    auto residual = [&](int c0, cx x) -> double {
+        cx pc[R];
+        phi_col(c0, pc);
+        double ss = 0.0;
+#pragma unroll
+        for (int j = 0; j < R; j++) {
+            res[j] = csub(y[j], nmul(pc[j], x));
+            ss = fma(res[j].re, res[j].re, fma(res[j].im, res[j].im, ss));
+        }
+        return sqrt(ss);
+    };
+    int sup = argmax_cols(y);
+    cx coef;
+    lsq1(sup, coef);
+    double best = residual(sup, coef);
+    int best_sup = sup;
+    cx best_coef = coef;
+    for (int it = 0; it < 10; it++) {
+        const int topc = argmax_cols(res);
+        if (topc == sup) {
+            cx mc;
+            lsq1(sup, mc);   // the merged solve (its rank counts, its value is unused)
+        } else {
+            const int m0 = sup < topc ? sup : topc, m1 = sup < topc ? topc : sup;
+            cx mc0, mc1;
+            lsq2(m0, m1, mc0, mc1);
+            sup = (cabs_(mc1) > cabs_(mc0)) ? m1 : m0;   // top 1 of |mcoef|, first max
+        }
+        lsq1(sup, coef);
+        const double nrm = residual(sup, coef);
+        if (nrm >= best * (1.0 - 1e-12)) break;
+        best = nrm;
+        best_sup = sup;
+        best_coef = coef;
+    }
+    o.nsup = 1;
+    o.sup[0] = cols[best_sup];
+    o.coef[0] = best_coef;
+}
+
+__device__ __forceinline__ bool sp1_item(int a, int r, int nc8) {
+    return a == 1 && nc8 >= 1 && nc8 <= 4 && (r == 3 || r == 6 || r == 9 || r == 12);
+}
+
+template <int R>
+__global__ void __launch_bounds__(128) k_gen_sp1(const cx *__restrict__ V, GenParams p,
+                                                 const int32_t *__restrict__ votes,
+                                                 const int64_t *__restrict__ wl,
+                                                 const unsigned long long *__restrict__ wl_count,
+                                                 const int32_t *__restrict__ cols_in,
+                                                 const int8_t *__restrict__ ncols_in,
+                                                 uint8_t *__restrict__ nent, int64_t *__restrict__ sloc,
+                                                 cx *__restrict__ sval, int64_t *__restrict__ stats) {
+    const int64_t cnt = (int64_t)*wl_count;
+    for (int64_t it = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; it < cnt;
+         it += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t t = wl[it];
+        const int a = votes[t];
+        const int nc8 = ncols_in[it];
+        if (!sp1_item(a, R, nc8)) continue;
+        const int64_t b = t / p.L, kb = t - b * p.L;
+        const int64_t *sh = p.shifts + b * p.shift_stride;
+        const cx *bphi = p.base_phi + b * p.phi_stride;
+        cx y[R], phase[R];
+        const double tk = DMUL(TWO_PI, (double)kb);
+#pragma unroll
+        for (int j = 0; j < R; j++) {
+            y[j] = ldcx(V + (b * p.nv + p.S + j) * p.L + kb);
+            phase[j] = gexp(mk(0.0, DMUL(tk, (double)sh[j]) / (double)p.n));
+        }
+        int cols[4];
+#pragma unroll
+        for (int c2 = 0; c2 < 4; c2++) cols[c2] = c2 < nc8 ? cols_in[it * GEN_MAX_COLS + c2] : 0;
+        SPOut o;
+        sp_a1_t<R>(y, phase, bphi, p.d, cols, nc8, o);
+        int ne = 0;
+        if (!(o.coef[0].re == 0.0 && o.coef[0].im == 0.0)) {   // np.nonzero(coef)
+            sloc[t * p.a_max] = (kb + (int64_t)o.sup[0] * p.L) & (p.n - 1);
+            stcx(sval + t * p.a_max, o.coef[0]);
+            ne = 1;
+        }
+        nent[t] = (uint8_t)ne;
+        if (o.rankdef)
+            atomicAdd((unsigned long long *)(stats + b * SFDT_GS_PER_SIGNAL + SFDT_GS_RANKDEF),
+                      (unsigned long long)o.rankdef);
+    }
+}
+
+// Subspace pursuit per voted bin on the kept columns (general.py:357-366).
+__global__ void __launch_bounds__(128) k_gen_bins(const cx *__restrict__ V, GenParams p,
+                                                  const int32_t *__restrict__ votes,
+                                                  const int64_t *__restrict__ wl,
+                                                  const unsigned long long *__restrict__ wl_count,
+                                                  const int32_t *__restrict__ cols_in,
+                                                  const int8_t *__restrict__ ncols_in, int skip_sp1,
+                                                  uint8_t *__restrict__ nent, int64_t *__restrict__ sloc,
+                                                  cx *__restrict__ sval, int64_t *__restrict__ stats) {
+    const int64_t cnt = (int64_t)*wl_count;
+    for (int64_t it = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; it < cnt;
+         it += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t t = wl[it];
+        const int a = votes[t];
+        const int r = p.r_eff;
+        if (skip_sp1 && sp1_item(a, r, ncols_in[it])) continue;   // k_gen_sp1's
+        const int64_t b = t / p.L, kb = t - b * p.L;
+        const int64_t *sh = p.shifts + b * p.shift_stride;
+        const cx *bphi = p.base_phi + b * p.phi_stride;
+        cx y[GEN_MAX_R];
+        for (int j = 0; j < r; j++) y[j] = ldcx(V + (b * p.nv + p.S + j) * p.L + kb);
+        int cols[GEN_MAX_COLS];
+        const int nc8 = ncols_in[it];
+        const bool all_cols = nc8 < 0;
+        const int ncols = all_cols ? (int)p.d : nc8;
+        for (int c2 = 0; c2 < (all_cols ? 0 : ncols); c2++) cols[c2] = cols_in[it * GEN_MAX_COLS + c2];
         // subspace pursuit on this bin's columns (general.py:357-366)
         cx phase[GEN_MAX_R];
         const double tk = DMUL(TWO_PI, (double)kb);
@@ -801,7 +1053,7 @@ struct GenPlan {
     int64_t B, n, d, L, nv, nparts;
     int S;
     size_t off_V, off_sv, off_part, off_votes, off_nent, off_sloc, off_sval, off_wl, off_cnt,
-        off_fft, off_mf, total;
+        off_fft, off_mf, off_cols, off_ncols, total;
 };
 
 static int make_gen_plan(const sfdt_general_args *a, GenPlan &p) {
@@ -831,6 +1083,12 @@ static int make_gen_plan(const sfdt_general_args *a, GenPlan &p) {
     p.off_wl = take(size_t(p.B) * p.L * 8);
     p.off_cnt = take(64);
     p.off_mf = take(size_t(p.B) * p.L * 16);
+    {
+        // voted bins per signal <= min(k, L) (each vote is one of the top k keys)
+        const int64_t cap = p.B * (a->k < p.L ? a->k : p.L);
+        p.off_cols = take(size_t(cap) * GEN_MAX_COLS * 4);
+        p.off_ncols = take(size_t(cap));
+    }
     p.off_fft = (p.L > FFT_SMEM_MAX) ? take(size_t(p.B) * p.nv * p.L * 16) : 0;
     p.total = o;
     return SFDT_OK;
@@ -954,9 +1212,25 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
         SFDT_CHECK_LAUNCH();
         launches++;
     }
-    k_gen_bins<<<(unsigned)(sms * 16), 128, 0, stream>>>(V, gp, votes, wl, wlc, mf_top, nent, sloc, sval,
-                                                         a->stats);
+    int32_t *colsb = (int32_t *)(w + p.off_cols);
+    int8_t *ncolsb = (int8_t *)(w + p.off_ncols);
+    k_gen_prune<<<(unsigned)(sms * 16), 128, 0, stream>>>(V, gp, votes, wl, wlc, mf_top, colsb, ncolsb);
     SFDT_CHECK_LAUNCH();
+    const int sp1 = a->r_eff == 3 || a->r_eff == 6 || a->r_eff == 9 || a->r_eff == 12;
+    if (sp1) {
+        switch (a->r_eff) {
+        case 3: k_gen_sp1<3><<<(unsigned)(sms * 16), 128, 0, stream>>>(V, gp, votes, wl, wlc, colsb, ncolsb, nent, sloc, sval, a->stats); break;
+        case 6: k_gen_sp1<6><<<(unsigned)(sms * 16), 128, 0, stream>>>(V, gp, votes, wl, wlc, colsb, ncolsb, nent, sloc, sval, a->stats); break;
+        case 9: k_gen_sp1<9><<<(unsigned)(sms * 16), 128, 0, stream>>>(V, gp, votes, wl, wlc, colsb, ncolsb, nent, sloc, sval, a->stats); break;
+        default: k_gen_sp1<12><<<(unsigned)(sms * 16), 128, 0, stream>>>(V, gp, votes, wl, wlc, colsb, ncolsb, nent, sloc, sval, a->stats); break;
+        }
+        SFDT_CHECK_LAUNCH();
+        launches++;
+    }
+    k_gen_bins<<<(unsigned)(sms * 16), 128, 0, stream>>>(V, gp, votes, wl, wlc, colsb, ncolsb, sp1, nent,
+                                                         sloc, sval, a->stats);
+    SFDT_CHECK_LAUNCH();
+    launches++;
     k_gen_count<<<(unsigned)p.B, 256, 0, stream>>>(votes, nent, p.L, a->stats);
     k_gen_scan<<<1, 1024, 0, stream>>>(a->stats, p.B, a->entry_offsets);
     k_gen_emit<<<(unsigned)p.B, 256, 0, stream>>>(votes, nent, sloc, sval, p.L, a->a_max, a->stats,

@@ -242,89 +242,40 @@ static __global__ void k_fft_large_a(const ViewSrc src, int logL, int logP,
 }
 
 // large views (L > FFT_SMEM_MAX): stage split through global memory.
-// Pass A runs the first logP stages on contiguous blocks of P points (in
-// smem); pass B runs the remaining stages, which act independently on the
-// residue classes i mod P, on tiles of R residues x Q = L/P rows.
-static __global__ void k_fft_large_b(cx *buf, int64_t nviews, int logL, int logP, int logR,
-                                     const cx *__restrict__ tw, cx *out, int nshift, int SV,
-                                     int64_t ldV, int scale, const double *__restrict__ thr,
-                                     uint8_t *__restrict__ act) {
-    extern __shared__ double4 smem_raw[];
-    cx *a = reinterpret_cast<cx *>(smem_raw);
-    const int L = 1 << logL, P = 1 << logP, R = 1 << logR;
-    const int logQ = logL - logP, Q = 1 << logQ;
-    const int tiles_per_view = P >> logR;
-    const int64_t g = blockIdx.x / tiles_per_view;
-    const int r0 = (int)(blockIdx.x % tiles_per_view) * R;
-    cx *src = buf + g * L;
-    // tile element (q, rr) <-> global index r0 + rr + P*q ; smem [q*R + rr]
-    for (int i = threadIdx.x; i < Q * R; i += blockDim.x) {
-        const int q = i >> logR, rr = i & (R - 1);
-        a[i] = src[r0 + rr + (int64_t)q * P];
-    }
-    __syncthreads();
-    for (int lh = logP; lh < logL; lh++) {
-        const int hq = 1 << (lh - logP);   // half in units of q
-        const int h = 1 << lh;
-        const cx *twh = tw + (h - 1);
-        for (int t = threadIdx.x; t < (Q >> 1) * R; t += blockDim.x) {
-            const int rr = t & (R - 1);
-            const int tq = t >> logR;                      // butterfly index over q
-            const int qk = tq & (hq - 1);
-            const int q0 = ((tq >> (lh - logP)) << (lh - logP + 1)) + qk;
-            const int k = r0 + rr + qk * P;                 // position within the stage block
-            const int i0 = q0 * R + rr, i1 = (q0 + hq) * R + rr;
-            const cx u = a[i0];
-            const cx x = gmul(a[i1], ldcx(twh + k));
-            a[i0] = cadd(u, x);
-            a[i1] = csub(u, x);
-        }
-        __syncthreads();
-    }
-    const double sc = 1.0 / (double)L;
-    const int64_t b = g / nshift;
-    const int s = (int)(g - b * nshift);
-    const double th = act ? thr[b] : 0.0;
-    for (int i = threadIdx.x; i < Q * R; i += blockDim.x) {
-        const int q = i >> logR, rr = i & (R - 1);
-        const cx y0 = a[i];
-        const cx y = scale ? mk(DMUL(y0.re, sc), DMUL(y0.im, sc)) : y0;
-        stcx(out + (b * SV + s) * ldV + r0 + rr + (int64_t)q * P, y);
-        if (act) {
-            const double m2 = y.re * y.re + y.im * y.im;
-            if (m2 > th * th * (1.0 + 1e-6) || (m2 >= th * th * (1.0 - 1e-6) && cabs_(y) > th))
-                act[b * (int64_t)L + r0 + rr + (int64_t)q * P] = 1;
-        }
-    }
-}
-
-// Pass B with the remaining LQ = logL - logP stages in registers (LQ <= 4):
-// thread = one residue r < P, holding its Q = 2^LQ rows; the butterflies,
-// their order within a stage and the twiddle index k = r + qk*P are those
-// of k_fft_large_b, so the result is bit-identical, without the per-stage
-// shared-memory round trips and barriers.  Loads/stores are coalesced
-// across threads (consecutive residues).
+// Pass A (above) runs the first logP stages on contiguous blocks of P
+// points in shared memory; the remaining stages act independently on the
+// residue classes i mod P and run as register passes of <= 4 stages.
+// Pass B in registers: LQ stages starting at stage s0 (half-size 2^s0) per
+// kernel, LQ <= 4.  Thread = one (view, high index, residue r < 2^s0),
+// holding the 2^LQ elements i = r + q*2^s0 + hi*2^(s0+LQ); the butterflies,
+// their order within a stage and the twiddle index k = r + qk*2^s0 are those
+// of the radix-2 stage loop, so the result is bit-identical.  Intermediate
+// passes work in place on the scratch; the last writes the views (scaled,
+// with the activity epilogue).  Loads/stores are coalesced across threads
+// (consecutive residues).
 template <int LQ>
-static __global__ void __launch_bounds__(256) k_fft_large_b_reg(const cx *__restrict__ buf, int64_t nviews,
-                                                                int logP, const cx *__restrict__ tw,
-                                                                cx *out, int nshift, int SV, int64_t ldV,
-                                                                int scale, const double *__restrict__ thr,
+static __global__ void __launch_bounds__(256) k_fft_large_b_reg(cx *buf, int64_t nviews, int logL, int s0,
+                                                                const cx *__restrict__ tw, cx *out,
+                                                                int nshift, int SV, int64_t ldV, int scale,
+                                                                const double *__restrict__ thr,
                                                                 uint8_t *__restrict__ act) {
     constexpr int Q = 1 << LQ;
-    const int P = 1 << logP;
-    const int logL = logP + LQ;
+    const int64_t P = int64_t(1) << s0;
     const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t g = gt >> logP;
+    const int64_t g = gt >> (logL - LQ);
     if (g >= nviews) return;
-    const int r = (int)(gt & (P - 1));
-    const cx *src = buf + (g << logL) + r;
+    const int64_t rem = gt & ((int64_t(1) << (logL - LQ)) - 1);
+    const int64_t r = rem & (P - 1);
+    const int64_t hi = rem >> s0;
+    const int64_t i0 = r + (hi << (s0 + LQ));
+    cx *src = buf + (g << logL) + i0;
     cx x[Q];
 #pragma unroll
     for (int q = 0; q < Q; q++) x[q] = ldcx(src + (int64_t)q * P);
 #pragma unroll
     for (int st = 0; st < LQ; st++) {
         const int hq = 1 << st;
-        const int h = P << st;
+        const int64_t h = P << st;
         const cx *twh = tw + (h - 1);
 #pragma unroll
         for (int q = 0; q < Q; q++) {
@@ -336,10 +287,15 @@ static __global__ void __launch_bounds__(256) k_fft_large_b_reg(const cx *__rest
             x[q + hq] = csub(u, t);
         }
     }
-    const double sc = 1.0 / (double)(1 << logL);
+    if (out == nullptr) {   // intermediate pass: in place
+#pragma unroll
+        for (int q = 0; q < Q; q++) src[(int64_t)q * P] = x[q];
+        return;
+    }
+    const double sc = 1.0 / (double)(int64_t(1) << logL);
     const int64_t b = g / nshift;
     const int s = (int)(g - b * nshift);
-    cx *o = out + (b * SV + s) * ldV + r;
+    cx *o = out + (b * SV + s) * ldV + i0;
     const double th = act ? thr[b] : 0.0;
 #pragma unroll
     for (int q = 0; q < Q; q++) {
@@ -348,9 +304,25 @@ static __global__ void __launch_bounds__(256) k_fft_large_b_reg(const cx *__rest
         if (act) {   // activity epilogue, as in k_fft_views
             const double m2 = y.re * y.re + y.im * y.im;
             if (m2 > th * th * (1.0 + 1e-6) || (m2 >= th * th * (1.0 - 1e-6) && cabs_(y) > th))
-                act[b * ((int64_t)P << LQ) + r + (int64_t)q * P] = 1;
+                act[(b << logL) + i0 + (int64_t)q * P] = 1;
         }
     }
+}
+
+template <int LQ>
+static inline void launch_large_b_reg(cx *buf, int64_t nviews, int logL, int s0, const cx *tw, cx *out,
+                                      int nshift, int SV, int64_t ldV, int scale, const double *thr,
+                                      uint8_t *act, cudaStream_t stream) {
+    const int64_t threads = nviews << (logL - LQ);
+    k_fft_large_b_reg<LQ><<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(
+        buf, nviews, logL, s0, tw, out, nshift, SV, ldV, scale, thr, act);
+}
+
+// kernel launches of one launch_fft_views call
+static inline int fft_view_launches(int64_t L) {
+    if (L <= FFT_SMEM_MAX) return 1;
+    const int rest = ilog2_64(L) - 12;
+    return 1 + (rest + 3) / 4;
 }
 
 static inline int fft_points_per_cta() {
@@ -410,27 +382,21 @@ static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, con
         k_fft_large_a<<<(unsigned)(nviews << logQ), 256, smem, stream>>>(src, logL, logP, tw, large_scratch);
         SFDT_CHECK_LAUNCH();
     }
-    if (logQ >= 1 && logQ <= 4) {
-        const int64_t threads = nviews << logP;
-        const unsigned grid = (unsigned)((threads + 255) / 256);
-        switch (logQ) {
-        case 1: k_fft_large_b_reg<1><<<grid, 256, 0, stream>>>(large_scratch, nviews, logP, tw, out, src.nshift, SV, ldV, scale, thr, act); break;
-        case 2: k_fft_large_b_reg<2><<<grid, 256, 0, stream>>>(large_scratch, nviews, logP, tw, out, src.nshift, SV, ldV, scale, thr, act); break;
-        case 3: k_fft_large_b_reg<3><<<grid, 256, 0, stream>>>(large_scratch, nviews, logP, tw, out, src.nshift, SV, ldV, scale, thr, act); break;
-        default: k_fft_large_b_reg<4><<<grid, 256, 0, stream>>>(large_scratch, nviews, logP, tw, out, src.nshift, SV, ldV, scale, thr, act); break;
+    // remaining stages logP .. logL-1 in register passes of <= 4 stages
+    // (the last one writes the views)
+    for (int s0 = logP; s0 < logL;) {
+        const int rem = logL - s0;
+        const int lq = rem >= 4 ? 4 : rem;
+        const bool last = s0 + lq == logL;
+        cx *o = last ? out : nullptr;
+        switch (lq) {
+        case 1: launch_large_b_reg<1>(large_scratch, nviews, logL, s0, tw, o, src.nshift, SV, ldV, scale, thr, act, stream); break;
+        case 2: launch_large_b_reg<2>(large_scratch, nviews, logL, s0, tw, o, src.nshift, SV, ldV, scale, thr, act, stream); break;
+        case 3: launch_large_b_reg<3>(large_scratch, nviews, logL, s0, tw, o, src.nshift, SV, ldV, scale, thr, act, stream); break;
+        default: launch_large_b_reg<4>(large_scratch, nviews, logL, s0, tw, o, src.nshift, SV, ldV, scale, thr, act, stream); break;
         }
         SFDT_CHECK_LAUNCH();
-        return SFDT_OK;
-    }
-    {
-        int logR = 13 - logQ;          // tiles of 2^13 points
-        if (logR > logP) logR = logP;
-        if (logR < 0) return SFDT_EINVAL;
-        const size_t smem = (size_t(1) << (logQ + logR)) * 16;
-        cudaFuncSetAttribute(k_fft_large_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_fft_large_b<<<(unsigned)(nviews * (P >> logR)), 256, smem, stream>>>(
-            large_scratch, nviews, logL, logP, logR, tw, out, src.nshift, SV, ldV, scale, thr, act);
-        SFDT_CHECK_LAUNCH();
+        s0 += lq;
     }
     return SFDT_OK;
 }

@@ -379,14 +379,16 @@ constexpr int MF_LIST = 4096;
 template <int R, bool STAGE>
 __global__ void __launch_bounds__(256, 2) k_gen_mf(const cx *__restrict__ V, GenParams p,
                                                 const int32_t *__restrict__ votes,
-                                                int32_t *__restrict__ mf_top) {
+                                                int32_t *__restrict__ mf_top, int64_t nchunk) {
     constexpr bool stage = STAGE;
     extern __shared__ cx s_phi[];
     __shared__ int s_list[MF_LIST];
     __shared__ double s_q2[8][256];
     __shared__ int s_n;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int64_t b = blockIdx.x;
+    // CTA = (signal, chunk of MF_LIST bins): long views of few signals
+    // still fill the GPU
+    const int64_t b = blockIdx.x / nchunk, chunk = blockIdx.x - b * nchunk;
     constexpr int r = R;
     const int64_t *sh = p.shifts + b * p.shift_stride;
     const cx *gphi = p.base_phi + b * p.phi_stride;
@@ -394,7 +396,7 @@ __global__ void __launch_bounds__(256, 2) k_gen_mf(const cx *__restrict__ V, Gen
         for (int64_t i = threadIdx.x; i < (int64_t)r * p.d; i += blockDim.x) s_phi[i] = ldcx(gphi + i);
     // explicit address spaces: LDS from the staged copy, LDG otherwise
     auto phi_at = [&](int64_t i) -> cx { return stage ? s_phi[i] : ldcx(gphi + i); };
-    for (int64_t c0 = 0; c0 < p.L; c0 += MF_LIST) {
+    for (int64_t c0 = chunk * MF_LIST; c0 < p.L && c0 < (chunk + 1) * MF_LIST; c0 += MF_LIST) {
         if (threadIdx.x == 0) s_n = 0;
         __syncthreads();
         const int64_t c1 = p.L < c0 + MF_LIST ? p.L : c0 + MF_LIST;
@@ -1144,7 +1146,7 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     src.dyn_stride = a->shift_stride;
     rc = launch_fft_views(src, p.B, p.L, a->twiddles, V, (int)p.nv, p.L, stream, fft_scratch);
     if (rc) return rc;
-    launches += (p.L > FFT_SMEM_MAX) ? 2 : 1;
+    launches += fft_view_launches(p.L);
 
     GenParams gp;
     gp.n = p.n;
@@ -1190,6 +1192,7 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     cudaMemsetAsync(nent, 0, size_t(p.B) * p.L, stream);
     int32_t *mf_top = (int32_t *)(w + p.off_mf);
     if (a->prune) {
+        const int64_t nch = (p.L + MF_LIST - 1) / MF_LIST;
         const size_t phi_bytes = size_t(a->r_eff) * p.d * 16;
         const int stage = phi_bytes <= MF_SMEM_MAX;
         const size_t smem = stage ? phi_bytes : 0;
@@ -1199,9 +1202,9 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
         if (stage) {                                                                               \
             cudaFuncSetAttribute(k_gen_mf<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
                                  (int)smem);                                                       \
-            k_gen_mf<R, true><<<(unsigned)p.B, 256, smem, stream>>>(V, gp, votes, mf_top);         \
+            k_gen_mf<R, true><<<(unsigned)(p.B * nch), 256, smem, stream>>>(V, gp, votes, mf_top, nch); \
         } else {                                                                                   \
-            k_gen_mf<R, false><<<(unsigned)p.B, 256, 0, stream>>>(V, gp, votes, mf_top);           \
+            k_gen_mf<R, false><<<(unsigned)(p.B * nch), 256, 0, stream>>>(V, gp, votes, mf_top, nch); \
         }                                                                                          \
         break;
             SFDT_MF(1) SFDT_MF(2) SFDT_MF(3) SFDT_MF(4) SFDT_MF(5) SFDT_MF(6)

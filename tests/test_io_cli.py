@@ -123,7 +123,7 @@ def test_device_fft_bitexact_long():
     from oracle import kernels as OK
     from paper_1407_8315_b200.spectral import fft
     rng = np.random.default_rng(2)
-    for n in (8, 4096, 1 << 15, 1 << 18):
+    for n in (8, 4096, 1 << 15, 1 << 17, 1 << 18, 1 << 21):   # 0 .. 3 register passes after the smem pass
         x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
         got = fft(x)
         assert np.array_equal(got.view(np.uint64), OK.fft_radix2(x).view(np.uint64)), n

@@ -66,42 +66,92 @@ __device__ __forceinline__ int swz(int p) {
     return (p & ~7) | (f & 7);
 }
 
+// NST radix-2 stages (half-sizes h .. h*2^(NST-1)) on the G = 2^NST
+// elements e0 + q*h of one group, in registers
+template <int NST>
+__device__ __forceinline__ void group_stages(cx (&x)[1 << NST], int e0, int h, const cx *__restrict__ tw) {
+    constexpr int G = 1 << NST;
+#pragma unroll
+    for (int st = 0; st < NST; st++) {
+        const int Hs = h << st;
+        const cx *twh = tw + (Hs - 1);
+#pragma unroll
+        for (int q = 0; q < G; q++) {
+            if (q & (1 << st)) continue;
+            const int e = e0 + q * h;
+            const cx u = x[q];
+            // the reference's w starts at exactly 1 + 0i, and (a*1 - b*0,
+            // a*0 + b*1) == (a, b) for finite a, b: the first twiddle of
+            // every stage block needs no multiply
+            const int kk = e & (Hs - 1);
+            const cx t = (Hs == 1) ? x[q + (1 << st)] : gmul(x[q + (1 << st)], ldcx(twh + kk));
+            x[q] = cadd(u, t);
+            x[q + (1 << st)] = csub(u, t);
+        }
+    }
+}
+
 template <int NST>
 __device__ __forceinline__ void fft_pass(cx *a, int nv, int logL, int lh, const cx *__restrict__ tw) {
     constexpr int G = 1 << NST;
     const int L = 1 << logL;
     const int h = 1 << lh;
-    const int gper = L >> NST;
-    const int ng = nv * gper;
+    const int lg = logL - NST;   // log2(groups per view)
+    const int ng = nv << lg;
+    // swz(base + q*h) = (swz(base) | q*h) ^ dq[q] when lh >= 3 (bits lh..
+    // lh+NST-1 of base are zero and the fold is XOR-linear); one table per
+    // pass instead of a fold per element
+    int dq[G];
+#pragma unroll
+    for (int q = 0; q < G; q++) dq[q] = swz(q << lh) & 7;
     for (int g = threadIdx.x; g < ng; g += blockDim.x) {
-        const int v = g / gper;
-        const int gg = g - v * gper;
+        const int v = g >> lg;
+        const int gg = g & ((1 << lg) - 1);
         const int lo = gg & (h - 1), hi = gg >> lh;
         const int base = v * L + (hi << (lh + NST)) + lo;
-        const int e0 = (hi << (lh + NST)) + lo;   // index within the view
+        const int e0 = (hi << (lh + NST)) + lo;
+        const int sb = swz(base);
+        auto at = [&](int q) { return lh >= 3 ? ((sb | (q << lh)) ^ dq[q]) : swz(base + q * h); };   // index within the view
         cx x[G];
 #pragma unroll
-        for (int q = 0; q < G; q++) x[q] = a[swz(base + q * h)];
+        for (int q = 0; q < G; q++) x[q] = a[at(q)];
+        group_stages<NST>(x, e0, h, tw);
 #pragma unroll
-        for (int st = 0; st < NST; st++) {
-            const int Hs = h << st;
-            const cx *twh = tw + (Hs - 1);
+        for (int q = 0; q < G; q++) a[at(q)] = x[q];
+    }
+}
+
+// Last pass straight to global memory: the group's outputs are scaled and
+// stored (with the activity epilogue) from registers instead of going back
+// through shared memory for a separate epilogue sweep.
+template <int NST, typename Epi>
+__device__ __forceinline__ void fft_pass_out(const cx *a, int nv, int logL, int lh, const cx *__restrict__ tw,
+                                             Epi &&epi) {
+    constexpr int G = 1 << NST;
+    const int L = 1 << logL;
+    const int h = 1 << lh;
+    const int lg = logL - NST;   // log2(groups per view)
+    const int ng = nv << lg;
+    // swz(base + q*h) = (swz(base) | q*h) ^ dq[q] when lh >= 3 (bits lh..
+    // lh+NST-1 of base are zero and the fold is XOR-linear); one table per
+    // pass instead of a fold per element
+    int dq[G];
 #pragma unroll
-            for (int q = 0; q < G; q++) {
-                if (q & (1 << st)) continue;
-                const int e = e0 + q * h;
-                const cx u = x[q];
-                // the reference's w starts at exactly 1 + 0i, and (a*1 - b*0,
-                // a*0 + b*1) == (a, b) for finite a, b: the first twiddle of
-                // every stage block needs no multiply
-                const int kk = e & (Hs - 1);
-                const cx t = (Hs == 1) ? x[q + (1 << st)] : gmul(x[q + (1 << st)], ldcx(twh + kk));
-                x[q] = cadd(u, t);
-                x[q + (1 << st)] = csub(u, t);
-            }
-        }
+    for (int q = 0; q < G; q++) dq[q] = swz(q << lh) & 7;
+    for (int g = threadIdx.x; g < ng; g += blockDim.x) {
+        const int v = g >> lg;
+        const int gg = g & ((1 << lg) - 1);
+        const int lo = gg & (h - 1), hi = gg >> lh;
+        const int base = v * L + (hi << (lh + NST)) + lo;
+        const int e0 = (hi << (lh + NST)) + lo;
+        const int sb = swz(base);
+        auto at = [&](int q) { return lh >= 3 ? ((sb | (q << lh)) ^ dq[q]) : swz(base + q * h); };
+        cx x[G];
 #pragma unroll
-        for (int q = 0; q < G; q++) a[swz(base + q * h)] = x[q];
+        for (int q = 0; q < G; q++) x[q] = a[at(q)];
+        group_stages<NST>(x, e0, h, tw);
+#pragma unroll
+        for (int q = 0; q < G; q++) epi(v, e0 + q * h, x[q]);
     }
 }
 
@@ -145,9 +195,66 @@ static __global__ void __launch_bounds__(256, MINB) k_fft_views(const ViewSrc sr
         s_sig[threadIdx.x] = b;
     }
     __syncthreads();
-    // gather: lanes vary the view (shift) fastest for one sample j, so one
-    // d-block's adjacent shifts share sectors; bit-reversed scatter to smem.
-    // Loads are issued in batches of 8 before their shared-memory stores.
+    const double sc = 1.0 / (double)L;   // exact power of two
+    // output epilogue: scale, store, activity (exact.py:178): |v| >
+    // zero_threshold*rms*d on any view; |v|^2 decides away from the
+    // boundary, hypot inside a 1e-6 band
+    auto epi = [&](int v, int k, cx y) {
+        if (scale) y = mk(DMUL(y.re, sc), DMUL(y.im, sc));
+        stcx(out + s_obase[v] + k, y);
+        if (act) {
+            const double th = thr[s_sig[v]];
+            const double q = y.re * y.re + y.im * y.im;
+            if (q > th * th * (1.0 + 1e-6) || (q >= th * th * (1.0 - 1e-6) && cabs_(y) > th))
+                act[s_sig[v] * (int64_t)L + k] = 1;
+        }
+    };
+    if (logL >= 6 && !src.jfast) {
+        // First pass fused with the gather: a thread loads the 8 inputs of
+        // one radix-8 group (positions hi*8 + q hold inputs j = bitrev(hi*8
+        // + q)) straight from the signal, runs stages 0-2 in registers and
+        // writes shared memory once.  Lanes vary the view fastest, so one
+        // d-block's adjacent shifts share sectors.
+        const int gper = L >> 3;
+        const int hbits = logL - 3;
+        for (int g = threadIdx.x; g < (gper << logvpc); g += blockDim.x) {
+            const int v = g & (vpc - 1), hi = g >> logvpc;
+            if (v >= nv) continue;
+            const int hb = (int)(__brev((unsigned)hi) >> (32 - hbits));
+            cx x[8];
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                const int q3 = ((q & 1) << 2) | (q & 2) | ((q >> 2) & 1);   // bitrev_3(q)
+                const int j = hb + (q3 << hbits);
+                const int64_t e = s_ibase[v] + (((int64_t)j * src.jstride + s_ioff[v]) & src.wrap);
+                if (src.is_c64) {
+                    const float2 f = __ldg(reinterpret_cast<const float2 *>(src.x) + e);
+                    x[q] = mk((double)f.x, (double)f.y);
+                } else {
+                    x[q] = ldcx(reinterpret_cast<const cx *>(src.x) + e);
+                }
+            }
+            group_stages<3>(x, hi << 3, 1, tw);
+#pragma unroll
+            for (int q = 0; q < 8; q++) a[swz(v * L + (hi << 3) + q)] = x[q];
+        }
+        __syncthreads();
+        int lh = 3;
+        while (logL - lh > 3) {
+            fft_pass<3>(a, nv, logL, lh, tw);
+            __syncthreads();
+            lh += 3;
+        }
+        // last pass straight to global memory
+        const int nst = logL - lh;
+        if (nst == 3) fft_pass_out<3>(a, nv, logL, lh, tw, epi);
+        else if (nst == 2) fft_pass_out<2>(a, nv, logL, lh, tw, epi);
+        else fft_pass_out<1>(a, nv, logL, lh, tw, epi);
+        return;
+    }
+    // small views: gather (lanes vary the view fastest for one sample j),
+    // bit-reversed scatter to smem, stages, epilogue sweep.  Loads are
+    // issued in batches of 8 before their shared-memory stores.
     const int total = L << logvpc;
     for (int i0 = 0; i0 < total; i0 += 8 * 256) {
         cx vals[8];
@@ -178,21 +285,7 @@ static __global__ void __launch_bounds__(256, MINB) k_fft_views(const ViewSrc sr
     }
     __syncthreads();
     fft_stages_smem(a, nv, logL, 0, logL, tw);
-    const double sc = 1.0 / (double)L;   // exact power of two
-    for (int i = threadIdx.x; i < nv * L; i += blockDim.x) {
-        const int v = i >> logL, k = i & (L - 1);
-        cx y = a[swz(i)];
-        if (scale) y = mk(DMUL(y.re, sc), DMUL(y.im, sc));
-        stcx(out + s_obase[v] + k, y);
-        if (act) {
-            // activity (exact.py:178): |v| > zero_threshold*rms*d on any view;
-            // |v|^2 decides away from the boundary, hypot inside a 1e-6 band
-            const double th = thr[s_sig[v]];
-            const double q = y.re * y.re + y.im * y.im;
-            if (q > th * th * (1.0 + 1e-6) || (q >= th * th * (1.0 - 1e-6) && cabs_(y) > th))
-                act[s_sig[v] * (int64_t)L + k] = 1;
-        }
-    }
+    for (int i = threadIdx.x; i < nv * L; i += blockDim.x) epi(i >> logL, i & (L - 1), a[swz(i)]);
 }
 
 // Pass A of the large-view FFT: CTA (view g, block c) owns bit-reversed

@@ -12,7 +12,7 @@ NM="ncu --metrics gpu__time_duration.sum --clock-control none -k regex:^k_ --csv
 $NM --log-file gpurun_out/launches_noniter_cfg2.csv $B --steps 3 --warmup 2 > /tmp/l1.log 2>&1
 $NM --log-file gpurun_out/launches_iter_cfg2.csv $B --solver iterative --steps 3 --warmup 2 > /tmp/l2.log 2>&1
 $NM --log-file gpurun_out/launches_general_cfg4.csv $B --config cfg4 --steps 3 --warmup 2 > /tmp/l3.log 2>&1
-NF="ncu --set full --clock-control none --import-source on -k regex:^k_"
+NF="ncu -f --set full --clock-control none --import-source on -k regex:^k_"
 $NF -c 12 -o /tmp/full_noniter_cfg2 $B --steps 1 --warmup 0 > /tmp/f1.log 2>&1
 $NF -c 40 -o /tmp/full_iter_cfg2 $B --solver iterative --steps 1 --warmup 0 > /tmp/f2.log 2>&1
 $NF -c 12 -o /tmp/full_general_cfg4 $B --config cfg4 --steps 1 --warmup 0 > /tmp/f3.log 2>&1

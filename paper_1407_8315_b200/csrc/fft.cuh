@@ -67,26 +67,32 @@ __device__ __forceinline__ int swz(int p) {
 }
 
 // NST radix-2 stages (half-sizes h .. h*2^(NST-1)) on the G = 2^NST
-// elements e0 + q*h of one group, in registers
+// elements e0 + q*h of one group, in registers.  With lo = e0 mod h (the
+// bits lh .. lh+NST-1 of e0 are zero) the butterfly twiddle index
+// (e0 + q*h) mod (h*2^st) is lo + (q mod 2^st)*h: each of the 2^st distinct
+// twiddles of stage st is loaded once and shared by its G/2^(st+1)
+// butterflies.
 template <int NST>
-__device__ __forceinline__ void group_stages(cx (&x)[1 << NST], int e0, int h, const cx *__restrict__ tw) {
+__device__ __forceinline__ void group_stages(cx (&x)[1 << NST], int lo, int h, const cx *__restrict__ tw) {
     constexpr int G = 1 << NST;
 #pragma unroll
     for (int st = 0; st < NST; st++) {
         const int Hs = h << st;
-        const cx *twh = tw + (Hs - 1);
+        const cx *twh = tw + (Hs - 1) + lo;
 #pragma unroll
-        for (int q = 0; q < G; q++) {
-            if (q & (1 << st)) continue;
-            const int e = e0 + q * h;
-            const cx u = x[q];
+        for (int qk = 0; qk < (1 << st); qk++) {
             // the reference's w starts at exactly 1 + 0i, and (a*1 - b*0,
             // a*0 + b*1) == (a, b) for finite a, b: the first twiddle of
             // every stage block needs no multiply
-            const int kk = e & (Hs - 1);
-            const cx t = (Hs == 1) ? x[q + (1 << st)] : gmul(x[q + (1 << st)], ldcx(twh + kk));
-            x[q] = cadd(u, t);
-            x[q + (1 << st)] = csub(u, t);
+            const bool one = (Hs == 1);
+            const cx w = one ? mk(1.0, 0.0) : ldcx(twh + qk * h);
+#pragma unroll
+            for (int q = qk; q < G; q += (2 << st)) {
+                const cx u = x[q];
+                const cx t = one ? x[q + (1 << st)] : gmul(x[q + (1 << st)], w);
+                x[q] = cadd(u, t);
+                x[q + (1 << st)] = csub(u, t);
+            }
         }
     }
 }
@@ -115,7 +121,7 @@ __device__ __forceinline__ void fft_pass(cx *a, int nv, int logL, int lh, const 
         cx x[G];
 #pragma unroll
         for (int q = 0; q < G; q++) x[q] = a[at(q)];
-        group_stages<NST>(x, e0, h, tw);
+        group_stages<NST>(x, lo, h, tw);
 #pragma unroll
         for (int q = 0; q < G; q++) a[at(q)] = x[q];
     }
@@ -149,7 +155,7 @@ __device__ __forceinline__ void fft_pass_out(const cx *a, int nv, int logL, int 
         cx x[G];
 #pragma unroll
         for (int q = 0; q < G; q++) x[q] = a[at(q)];
-        group_stages<NST>(x, e0, h, tw);
+        group_stages<NST>(x, lo, h, tw);
 #pragma unroll
         for (int q = 0; q < G; q++) epi(v, e0 + q * h, x[q]);
     }
@@ -234,7 +240,7 @@ static __global__ void __launch_bounds__(256, MINB) k_fft_views(const ViewSrc sr
                     x[q] = ldcx(reinterpret_cast<const cx *>(src.x) + e);
                 }
             }
-            group_stages<3>(x, hi << 3, 1, tw);
+            group_stages<3>(x, 0, 1, tw);
 #pragma unroll
             for (int q = 0; q < 8; q++) a[swz(v * L + (hi << 3) + q)] = x[q];
         }

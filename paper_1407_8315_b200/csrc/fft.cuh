@@ -375,15 +375,17 @@ static __global__ void __launch_bounds__(256) k_fft_large_b_reg(cx *buf, int64_t
     for (int st = 0; st < LQ; st++) {
         const int hq = 1 << st;
         const int64_t h = P << st;
-        const cx *twh = tw + (h - 1);
+        const cx *twh = tw + (h - 1) + r;
 #pragma unroll
-        for (int q = 0; q < Q; q++) {
-            if (q & hq) continue;
-            const int qk = q & (hq - 1);
-            const cx u = x[q];
-            const cx t = gmul(x[q + hq], ldcx(twh + r + qk * P));
-            x[q] = cadd(u, t);
-            x[q + hq] = csub(u, t);
+        for (int qk = 0; qk < hq; qk++) {   // each distinct twiddle loaded once
+            const cx w = ldcx(twh + qk * P);
+#pragma unroll
+            for (int q = qk; q < Q; q += 2 * hq) {
+                const cx u = x[q];
+                const cx t = gmul(x[q + hq], w);
+                x[q] = cadd(u, t);
+                x[q + hq] = csub(u, t);
+            }
         }
     }
     if (out == nullptr) {   // intermediate pass: in place

@@ -931,12 +931,19 @@ __global__ void __launch_bounds__(128) k_gen_bins(const cx *__restrict__ V, GenP
 }
 
 // -------------------------------------------------------------- compaction
+// A signal's bins are split into segments of GEN_SEG bins (one CTA each) so
+// long views of few signals fill the GPU: per-segment class counts, folded
+// per signal, and each segment emitted at its signal's class bases plus
+// the counts of the segments before it.
+constexpr int64_t GEN_SEG = 8192;
+
 __global__ void __launch_bounds__(256) k_gen_count(const int32_t *__restrict__ votes,
                                                    const uint8_t *__restrict__ nent, int64_t L,
-                                                   int64_t *__restrict__ stats) {
-    const int64_t b = blockIdx.x;
+                                                   int64_t nseg, long long *__restrict__ segcnt) {
+    const int64_t b = blockIdx.x / nseg, g = blockIdx.x - b * nseg;
+    const int64_t k0 = g * GEN_SEG, k1 = (k0 + GEN_SEG < L) ? k0 + GEN_SEG : L;
     long long c[4] = {0, 0, 0, 0};
-    for (int64_t kb = threadIdx.x; kb < L; kb += blockDim.x) {
+    for (int64_t kb = k0 + threadIdx.x; kb < k1; kb += blockDim.x) {
         const int v = votes[b * L + kb];
         if (v >= 1) c[v - 1] += nent[b * L + kb];
     }
@@ -948,15 +955,23 @@ __global__ void __launch_bounds__(256) k_gen_count(const int32_t *__restrict__ v
             for (int q = 0; q < 4; q++) red[q][threadIdx.x] += red[q][threadIdx.x + s];
         __syncthreads();
     }
-    if (threadIdx.x == 0) {
-        int64_t *st = stats + b * SFDT_GS_PER_SIGNAL;
-        long long tot = 0;
-        for (int q = 0; q < 4; q++) {
-            st[SFDT_GS_CLASS0 + q] = red[q][0];
-            tot += red[q][0];
-        }
-        st[SFDT_GS_NENTRIES] = tot;
+    if (threadIdx.x < 4) segcnt[blockIdx.x * 4 + threadIdx.x] = red[threadIdx.x][0];
+}
+
+__global__ void k_gen_fin(const long long *__restrict__ segcnt, int64_t B, int64_t nseg,
+                          int64_t *__restrict__ stats) {
+    const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    long long r[4] = {0, 0, 0, 0};
+    for (int64_t g = 0; g < nseg; g++)
+        for (int q = 0; q < 4; q++) r[q] += segcnt[(b * nseg + g) * 4 + q];
+    int64_t *st = stats + b * SFDT_GS_PER_SIGNAL;
+    long long tot = 0;
+    for (int q = 0; q < 4; q++) {
+        st[SFDT_GS_CLASS0 + q] = r[q];
+        tot += r[q];
     }
+    st[SFDT_GS_NENTRIES] = tot;
 }
 
 __global__ void k_gen_scan(const int64_t *__restrict__ stats, int64_t B, int64_t *__restrict__ offsets) {
@@ -991,16 +1006,20 @@ __global__ void __launch_bounds__(256) k_gen_emit(const int32_t *__restrict__ vo
                                                   const cx *__restrict__ sval, int64_t L, int a_max,
                                                   const int64_t *__restrict__ stats,
                                                   const int64_t *__restrict__ eoff,
-                                                  int64_t *__restrict__ locs, cx *__restrict__ vals) {
+                                                  int64_t *__restrict__ locs, cx *__restrict__ vals,
+                                                  int64_t nseg, const long long *__restrict__ segcnt) {
     __shared__ unsigned long long wtot[8];
-    const int64_t b = blockIdx.x;
+    const int64_t b = blockIdx.x / nseg, g = blockIdx.x - b * nseg;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t *st = stats + b * SFDT_GS_PER_SIGNAL;
     long long base[4];
     base[0] = eoff[b];
     for (int c = 1; c < 4; c++) base[c] = base[c - 1] + st[SFDT_GS_CLASS0 + c - 1];
+    for (int64_t g2 = 0; g2 < g; g2++)
+        for (int c = 0; c < 4; c++) base[c] += segcnt[(b * nseg + g2) * 4 + c];
     long long carry[4] = {0, 0, 0, 0};
-    for (int64_t t0 = 0; t0 < L; t0 += 1024) {
+    const int64_t k0 = g * GEN_SEG, k1 = (k0 + GEN_SEG < L) ? k0 + GEN_SEG : L;
+    for (int64_t t0 = k0; t0 < k1; t0 += 1024) {
         int ci[4], ne[4];
         unsigned long long packed = 0;
 #pragma unroll
@@ -1008,7 +1027,7 @@ __global__ void __launch_bounds__(256) k_gen_emit(const int32_t *__restrict__ vo
             const int64_t kb = t0 + 4 * threadIdx.x + u;
             ci[u] = -1;
             ne[u] = 0;
-            if (kb < L) {
+            if (kb < k1) {
                 const int v = votes[b * L + kb];
                 if (v >= 1) {
                     ci[u] = v - 1;
@@ -1055,7 +1074,7 @@ struct GenPlan {
     int64_t B, n, d, L, nv, nparts;
     int S;
     size_t off_V, off_sv, off_part, off_votes, off_nent, off_sloc, off_sval, off_wl, off_cnt,
-        off_fft, off_mf, off_cols, off_ncols, total;
+        off_fft, off_mf, off_cols, off_ncols, off_seg, total;
 };
 
 static int make_gen_plan(const sfdt_general_args *a, GenPlan &p) {
@@ -1091,6 +1110,7 @@ static int make_gen_plan(const sfdt_general_args *a, GenPlan &p) {
         p.off_cols = take(size_t(cap) * GEN_MAX_COLS * 4);
         p.off_ncols = take(size_t(cap));
     }
+    p.off_seg = take(size_t(p.B) * ((p.L + GEN_SEG - 1) / GEN_SEG) * 4 * 8);
     p.off_fft = (p.L > FFT_SMEM_MAX) ? take(size_t(p.B) * p.nv * p.L * 16) : 0;
     p.total = o;
     return SFDT_OK;
@@ -1234,12 +1254,16 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
                                                          sloc, sval, a->stats);
     SFDT_CHECK_LAUNCH();
     launches++;
-    k_gen_count<<<(unsigned)p.B, 256, 0, stream>>>(votes, nent, p.L, a->stats);
+    const int64_t nseg = (p.L + GEN_SEG - 1) / GEN_SEG;
+    long long *segcnt = (long long *)(w + p.off_seg);
+    k_gen_count<<<(unsigned)(p.B * nseg), 256, 0, stream>>>(votes, nent, p.L, nseg, segcnt);
+    k_gen_fin<<<(unsigned)((p.B + 255) / 256), 256, 0, stream>>>(segcnt, p.B, nseg, a->stats);
     k_gen_scan<<<1, 1024, 0, stream>>>(a->stats, p.B, a->entry_offsets);
-    k_gen_emit<<<(unsigned)p.B, 256, 0, stream>>>(votes, nent, sloc, sval, p.L, a->a_max, a->stats,
-                                                  a->entry_offsets, a->locs, (cx *)a->vals);
+    k_gen_emit<<<(unsigned)(p.B * nseg), 256, 0, stream>>>(votes, nent, sloc, sval, p.L, a->a_max, a->stats,
+                                                           a->entry_offsets, a->locs, (cx *)a->vals, nseg,
+                                                           segcnt);
     SFDT_CHECK_LAUNCH();
-    launches += 6;
+    launches += 7;
     a->kernel_launches = launches;
     return SFDT_OK;
 }

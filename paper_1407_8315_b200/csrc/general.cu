@@ -250,6 +250,217 @@ __global__ void __launch_bounds__(1024) k_gen_vote(const double *__restrict__ sv
     }
 }
 
+// ------------------------------------------------ vote, long views
+// The same exact top-K selection for signals with many keys (M = L*a_max >
+// VOTE_BIG), spread over CTAs of VCH keys: each 8-bit radix pass builds
+// per-chunk histograms (warp-aggregated) summed into a per-signal global
+// histogram, one warp per signal picks the digit; then per-chunk counts of
+// keys equal to the threshold give every chunk its tie rank base, the
+// chunks vote, and a bin-parallel pass applies the zero-vote guard, cap,
+// histogram and worklist.  Identical result to k_gen_vote.
+constexpr int64_t VOTE_BIG = 65536;
+constexpr int64_t VCH = 16384;
+
+struct VSel {
+    unsigned long long prefix, mask;
+    long long remaining;
+    double thr;
+};
+
+// per signal: state, zero-vote threshold (rms of the consecutive syndromes),
+// stats fields the later passes accumulate into
+__global__ void k_vsel_init(const double *__restrict__ partial, int nparts, GenParams p, int64_t B,
+                            VSel *__restrict__ vs, int64_t *__restrict__ stats) {
+    const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    const int64_t M = p.L * p.a_max;
+    double esum = 0.0;   // same summation order as k_gen_vote
+    for (int i = 0; i < nparts; i++) esum += partial[b * nparts + i];
+    const double rms_syn = sqrt(esum / (double)(p.L * p.S));
+    vs[b].prefix = 0;
+    vs[b].mask = 0;
+    vs[b].remaining = p.k < M ? p.k : M;
+    vs[b].thr = p.zvr * rms_syn;
+    int64_t *st = stats + b * SFDT_GS_PER_SIGNAL;
+    for (int a = 0; a <= 4; a++) st[SFDT_GS_HIST0 + a] = 0;
+    st[SFDT_GS_NVOTED] = 0;
+    st[SFDT_GS_RANKDEF] = 0;
+}
+
+__global__ void __launch_bounds__(256) k_vsel_hist(const double *__restrict__ sv, GenParams p, int64_t nch,
+                                                   int shift, const VSel *__restrict__ vs,
+                                                   unsigned int *__restrict__ ghist) {
+    const int64_t b = blockIdx.x / nch, ch = blockIdx.x - b * nch;
+    const int64_t M = p.L * p.a_max;
+    __shared__ unsigned int hist[256];
+    const int lane = threadIdx.x & 31;
+    hist[threadIdx.x] = 0;
+    __syncthreads();
+    const unsigned long long pre = vs[b].prefix, msk = vs[b].mask;
+    const int64_t i1 = (ch + 1) * VCH < M ? (ch + 1) * VCH : M;
+    const double *svb = sv + b * M;
+    for (int64_t i0 = ch * VCH; i0 < i1; i0 += blockDim.x) {   // block-uniform trip count
+        const int64_t i = i0 + threadIdx.x;
+        int dg = 256;
+        if (i < i1) {
+            const unsigned long long key = dkey(svb[i]);
+            if ((key & msk) == pre) dg = (int)((key >> shift) & 255);
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, dg);
+        if (dg < 256 && lane == __ffs(peers) - 1) atomicAdd(&hist[dg], (unsigned)__popc(peers));
+    }
+    __syncthreads();
+    const unsigned c = hist[threadIdx.x];
+    if (c) atomicAdd(&ghist[b * 256 + threadIdx.x], c);
+}
+
+// one warp per signal: choose the digit (as k_gen_vote), clear the histogram
+__global__ void k_vsel_pick(int64_t B, int shift, VSel *__restrict__ vs, unsigned int *__restrict__ ghist) {
+    const int64_t b = blockIdx.x;
+    const int lane = threadIdx.x;
+    unsigned c[8], lsum = 0;
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+        c[q] = ghist[b * 256 + 255 - 8 * lane - q];
+        lsum += c[q];
+    }
+#pragma unroll
+    for (int q = 0; q < 8; q++) ghist[b * 256 + 255 - 8 * lane - q] = 0;
+    unsigned inc = lsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    const long long rem = vs[b].remaining;
+    if (rem <= 0) return;
+    const long long before = (long long)(inc - lsum);
+    if (before < rem && before + (long long)lsum >= rem) {
+        long long cum = before;
+        int D = 255 - 8 * lane - 7;
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            if (cum + (long long)c[q] >= rem) {
+                D = 255 - 8 * lane - q;
+                break;
+            }
+            cum += c[q];
+        }
+        vs[b].remaining = rem - cum;
+        vs[b].prefix |= (unsigned long long)D << shift;
+        vs[b].mask |= 0xFFull << shift;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_vsel_eqcount(const double *__restrict__ sv, GenParams p, int64_t nch,
+                                                      const VSel *__restrict__ vs, long long *__restrict__ eqc) {
+    const int64_t b = blockIdx.x / nch, ch = blockIdx.x - b * nch;
+    const int64_t M = p.L * p.a_max;
+    const unsigned long long tau = vs[b].prefix;
+    const int64_t i1 = (ch + 1) * VCH < M ? (ch + 1) * VCH : M;
+    const double *svb = sv + b * M;
+    long long n = 0;
+    for (int64_t i = ch * VCH + threadIdx.x; i < i1; i += blockDim.x) n += dkey(svb[i]) == tau;
+    __shared__ long long red[256];
+    red[threadIdx.x] = n;
+    __syncthreads();
+    for (int s2 = 128; s2 > 0; s2 >>= 1) {
+        if (threadIdx.x < s2) red[threadIdx.x] += red[threadIdx.x + s2];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) eqc[blockIdx.x] = red[0];
+}
+
+__global__ void __launch_bounds__(256) k_vsel_vote(const double *__restrict__ sv, GenParams p, int64_t nch,
+                                                   const VSel *__restrict__ vs,
+                                                   const long long *__restrict__ eqc,
+                                                   int32_t *__restrict__ votes) {
+    const int64_t b = blockIdx.x / nch, ch = blockIdx.x - b * nch;
+    const int64_t M = p.L * p.a_max;
+    const int64_t take = p.k < M ? p.k : M;
+    if (take <= 0) return;
+    const unsigned long long tau = vs[b].prefix;
+    const long long need_eq = vs[b].remaining;
+    long long eq_carry = 0;   // keys == tau in the chunks before this one
+    for (int64_t c2 = 0; c2 < ch; c2++) eq_carry += eqc[b * nch + c2];
+    const int64_t i1 = (ch + 1) * VCH < M ? (ch + 1) * VCH : M;
+    const double *svb = sv + b * M;
+    int32_t *vb = votes + b * p.L;
+    __shared__ int wsum[8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t i0 = ch * VCH; i0 < i1; i0 += blockDim.x) {
+        const int64_t i = i0 + threadIdx.x;
+        unsigned long long key = 0;
+        bool gt = false, eq = false;
+        if (i < i1) {
+            key = dkey(svb[i]);
+            gt = key > tau;
+            eq = key == tau;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, eq);
+        if (lane == 0) wsum[warp] = __popc(m);
+        __syncthreads();
+        int before = 0, total = 0;
+        for (int w2 = 0; w2 < 8; w2++) {
+            before += (w2 < warp) ? wsum[w2] : 0;
+            total += wsum[w2];
+        }
+        const long long rank = eq_carry + before + __popc(m & ((1u << lane) - 1));
+        if (gt || (eq && rank < need_eq)) atomicAdd(&vb[i / p.a_max], 1);
+        eq_carry += total;
+        __syncthreads();
+    }
+}
+
+// zero-vote guard, cap, histogram, worklist (bins of a chunk of the signal)
+__global__ void __launch_bounds__(256) k_vsel_fin(const double *__restrict__ sv, GenParams p, int64_t nchL,
+                                                  const VSel *__restrict__ vs, int32_t *__restrict__ votes,
+                                                  int64_t *__restrict__ stats, int64_t *__restrict__ wl,
+                                                  unsigned long long *__restrict__ wl_count) {
+    const int64_t b = blockIdx.x / nchL, ch = blockIdx.x - b * nchL;
+    const int64_t M = p.L * p.a_max;
+    const double thr = vs[b].thr;
+    const int cap = (int)(p.a_max < p.d ? p.a_max : p.d);
+    int32_t *vb = votes + b * p.L;
+    const double *svb = sv + b * M;
+    __shared__ unsigned long long s_hist[5];
+    __shared__ int s_n;
+    __shared__ unsigned long long s_base;
+    if (threadIdx.x < 5) s_hist[threadIdx.x] = 0;
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    const int64_t k0 = ch * VCH, k1 = (k0 + VCH < p.L) ? k0 + VCH : p.L;
+    unsigned long long hloc[5] = {0, 0, 0, 0, 0};
+    for (int64_t kb = k0 + threadIdx.x; kb < k1; kb += blockDim.x) {
+        int v = vb[kb];
+        if (svb[kb * p.a_max] <= thr) v = 0;
+        if (v > cap) v = cap;
+        vb[kb] = v;
+        hloc[v]++;
+    }
+    for (int a = 0; a <= 4; a++)
+        if (hloc[a]) atomicAdd(&s_hist[a], hloc[a]);
+    __syncthreads();
+    if (threadIdx.x < 5 && s_hist[threadIdx.x])
+        atomicAdd((unsigned long long *)(stats + b * SFDT_GS_PER_SIGNAL + SFDT_GS_HIST0 + threadIdx.x),
+                  s_hist[threadIdx.x]);
+    if (threadIdx.x == 0) {
+        const unsigned long long nv = s_hist[1] + s_hist[2] + s_hist[3] + s_hist[4];
+        if (nv) {
+            atomicAdd((unsigned long long *)(stats + b * SFDT_GS_PER_SIGNAL + SFDT_GS_NVOTED), nv);
+            s_base = atomicAdd(wl_count, nv);
+        }
+    }
+    __syncthreads();
+    // worklist append (order within the list is irrelevant downstream)
+    for (int64_t kb = k0 + threadIdx.x; kb < k1; kb += blockDim.x) {
+        if (vb[kb] >= 1) {
+            const int slot = atomicAdd(&s_n, 1);
+            wl[s_base + slot] = b * p.L + kb;
+        }
+    }
+}
+
 // ------------------------------------------------------------- per bin
 // correlation |sum_j conj(phi_j) v_j| with the column given by its phases
 __device__ __forceinline__ double corr_abs(const cx *phi_col, const cx *v, int r) {
@@ -835,8 +1046,14 @@ __device__ __forceinline__ void sp_a1_t(const cx (&y)[R], const cx (&phase)[R], 
     o.coef[0] = best_coef;
 }
 
+// r_eff values with a register-resident pursuit instance: 3*a_max, or d
+// when d < 3*a_max
+__host__ __device__ __forceinline__ bool sp1_r(int r) {
+    return r == 1 || r == 2 || r == 3 || r == 4 || r == 6 || r == 8 || r == 9 || r == 12;
+}
+
 __device__ __forceinline__ bool sp1_item(int a, int r, int nc8) {
-    return a == 1 && nc8 >= 1 && nc8 <= 4 && (r == 3 || r == 6 || r == 9 || r == 12);
+    return a == 1 && nc8 >= 1 && nc8 <= 4 && sp1_r(r);
 }
 
 template <int R>
@@ -1074,7 +1291,7 @@ struct GenPlan {
     int64_t B, n, d, L, nv, nparts;
     int S;
     size_t off_V, off_sv, off_part, off_votes, off_nent, off_sloc, off_sval, off_wl, off_cnt,
-        off_fft, off_mf, off_cols, off_ncols, off_seg, total;
+        off_fft, off_mf, off_cols, off_ncols, off_seg, off_vsel, off_ghist, off_eqc, total;
 };
 
 static int make_gen_plan(const sfdt_general_args *a, GenPlan &p) {
@@ -1111,6 +1328,9 @@ static int make_gen_plan(const sfdt_general_args *a, GenPlan &p) {
         p.off_ncols = take(size_t(cap));
     }
     p.off_seg = take(size_t(p.B) * ((p.L + GEN_SEG - 1) / GEN_SEG) * 4 * 8);
+    p.off_vsel = take(size_t(p.B) * sizeof(VSel));
+    p.off_ghist = take(size_t(p.B) * 256 * 4);
+    p.off_eqc = take(size_t(p.B) * ((p.L * a->a_max + VCH - 1) / VCH) * 8);
     p.off_fft = (p.L > FFT_SMEM_MAX) ? take(size_t(p.B) * p.nv * p.L * 16) : 0;
     p.total = o;
     return SFDT_OK;
@@ -1197,7 +1417,24 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     }
     SFDT_CHECK_LAUNCH();
     cudaMemsetAsync(wlc, 0, 8, stream);
-    {
+    if (p.L * a->a_max > VOTE_BIG) {
+        const int64_t M = p.L * a->a_max;
+        const int64_t nch = (M + VCH - 1) / VCH, nchL = (p.L + VCH - 1) / VCH;
+        VSel *vs = (VSel *)(w + p.off_vsel);
+        unsigned int *ghist = (unsigned int *)(w + p.off_ghist);
+        long long *eqc = (long long *)(w + p.off_eqc);
+        cudaMemsetAsync(ghist, 0, size_t(p.B) * 256 * 4, stream);
+        cudaMemsetAsync(votes, 0, size_t(p.B) * p.L * 4, stream);
+        k_vsel_init<<<(unsigned)((p.B + 127) / 128), 128, 0, stream>>>(part, (int)p.nparts, gp, p.B, vs, a->stats);
+        for (int shift = 56; shift >= 0; shift -= 8) {
+            k_vsel_hist<<<(unsigned)(p.B * nch), 256, 0, stream>>>(sv, gp, nch, shift, vs, ghist);
+            k_vsel_pick<<<(unsigned)p.B, 32, 0, stream>>>(p.B, shift, vs, ghist);
+        }
+        k_vsel_eqcount<<<(unsigned)(p.B * nch), 256, 0, stream>>>(sv, gp, nch, vs, eqc);
+        k_vsel_vote<<<(unsigned)(p.B * nch), 256, 0, stream>>>(sv, gp, nch, vs, eqc, votes);
+        k_vsel_fin<<<(unsigned)(p.B * nchL), 256, 0, stream>>>(sv, gp, nchL, vs, votes, a->stats, wl, wlc);
+        launches += 1 + 16 + 3 - 1;   // the -1: k_gen_vote is counted below
+    } else {
         const int64_t M = p.L * a->a_max;
         const size_t smem = M <= VOTE_SMEM_KEYS ? size_t(M) * 8 : 0;
         cudaFuncSetAttribute(k_gen_vote, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1239,13 +1476,15 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     int8_t *ncolsb = (int8_t *)(w + p.off_ncols);
     k_gen_prune<<<(unsigned)(sms * 16), 128, 0, stream>>>(V, gp, votes, wl, wlc, mf_top, colsb, ncolsb);
     SFDT_CHECK_LAUNCH();
-    const int sp1 = a->r_eff == 3 || a->r_eff == 6 || a->r_eff == 9 || a->r_eff == 12;
+    const int sp1 = sp1_r(a->r_eff);
     if (sp1) {
+        const unsigned g1 = (unsigned)(sms * 16);
         switch (a->r_eff) {
-        case 3: k_gen_sp1<3><<<(unsigned)(sms * 16), 128, 0, stream>>>(V, gp, votes, wl, wlc, colsb, ncolsb, nent, sloc, sval, a->stats); break;
-        case 6: k_gen_sp1<6><<<(unsigned)(sms * 16), 128, 0, stream>>>(V, gp, votes, wl, wlc, colsb, ncolsb, nent, sloc, sval, a->stats); break;
-        case 9: k_gen_sp1<9><<<(unsigned)(sms * 16), 128, 0, stream>>>(V, gp, votes, wl, wlc, colsb, ncolsb, nent, sloc, sval, a->stats); break;
-        default: k_gen_sp1<12><<<(unsigned)(sms * 16), 128, 0, stream>>>(V, gp, votes, wl, wlc, colsb, ncolsb, nent, sloc, sval, a->stats); break;
+#define SFDT_SP1(R) \
+    case R: k_gen_sp1<R><<<g1, 128, 0, stream>>>(V, gp, votes, wl, wlc, colsb, ncolsb, nent, sloc, sval, a->stats); break;
+            SFDT_SP1(1) SFDT_SP1(2) SFDT_SP1(3) SFDT_SP1(4) SFDT_SP1(6) SFDT_SP1(8) SFDT_SP1(9) SFDT_SP1(12)
+#undef SFDT_SP1
+        default: break;
         }
         SFDT_CHECK_LAUNCH();
         launches++;

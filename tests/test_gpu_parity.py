@@ -388,7 +388,7 @@ def test_general_batch_vs_oracle_cfg4_shape():
 
 @pytest.mark.parametrize("n,k,a_max,d,prune", [(4096, 8, 3, None, True), (4096, 8, 2, 16, True),
                                                (8192, 64, 3, 8, True), (4096, 4, 3, 64, False),
-                                               (4096, 16, 4, None, True)])
+                                               (4096, 16, 4, None, True), (4096, 32, 3, 4, True)])
 def test_general_small_configs(n, k, a_max, d, prune):
     x, _ = general_signal(n, k, 25.0, n + k)
     cfg = P.GeneralConfig(n=n, k=k, a_max=a_max, d=d, rng_seed=3, prune=prune)
@@ -551,3 +551,22 @@ def test_full_size_cfg4_batch_invariance_and_oracle():
         _general_check(eb, locs, vals, f"b={b}")
     del X, res
     torch.cuda.empty_cache()
+
+
+def test_general_long_view_vote():
+    """Signals with more than 65536 vote keys (L*a_max) take the multi-CTA
+    top-K selection; votes, singular values and entries against the oracle."""
+    n, k, B = 1 << 17, 1024, 2
+    seeds = [(11, b) for b in range(B)]
+    X = np.stack([general_signal(n, k, 20.0, s)[0] for s in seeds])
+    cfg = P.GeneralConfig(n=n, k=k)
+    assert (n // cfg.resolved_d()) * cfg.a_max > 65536
+    res = P.solve_general_batch(X, cfg, seeds=seeds)
+    votes = res.votes()
+    for b in range(B):
+        want, wtr = OS.general(X[b], k, rng_seed=seeds[b], return_internals=True)
+        assert np.array_equal(votes[b], wtr["votes"]), f"b={b} votes differ"
+        locs = np.fromiter(want.keys(), dtype=np.int64, count=len(want))
+        vals = np.fromiter(want.values(), dtype=np.complex128, count=len(want))
+        _general_check(res.spectrum(b).entries, locs, vals, f"b={b}")
+        assert res.trace(b).collision_histogram == wtr["collision_histogram"]

@@ -176,6 +176,58 @@ __device__ __forceinline__ void fft_stages_smem(cx *a, int nv, int logL, int lh0
     }
 }
 
+// Views of length L = 2^logL >= 64 (nv per CTA, view-fastest lanes): the
+// first radix-8 pass fused with the strided gather from the signal, the
+// middle passes through shared memory, the last pass fused with the
+// epilogue epi(view, k, value).  Input j of view v sits at
+// s_ibase[v] + ((j*jstride + s_ioff[v]) & src.wrap).
+template <typename Epi>
+__device__ __forceinline__ void fft_fused_views(cx *a, const ViewSrc &src, int64_t jstride,
+                                                const int64_t *s_ibase, const int64_t *s_ioff, int nv,
+                                                int logvpc, int logL, const cx *__restrict__ tw, Epi &&epi) {
+    const int L = 1 << logL, vpc = 1 << logvpc;
+    // First pass fused with the gather: a thread loads the 8 inputs of
+    // one radix-8 group (positions hi*8 + q hold inputs j = bitrev(hi*8
+    // + q)) straight from the signal, runs stages 0-2 in registers and
+    // writes shared memory once.  Lanes vary the view fastest, so one
+    // d-block's adjacent shifts share sectors.
+    const int gper = L >> 3;
+    const int hbits = logL - 3;
+    for (int g = threadIdx.x; g < (gper << logvpc); g += blockDim.x) {
+        const int v = g & (vpc - 1), hi = g >> logvpc;
+        if (v >= nv) continue;
+        const int hb = (int)(__brev((unsigned)hi) >> (32 - hbits));
+        cx x[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            const int q3 = ((q & 1) << 2) | (q & 2) | ((q >> 2) & 1);   // bitrev_3(q)
+            const int j = hb + (q3 << hbits);
+            const int64_t e = s_ibase[v] + (((int64_t)j * jstride + s_ioff[v]) & src.wrap);
+            if (src.is_c64) {
+                const float2 f = __ldg(reinterpret_cast<const float2 *>(src.x) + e);
+                x[q] = mk((double)f.x, (double)f.y);
+            } else {
+                x[q] = ldcx(reinterpret_cast<const cx *>(src.x) + e);
+            }
+        }
+        group_stages<3>(x, 0, 1, tw);
+#pragma unroll
+        for (int q = 0; q < 8; q++) a[swz(v * L + (hi << 3) + q)] = x[q];
+    }
+    __syncthreads();
+    int lh = 3;
+    while (logL - lh > 3) {
+        fft_pass<3>(a, nv, logL, lh, tw);
+        __syncthreads();
+        lh += 3;
+    }
+    // last pass straight to global memory
+    const int nst = logL - lh;
+    if (nst == 3) fft_pass_out<3>(a, nv, logL, lh, tw, epi);
+    else if (nst == 2) fft_pass_out<2>(a, nv, logL, lh, tw, epi);
+    else fft_pass_out<1>(a, nv, logL, lh, tw, epi);
+}
+
 template <int MINB>
 static __global__ void __launch_bounds__(256, MINB) k_fft_views(const ViewSrc src, int64_t B, int logL, int logvpc,
                                    const cx *__restrict__ tw, cx *__restrict__ out, int SV,
@@ -216,46 +268,7 @@ static __global__ void __launch_bounds__(256, MINB) k_fft_views(const ViewSrc sr
         }
     };
     if (logL >= 6 && !src.jfast) {
-        // First pass fused with the gather: a thread loads the 8 inputs of
-        // one radix-8 group (positions hi*8 + q hold inputs j = bitrev(hi*8
-        // + q)) straight from the signal, runs stages 0-2 in registers and
-        // writes shared memory once.  Lanes vary the view fastest, so one
-        // d-block's adjacent shifts share sectors.
-        const int gper = L >> 3;
-        const int hbits = logL - 3;
-        for (int g = threadIdx.x; g < (gper << logvpc); g += blockDim.x) {
-            const int v = g & (vpc - 1), hi = g >> logvpc;
-            if (v >= nv) continue;
-            const int hb = (int)(__brev((unsigned)hi) >> (32 - hbits));
-            cx x[8];
-#pragma unroll
-            for (int q = 0; q < 8; q++) {
-                const int q3 = ((q & 1) << 2) | (q & 2) | ((q >> 2) & 1);   // bitrev_3(q)
-                const int j = hb + (q3 << hbits);
-                const int64_t e = s_ibase[v] + (((int64_t)j * src.jstride + s_ioff[v]) & src.wrap);
-                if (src.is_c64) {
-                    const float2 f = __ldg(reinterpret_cast<const float2 *>(src.x) + e);
-                    x[q] = mk((double)f.x, (double)f.y);
-                } else {
-                    x[q] = ldcx(reinterpret_cast<const cx *>(src.x) + e);
-                }
-            }
-            group_stages<3>(x, 0, 1, tw);
-#pragma unroll
-            for (int q = 0; q < 8; q++) a[swz(v * L + (hi << 3) + q)] = x[q];
-        }
-        __syncthreads();
-        int lh = 3;
-        while (logL - lh > 3) {
-            fft_pass<3>(a, nv, logL, lh, tw);
-            __syncthreads();
-            lh += 3;
-        }
-        // last pass straight to global memory
-        const int nst = logL - lh;
-        if (nst == 3) fft_pass_out<3>(a, nv, logL, lh, tw, epi);
-        else if (nst == 2) fft_pass_out<2>(a, nv, logL, lh, tw, epi);
-        else fft_pass_out<1>(a, nv, logL, lh, tw, epi);
+        fft_fused_views(a, src, src.jstride, s_ibase, s_ioff, nv, logvpc, logL, tw, epi);
         return;
     }
     // small views: gather (lanes vary the view fastest for one sample j),
@@ -307,37 +320,19 @@ static __global__ void k_fft_large_a(const ViewSrc src, int logL, int logP,
     const int64_t b = g / src.nshift;
     const int s = (int)(g - b * src.nshift);
     const int rc = logQ ? (int)(__brev((unsigned)c) >> (32 - logQ)) : 0;
-    // addressing once per CTA; loads issued 8 at a time before their
-    // shared-memory stores (every load is its own sector: stride Q*d)
-    const int64_t o = (s >= src.dyn_first) ? __ldg(src.dyn_off + b * src.dyn_stride + (s - src.dyn_first))
-                                           : src.off[s];
-    const int64_t ib = b * src.sig_stride;
-    for (int i0 = 0; i0 < P; i0 += 8 * 256) {
-        cx vals[8];
-#pragma unroll
-        for (int u = 0; u < 8; u++) {
-            const int i = i0 + u * 256 + threadIdx.x;
-            if (i < P) {
-                const int64_t j = (int64_t)(__brev((unsigned)i) >> (32 - logP)) * Q + rc;
-                const int64_t e = ib + ((j * src.jstride + o) & src.wrap);
-                if (src.is_c64) {
-                    const float2 f = __ldg(reinterpret_cast<const float2 *>(src.x) + e);
-                    vals[u] = mk((double)f.x, (double)f.y);
-                } else {
-                    vals[u] = ldcx(reinterpret_cast<const cx *>(src.x) + e);
-                }
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < 8; u++) {
-            const int i = i0 + u * 256 + threadIdx.x;
-            if (i < P) a[swz(i)] = vals[u];
-        }
+    // block c of view g is itself a P-point view: input i of the block is
+    // view sample rev_P(i)*Q + rc, i.e. stride Q*d from offset shift + rc*d
+    __shared__ int64_t s_ib[1], s_io[1];
+    if (threadIdx.x == 0) {
+        const int64_t o = (s >= src.dyn_first) ? src.dyn_off[b * src.dyn_stride + (s - src.dyn_first)]
+                                               : src.off[s];
+        s_ib[0] = b * src.sig_stride;
+        s_io[0] = o + (int64_t)rc * src.jstride;
     }
     __syncthreads();
-    fft_stages_smem(a, 1, logP, 0, logP, tw);
     cx *dst = scratch + (g << logL) + ((int64_t)c << logP);
-    for (int i = threadIdx.x; i < P; i += blockDim.x) dst[i] = a[swz(i)];
+    fft_fused_views(a, src, src.jstride << logQ, s_ib, s_io, 1, 0, logP, tw,
+                    [&](int, int k, cx y) { dst[k] = y; });
 }
 
 // large views (L > FFT_SMEM_MAX): stage split through global memory.

@@ -163,6 +163,33 @@ __global__ void k_rms(const double *__restrict__ partial, int64_t nchunk, int64_
     }
 }
 
+// the same tree for nchunk <= 64 with one warp per signal: the 1024-slot
+// tree's levels above 32 only add exact zeros, so lane t starting from
+// p[t] + p[t+32] and halving by shuffles reproduces it bit for bit
+__global__ void k_rms_warp(const double *__restrict__ partial, int64_t B, int64_t nchunk, int64_t n, double zt,
+                           int64_t d, double *__restrict__ rms, double *__restrict__ thr) {
+    const int64_t b = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (b >= B) return;
+    const double *pb = partial + b * nchunk;
+    double v = (lane < nchunk ? pb[lane] : 0.0) + (lane + 32 < nchunk ? pb[lane + 32] : 0.0);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) {
+        const double r = sqrt(v / (double)n);
+        rms[b] = r;
+        thr[b] = DMUL(DMUL(zt, r), (double)d);
+    }
+}
+
+static inline void launch_rms(const double *partial, int64_t B, int64_t nchunk, int64_t n, double zt,
+                              int64_t d, double *rms, double *thr, cudaStream_t st) {
+    if (nchunk <= 64)
+        k_rms_warp<<<(unsigned)((B + 7) / 8), 256, 0, st>>>(partial, B, nchunk, n, zt, d, rms, thr);
+    else
+        k_rms<<<(unsigned)B, 1024, 0, st>>>(partial, nchunk, n, zt, d, rms, thr);
+}
+
 // thresholds from a known rms (rms_in): copy rms out, zt*rms*d
 __global__ void k_thr_from_rms(const double *__restrict__ rms_in, int64_t B, double zt, int64_t d,
                                double *__restrict__ rms_out, double *__restrict__ thr) {
@@ -717,30 +744,54 @@ __global__ void k_noniter_fin(const long long *__restrict__ segcnt, int64_t B, i
     st[27] = r[4];
 }
 
-// exclusive scan of per-signal counts -> offsets (single CTA, B up to any size)
-__global__ void k_scan_offsets(const int64_t *__restrict__ stats, int64_t B, int field,
-                               int64_t *__restrict__ offsets) {
-    __shared__ long long carry;
-    __shared__ long long buf[1024];
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (int64_t base = 0; base < B; base += 1024) {
-        const int64_t i = base + threadIdx.x;
-        long long v = (i < B) ? stats[i * SFDT_ST_PER_SIGNAL + field] : 0;
-        buf[threadIdx.x] = v;
-        __syncthreads();
-        for (int s = 1; s < 1024; s <<= 1) {
-            long long add = (threadIdx.x >= s) ? buf[threadIdx.x - s] : 0;
-            __syncthreads();
-            buf[threadIdx.x] += add;
-            __syncthreads();
+// exclusive scans of up to three per-signal stats fields -> offsets (one
+// CTA, B up to any size; out[B] = total).  Warp-shuffle block scan.
+struct ScanFields {
+    int field[3];
+    int64_t *out[3];
+    int nf;
+};
+
+__global__ void __launch_bounds__(1024) k_scan_offsets(const int64_t *__restrict__ stats, int64_t B,
+                                                       ScanFields f) {
+    // thread t owns signals [t*per, (t+1)*per): its sums (independent loads,
+    // one memory latency), one block scan of the thread sums, then its
+    // offsets -- instead of a barrier-bound pass per 1024 signals
+    __shared__ long long wtot[3][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t per = (B + blockDim.x - 1) / blockDim.x;
+    const int64_t i0 = threadIdx.x * per, i1 = (i0 + per < B) ? i0 + per : B;
+    long long sum[3] = {0, 0, 0}, inc[3];
+    for (int64_t i = i0; i < i1; i++)
+#pragma unroll
+        for (int q = 0; q < 3; q++)
+            if (q < f.nf) sum[q] += stats[i * SFDT_ST_PER_SIGNAL + f.field[q]];
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        inc[q] = sum[q];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long y = __shfl_up_sync(0xffffffffu, inc[q], o);
+            if (lane >= o) inc[q] += y;
         }
-        if (i < B) offsets[i] = carry + buf[threadIdx.x] - v;
-        __syncthreads();
-        if (threadIdx.x == 1023) carry += buf[1023];
-        __syncthreads();
+        if (lane == 31) wtot[q][warp] = inc[q];
     }
-    if (threadIdx.x == 0) offsets[B] = carry;
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        if (q >= f.nf) continue;
+        long long run = inc[q] - sum[q], total = 0;
+        for (int w2 = 0; w2 < (int)(blockDim.x >> 5); w2++) {
+            const long long c = wtot[q][w2];
+            run += (w2 < warp) ? c : 0;
+            total += c;
+        }
+        for (int64_t i = i0; i < i1; i++) {
+            f.out[q][i] = run;
+            run += stats[i * SFDT_ST_PER_SIGNAL + f.field[q]];
+        }
+        if (threadIdx.x == 0) f.out[q][B] = total;
+    }
 }
 
 // emit entries in (a, bin) order and unresolved bins ascending.  One CTA per
@@ -1314,8 +1365,8 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
                                                                               a->zero_threshold, p.d,
                                                                               a->rms + c0, thr + c0);
             else
-                k_rms<<<(unsigned)nb, 1024, 0, aux>>>(partial + c0 * p.nchunk, p.nchunk, p.n,
-                                                      a->zero_threshold, p.d, a->rms + c0, thr + c0);
+                launch_rms(partial + c0 * p.nchunk, nb, p.nchunk, p.n, a->zero_threshold, p.d, a->rms + c0,
+                           thr + c0, aux);
             SFDT_CHECK_LAUNCH();
             // after the rms the FFT epilogue can also mark the active bins
             const bool dense = !overlap;
@@ -1357,15 +1408,17 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
         k_noniter_fin<<<(unsigned)((p.B + 255) / 256), 256, 0, stream>>>(segcnt, p.B, nseg, p.L, (int)p.S,
                                                                          p.d, a->stats);
         SFDT_CHECK_LAUNCH();
-        k_scan_offsets<<<1, 1024, 0, stream>>>(a->stats, p.B, SFDT_ST_NENTRIES, a->entry_offsets);
-        k_scan_offsets<<<1, 1024, 0, stream>>>(a->stats, p.B, SFDT_ST_NUNRESOLVED, a->unres_offsets);
+        {
+            ScanFields f{{SFDT_ST_NENTRIES, SFDT_ST_NUNRESOLVED, 0}, {a->entry_offsets, a->unres_offsets, nullptr}, 2};
+            k_scan_offsets<<<1, 1024, 0, stream>>>(a->stats, p.B, f);
+        }
         SFDT_CHECK_LAUNCH();
         k_noniter_emit<256><<<(unsigned)(p.B * nseg), 256, 0, stream>>>(
             status, bloc, bval, p.L, a->a_max, a->stats, a->entry_offsets, a->unres_offsets,
             a->locs, (cx *)a->vals, a->unres_bins, nseg, segcnt);
         SFDT_CHECK_LAUNCH();
         if (a->dup_offsets) cudaMemsetAsync(a->dup_offsets, 0, sizeof(int64_t) * (p.B + 1), stream);
-        launches += 5;
+        launches += 4;   // count, fin, scan, emit
         a->kernel_launches = launches;
         return SFDT_OK;
     }
@@ -1378,8 +1431,7 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
         k_thr_from_rms<<<(unsigned)((p.B + 255) / 256), 256, 0, stream>>>(a->rms_in, p.B, a->zero_threshold,
                                                                           p.d, a->rms, thr);
     else
-        k_rms<<<(unsigned)p.B, 1024, 0, stream>>>(partial, p.nchunk, p.n, a->zero_threshold, p.d,
-                                                 a->rms, thr);
+        launch_rms(partial, p.B, p.nchunk, p.n, a->zero_threshold, p.d, a->rms, thr, stream);
     SFDT_CHECK_LAUNCH();
     launches += 1;
 
@@ -1448,10 +1500,11 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
                                                          pi, resid,
                                                          thr + p.B * p.npass, ndef, a->stats);
     SFDT_CHECK_LAUNCH();
-    k_scan_offsets<<<1, 1024, 0, stream>>>(a->stats, p.B, SFDT_ST_NENTRIES, a->entry_offsets);
-    k_scan_offsets<<<1, 1024, 0, stream>>>(a->stats, p.B, SFDT_ST_NUNRESOLVED, a->unres_offsets);
-    if (a->dup_offsets)
-        k_scan_offsets<<<1, 1024, 0, stream>>>(a->stats, p.B, SFDT_ST_NDUP, a->dup_offsets);
+    {
+        ScanFields f{{SFDT_ST_NENTRIES, SFDT_ST_NUNRESOLVED, SFDT_ST_NDUP},
+                     {a->entry_offsets, a->unres_offsets, a->dup_offsets}, a->dup_offsets ? 3 : 2};
+        k_scan_offsets<<<1, 1024, 0, stream>>>(a->stats, p.B, f);
+    }
     SFDT_CHECK_LAUNCH();
     k_iter_emit<256><<<(unsigned)((p.B + 7) / 8), 256, 0, stream>>>(st, p.B, p.L, a->a_max, (int)p.npass, pi,
                                                         m_final, a->entry_offsets, a->unres_offsets,
@@ -1459,7 +1512,7 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
                                                         a->locs, (cx *)a->vals, a->unres_bins,
                                                         a->dup_locs);
     SFDT_CHECK_LAUNCH();
-    launches += (int)p.npass * (1 + 2 + fft_view_launches(p.L)) + 1 + 1 + 2 + (a->dup_offsets ? 1 : 0) + 1;
+    launches += (int)p.npass * (1 + 2 + fft_view_launches(p.L)) + 1 + 1 + 1 + 1;   // final, count, scan, emit
     a->kernel_launches = launches;
     return SFDT_OK;
 }

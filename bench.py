@@ -325,6 +325,23 @@ class Solver:
                                        n_signals=n_signals)
 
 
+def pcie_h2d_peak(Xh, dev):
+    """Best-of-3 pinned host -> device copy bandwidth (GB/s) of up to 1 GiB of Xh."""
+    import torch
+    src = Xh.reshape(-1).view(torch.uint8)[: 1 << 30]
+    dst = torch.empty_like(src, device=dev)
+    best = 0.0
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dst.copy_(src, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        best = max(best, src.numel() / (e0.elapsed_time(e1) / 1e3) / 1e9)
+    del dst
+    return best
+
+
 def gpu_arm(a):
     import torch
     import torch.distributed as dist
@@ -403,10 +420,18 @@ def gpu_arm(a):
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
+        h2d = int(hr.h2d_bytes)
+        link = pcie_h2d_peak(Xh, dev)
         e2e = {"value": world * a.batch * a.e2e_steps / e2e_s, "unit": "signals/s",
-               "h2d_bytes_per_step": a.batch * a.n * Xh.element_size(),
+               "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": int(hr.d2h_bytes),
-               "api": "paper_1407_8315_b200.solve_host_batch (pinned host -> GPU -> host results)",
+               "api": ("paper_1407_8315_b200.solve_host_batch (pinned host -> GPU -> host results"
+                       + ("; zero-copy: the view gather reads the (2*a_max+r_eff)*L samples of each "
+                          "signal from mapped host memory" if hr.zero_copy else "") + ")"),
+               "pcie": {"bound": "pcie", "h2d_achieved_gbs": h2d * a.e2e_steps / e2e_s / 1e9,
+                        "h2d_peak_gbs": link,
+                        "peak_source": "measured in this run: best of 3 pinned 1 GiB cudaMemcpy H2D",
+                        "frac": h2d * a.e2e_steps / e2e_s / 1e9 / link},
                "clocks": clocks_e2e.summary()}
         del Xh
 

@@ -171,14 +171,26 @@ class GeneralPlan:
 
 
 def solve_general_batch(X, cfg: GeneralConfig, seeds=None, device=None,
-                        plan: GeneralPlan | None = None) -> GeneralBatch:
+                        plan: GeneralPlan | None = None, zero_copy: bool = False) -> GeneralBatch:
     """Batched solve_general.  seeds: None (cfg.rng_seed for every signal) or
     one rng_seed per signal (per-signal shift draws); plan: precomputed
-    GeneralPlan for repeated batches."""
+    GeneralPlan for repeated batches.
+
+    zero_copy: X is a pinned (page-locked) HOST tensor and stays there.  The
+    general path reads only the (2*a_max + r_eff)*L view samples of each
+    signal (general.py:288-294), so the view gather loads them
+    straight from mapped host memory over PCIe (UVA) instead of copying all
+    N samples to HBM first."""
     t0 = time.perf_counter()
     dev = require_cuda(device if device is not None else
                        (X.device if isinstance(X, torch.Tensor) and X.is_cuda else None))
-    X = as_device_signals(X, dev)
+    if zero_copy:
+        if not (isinstance(X, torch.Tensor) and X.device.type == "cpu" and X.is_pinned()):
+            raise ValueError("zero_copy needs a pinned host tensor (tensor.pin_memory())")
+        if X.dtype not in (torch.complex128, torch.complex64) or not X.is_contiguous():
+            raise ValueError("zero_copy needs a contiguous complex128/complex64 tensor")
+    else:
+        X = as_device_signals(X, dev)
     if X.dim() == 1:
         X = X.unsqueeze(0)
     if X.dim() != 2:
@@ -224,7 +236,7 @@ def solve_general_batch(X, cfg: GeneralConfig, seeds=None, device=None,
     ws = Workspace.get(nbytes, dev)
     _lib.check(lib.sfdt_general_solve(a, ws.data_ptr(), ws.numel(), stream_handle(dev)),
                "sfdt_general_solve")
-    o["_keep"] = (sh_d, phi_d, tw)
+    o["_keep"] = (sh_d, phi_d, tw, X)   # X: a zero-copy host source stays alive with the results
     return GeneralBatch(n, cfg, d, r_eff, sh, o, time.perf_counter() - t0, int(a.kernel_launches))
 
 

@@ -204,3 +204,44 @@ def test_collision_census():
     for n_plus, r in res.items():
         assert abs(r["per_bin_probability"].sum() - 1.0) < 1e-12
         assert r["d"] == (1 << 12) // n_plus // 16
+
+
+@pytest.mark.parametrize("dtype", [torch.complex128, torch.complex64])
+def test_host_batch_general_zero_copy(dtype):
+    """solve_host_batch on pinned host signals: the general solver's view
+    gather reads mapped host memory (zero-copy) -- results must equal the
+    device-resident batch bitwise, including a cycled pool that wraps."""
+    from tests.synth import general_signal
+    n, k, H = 1 << 14, 16, 5
+    X = np.stack([general_signal(n, k, 20.0, 40 + b)[0] for b in range(H)])
+    Xh = torch.from_numpy(X).to(dtype).pin_memory()
+    cfg = P.GeneralConfig(n=n, k=k, rng_seed=11)
+    dev = P.solve_general_batch(Xh.cuda(), cfg)
+    hr = P.solve_host_batch(Xh, cfg, chunk=3, n_signals=7)
+    assert hr.zero_copy
+    L = n // cfg.resolved_d()
+    assert hr.h2d_bytes == 7 * (2 * cfg.a_max + min(cfg.r, cfg.resolved_d())) * L * Xh.element_size()
+    for b in range(7):
+        got, want = hr.spectrum(b).entries, dev.spectrum(b % H).entries
+        assert list(got) == list(want), f"b={b}"
+        assert np.array_equal(np.fromiter(got.values(), complex), np.fromiter(want.values(), complex))
+    # the streamed (copying) path gives the same answer
+    hs = P.solve_host_batch(Xh, cfg, chunk=2, zero_copy=False)
+    assert not hs.zero_copy and hs.h2d_bytes == H * n * Xh.element_size()
+    for b in range(H):
+        assert hs.spectrum(b).entries == dev.spectrum(b).entries
+
+
+def test_host_batch_exact_streams_whole_rows():
+    from tests.synth import exact_signal
+    n, k, H = 1 << 14, 32, 3
+    X = np.stack([exact_signal(n, k, 60 + b, "unit")[0] for b in range(H)])
+    Xh = torch.from_numpy(X).pin_memory()
+    cfg = P.ExactConfig(n=n, k=k)
+    with pytest.raises(ValueError):
+        P.solve_host_batch(Xh, cfg, zero_copy=True)
+    hr = P.solve_host_batch(Xh, cfg, chunk=2, n_signals=5)
+    assert not hr.zero_copy and hr.h2d_bytes == 5 * n * 16
+    for b in range(5):
+        want, _ = OS.exact_noniterative(X[b % H], k)
+        assert list(hr.spectrum(b).entries) == list(want)

@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--mu", type=int, default=None)
     ap.add_argument("--cfg5-general", action="store_true")
+    ap.add_argument("--no-prune", action="store_true",
+                    help="general path without pruning (pursuit over all d columns; the paper's "
+                         "'without pruning' rows)")
     ap.add_argument("--dtype", default="c128", choices=["c128", "c64"])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-chunk", type=int, default=256)
@@ -109,7 +112,7 @@ def workload(a):
         desc = (f"{a.config}: generally K-sparse, B={a.batch}, N=2^{a.n.bit_length() - 1}, K={a.k} "
                 f"unit tones + {a.snr:g} dB time-domain complex Gaussian noise, "
                 f"{'complex64 storage' if a.dtype == 'c64' else 'complex128'}; solve_general "
-                "a_max=3 r=9 per-signal rng_seed")
+                f"a_max=3 r=9 per-signal rng_seed{', prune=False' if a.no_prune else ''}")
     return {
         "workload": desc, "batch": a.batch, "n": a.n, "k": a.k, "d": d, "L": a.n // d,
         "solver": a.solver if a.kind == "exact" else "general", "dtype_storage": a.dtype,
@@ -128,7 +131,8 @@ def _cpu_task(i):
     c = _CPU
     x = c["pool"][i % len(c["pool"])]
     if c["kind"] == "general":
-        OS.general(x, c["k"], rng_seed=(c["seed"], i % len(c["pool"])), kernels=c["kernels"])
+        OS.general(x, c["k"], rng_seed=(c["seed"], i % len(c["pool"])), kernels=c["kernels"],
+                   prune=c["prune"])
     elif c["solver"] == "iterative":
         OS.exact_iterative(x, c["k"], c["mu"], kernels=c["kernels"])
     else:
@@ -159,7 +163,7 @@ def cpu_reference(a, steps, warmup, seconds_per_step):
     cores = len(os.sched_getaffinity(0))
     npool = max(2, min(16 if a.n >= (1 << 22) else 64, max(8, cores)))
     _CPU.update(pool=[cpu_signal(a, i) for i in range(npool)], kind=a.kind, k=a.k, mu=a.mu,
-                solver=a.solver, seed=a.seed, kernels=kind)
+                solver=a.solver, seed=a.seed, kernels=kind, prune=not a.no_prune)
     t0 = time.perf_counter()
     for i in range(2):
         _cpu_task(i)
@@ -299,7 +303,7 @@ class Solver:
             self.cfg = P.ExactConfig(n=a.n, k=a.k, mu=a.mu)
             self.iterative = a.solver == "iterative"
         else:
-            self.cfg = P.GeneralConfig(n=a.n, k=a.k)
+            self.cfg = P.GeneralConfig(n=a.n, k=a.k, prune=not a.no_prune)
             self.seeds = [(a.seed, rank, b) for b in range(a.batch)]
             self.plan = P.GeneralPlan(self.cfg, a.batch, self.seeds, dev)
 
@@ -312,7 +316,7 @@ class Solver:
     def oracle(self, x, b):
         from oracle import solvers as OS
         if self.a.kind == "general":
-            want, _ = OS.general(x, self.a.k, rng_seed=self.seeds[b])
+            want, _ = OS.general(x, self.a.k, rng_seed=self.seeds[b], prune=not self.a.no_prune)
         elif self.iterative:
             want, _ = OS.exact_iterative(x, self.a.k, self.a.mu)
         else:

@@ -16,6 +16,9 @@
 //                (general.py:224-269, 357-366)
 //   count/scan/emit  compact (loc, value) lists in dict insertion order
 //                (vote class a ascending, bin ascending, column ascending)
+#include <climits>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "decode.cuh"
 #include "fft.cuh"
@@ -476,11 +479,52 @@ struct SPOut {
     int rankdef;
 };
 
+// Warp merge of per-lane top lists (each sorted best-first by score desc,
+// then column asc) into the warp's top `cnt` in the same order -- the result
+// of inserting every column sequentially in ascending order.  A NaN score
+// ranks after every number (numpy's argsort puts NaN last).  All 32 lanes
+// call it and all receive the merged list.
+__device__ __forceinline__ bool sp_better(double v2, int t2, double v, int t) {
+    const bool n2 = v2 != v2, n1 = v != v;
+    if (n2 != n1) return n1;            // a number beats a NaN
+    if (!n2 && v2 != v) return v2 > v;
+    return t2 < t;
+}
+
+__device__ __forceinline__ int warp_topk_merge(const double *sc, const int *id, int nloc, int cnt,
+                                               double *osc, int *oid) {
+    int h = 0, on = 0;
+    for (int round = 0; round < cnt; round++) {
+        double v = h < nloc ? sc[h] : 0.0;
+        int t = h < nloc ? id[h] : INT_MAX;   // INT_MAX: this lane is exhausted
+#pragma unroll
+        for (int off = 16; off; off >>= 1) {
+            const double v2 = __shfl_xor_sync(0xffffffffu, v, off);
+            const int t2 = __shfl_xor_sync(0xffffffffu, t, off);
+            if (t2 != INT_MAX && (t == INT_MAX || sp_better(v2, t2, v, t))) {
+                v = v2;
+                t = t2;
+            }
+        }
+        if (t == INT_MAX) break;
+        osc[on] = v;
+        oid[on] = t;
+        on++;
+        if (h < nloc && id[h] == t) h++;
+    }
+    return on;
+}
+
 // subspace pursuit over columns c < ncols (column index -> candidate t via
-// cols[] unless all_cols); phi[j, t] = phase_j * base_phi[j, t]
+// cols[] unless all_cols); phi[j, t] = phase_j * base_phi[j, t].
+// nlanes = 1: one thread per bin.  nlanes = 32: one warp per bin -- lane l
+// scores columns l, l+32, ... (the same per-column arithmetic) and the
+// lane lists are merged by warp_topk_merge, so the selections, and with
+// them every least-squares solve (run redundantly by all lanes), are
+// bit-identical to the single-thread form.
 __device__ void subspace_pursuit_dev(const cx *y, const cx *phase, const cx *bphi, int64_t d,
                                      int r, const int *cols, int ncols, bool all_cols, int a_sp,
-                                     SPOut &o) {
+                                     SPOut &o, int lane = 0, int nlanes = 1) {
     const int a_eff = a_sp < ncols ? a_sp : ncols;
     auto col_t = [&](int c) -> int64_t { return all_cols ? (int64_t)c : (int64_t)cols[c]; };
     auto phi_col = [&](int c, cx *out) {
@@ -491,11 +535,24 @@ __device__ void subspace_pursuit_dev(const cx *y, const cx *phase, const cx *bph
     // initial support: top a_eff of |phi^H y|, stable, then sorted
     double tsc[GEN_MAX_SUP];
     int tid_[GEN_MAX_SUP];
-    int nt = 0;
-    for (int c = 0; c < ncols; c++) {
-        phi_col(c, pc);
-        topk_insert(tsc, tid_, nt, a_eff, corr_abs(pc, y, r), c);
-    }
+    // top a_eff columns of |phi^H v| (stable), best first
+    auto top_cols = [&](const cx *v) -> int {
+        int n0 = 0;
+        for (int c = lane; c < ncols; c += nlanes) {
+            phi_col(c, pc);
+            topk_insert(tsc, tid_, n0, a_eff, corr_abs(pc, v, r), c);
+        }
+        if (nlanes == 1) return n0;
+        double msc[GEN_MAX_SUP];
+        int mid[GEN_MAX_SUP];
+        const int nm = warp_topk_merge(tsc, tid_, n0, a_eff, msc, mid);
+        for (int i = 0; i < nm; i++) {
+            tsc[i] = msc[i];
+            tid_[i] = mid[i];
+        }
+        return nm;
+    };
+    int nt = top_cols(y);
     int sup[GEN_MAX_SUP];
     int nsup = nt;
     for (int i = 0; i < nt; i++) sup[i] = tid_[i];
@@ -528,11 +585,7 @@ __device__ void subspace_pursuit_dev(const cx *y, const cx *phase, const cx *bph
     }
     for (int it = 0; it < 10; it++) {
         // merged = union(support, top a_eff of |phi^H residual|)
-        nt = 0;
-        for (int c = 0; c < ncols; c++) {
-            phi_col(c, pc);
-            topk_insert(tsc, tid_, nt, a_eff, corr_abs(pc, res, r), c);
-        }
+        nt = top_cols(res);
         int topc[GEN_MAX_SUP];
         for (int i = 0; i < nt; i++) topc[i] = tid_[i];
         sort_ints(topc, nt);
@@ -1106,7 +1159,7 @@ __global__ void __launch_bounds__(128) k_gen_bins(const cx *__restrict__ V, GenP
                                                   const int64_t *__restrict__ wl,
                                                   const unsigned long long *__restrict__ wl_count,
                                                   const int32_t *__restrict__ cols_in,
-                                                  const int8_t *__restrict__ ncols_in, int skip_sp1,
+                                                  const int8_t *__restrict__ ncols_in, int skip,
                                                   uint8_t *__restrict__ nent, int64_t *__restrict__ sloc,
                                                   cx *__restrict__ sval, int64_t *__restrict__ stats) {
     const int64_t cnt = (int64_t)*wl_count;
@@ -1115,7 +1168,8 @@ __global__ void __launch_bounds__(128) k_gen_bins(const cx *__restrict__ V, GenP
         const int64_t t = wl[it];
         const int a = votes[t];
         const int r = p.r_eff;
-        if (skip_sp1 && sp1_item(a, r, ncols_in[it])) continue;   // k_gen_sp1's
+        if ((skip & 1) && sp1_item(a, r, ncols_in[it])) continue;   // k_gen_sp1's
+        if ((skip & 2) && ncols_in[it] < 0) continue;               // k_gen_bins_warp's
         const int64_t b = t / p.L, kb = t - b * p.L;
         const int64_t *sh = p.shifts + b * p.shift_stride;
         const cx *bphi = p.base_phi + b * p.phi_stride;
@@ -1144,6 +1198,52 @@ __global__ void __launch_bounds__(128) k_gen_bins(const cx *__restrict__ V, GenP
         if (o.rankdef)
             atomicAdd((unsigned long long *)(stats + b * SFDT_GS_PER_SIGNAL + SFDT_GS_RANKDEF),
                       (unsigned long long)o.rankdef);
+    }
+}
+
+// One WARP per bin for the bins whose pursuit scores all d columns (no
+// pruning, general.py:352-354): the column scans of subspace pursuit are
+// spread over the lanes (k_gen_bins skips these bins).
+__global__ void __launch_bounds__(256) k_gen_bins_warp(const cx *__restrict__ V, GenParams p,
+                                                       const int32_t *__restrict__ votes,
+                                                       const int64_t *__restrict__ wl,
+                                                       const unsigned long long *__restrict__ wl_count,
+                                                       const int8_t *__restrict__ ncols_in,
+                                                       uint8_t *__restrict__ nent, int64_t *__restrict__ sloc,
+                                                       cx *__restrict__ sval, int64_t *__restrict__ stats) {
+    const int64_t cnt = (int64_t)*wl_count;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = int64_t(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t it = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); it < cnt; it += nw) {
+        if (ncols_in[it] >= 0) continue;   // pruned bins: k_gen_sp1 / k_gen_bins
+        const int64_t t = wl[it];
+        const int a = votes[t];
+        const int r = p.r_eff;
+        const int64_t b = t / p.L, kb = t - b * p.L;
+        const int64_t *sh = p.shifts + b * p.shift_stride;
+        const cx *bphi = p.base_phi + b * p.phi_stride;
+        cx y[GEN_MAX_R], phase[GEN_MAX_R];
+        const double tk = DMUL(TWO_PI, (double)kb);
+        for (int j = 0; j < r; j++) {
+            y[j] = ldcx(V + (b * p.nv + p.S + j) * p.L + kb);
+            phase[j] = gexp(mk(0.0, DMUL(tk, (double)sh[j]) / (double)p.n));
+        }
+        const int a_sp = a < r ? a : r;
+        SPOut o;
+        subspace_pursuit_dev(y, phase, bphi, p.d, r, nullptr, (int)p.d, true, a_sp, o, lane, 32);
+        if (lane == 0) {
+            int ne = 0;
+            for (int i = 0; i < o.nsup; i++) {
+                if (o.coef[i].re == 0.0 && o.coef[i].im == 0.0) continue;   // np.nonzero(coef)
+                sloc[t * p.a_max + ne] = (kb + (int64_t)o.sup[i] * p.L) & (p.n - 1);
+                stcx(sval + t * p.a_max + ne, o.coef[i]);
+                ne++;
+            }
+            nent[t] = (uint8_t)ne;
+            if (o.rankdef)
+                atomicAdd((unsigned long long *)(stats + b * SFDT_GS_PER_SIGNAL + SFDT_GS_RANKDEF),
+                          (unsigned long long)o.rankdef);
+        }
     }
 }
 
@@ -1489,8 +1589,26 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
         SFDT_CHECK_LAUNCH();
         launches++;
     }
-    k_gen_bins<<<(unsigned)(sms * 16), 128, 0, stream>>>(V, gp, votes, wl, wlc, colsb, ncolsb, sp1, nent,
-                                                         sloc, sval, a->stats);
+    // Bins pursued over all d columns (prune off, or count >= d): one warp
+    // per bin while the bins are few -- at most K voted bins per signal, and
+    // up to ~224 warps per SM the warp form's shorter chains win (measured
+    // at N=2^22, B=64, d=2048/512/128: 7.33 -> 1.33 ms, 3.64 -> 2.19 ms,
+    // 2.75 -> 5.53 ms); beyond that, thread per bin (32 bins per warp in
+    // lockstep) keeps the FP64 pipe busier than 32 lanes on one bin's
+    // redundant least squares.  SFDT_GEN_WARP=0/1 forces either form.
+    const char *ev = getenv("SFDT_GEN_WARP");
+    const bool all_d = !a->prune || p.d <= 2 * (int64_t)a->keep_per_collision * a->a_max;
+    const bool few = (int64_t)a->k * p.B <= 224 * (int64_t)sms;
+    const int warp_all = all_d && (ev ? ev[0] == '1' : few);
+    if (warp_all) {
+        k_gen_bins_warp<<<(unsigned)(sms * 16), 256, 0, stream>>>(V, gp, votes, wl, wlc, ncolsb, nent, sloc,
+                                                                  sval, a->stats);
+        SFDT_CHECK_LAUNCH();
+        launches++;
+    }
+    k_gen_bins<<<(unsigned)(sms * 16), 128, 0, stream>>>(V, gp, votes, wl, wlc, colsb, ncolsb,
+                                                         sp1 | (warp_all ? 2 : 0), nent, sloc, sval,
+                                                         a->stats);
     SFDT_CHECK_LAUNCH();
     launches++;
     const int64_t nseg = (p.L + GEN_SEG - 1) / GEN_SEG;

@@ -386,6 +386,25 @@ def test_general_batch_vs_oracle_cfg4_shape():
         assert tr.collision_histogram == wtr["collision_histogram"]
 
 
+@pytest.mark.parametrize("warp", ["1", "0"])
+def test_general_noprune_cfg4_shape(warp, monkeypatch):
+    """prune=False at the config-4 shape (d=256): subspace pursuit over all d
+    columns per voted bin -- the warp-per-bin kernel (default) and the
+    thread-per-bin form (SFDT_GEN_WARP=0) -- against the oracle."""
+    monkeypatch.setenv("SFDT_GEN_WARP", warp)
+    n, k, B = 1 << 20, 128, 2
+    seeds = [(17, b) for b in range(B)]
+    X = np.stack([general_signal(n, k, 20.0, s)[0] for s in seeds])
+    cfg = P.GeneralConfig(n=n, k=k, prune=False)
+    res = P.solve_general_batch(X, cfg, seeds=seeds)
+    for b in range(B):
+        want, wtr = OS.general(X[b], k, rng_seed=seeds[b], prune=False)
+        locs = np.fromiter(want.keys(), dtype=np.int64, count=len(want))
+        vals = np.fromiter(want.values(), dtype=np.complex128, count=len(want))
+        _general_check(res.spectrum(b).entries, locs, vals, f"b={b}")
+        assert res.trace(b).collision_histogram == wtr["collision_histogram"]
+
+
 @pytest.mark.parametrize("n,k,a_max,d,prune", [(4096, 8, 3, None, True), (4096, 8, 2, 16, True),
                                                (8192, 64, 3, 8, True), (4096, 4, 3, 64, False),
                                                (4096, 16, 4, None, True), (4096, 32, 3, 4, True)])

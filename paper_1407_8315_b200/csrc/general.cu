@@ -18,6 +18,11 @@
 //                (vote class a ascending, bin ascending, column ascending)
 #include <climits>
 #include <cstdlib>
+#include <type_traits>
+
+#ifndef SFDT_SP_TMAX
+#define SFDT_SP_TMAX 4   // largest least-squares support with a register-resident instance
+#endif
 
 #include "common.cuh"
 #include "decode.cuh"
@@ -522,14 +527,25 @@ __device__ __forceinline__ int warp_topk_merge(const double *sc, const int *id, 
 // lane lists are merged by warp_topk_merge, so the selections, and with
 // them every least-squares solve (run redundantly by all lanes), are
 // bit-identical to the single-thread form.
-__device__ void subspace_pursuit_dev(const cx *y, const cx *phase, const cx *bphi, int64_t d,
-                                     int r, const int *cols, int ncols, bool all_cols, int a_sp,
-                                     SPOut &o, int lane = 0, int nlanes = 1) {
+//
+// RT > 0: r = RT at compile time -- the row loops unroll and full-rank least
+// squares run as the register-resident lstsq_qr_t<RT, C> (the same
+// operations in the same order as lstsq_qr, so the same bits), which keeps
+// a multi-collision bin's long serial chain out of local memory.
+template <int RT = 0>
+__device__ __forceinline__ void subspace_pursuit_dev(const cx *y, const cx *phase, const cx *bphi, int64_t d,
+                                                     int r_rt, const int *cols, int ncols, bool all_cols,
+                                                     int a_sp, SPOut &o, int lane = 0, int nlanes = 1) {
+    const int r = RT > 0 ? RT : r_rt;
     const int a_eff = a_sp < ncols ? a_sp : ncols;
     auto col_t = [&](int c) -> int64_t { return all_cols ? (int64_t)c : (int64_t)cols[c]; };
     auto phi_col = [&](int c, cx *out) {
         const int64_t t = col_t(c);
-        for (int j = 0; j < r; j++) out[j] = nmul(phase[j], ldcx(bphi + (int64_t)j * d + t));
+#pragma unroll
+        for (int j = 0; j < (RT > 0 ? RT : GEN_MAX_R); j++) {
+            if (RT == 0 && j >= r) break;
+            out[j] = nmul(phase[j], ldcx(bphi + (int64_t)j * d + t));
+        }
     };
     cx pc[GEN_MAX_R];
     // initial support: top a_eff of |phi^H y|, stable, then sorted
@@ -560,8 +576,51 @@ __device__ void subspace_pursuit_dev(const cx *y, const cx *phase, const cx *bph
     cx A[GEN_MAX_R * GEN_MAX_SUP], coef[GEN_MAX_SUP], res[GEN_MAX_R];
     o.rankdef = 0;
     auto lsq = [&](const int *s, int ns, cx *x) {
-        for (int c = 0; c < ns; c++) phi_col(s[c], A + c * r);
-        if (lstsq_qr(A, r, ns, y, x)) return;   // full rank: unique LS solution
+        if constexpr (RT > 0) {
+            cx yy[RT > 0 ? RT : 1];
+#pragma unroll
+            for (int j = 0; j < RT; j++) yy[j] = y[j];
+            bool ok = false;
+            auto fixed = [&](auto cc) {
+                constexpr int C = decltype(cc)::value;
+                cx Af[C][RT], xx[C];
+#pragma unroll
+                for (int c = 0; c < C; c++) phi_col(s[c], Af[c]);
+                ok = lstsq_qr_t<RT, C>(Af, yy, xx);
+                if (ok)
+#pragma unroll
+                    for (int c = 0; c < C; c++) x[c] = xx[c];
+            };
+            switch (ns) {
+#if SFDT_SP_TMAX >= 1
+            case 1: fixed(std::integral_constant<int, 1>{}); break;
+#endif
+#if SFDT_SP_TMAX >= 2
+            case 2: fixed(std::integral_constant<int, 2>{}); break;
+#endif
+#if SFDT_SP_TMAX >= 3
+            case 3: fixed(std::integral_constant<int, 3>{}); break;
+#endif
+#if SFDT_SP_TMAX >= 4
+            case 4: fixed(std::integral_constant<int, 4>{}); break;
+#endif
+#if SFDT_SP_TMAX >= 5
+            case 5: fixed(std::integral_constant<int, 5>{}); break;
+#endif
+#if SFDT_SP_TMAX >= 6
+            case 6: fixed(std::integral_constant<int, 6>{}); break;
+#endif
+            default:   // larger supports (a_max = 4): the runtime-sized form
+                for (int c = 0; c < ns; c++) phi_col(s[c], A + c * r);
+                if (lstsq_qr(A, r, ns, y, x)) return;
+                break;
+            }
+            if (ok) return;   // full rank: unique LS solution
+            for (int c = 0; c < ns; c++) phi_col(s[c], A + c * r);
+        } else {
+            for (int c = 0; c < ns; c++) phi_col(s[c], A + c * r);
+            if (lstsq_qr(A, r, ns, y, x)) return;   // full rank: unique LS solution
+        }
         const int rk = lstsq_min_norm(A, r, ns, y, x);
         if (rk < ns) o.rankdef++;
     };
@@ -941,64 +1000,6 @@ __global__ void __launch_bounds__(128) k_gen_prune(const cx *__restrict__ V, Gen
 // order as subspace_pursuit_dev with a_eff = 1: stable first-max
 // selections, Householder least squares with the min-norm fallback, the
 // 1e-12 stopping rule.  A is overwritten (rebuilt for the fallback).
-template <int R, int C>
-__device__ __forceinline__ bool lstsq_qr_t(cx (&A)[C][R], const cx (&y_in)[R], cx (&x)[C]) {
-    if (C > R) return false;
-    cx y[R];
-#pragma unroll
-    for (int i = 0; i < R; i++) y[i] = y_in[i];
-    double rmax = 0.0, rmin = 1e300;
-#pragma unroll
-    for (int j = 0; j < C; j++) {
-        double nrm2 = 0.0;
-#pragma unroll
-        for (int i = j; i < R; i++) nrm2 = fma(A[j][i].re, A[j][i].re, fma(A[j][i].im, A[j][i].im, nrm2));
-        const double nrm = sqrt(nrm2);
-        if (nrm == 0.0) return false;
-        const cx x0 = A[j][j];
-        const double ax0 = cabs_(x0);
-        const cx ph = ax0 > 0.0 ? mk(x0.re / ax0, x0.im / ax0) : mk(1.0, 0.0);
-        const cx alpha = mk(-ph.re * nrm, -ph.im * nrm);
-        cx v[R];
-        double vv = 0.0;
-#pragma unroll
-        for (int i = j; i < R; i++) {
-            v[i] = (i == j) ? csub(x0, alpha) : A[j][i];
-            vv = fma(v[i].re, v[i].re, fma(v[i].im, v[i].im, vv));
-        }
-        if (vv > 0.0) {
-            const double beta = 2.0 / vv;
-#pragma unroll
-            for (int k = j; k < C; k++) {
-                cx dot = mk(0.0, 0.0);
-#pragma unroll
-                for (int i = j; i < R; i++) dot = cadd(dot, nmul(cconj(v[i]), A[k][i]));
-                dot = mk(dot.re * beta, dot.im * beta);
-#pragma unroll
-                for (int i = j; i < R; i++) A[k][i] = csub(A[k][i], nmul(v[i], dot));
-            }
-            cx dot = mk(0.0, 0.0);
-#pragma unroll
-            for (int i = j; i < R; i++) dot = cadd(dot, nmul(cconj(v[i]), y[i]));
-            dot = mk(dot.re * beta, dot.im * beta);
-#pragma unroll
-            for (int i = j; i < R; i++) y[i] = csub(y[i], nmul(v[i], dot));
-        }
-        const double rjj = cabs_(A[j][j]);
-        rmax = rjj > rmax ? rjj : rmax;
-        rmin = rjj < rmin ? rjj : rmin;
-    }
-    if (!(rmin > 1e-7 * rmax)) return false;
-#pragma unroll
-    for (int j = C - 1; j >= 0; j--) {
-        cx acc = y[j];
-#pragma unroll
-        for (int k = j + 1; k < C; k++) acc = csub(acc, nmul(A[k][j], x[k]));
-        x[j] = ndiv(acc, A[j][j]);
-    }
-    return true;
-}
-
 template <int R>
 __device__ __forceinline__ void sp_a1_t(const cx (&y)[R], const cx (&phase)[R], const cx *bphi, int64_t d,
                                         const int *cols, int ncols, SPOut &o) {
@@ -1154,6 +1155,7 @@ __global__ void __launch_bounds__(128) k_gen_sp1(const cx *__restrict__ V, GenPa
 }
 
 // Subspace pursuit per voted bin on the kept columns (general.py:357-366).
+template <int RT>
 __global__ void __launch_bounds__(128) k_gen_bins(const cx *__restrict__ V, GenParams p,
                                                   const int32_t *__restrict__ votes,
                                                   const int64_t *__restrict__ wl,
@@ -1167,14 +1169,18 @@ __global__ void __launch_bounds__(128) k_gen_bins(const cx *__restrict__ V, GenP
          it += int64_t(gridDim.x) * blockDim.x) {
         const int64_t t = wl[it];
         const int a = votes[t];
-        const int r = p.r_eff;
+        const int r = RT > 0 ? RT : p.r_eff;
         if ((skip & 1) && sp1_item(a, r, ncols_in[it])) continue;   // k_gen_sp1's
         if ((skip & 2) && ncols_in[it] < 0) continue;               // k_gen_bins_warp's
         const int64_t b = t / p.L, kb = t - b * p.L;
         const int64_t *sh = p.shifts + b * p.shift_stride;
         const cx *bphi = p.base_phi + b * p.phi_stride;
         cx y[GEN_MAX_R];
-        for (int j = 0; j < r; j++) y[j] = ldcx(V + (b * p.nv + p.S + j) * p.L + kb);
+#pragma unroll
+        for (int j = 0; j < (RT > 0 ? RT : GEN_MAX_R); j++) {
+            if (RT == 0 && j >= r) break;
+            y[j] = ldcx(V + (b * p.nv + p.S + j) * p.L + kb);
+        }
         int cols[GEN_MAX_COLS];
         const int nc8 = ncols_in[it];
         const bool all_cols = nc8 < 0;
@@ -1183,10 +1189,14 @@ __global__ void __launch_bounds__(128) k_gen_bins(const cx *__restrict__ V, GenP
         // subspace pursuit on this bin's columns (general.py:357-366)
         cx phase[GEN_MAX_R];
         const double tk = DMUL(TWO_PI, (double)kb);
-        for (int j = 0; j < r; j++) phase[j] = gexp(mk(0.0, DMUL(tk, (double)sh[j]) / (double)p.n));
+#pragma unroll
+        for (int j = 0; j < (RT > 0 ? RT : GEN_MAX_R); j++) {
+            if (RT == 0 && j >= r) break;
+            phase[j] = gexp(mk(0.0, DMUL(tk, (double)sh[j]) / (double)p.n));
+        }
         const int a_sp = a < r ? a : r;
         SPOut o;
-        subspace_pursuit_dev(y, phase, bphi, p.d, r, cols, ncols, all_cols, a_sp, o);
+        subspace_pursuit_dev<RT>(y, phase, bphi, p.d, r, cols, ncols, all_cols, a_sp, o);
         int ne = 0;
         for (int i = 0; i < o.nsup; i++) {
             if (o.coef[i].re == 0.0 && o.coef[i].im == 0.0) continue;   // np.nonzero(coef)
@@ -1606,9 +1616,23 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
         SFDT_CHECK_LAUNCH();
         launches++;
     }
-    k_gen_bins<<<(unsigned)(sms * 16), 128, 0, stream>>>(V, gp, votes, wl, wlc, colsb, ncolsb,
-                                                         sp1 | (warp_all ? 2 : 0), nent, sloc, sval,
-                                                         a->stats);
+    {
+        const int skip = sp1 | (warp_all ? 2 : 0);
+        const unsigned gb = (unsigned)(sms * 16);
+        switch (a->r_eff) {
+#define SFDT_BINS(R)                                                                              \
+    case R:                                                                                       \
+        k_gen_bins<R><<<gb, 128, 0, stream>>>(V, gp, votes, wl, wlc, colsb, ncolsb, skip, nent, sloc, \
+                                              sval, a->stats);                                    \
+        break;
+            SFDT_BINS(6) SFDT_BINS(8) SFDT_BINS(9) SFDT_BINS(12)
+#undef SFDT_BINS
+        default:
+            k_gen_bins<0><<<gb, 128, 0, stream>>>(V, gp, votes, wl, wlc, colsb, ncolsb, skip, nent, sloc,
+                                                  sval, a->stats);
+            break;
+        }
+    }
     SFDT_CHECK_LAUNCH();
     launches++;
     const int64_t nseg = (p.L + GEN_SEG - 1) / GEN_SEG;

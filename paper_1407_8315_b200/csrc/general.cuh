@@ -233,6 +233,66 @@ __device__ __forceinline__ bool lstsq_qr(const cx *A_in, int r, int c, const cx 
     return true;
 }
 
+// Register-resident form of lstsq_qr for compile-time R x C (same operations,
+// same order).  A is overwritten.
+template <int R, int C>
+__device__ __forceinline__ bool lstsq_qr_t(cx (&A)[C][R], const cx (&y_in)[R], cx (&x)[C]) {
+    if (C > R) return false;
+    cx y[R];
+#pragma unroll
+    for (int i = 0; i < R; i++) y[i] = y_in[i];
+    double rmax = 0.0, rmin = 1e300;
+#pragma unroll
+    for (int j = 0; j < C; j++) {
+        double nrm2 = 0.0;
+#pragma unroll
+        for (int i = j; i < R; i++) nrm2 = fma(A[j][i].re, A[j][i].re, fma(A[j][i].im, A[j][i].im, nrm2));
+        const double nrm = sqrt(nrm2);
+        if (nrm == 0.0) return false;
+        const cx x0 = A[j][j];
+        const double ax0 = cabs_(x0);
+        const cx ph = ax0 > 0.0 ? mk(x0.re / ax0, x0.im / ax0) : mk(1.0, 0.0);
+        const cx alpha = mk(-ph.re * nrm, -ph.im * nrm);
+        cx v[R];
+        double vv = 0.0;
+#pragma unroll
+        for (int i = j; i < R; i++) {
+            v[i] = (i == j) ? csub(x0, alpha) : A[j][i];
+            vv = fma(v[i].re, v[i].re, fma(v[i].im, v[i].im, vv));
+        }
+        if (vv > 0.0) {
+            const double beta = 2.0 / vv;
+#pragma unroll
+            for (int k = j; k < C; k++) {
+                cx dot = mk(0.0, 0.0);
+#pragma unroll
+                for (int i = j; i < R; i++) dot = cadd(dot, nmul(cconj(v[i]), A[k][i]));
+                dot = mk(dot.re * beta, dot.im * beta);
+#pragma unroll
+                for (int i = j; i < R; i++) A[k][i] = csub(A[k][i], nmul(v[i], dot));
+            }
+            cx dot = mk(0.0, 0.0);
+#pragma unroll
+            for (int i = j; i < R; i++) dot = cadd(dot, nmul(cconj(v[i]), y[i]));
+            dot = mk(dot.re * beta, dot.im * beta);
+#pragma unroll
+            for (int i = j; i < R; i++) y[i] = csub(y[i], nmul(v[i], dot));
+        }
+        const double rjj = cabs_(A[j][j]);
+        rmax = rjj > rmax ? rjj : rmax;
+        rmin = rjj < rmin ? rjj : rmin;
+    }
+    if (!(rmin > 1e-7 * rmax)) return false;
+#pragma unroll
+    for (int j = C - 1; j >= 0; j--) {
+        cx acc = y[j];
+#pragma unroll
+        for (int k = j + 1; k < C; k++) acc = csub(acc, nmul(A[k][j], x[k]));
+        x[j] = ndiv(acc, A[j][j]);
+    }
+    return true;
+}
+
 // top-`cnt` selection by score with the reference's tie rule (np.argsort
 // kind="stable" on -score: larger first, then lower index first)
 __device__ __forceinline__ void topk_insert(double *sc, int *id, int &len, int cnt, double v, int t) {

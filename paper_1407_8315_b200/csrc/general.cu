@@ -103,12 +103,13 @@ __global__ void __launch_bounds__(128) k_rows_svd(const cx *__restrict__ syn, in
 // caching them in registers (64 registers halve the resident CTAs: 468 ->
 // 637 us); keys are re-read from L2
 constexpr int VOTE_SMEM_KEYS = 0;
+constexpr int VOTE_CAND = 2048;   // candidate keys compacted to shared memory
 
 __device__ __forceinline__ unsigned long long dkey(double v) {
     return (unsigned long long)__double_as_longlong(v);   // sigma >= 0: bit order == value order
 }
 
-__global__ void __launch_bounds__(1024) k_gen_vote(const double *__restrict__ sv,
+__global__ void __launch_bounds__(1024, 2) k_gen_vote(const double *__restrict__ sv,
                                                    const double *__restrict__ partial, int nparts,
                                                    GenParams p, int32_t *__restrict__ votes,
                                                    int64_t *__restrict__ stats,
@@ -129,14 +130,16 @@ __global__ void __launch_bounds__(1024) k_gen_vote(const double *__restrict__ sv
     __shared__ unsigned long long s_prefix, s_mask;
     __shared__ long long s_remaining;
     __shared__ int wsum[32];
-    __shared__ long long s_hist[5];
+    __shared__ unsigned long long s_ck[VOTE_CAND];
+    __shared__ unsigned int s_h32[5];
+    __shared__ long long s_ncand;
+    __shared__ int s_nc;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
         s_prefix = 0;
         s_mask = 0;
         s_remaining = take;
     }
-    if (threadIdx.x < 5) s_hist[threadIdx.x] = 0;
     for (int64_t i = threadIdx.x; i < p.L; i += blockDim.x) vb[i] = 0;
     // visit every flat index in order of i0 = 0, blockDim, ... (block-uniform
     // trip count; f may contain block barriers)
@@ -152,17 +155,46 @@ __global__ void __launch_bounds__(1024) k_gen_vote(const double *__restrict__ sv
     // __match_any_sync (sigma keys share their top bytes, so plain shared
     // atomics serialise); digit choice: warp 0 scans the 256 counts from the
     // top, 8 per lane.
+    //
+    // Once the keys sharing the chosen prefix fit VOTE_CAND, they are
+    // compacted into shared memory and the remaining passes scan only them
+    // (config 4: 2 full passes + 1 compaction pass instead of 8 full passes).
+    if (threadIdx.x == 0) s_ncand = M;
+    __syncthreads();
+    bool cand = false;   // block-uniform
     if (take > 0) {
         for (int shift = 56; shift >= 0; shift -= 8) {
+            const unsigned long long pre = s_prefix, msk = s_mask;
+            if (!cand && s_ncand <= VOTE_CAND) {
+                if (threadIdx.x == 0) s_nc = 0;
+                __syncthreads();
+                for_keys([&](int64_t i, unsigned long long key) {
+                    const bool m = i < M && (key & msk) == pre;
+                    const unsigned bal = __ballot_sync(0xffffffffu, m);
+                    int base = 0;
+                    if (lane == 0 && bal) base = atomicAdd(&s_nc, __popc(bal));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    if (m) s_ck[base + __popc(bal & ((1u << lane) - 1))] = key;
+                });
+                cand = true;
+            }
             for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
             __syncthreads();
-            const unsigned long long pre = s_prefix, msk = s_mask;
-            for_keys([&](int64_t i, unsigned long long key) {
+            auto hist_key = [&](bool valid, unsigned long long key) {
                 int dg = 256;   // not a candidate
-                if (i < M && (key & msk) == pre) dg = (int)((key >> shift) & 255);
+                if (valid && (key & msk) == pre) dg = (int)((key >> shift) & 255);
                 const unsigned peers = __match_any_sync(0xffffffffu, dg);
                 if (dg < 256 && lane == __ffs(peers) - 1) atomicAdd(&hist[dg], (unsigned)__popc(peers));
-            });
+            };
+            if (cand) {
+                const int nc = s_nc;
+                for (int i0 = 0; i0 < nc; i0 += blockDim.x) {
+                    const int i = i0 + threadIdx.x;
+                    hist_key(i < nc, i < nc ? s_ck[i] : 0ull);
+                }
+            } else {
+                for_keys([&](int64_t i, unsigned long long key) { hist_key(i < M, key); });
+            }
             __syncthreads();
             if (warp == 0) {
                 // lane l owns digits 255-8l .. 248-8l (descending)
@@ -184,15 +216,18 @@ __global__ void __launch_bounds__(1024) k_gen_vote(const double *__restrict__ sv
                 if (mine) {
                     long long cum = before;
                     int D = 255 - 8 * lane - 7;
+                    unsigned cD = c[7];
 #pragma unroll
                     for (int q = 0; q < 8; q++) {
                         if (cum + (long long)c[q] >= rem) {
                             D = 255 - 8 * lane - q;
+                            cD = c[q];
                             break;
                         }
                         cum += c[q];
                     }
                     s_remaining = rem - cum;
+                    s_ncand = cD;
                     s_prefix = pre | ((unsigned long long)D << shift);
                     s_mask = msk | (0xFFull << shift);
                 }
@@ -205,7 +240,11 @@ __global__ void __launch_bounds__(1024) k_gen_vote(const double *__restrict__ sv
     // selection in flat order: keys > tau all; keys == tau by ascending flat
     // index (lexsort tie-break: bin asc, then rank asc)
     long long eq_carry = 0;
-    if (take > 0)
+    const bool all_eq = take > 0 && need_eq == s_ncand;   // every key == tau is taken (the usual case)
+    if (all_eq) {
+        for (int64_t i = threadIdx.x; i < M; i += blockDim.x)
+            if (dkey(svb[i]) >= tau) atomicAdd(&vb[i / p.a_max], 1);
+    } else if (take > 0)
         for_keys([&](int64_t i, unsigned long long key) {
             const bool gt = i < M && key > tau;
             const bool eq = i < M && key == tau;
@@ -234,27 +273,49 @@ __global__ void __launch_bounds__(1024) k_gen_vote(const double *__restrict__ sv
         s_thr = p.zvr * rms_syn;
     }
     __syncthreads();
+    // (histogram counts in registers and 32-bit shared atomics; worklist
+    // slots reserved once per block after a block-wide count)
     const int cap = (int)(p.a_max < p.d ? p.a_max : p.d);
-    long long hloc[5] = {0, 0, 0, 0, 0};
+    if (threadIdx.x < 5) s_h32[threadIdx.x] = 0;
+    if (threadIdx.x == 0) s_nc = 0;
+    __syncthreads();
+    unsigned h0 = 0, h1 = 0, h2 = 0, h3 = 0, h4 = 0;
     for (int64_t kb = threadIdx.x; kb < p.L; kb += blockDim.x) {
         int v = vb[kb];
         if (svb[kb * p.a_max] <= s_thr) v = 0;
         if (v > cap) v = cap;
         vb[kb] = v;
-        hloc[v]++;
-        if (v >= 1) {
-            const unsigned long long slot = atomicAdd(wl_count, 1ull);
-            wl[slot] = b * p.L + kb;
-        }
+        h0 += v == 0;
+        h1 += v == 1;
+        h2 += v == 2;
+        h3 += v == 3;
+        h4 += v == 4;
     }
-    for (int a = 0; a <= 4; a++)
-        if (hloc[a]) atomicAdd((unsigned long long *)&s_hist[a], (unsigned long long)hloc[a]);
+    if (h0) atomicAdd(&s_h32[0], h0);
+    if (h1) atomicAdd(&s_h32[1], h1);
+    if (h2) atomicAdd(&s_h32[2], h2);
+    if (h3) atomicAdd(&s_h32[3], h3);
+    if (h4) atomicAdd(&s_h32[4], h4);
     __syncthreads();
+    __shared__ unsigned long long s_base;
     if (threadIdx.x == 0) {
         int64_t *st = stats + b * SFDT_GS_PER_SIGNAL;
-        for (int a = 0; a <= 4; a++) st[SFDT_GS_HIST0 + a] = s_hist[a];
-        st[SFDT_GS_NVOTED] = s_hist[1] + s_hist[2] + s_hist[3] + s_hist[4];
+        for (int a = 0; a <= 4; a++) st[SFDT_GS_HIST0 + a] = s_h32[a];
+        const unsigned nv = s_h32[1] + s_h32[2] + s_h32[3] + s_h32[4];
+        st[SFDT_GS_NVOTED] = nv;
         st[SFDT_GS_RANKDEF] = 0;
+        s_base = nv ? atomicAdd(wl_count, (unsigned long long)nv) : 0ull;
+    }
+    __syncthreads();
+    // worklist append (order within the list is irrelevant downstream)
+    for (int64_t k0 = 0; k0 < p.L; k0 += blockDim.x) {
+        const int64_t kb = k0 + threadIdx.x;
+        const bool on = kb < p.L && vb[kb] >= 1;
+        const unsigned bal = __ballot_sync(0xffffffffu, on);
+        int base = 0;
+        if (lane == 0 && bal) base = atomicAdd(&s_nc, __popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (on) wl[s_base + base + __popc(bal & ((1u << lane) - 1))] = b * p.L + kb;
     }
 }
 
@@ -389,11 +450,20 @@ __global__ void __launch_bounds__(256) k_vsel_vote(const double *__restrict__ sv
     if (take <= 0) return;
     const unsigned long long tau = vs[b].prefix;
     const long long need_eq = vs[b].remaining;
-    long long eq_carry = 0;   // keys == tau in the chunks before this one
-    for (int64_t c2 = 0; c2 < ch; c2++) eq_carry += eqc[b * nch + c2];
+    long long eq_carry = 0, eq_all = 0;   // keys == tau in the chunks before this one / in all
+    for (int64_t c2 = 0; c2 < nch; c2++) {
+        const long long e = eqc[b * nch + c2];
+        eq_carry += c2 < ch ? e : 0;
+        eq_all += e;
+    }
     const int64_t i1 = (ch + 1) * VCH < M ? (ch + 1) * VCH : M;
     const double *svb = sv + b * M;
     int32_t *vb = votes + b * p.L;
+    if (need_eq == eq_all) {   // every key == tau is taken: no tie ranks needed
+        for (int64_t i = ch * VCH + threadIdx.x; i < i1; i += blockDim.x)
+            if (dkey(svb[i]) >= tau) atomicAdd(&vb[i / p.a_max], 1);
+        return;
+    }
     __shared__ int wsum[8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int64_t i0 = ch * VCH; i0 < i1; i0 += blockDim.x) {
@@ -431,29 +501,36 @@ __global__ void __launch_bounds__(256) k_vsel_fin(const double *__restrict__ sv,
     const int cap = (int)(p.a_max < p.d ? p.a_max : p.d);
     int32_t *vb = votes + b * p.L;
     const double *svb = sv + b * M;
-    __shared__ unsigned long long s_hist[5];
+    __shared__ unsigned int s_hist[5];
     __shared__ int s_n;
     __shared__ unsigned long long s_base;
     if (threadIdx.x < 5) s_hist[threadIdx.x] = 0;
     if (threadIdx.x == 0) s_n = 0;
     __syncthreads();
     const int64_t k0 = ch * VCH, k1 = (k0 + VCH < p.L) ? k0 + VCH : p.L;
-    unsigned long long hloc[5] = {0, 0, 0, 0, 0};
+    unsigned h0 = 0, h1 = 0, h2 = 0, h3 = 0, h4 = 0;
     for (int64_t kb = k0 + threadIdx.x; kb < k1; kb += blockDim.x) {
         int v = vb[kb];
         if (svb[kb * p.a_max] <= thr) v = 0;
         if (v > cap) v = cap;
         vb[kb] = v;
-        hloc[v]++;
+        h0 += v == 0;
+        h1 += v == 1;
+        h2 += v == 2;
+        h3 += v == 3;
+        h4 += v == 4;
     }
-    for (int a = 0; a <= 4; a++)
-        if (hloc[a]) atomicAdd(&s_hist[a], hloc[a]);
+    if (h0) atomicAdd(&s_hist[0], h0);
+    if (h1) atomicAdd(&s_hist[1], h1);
+    if (h2) atomicAdd(&s_hist[2], h2);
+    if (h3) atomicAdd(&s_hist[3], h3);
+    if (h4) atomicAdd(&s_hist[4], h4);
     __syncthreads();
     if (threadIdx.x < 5 && s_hist[threadIdx.x])
         atomicAdd((unsigned long long *)(stats + b * SFDT_GS_PER_SIGNAL + SFDT_GS_HIST0 + threadIdx.x),
-                  s_hist[threadIdx.x]);
+                  (unsigned long long)s_hist[threadIdx.x]);
     if (threadIdx.x == 0) {
-        const unsigned long long nv = s_hist[1] + s_hist[2] + s_hist[3] + s_hist[4];
+        const unsigned long long nv = (unsigned long long)s_hist[1] + s_hist[2] + s_hist[3] + s_hist[4];
         if (nv) {
             atomicAdd((unsigned long long *)(stats + b * SFDT_GS_PER_SIGNAL + SFDT_GS_NVOTED), nv);
             s_base = atomicAdd(wl_count, nv);
@@ -461,11 +538,15 @@ __global__ void __launch_bounds__(256) k_vsel_fin(const double *__restrict__ sv,
     }
     __syncthreads();
     // worklist append (order within the list is irrelevant downstream)
-    for (int64_t kb = k0 + threadIdx.x; kb < k1; kb += blockDim.x) {
-        if (vb[kb] >= 1) {
-            const int slot = atomicAdd(&s_n, 1);
-            wl[s_base + slot] = b * p.L + kb;
-        }
+    const int lane = threadIdx.x & 31;
+    for (int64_t kq = k0; kq < k1; kq += blockDim.x) {
+        const int64_t kb = kq + threadIdx.x;
+        const bool on = kb < k1 && vb[kb] >= 1;
+        const unsigned bal = __ballot_sync(0xffffffffu, on);
+        int base = 0;
+        if (lane == 0 && bal) base = atomicAdd(&s_n, __popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (on) wl[s_base + base + __popc(bal & ((1u << lane) - 1))] = b * p.L + kb;
     }
 }
 

@@ -1034,14 +1034,52 @@ __global__ void __launch_bounds__(128) k_gen_prune(const cx *__restrict__ V, Gen
                 const cx base = gexp(mk(0.0, DMUL(TWO_PI, (double)kb) / (double)p.n));
                 const cx wd = gexp(mk(0.0, TWO_PI / (double)p.d));
                 cx zt = base;
-                for (int64_t tt = 0; tt < p.d; tt++) {
+                // |acc|^2 pre-filter: once the kept list is full, a candidate
+                // whose squared magnitude exceeds cut^2 (1 + 1e-13) is
+                // certainly not below the cut (hypot and the square differ by
+                // a few ulps), so the hypot and the insertion are skipped
+                double cut2 = INFINITY;
+                // Horner in descending order with the coefficients in
+                // registers (constant indices, predicated on the order)
+                const cx cr[4] = {c[0], order > 1 ? c[1] : mk(0.0, 0.0), order > 2 ? c[2] : mk(0.0, 0.0),
+                                  order > 3 ? c[3] : mk(0.0, 0.0)};
+                auto horner = [&](cx z) -> cx {
                     cx acc = mk(1.0, 0.0);
-                    for (int j = order - 1; j >= 0; j--) acc = cadd(gmul(acc, zt), c[j]);
-                    botk_insert(ks, kp, nk, cnti, cabs_(acc), (int)tt);
-                    if ((tt & 511) == 511)
-                        zt = gmul(base, gexp(mk(0.0, DMUL(TWO_PI, (double)(tt + 1)) / (double)p.d)));
-                    else
-                        zt = gmul(zt, wd);
+#pragma unroll
+                    for (int j = 3; j >= 0; j--)
+                        if (j < order) acc = cadd(gmul(acc, z), cr[j]);
+                    return acc;
+                };
+                auto offer = [&](cx acc, int tt) {
+                    const double q = acc.re * acc.re + acc.im * acc.im;
+                    if (!(q > cut2)) {
+                        botk_insert(ks, kp, nk, cnti, cabs_(acc), tt);
+                        if (nk == cnti) cut2 = ks[cnti - 1] * ks[cnti - 1] * (1.0 + 1e-13);
+                    }
+                };
+                // the recurrence z *= wd, re-seeded at every 512th candidate
+                auto advance = [&](cx z, int64_t tt) -> cx {
+                    return ((tt & 511) == 511)
+                        ? gmul(base, gexp(mk(0.0, DMUL(TWO_PI, (double)(tt + 1)) / (double)p.d)))
+                        : gmul(z, wd);
+                };
+                if ((p.d & 3) == 0) {
+                    // four candidates per step: independent Horner chains
+                    for (int64_t tt = 0; tt < p.d; tt += 4) {
+                        const cx z0 = zt, z1 = advance(z0, tt), z2 = advance(z1, tt + 1),
+                                 z3 = advance(z2, tt + 2);
+                        zt = advance(z3, tt + 3);
+                        const cx a0 = horner(z0), a1 = horner(z1), a2 = horner(z2), a3 = horner(z3);
+                        offer(a0, (int)tt);
+                        offer(a1, (int)tt + 1);
+                        offer(a2, (int)tt + 2);
+                        offer(a3, (int)tt + 3);
+                    }
+                } else {
+                    for (int64_t tt = 0; tt < p.d; tt++) {
+                        offer(horner(zt), (int)tt);
+                        zt = advance(zt, tt);
+                    }
                 }
             } else {
                 // _correlation_keep (general.py:158-165)

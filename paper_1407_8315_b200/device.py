@@ -100,3 +100,21 @@ def as_device_signals(x, device: torch.device, allow_c64: bool = True):
     if t.device != device:
         t = t.to(device, non_blocking=True)
     return t.contiguous()
+
+
+def host_copy(tensors: dict) -> dict:
+    """Device tensors -> host numpy arrays with ONE stream sync: every copy is
+    issued non-blocking into pinned staging on the current stream, then the
+    stream is synchronised once (instead of a sync per .cpu())."""
+    out, stream = {}, None
+    for k, t in tensors.items():
+        if t.is_cuda:
+            stream = torch.cuda.current_stream(t.device)
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            h.copy_(t, non_blocking=True)
+            out[k] = h
+        else:
+            out[k] = t
+    if stream is not None:
+        stream.synchronize()
+    return {k: v.numpy() for k, v in out.items()}

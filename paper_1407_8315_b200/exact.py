@@ -28,7 +28,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .device import (Workspace, as_device_signals, aux_stream, ptr, require_cuda, stream_handle,
+from .device import (Workspace, host_copy, as_device_signals, aux_stream, ptr, require_cuda, stream_handle,
                      twiddles)
 from .spectral import SparseSpectrum, check_signal_shape
 
@@ -129,23 +129,22 @@ class ExactBatch:
         return self.t["stats"].shape[0]
 
     def to_host(self) -> dict:
-        """Copy the compacted results to host numpy arrays (one sync)."""
+        """Copy the compacted results to host numpy arrays: the fixed-size
+        fields, then the used prefix of the variable-size lists (two
+        stream syncs, pinned staging)."""
         if self._host is None:
             t = self.t
-            off = t["entry_offsets"].cpu().numpy()
-            uoff = t["unres_offsets"].cpu().numpy()
-            total, utotal = int(off[-1]), int(uoff[-1])
-            h = {
-                "entry_offsets": off, "unres_offsets": uoff,
-                "locs": t["locs"][:total].cpu().numpy(),
-                "vals": torch.view_as_complex(t["vals"][:total]).cpu().numpy(),
-                "unres_bins": t["unres_bins"][:utotal].cpu().numpy(),
-                "stats": t["stats"].cpu().numpy(), "rms": t["rms"].cpu().numpy(),
-            }
+            fixed = ["entry_offsets", "unres_offsets", "stats", "rms"]
             if t.get("dup_offsets") is not None:
-                doff = t["dup_offsets"].cpu().numpy()
-                h["dup_offsets"] = doff
-                h["dup_locs"] = t["dup_locs"][:int(doff[-1])].cpu().numpy()
+                fixed.append("dup_offsets")
+            h = host_copy({k: t[k] for k in fixed})
+            total, utotal = int(h["entry_offsets"][-1]), int(h["unres_offsets"][-1])
+            var = {"locs": t["locs"][:total], "vals": t["vals"][:total],
+                   "unres_bins": t["unres_bins"][:utotal]}
+            if "dup_offsets" in h:
+                var["dup_locs"] = t["dup_locs"][:int(h["dup_offsets"][-1])]
+            h.update(host_copy(var))
+            h["vals"] = h["vals"].view(np.complex128).reshape(-1)
             self._host = h
         return self._host
 

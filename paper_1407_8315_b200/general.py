@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .device import Workspace, as_device_signals, ptr, require_cuda, stream_handle, twiddles
+from .device import Workspace, as_device_signals, host_copy, ptr, require_cuda, stream_handle, twiddles
 from .spectral import SparseSpectrum, check_signal_shape
 
 
@@ -108,15 +108,14 @@ class GeneralBatch:
         return self.t["stats"].shape[0]
 
     def to_host(self) -> dict:
+        """Compacted results to host numpy arrays (two stream syncs)."""
         if self._host is None:
             t = self.t
-            off = t["entry_offsets"].cpu().numpy()
-            total = int(off[-1])
-            self._host = {
-                "entry_offsets": off, "locs": t["locs"][:total].cpu().numpy(),
-                "vals": torch.view_as_complex(t["vals"][:total]).cpu().numpy(),
-                "stats": t["stats"].cpu().numpy(),
-            }
+            h = host_copy({"entry_offsets": t["entry_offsets"], "stats": t["stats"]})
+            total = int(h["entry_offsets"][-1])
+            h.update(host_copy({"locs": t["locs"][:total], "vals": t["vals"][:total]}))
+            h["vals"] = h["vals"].view(np.complex128).reshape(-1)
+            self._host = h
         return self._host
 
     def spectrum(self, b: int) -> SparseSpectrum:

@@ -1,0 +1,140 @@
+"""CUDA-graph replay of a batched solve (latency path for small batches).
+
+A single-signal solve (config 1: N=2^16) is a dozen short kernels; launched
+one by one from Python it is bound by host launch overhead, not by the GPU.
+SolveGraph captures one complete solve -- exact (solve_noniterative /
+solve_iterative) or general (solve_general) -- for a fixed (config, batch,
+dtype) into a CUDA graph and replays it:
+
+    g = SolveGraph(ExactConfig(n=1 << 16, k=64), batch=1)
+    res = g.solve(x)            # x: (B, n) or (n,) device / host tensor or numpy
+    res.spectrum(0), res.trace(0)
+
+    g = SolveGraph(cfg, batch=1, host_io=True)
+    g.host_input[0] = x          # pinned staging buffer (or pass x to solve_host)
+    res = g.solve_host()         # H2D + solve + D2H of the results, one graph
+
+The captured kernels are exactly those of exact_batch / solve_general_batch
+(same arguments, same library entry points); only their launch is replayed.
+Results live in the graph's static buffers: a result is valid until the next
+solve() / solve_host() of the same SolveGraph (call .clone() to keep one).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from .device import require_cuda
+from .exact import ExactBatch, ExactConfig, exact_batch
+from .general import GeneralBatch, GeneralConfig, GeneralPlan, solve_general_batch
+from .spectral import check_signal_shape
+
+
+class SolveGraph:
+    def __init__(self, cfg, batch: int = 1, iterative: bool = False,
+                 dtype=torch.complex128, device=None, seeds=None, host_io: bool = False):
+        if not isinstance(cfg, (ExactConfig, GeneralConfig)):
+            raise TypeError("cfg must be an ExactConfig or a GeneralConfig")
+        if dtype not in (torch.complex128, torch.complex64):
+            raise ValueError("dtype must be torch.complex128 or torch.complex64")
+        dev = require_cuda(device)
+        n = check_signal_shape((cfg.n,))
+        self.cfg, self.batch, self.n, self.device = cfg, int(batch), n, dev
+        self.iterative = bool(iterative)
+        self.general = isinstance(cfg, GeneralConfig)
+        self.plan = GeneralPlan(cfg, self.batch, seeds, dev) if self.general else None
+        self.X = torch.zeros((self.batch, n), dtype=dtype, device=dev)
+        self.host_io = bool(host_io)
+        self.host_input = torch.zeros((self.batch, n), dtype=dtype, pin_memory=True) if host_io else None
+
+        # warm-up on a side stream: twiddle tables, the workspace, output
+        # capacities and kernel attributes are set up outside the capture
+        cur = torch.cuda.current_stream(dev)
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            self._launch()
+        cur.wait_stream(side)
+        torch.cuda.synchronize(dev)
+
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            if host_io:
+                self.X.copy_(self.host_input, non_blocking=True)
+            proto = self._launch()
+            self.t = proto.t
+            self.kernel_launches = proto.kernel_launches
+            if host_io:
+                # results straight back into pinned buffers (whole capacity;
+                # the offsets say how much of each list is used)
+                self._host_out = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
+                                  for k, v in self.t.items()
+                                  if isinstance(v, torch.Tensor) and not k.startswith("_")}
+                for k, h in self._host_out.items():
+                    h.copy_(self.t[k], non_blocking=True)
+        torch.cuda.synchronize(dev)
+
+    def _launch(self):
+        if self.general:
+            return solve_general_batch(self.X, self.cfg, device=self.device, plan=self.plan)
+        return exact_batch(self.X, self.cfg, self.iterative, self.device)
+
+    def _wrap(self):
+        if self.general:
+            res = GeneralBatch(self.n, self.cfg, self.cfg.resolved_d(), min(self.cfg.r, self.cfg.resolved_d()),
+                               self.plan.sh, self.t, 0.0, self.kernel_launches)
+        else:
+            res = ExactBatch(self.n, self.iterative, self.t, 0.0)
+            res.kernel_launches = self.kernel_launches
+        return res
+
+    def solve(self, X=None):
+        """Replay on the current stream; X (optional) is copied into the
+        graph's input buffer first (device-to-device, or host-to-device).
+        Returns device-resident results (ExactBatch / GeneralBatch)."""
+        if X is not None:
+            if not isinstance(X, torch.Tensor):
+                X = torch.from_numpy(np.ascontiguousarray(X))
+            self.X.copy_(X.reshape(self.X.shape), non_blocking=True)
+        self.graph.replay()
+        return self._wrap()
+
+    def solve_host(self, x=None):
+        """host_io graphs: H2D of host_input, the solve and the D2H of every
+        result buffer as ONE graph replay, then one stream sync.  x (optional)
+        is first copied into the pinned host_input."""
+        if not self.host_io:
+            raise ValueError("SolveGraph was built without host_io=True")
+        if x is not None:
+            if not isinstance(x, torch.Tensor):
+                x = torch.from_numpy(np.ascontiguousarray(x))
+            self.host_input.copy_(x.reshape(self.host_input.shape))
+        self.graph.replay()
+        torch.cuda.current_stream(self.device).synchronize()
+        res = self._wrap()
+        h = {k: v.numpy() for k, v in self._host_out.items()}
+        res._host = _host_view(h, self.general)
+        return res
+
+    @property
+    def h2d_bytes(self) -> int:
+        return self.X.numel() * self.X.element_size()
+
+
+def _host_view(full: dict, general: bool) -> dict:
+    """Slice whole-capacity host copies down to the used prefixes (the layout
+    ExactBatch.to_host / GeneralBatch.to_host produce)."""
+    h = {"entry_offsets": full["entry_offsets"], "stats": full["stats"]}
+    total = int(full["entry_offsets"][-1])
+    h["locs"] = full["locs"][:total]
+    h["vals"] = full["vals"][:total].reshape(-1, 2).view(np.complex128).reshape(-1)
+    if general:
+        return h
+    h["unres_offsets"] = full["unres_offsets"]
+    h["unres_bins"] = full["unres_bins"][:int(full["unres_offsets"][-1])]
+    h["rms"] = full["rms"]
+    if full.get("dup_offsets") is not None:
+        h["dup_offsets"] = full["dup_offsets"]
+        h["dup_locs"] = full["dup_locs"][:int(full["dup_offsets"][-1])]
+    return h

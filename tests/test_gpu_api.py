@@ -245,3 +245,37 @@ def test_host_batch_exact_streams_whole_rows():
     for b in range(5):
         want, _ = OS.exact_noniterative(X[b % H], k)
         assert list(hr.spectrum(b).entries) == list(want)
+
+
+@pytest.mark.parametrize("kind", ["noniterative", "iterative", "general"])
+def test_solve_graph_matches_batch(kind):
+    """SolveGraph replays the same kernels as exact_batch / solve_general_batch:
+    results identical, across replays with different inputs, for the device
+    and the host_io (H2D + solve + D2H in one graph) forms."""
+    from tests.synth import exact_signal, general_signal
+    n, B = 1 << 14, 2
+    if kind == "general":
+        k = 16
+        cfg = P.GeneralConfig(n=n, k=k, rng_seed=5)
+        sigs = [np.stack([general_signal(n, k, 20.0, 70 + 10 * r + b)[0] for b in range(B)]) for r in range(2)]
+        ref = lambda X: P.solve_general_batch(X, cfg)
+    else:
+        k = 32
+        cfg = P.ExactConfig(n=n, k=k)
+        sigs = [np.stack([exact_signal(n, k, 80 + 10 * r + b, "mag1_10")[0] for b in range(B)]) for r in range(2)]
+        ref = lambda X: P.exact_batch(X, cfg, kind == "iterative")
+    g = P.SolveGraph(cfg, batch=B, iterative=kind == "iterative")
+    gh = P.SolveGraph(cfg, batch=B, iterative=kind == "iterative", host_io=True)
+    for X in sigs:
+        want = ref(X)
+        got = g.solve(torch.from_numpy(X).cuda())
+        goth = gh.solve_host(X)
+        for b in range(B):
+            w = want.spectrum(b).entries
+            assert got.spectrum(b).entries == w
+            assert goth.spectrum(b).entries == w
+            if kind != "general":
+                for tr in (got.trace(b), goth.trace(b)):
+                    wt = want.trace(b)
+                    assert tr.iterations == wt.iterations and tr.full_success == wt.full_success
+                    assert tr.unresolved_bins == wt.unresolved_bins and tr.fft_samples == wt.fft_samples

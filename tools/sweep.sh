@@ -14,6 +14,10 @@ for k in 64 256 1024 4096 16384; do
   python bench.py --config cfg5 --k $k --no-cpu --no-e2e --steps 10 --warmup 3 > $O/c5e_$k.json 2> $O/c5e_$k.err
   python bench.py --config cfg5 --cfg5-general --k $k --no-cpu --no-e2e --steps 5 --warmup 3 > $O/c5g_$k.json 2> $O/c5g_$k.err
 done
+python bench.py --config cfg4 --no-prune --no-cpu --no-e2e --steps 5 --warmup 3 > $O/cfg4_noprune.json 2> $O/cfg4_noprune.err
+for k in 64 256 1024; do
+  python bench.py --config cfg5 --cfg5-general --no-prune --k $k --no-cpu --no-e2e --steps 5 --warmup 3 > $O/c5g_noprune_$k.json 2> $O/c5g_noprune_$k.err
+done
 python bench.py --config cfg5 --k 1024 --dtype c64 --no-cpu --no-e2e --steps 10 --warmup 3 > $O/c5e_1024_c64.json 2> $O/c5e_1024_c64.err
 for f in $O/*.json; do python -c "
 import json,sys

@@ -33,6 +33,15 @@ __host__ __device__ __forceinline__ int ilog2_64(int64_t v) {
     return r;
 }
 
+// Grid of a grid-stride worklist kernel: `cap` CTAs fill the GPU, but a
+// small batch (config 1: 256 bins) must not launch a thousand idle CTAs --
+// the worklist never exceeds max_items, so no more CTAs than it needs.
+static inline unsigned wl_grid(int64_t max_items, int items_per_cta, int64_t cap) {
+    int64_t g = (max_items + items_per_cta - 1) / items_per_cta;
+    if (g > cap) g = cap;
+    return (unsigned)(g < 1 ? 1 : g);
+}
+
 // python-style non-negative modulo for power-of-two n
 __host__ __device__ __forceinline__ int64_t pmod(int64_t a, int64_t n) { return a & (n - 1); }
 

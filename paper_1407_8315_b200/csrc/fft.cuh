@@ -438,7 +438,12 @@ static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, con
     if (nviews == 0) return SFDT_OK;
     if (L <= FFT_SMEM_MAX) {
         int logvpc = 0;
-        while ((L << (logvpc + 1)) <= fft_points_per_cta() && (1 << (logvpc + 1)) <= 2 * src.nshift) logvpc++;
+        // views per CTA: up to fft_points_per_cta() points, but small
+        // batches keep >= 2 CTAs per SM instead of packing views (config 1:
+        // 8 CTAs of one view rather than one CTA of eight)
+        while ((L << (logvpc + 1)) <= fft_points_per_cta() && (1 << (logvpc + 1)) <= 2 * src.nshift &&
+               (nviews >> (logvpc + 1)) >= 296)
+            logvpc++;
         const size_t smem = (size_t(L) << logvpc) * 16;
         const unsigned grid = (unsigned)((nviews + (1 << logvpc) - 1) >> logvpc);
         // <= 32 KiB per CTA: cap registers at 64 for 4 CTAs/SM (measured

@@ -1703,11 +1703,13 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     }
     int32_t *colsb = (int32_t *)(w + p.off_cols);
     int8_t *ncolsb = (int8_t *)(w + p.off_ncols);
-    k_gen_prune<<<(unsigned)(sms * 16), 128, 0, stream>>>(V, gp, votes, wl, wlc, mf_top, colsb, ncolsb);
+    // voted bins per signal <= min(K, L): bounds every worklist below
+    const int64_t max_voted = p.B * (a->k < p.L ? (int64_t)a->k : p.L);
+    k_gen_prune<<<wl_grid(max_voted, 128, sms * 16), 128, 0, stream>>>(V, gp, votes, wl, wlc, mf_top, colsb, ncolsb);
     SFDT_CHECK_LAUNCH();
     const int sp1 = sp1_r(a->r_eff);
     if (sp1) {
-        const unsigned g1 = (unsigned)(sms * 16);
+        const unsigned g1 = wl_grid(max_voted, 128, sms * 16);
         switch (a->r_eff) {
 #define SFDT_SP1(R) \
     case R: k_gen_sp1<R><<<g1, 128, 0, stream>>>(V, gp, votes, wl, wlc, colsb, ncolsb, nent, sloc, sval, a->stats); break;
@@ -1730,14 +1732,14 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     const bool few = (int64_t)a->k * p.B <= 224 * (int64_t)sms;
     const int warp_all = all_d && (ev ? ev[0] == '1' : few);
     if (warp_all) {
-        k_gen_bins_warp<<<(unsigned)(sms * 16), 256, 0, stream>>>(V, gp, votes, wl, wlc, ncolsb, nent, sloc,
+        k_gen_bins_warp<<<wl_grid(max_voted, 8, sms * 16), 256, 0, stream>>>(V, gp, votes, wl, wlc, ncolsb, nent, sloc,
                                                                   sval, a->stats);
         SFDT_CHECK_LAUNCH();
         launches++;
     }
     {
         const int skip = sp1 | (warp_all ? 2 : 0);
-        const unsigned gb = (unsigned)(sms * 16);
+        const unsigned gb = wl_grid(max_voted, 128, sms * 16);
         switch (a->r_eff) {
 #define SFDT_BINS(R)                                                                              \
     case R:                                                                                       \

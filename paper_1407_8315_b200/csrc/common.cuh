@@ -42,6 +42,20 @@ static inline unsigned wl_grid(int64_t max_items, int items_per_cta, int64_t cap
     return (unsigned)(g < 1 ? 1 : g);
 }
 
+// CTAs of `kernel` resident on the whole GPU at once.  Grid-stride kernels
+// whose items are a few long serial chains (the multi-collision decodes and
+// pursuits) must not be launched in several waves: a later wave's chains
+// would only start when the earlier wave's longest chain ends.
+template <typename K>
+static inline int64_t one_wave(K kernel, int threads, size_t smem = 0) {
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem) != cudaSuccess || per < 1)
+        per = 1;
+    return (int64_t)sms * per;
+}
+
 // python-style non-negative modulo for power-of-two n
 __host__ __device__ __forceinline__ int64_t pmod(int64_t a, int64_t n) { return a & (n - 1); }
 

@@ -416,7 +416,7 @@ static int launch_decode_noniter(const cx *V, int64_t B, int64_t L, int a_max, i
         cudaMemsetAsync(awlc, 0, sizeof(unsigned long long), stream);
         k_act_compact<<<(unsigned)((nbins + 4095) / 4096), 1024, 0, stream>>>(act, nbins, status, awl, awlc);
         SFDT_CHECK_LAUNCH();
-        k_decode_a1_dense<S><<<wl_grid(nbins, 128, sms * 16), 128, 0, stream>>>(V, L, a_max, n, status, bin_loc,
+        k_decode_a1_dense<S><<<wl_grid(nbins, 128, one_wave(k_decode_a1_dense<S>, 128)), 128, 0, stream>>>(V, L, a_max, n, status, bin_loc,
                                                                        bin_val, awl, awlc, wl, wl_count);
     } else {
         k_decode_a1<S><<<(unsigned)((nbins + 127) / 128), 128, 0, stream>>>(V, B, L, a_max, n, thr, status,
@@ -424,7 +424,7 @@ static int launch_decode_noniter(const cx *V, int64_t B, int64_t L, int a_max, i
     }
     SFDT_CHECK_LAUNCH();
     if (a_max > 1) {
-        k_decode_multi<S><<<wl_grid(nbins, 128, sms * 8), 128, 0, stream>>>(V, L, a_max, n, status, bin_loc, bin_val,
+        k_decode_multi<S><<<wl_grid(nbins, 128, one_wave(k_decode_multi<S>, 128)), 128, 0, stream>>>(V, L, a_max, n, status, bin_loc, bin_val,
                                                                   wl, wl_count);
         SFDT_CHECK_LAUNCH();
     }
@@ -1481,12 +1481,16 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
             int dev = 0, sms = 148;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            const unsigned g = wl_grid(nb, 128, sms * 16);
+            (void)sms;
             switch (l) {
-            case 0: k_iter_decode<0><<<g, 128, 0, stream>>>(st, p.L, (int)p.S, a->a_max, p.n, m, awl, awlc); break;
-            case 1: k_iter_decode<1><<<g, 128, 0, stream>>>(st, p.L, (int)p.S, a->a_max, p.n, m, awl, awlc); break;
-            case 2: k_iter_decode<2><<<g, 128, 0, stream>>>(st, p.L, (int)p.S, a->a_max, p.n, m, awl, awlc); break;
-            default: k_iter_decode<3><<<g, 128, 0, stream>>>(st, p.L, (int)p.S, a->a_max, p.n, m, awl, awlc); break;
+#define SFDT_ITD(Lv)                                                                                  \
+    k_iter_decode<Lv><<<wl_grid(nb, 128, one_wave(k_iter_decode<Lv>, 128)), 128, 0, stream>>>(          \
+        st, p.L, (int)p.S, a->a_max, p.n, m, awl, awlc);
+            case 0: SFDT_ITD(0) break;
+            case 1: SFDT_ITD(1) break;
+            case 2: SFDT_ITD(2) break;
+            default: SFDT_ITD(3) break;
+#undef SFDT_ITD
             }
             SFDT_CHECK_LAUNCH();
         }

@@ -984,6 +984,16 @@ __global__ void __launch_bounds__(256, 2) k_gen_mf(const cx *__restrict__ V, Gen
     }
 }
 
+// r_eff values with a register-resident pursuit instance: 3*a_max, or d
+// when d < 3*a_max
+__host__ __device__ __forceinline__ bool sp1_r(int r) {
+    return r == 1 || r == 2 || r == 3 || r == 4 || r == 6 || r == 8 || r == 9 || r == 12;
+}
+
+__device__ __forceinline__ bool sp1_item(int a, int r, int nc8) {
+    return a == 1 && nc8 >= 1 && nc8 <= 4 && sp1_r(r);
+}
+
 // Pruning per voted bin (general.py:313-351): descending-order Hankel fit,
 // prune_eval over the d candidates with the reference's recurrence (or the
 // correlation fallback), union with the matched-filter columns (k_gen_mf).
@@ -995,7 +1005,9 @@ __global__ void __launch_bounds__(128) k_gen_prune(const cx *__restrict__ V, Gen
                                                    const int64_t *__restrict__ wl,
                                                    const unsigned long long *__restrict__ wl_count,
                                                    const int32_t *__restrict__ mf_top,
-                                                   int32_t *__restrict__ cols_out, int8_t *__restrict__ ncols_out) {
+                                                   int32_t *__restrict__ cols_out, int8_t *__restrict__ ncols_out,
+                                                   int heavy_flags, int64_t *__restrict__ hl,
+                                                   unsigned long long *__restrict__ hlc) {
     const int64_t cnt = (int64_t)*wl_count;
     for (int64_t it = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; it < cnt;
          it += int64_t(gridDim.x) * blockDim.x) {
@@ -1109,6 +1121,12 @@ __global__ void __launch_bounds__(128) k_gen_prune(const cx *__restrict__ V, Gen
         } else {
             ncols_out[it] = -1;
         }
+        // the bins k_gen_bins pursues go to a separate list so that each gets
+        // its own warp there (bit 0: k_gen_sp1 takes its items, bit 1:
+        // k_gen_bins_warp takes the all-column bins)
+        const int nc = all_cols ? -1 : ncols;
+        const bool heavy = !((heavy_flags & 1) && sp1_item(a, r, nc)) && !((heavy_flags & 2) && nc < 0);
+        if (heavy) hl[atomicAdd(hlc, 1ull)] = it;
     }
 }
 
@@ -1219,16 +1237,6 @@ __device__ __forceinline__ void sp_a1_t(const cx (&y)[R], const cx (&phase)[R], 
     o.coef[0] = best_coef;
 }
 
-// r_eff values with a register-resident pursuit instance: 3*a_max, or d
-// when d < 3*a_max
-__host__ __device__ __forceinline__ bool sp1_r(int r) {
-    return r == 1 || r == 2 || r == 3 || r == 4 || r == 6 || r == 8 || r == 9 || r == 12;
-}
-
-__device__ __forceinline__ bool sp1_item(int a, int r, int nc8) {
-    return a == 1 && nc8 >= 1 && nc8 <= 4 && sp1_r(r);
-}
-
 template <int R>
 __global__ void __launch_bounds__(128) k_gen_sp1(const cx *__restrict__ V, GenParams p,
                                                  const int32_t *__restrict__ votes,
@@ -1273,24 +1281,32 @@ __global__ void __launch_bounds__(128) k_gen_sp1(const cx *__restrict__ V, GenPa
     }
 }
 
-// Subspace pursuit per voted bin on the kept columns (general.py:357-366).
+// Subspace pursuit per voted bin on the kept columns (general.py:357-366),
+// for the bins on k_gen_prune's list (multi-collision bins and the rest
+// k_gen_sp1 / k_gen_bins_warp do not take).  Each bin is a long serial FP64
+// chain (~1e5 cycles, measured), so the list is dealt out lane-major: item q
+// goes to lane q / nwarps of warp q % nwarps -- with fewer items than warps
+// no two chains share a warp (divergent lanes would run them one after the
+// other).
 template <int RT>
 __global__ void __launch_bounds__(128) k_gen_bins(const cx *__restrict__ V, GenParams p,
                                                   const int32_t *__restrict__ votes,
                                                   const int64_t *__restrict__ wl,
-                                                  const unsigned long long *__restrict__ wl_count,
+                                                  const int64_t *__restrict__ hl,
+                                                  const unsigned long long *__restrict__ hl_count,
                                                   const int32_t *__restrict__ cols_in,
-                                                  const int8_t *__restrict__ ncols_in, int skip,
+                                                  const int8_t *__restrict__ ncols_in,
                                                   uint8_t *__restrict__ nent, int64_t *__restrict__ sloc,
                                                   cx *__restrict__ sval, int64_t *__restrict__ stats) {
-    const int64_t cnt = (int64_t)*wl_count;
-    for (int64_t it = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; it < cnt;
-         it += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t cnt = (int64_t)*hl_count;
+    const int64_t nwarps = int64_t(gridDim.x) * (blockDim.x >> 5);
+    const int64_t gw = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    for (int64_t q = int64_t(lane) * nwarps + gw; q < cnt; q += 32 * nwarps) {
+        const int64_t it = hl[q];
         const int64_t t = wl[it];
         const int a = votes[t];
         const int r = RT > 0 ? RT : p.r_eff;
-        if ((skip & 1) && sp1_item(a, r, ncols_in[it])) continue;   // k_gen_sp1's
-        if ((skip & 2) && ncols_in[it] < 0) continue;               // k_gen_bins_warp's
         const int64_t b = t / p.L, kb = t - b * p.L;
         const int64_t *sh = p.shifts + b * p.shift_stride;
         const cx *bphi = p.base_phi + b * p.phi_stride;
@@ -1520,7 +1536,7 @@ struct GenPlan {
     int64_t B, n, d, L, nv, nparts;
     int S;
     size_t off_V, off_sv, off_part, off_votes, off_nent, off_sloc, off_sval, off_wl, off_cnt,
-        off_fft, off_mf, off_cols, off_ncols, off_seg, off_vsel, off_ghist, off_eqc, total;
+        off_fft, off_mf, off_cols, off_ncols, off_hl, off_seg, off_vsel, off_ghist, off_eqc, total;
 };
 
 static int make_gen_plan(const sfdt_general_args *a, GenPlan &p) {
@@ -1548,13 +1564,14 @@ static int make_gen_plan(const sfdt_general_args *a, GenPlan &p) {
     p.off_sloc = take(size_t(p.B) * p.L * a->a_max * 8);
     p.off_sval = take(size_t(p.B) * p.L * a->a_max * 16);
     p.off_wl = take(size_t(p.B) * p.L * 8);
-    p.off_cnt = take(64);
+    p.off_cnt = take(64);   // worklist count, heavy-list count
     p.off_mf = take(size_t(p.B) * p.L * 16);
     {
         // voted bins per signal <= min(k, L) (each vote is one of the top k keys)
         const int64_t cap = p.B * (a->k < p.L ? a->k : p.L);
         p.off_cols = take(size_t(cap) * GEN_MAX_COLS * 4);
         p.off_ncols = take(size_t(cap));
+        p.off_hl = take(size_t(cap) * 8);
     }
     p.off_seg = take(size_t(p.B) * ((p.L + GEN_SEG - 1) / GEN_SEG) * 4 * 8);
     p.off_vsel = take(size_t(p.B) * sizeof(VSel));
@@ -1705,21 +1722,7 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     int8_t *ncolsb = (int8_t *)(w + p.off_ncols);
     // voted bins per signal <= min(K, L): bounds every worklist below
     const int64_t max_voted = p.B * (a->k < p.L ? (int64_t)a->k : p.L);
-    k_gen_prune<<<wl_grid(max_voted, 128, sms * 16), 128, 0, stream>>>(V, gp, votes, wl, wlc, mf_top, colsb, ncolsb);
-    SFDT_CHECK_LAUNCH();
     const int sp1 = sp1_r(a->r_eff);
-    if (sp1) {
-        const unsigned g1 = wl_grid(max_voted, 128, sms * 16);
-        switch (a->r_eff) {
-#define SFDT_SP1(R) \
-    case R: k_gen_sp1<R><<<g1, 128, 0, stream>>>(V, gp, votes, wl, wlc, colsb, ncolsb, nent, sloc, sval, a->stats); break;
-            SFDT_SP1(1) SFDT_SP1(2) SFDT_SP1(3) SFDT_SP1(4) SFDT_SP1(6) SFDT_SP1(8) SFDT_SP1(9) SFDT_SP1(12)
-#undef SFDT_SP1
-        default: break;
-        }
-        SFDT_CHECK_LAUNCH();
-        launches++;
-    }
     // Bins pursued over all d columns (prune off, or count >= d): one warp
     // per bin while the bins are few -- at most K voted bins per signal, and
     // up to ~224 warps per SM the warp form's shorter chains win (measured
@@ -1731,27 +1734,44 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     const bool all_d = !a->prune || p.d <= 2 * (int64_t)a->keep_per_collision * a->a_max;
     const bool few = (int64_t)a->k * p.B <= 224 * (int64_t)sms;
     const int warp_all = all_d && (ev ? ev[0] == '1' : few);
+    int64_t *hl = (int64_t *)(w + p.off_hl);
+    unsigned long long *hlc = wlc + 1;
+    cudaMemsetAsync(hlc, 0, 8, stream);
+    k_gen_prune<<<wl_grid(max_voted, 128, one_wave(k_gen_prune, 128)), 128, 0, stream>>>(
+        V, gp, votes, wl, wlc, mf_top, colsb, ncolsb, sp1 | (warp_all ? 2 : 0), hl, hlc);
+    SFDT_CHECK_LAUNCH();
+    if (sp1) {
+        switch (a->r_eff) {
+#define SFDT_SP1(R)                                                                                     \
+    case R:                                                                                             \
+        k_gen_sp1<R><<<wl_grid(max_voted, 128, one_wave(k_gen_sp1<R>, 128)), 128, 0, stream>>>(        \
+            V, gp, votes, wl, wlc, colsb, ncolsb, nent, sloc, sval, a->stats);                          \
+        break;
+            SFDT_SP1(1) SFDT_SP1(2) SFDT_SP1(3) SFDT_SP1(4) SFDT_SP1(6) SFDT_SP1(8) SFDT_SP1(9) SFDT_SP1(12)
+#undef SFDT_SP1
+        default: break;
+        }
+        SFDT_CHECK_LAUNCH();
+        launches++;
+    }
     if (warp_all) {
-        k_gen_bins_warp<<<wl_grid(max_voted, 8, sms * 16), 256, 0, stream>>>(V, gp, votes, wl, wlc, ncolsb, nent, sloc,
-                                                                  sval, a->stats);
+        k_gen_bins_warp<<<wl_grid(max_voted, 8, one_wave(k_gen_bins_warp, 256)), 256, 0, stream>>>(
+            V, gp, votes, wl, wlc, ncolsb, nent, sloc, sval, a->stats);
         SFDT_CHECK_LAUNCH();
         launches++;
     }
     {
-        const int skip = sp1 | (warp_all ? 2 : 0);
-        const unsigned gb = wl_grid(max_voted, 128, sms * 16);
+        // one wave; up to one heavy bin per warp (k_gen_bins)
         switch (a->r_eff) {
-#define SFDT_BINS(R)                                                                              \
-    case R:                                                                                       \
-        k_gen_bins<R><<<gb, 128, 0, stream>>>(V, gp, votes, wl, wlc, colsb, ncolsb, skip, nent, sloc, \
-                                              sval, a->stats);                                    \
+#define SFDT_BINS(R)                                                                                    \
+    case R:                                                                                             \
+        k_gen_bins<R><<<wl_grid(32 * max_voted, 128, one_wave(k_gen_bins<R>, 128)), 128, 0, stream>>>(  \
+            V, gp, votes, wl, hl, hlc, colsb, ncolsb, nent, sloc, sval, a->stats);                      \
         break;
             SFDT_BINS(6) SFDT_BINS(8) SFDT_BINS(9) SFDT_BINS(12)
-#undef SFDT_BINS
         default:
-            k_gen_bins<0><<<gb, 128, 0, stream>>>(V, gp, votes, wl, wlc, colsb, ncolsb, skip, nent, sloc,
-                                                  sval, a->stats);
-            break;
+            SFDT_BINS(0)
+#undef SFDT_BINS
         }
     }
     SFDT_CHECK_LAUNCH();

@@ -137,7 +137,10 @@ __device__ __forceinline__ int lstsq_min_norm(const cx *A, int r, int c, const c
                     apq = cadd(apq, nmul(cconj(wp), wq));
                 }
                 const double g = cabs_(apq);
-                if (g == 0.0 || g <= 1e-16 * sqrt(app * aqq)) continue;
+                // converged at eps: below it the rotations only move roundoff
+                // (1e-16 < eps/2 kept rotating noise for all 40 sweeps on
+                // nearly dependent supports -- the pursuit's longest chains)
+                if (g == 0.0 || g <= 2.220446049250313e-16 * sqrt(app * aqq)) continue;
                 rotated = true;
                 const double theta = (aqq - app) / (2.0 * g);
                 const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));

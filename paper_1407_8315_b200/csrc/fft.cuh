@@ -37,6 +37,9 @@ struct ViewSrc {
     int dyn_first;
     int64_t dyn_stride;
     int jfast;           // 1: lanes walk j (contiguous rows), 0: lanes walk the views
+    // per-signal number of views to compute: views v >= nview[b] are skipped
+    // (their slots are never read); nullptr = all nshift views
+    const int32_t *nview;
 };
 
 __device__ __forceinline__ cx view_load(const ViewSrc &src, int64_t b, int v, int64_t j) {
@@ -242,6 +245,18 @@ static __global__ void __launch_bounds__(256, MINB) k_fft_views(const ViewSrc sr
     const int nv = (int)((nviews - g0) < vpc ? (nviews - g0) : vpc);
     // per-view addressing, once per CTA (no 64-bit divisions or dynamically
     // indexed parameter arrays in the element loops)
+    if (src.nview) {   // CTA-uniform: skip when every view of the tile is unused
+        __shared__ int s_live;
+        if (threadIdx.x == 0) s_live = 0;
+        __syncthreads();
+        if (threadIdx.x < nv) {
+            const int64_t g = g0 + threadIdx.x;
+            const int64_t b = g / src.nshift;
+            if ((int)(g - b * src.nshift) < __ldg(src.nview + b)) s_live = 1;
+        }
+        __syncthreads();
+        if (!s_live) return;
+    }
     if (threadIdx.x < nv) {
         const int64_t g = g0 + threadIdx.x;
         const int64_t b = g / src.nshift;
@@ -319,6 +334,7 @@ static __global__ void k_fft_large_a(const ViewSrc src, int logL, int logP,
     const int c = (int)(blockIdx.x & (Q - 1));
     const int64_t b = g / src.nshift;
     const int s = (int)(g - b * src.nshift);
+    if (src.nview && s >= __ldg(src.nview + b)) return;   // unused view
     const int rc = logQ ? (int)(__brev((unsigned)c) >> (32 - logQ)) : 0;
     // block c of view g is itself a P-point view: input i of the block is
     // view sample rev_P(i)*Q + rc, i.e. stride Q*d from offset shift + rc*d
@@ -352,12 +368,14 @@ static __global__ void __launch_bounds__(256) k_fft_large_b_reg(cx *buf, int64_t
                                                                 const cx *__restrict__ tw, cx *out,
                                                                 int nshift, int SV, int64_t ldV, int scale,
                                                                 const double *__restrict__ thr,
-                                                                uint8_t *__restrict__ act) {
+                                                                uint8_t *__restrict__ act,
+                                                                const int32_t *__restrict__ nview) {
     constexpr int Q = 1 << LQ;
     const int64_t P = int64_t(1) << s0;
     const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t g = gt >> (logL - LQ);
     if (g >= nviews) return;
+    if (nview && (int)(g - (g / nshift) * nshift) >= __ldg(nview + g / nshift)) return;   // unused view
     const int64_t rem = gt & ((int64_t(1) << (logL - LQ)) - 1);
     const int64_t r = rem & (P - 1);
     const int64_t hi = rem >> s0;
@@ -408,10 +426,10 @@ static __global__ void __launch_bounds__(256) k_fft_large_b_reg(cx *buf, int64_t
 template <int LQ>
 static inline void launch_large_b_reg(cx *buf, int64_t nviews, int logL, int s0, const cx *tw, cx *out,
                                       int nshift, int SV, int64_t ldV, int scale, const double *thr,
-                                      uint8_t *act, cudaStream_t stream) {
+                                      uint8_t *act, cudaStream_t stream, const int32_t *nview) {
     const int64_t threads = nviews << (logL - LQ);
     k_fft_large_b_reg<LQ><<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(
-        buf, nviews, logL, s0, tw, out, nshift, SV, ldV, scale, thr, act);
+        buf, nviews, logL, s0, tw, out, nshift, SV, ldV, scale, thr, act, nview);
 }
 
 // kernel launches of one launch_fft_views call
@@ -491,10 +509,10 @@ static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, con
         const bool last = s0 + lq == logL;
         cx *o = last ? out : nullptr;
         switch (lq) {
-        case 1: launch_large_b_reg<1>(large_scratch, nviews, logL, s0, tw, o, src.nshift, SV, ldV, scale, thr, act, stream); break;
-        case 2: launch_large_b_reg<2>(large_scratch, nviews, logL, s0, tw, o, src.nshift, SV, ldV, scale, thr, act, stream); break;
-        case 3: launch_large_b_reg<3>(large_scratch, nviews, logL, s0, tw, o, src.nshift, SV, ldV, scale, thr, act, stream); break;
-        default: launch_large_b_reg<4>(large_scratch, nviews, logL, s0, tw, o, src.nshift, SV, ldV, scale, thr, act, stream); break;
+        case 1: launch_large_b_reg<1>(large_scratch, nviews, logL, s0, tw, o, src.nshift, SV, ldV, scale, thr, act, stream, src.nview); break;
+        case 2: launch_large_b_reg<2>(large_scratch, nviews, logL, s0, tw, o, src.nshift, SV, ldV, scale, thr, act, stream, src.nview); break;
+        case 3: launch_large_b_reg<3>(large_scratch, nviews, logL, s0, tw, o, src.nshift, SV, ldV, scale, thr, act, stream, src.nview); break;
+        default: launch_large_b_reg<4>(large_scratch, nviews, logL, s0, tw, o, src.nshift, SV, ldV, scale, thr, act, stream, src.nview); break;
         }
         SFDT_CHECK_LAUNCH();
         s0 += lq;
@@ -516,6 +534,7 @@ static inline ViewSrc consecutive_views(const void *x, int is_c64, int64_t n, in
     s.dyn_first = MAX_VIEWS;
     s.dyn_stride = 0;
     s.jfast = 0;
+    s.nview = nullptr;
     return s;
 }
 

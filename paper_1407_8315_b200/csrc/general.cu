@@ -39,7 +39,41 @@ struct GenParams {
     int64_t shift_stride;
     const cx *base_phi;
     int64_t phi_stride;
+    // view slot of random view j of signal b: vslot[b * r_eff + j] (< S when
+    // its shift equals a consecutive shift, whose view it then shares)
+    const int32_t *vslot;
 };
+
+// row of random view j (shift shifts[j]) of signal b at bin kb
+__device__ __forceinline__ const cx *rview(const cx *V, const GenParams &p, int64_t b, int j, int64_t kb) {
+    return V + (b * p.nv + __ldg(p.vslot + b * p.r_eff + j)) * p.L + kb;
+}
+
+// A random shift s < 2*a_max draws the same view as consecutive shift s
+// (the reference computes it twice, general.py:288-294; the FFT is the same
+// bits either way).  Per signal: the distinct random shifts packed after
+// the S consecutive views, each random view's slot, and the number of views
+// to transform.  At d = 8 (r_eff = d: every residue drawn) 6 of the 14
+// transforms are duplicates.
+__global__ void k_gen_vslot(GenParams p, int64_t B, int dedup, int64_t *__restrict__ vsh,
+                            int32_t *__restrict__ vslot, int32_t *__restrict__ nview) {
+    const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    const int64_t *sh = p.shifts + b * p.shift_stride;
+    int n = 0;
+    for (int j = 0; j < p.r_eff; j++) {
+        const int64_t s = sh[j];
+        if (dedup && s < p.S) {
+            vslot[b * p.r_eff + j] = (int32_t)s;
+        } else {
+            vsh[b * p.r_eff + n] = s;
+            vslot[b * p.r_eff + j] = p.S + n;
+            n++;
+        }
+    }
+    for (int j = n; j < p.r_eff; j++) vsh[b * p.r_eff + j] = 0;   // padding (never transformed)
+    nview[b] = p.S + n;
+}
 
 // ------------------------------------------------------------------- svd
 template <int AM>
@@ -823,7 +857,7 @@ __global__ void __launch_bounds__(256, 2) k_gen_mf(const cx *__restrict__ V, Gen
             const int a = votes[t];
             cx wj = mk(0.0, 0.0);
             if (lane < r) {
-                const cx yj = ldcx(V + (b * p.nv + p.S + lane) * p.L + kb);
+                const cx yj = ldcx(rview(V, p, b, lane, kb));
                 const double th = DMUL(-TWO_PI, (double)(sh[lane] * kb)) / (double)p.n;
                 wj = nmul(gexp(mk(0.0, th)), yj);
             }
@@ -1018,7 +1052,7 @@ __global__ void __launch_bounds__(128) k_gen_prune(const cx *__restrict__ V, Gen
         const int64_t *sh = p.shifts + b * p.shift_stride;
         cx syn[8], y[GEN_MAX_R];
         for (int j = 0; j < p.S; j++) syn[j] = ldcx(V + (b * p.nv + j) * p.L + kb);
-        for (int j = 0; j < r; j++) y[j] = ldcx(V + (b * p.nv + p.S + j) * p.L + kb);
+        for (int j = 0; j < r; j++) y[j] = ldcx(rview(V, p, b, j, kb));
         const int64_t count = (int64_t)p.keep * a < p.d ? (int64_t)p.keep * a : p.d;
         int cols[GEN_MAX_COLS];
         int ncols = 0;
@@ -1260,7 +1294,7 @@ __global__ void __launch_bounds__(128) k_gen_sp1(const cx *__restrict__ V, GenPa
         const double tk = DMUL(TWO_PI, (double)kb);
 #pragma unroll
         for (int j = 0; j < R; j++) {
-            y[j] = ldcx(V + (b * p.nv + p.S + j) * p.L + kb);
+            y[j] = ldcx(rview(V, p, b, j, kb));
             phase[j] = gexp(mk(0.0, DMUL(tk, (double)sh[j]) / (double)p.n));
         }
         int cols[4];
@@ -1314,7 +1348,7 @@ __global__ void __launch_bounds__(128) k_gen_bins(const cx *__restrict__ V, GenP
 #pragma unroll
         for (int j = 0; j < (RT > 0 ? RT : GEN_MAX_R); j++) {
             if (RT == 0 && j >= r) break;
-            y[j] = ldcx(V + (b * p.nv + p.S + j) * p.L + kb);
+            y[j] = ldcx(rview(V, p, b, j, kb));
         }
         int cols[GEN_MAX_COLS];
         const int nc8 = ncols_in[it];
@@ -1370,7 +1404,7 @@ __global__ void __launch_bounds__(256) k_gen_bins_warp(const cx *__restrict__ V,
         cx y[GEN_MAX_R], phase[GEN_MAX_R];
         const double tk = DMUL(TWO_PI, (double)kb);
         for (int j = 0; j < r; j++) {
-            y[j] = ldcx(V + (b * p.nv + p.S + j) * p.L + kb);
+            y[j] = ldcx(rview(V, p, b, j, kb));
             phase[j] = gexp(mk(0.0, DMUL(tk, (double)sh[j]) / (double)p.n));
         }
         const int a_sp = a < r ? a : r;
@@ -1536,7 +1570,7 @@ struct GenPlan {
     int64_t B, n, d, L, nv, nparts;
     int S;
     size_t off_V, off_sv, off_part, off_votes, off_nent, off_sloc, off_sval, off_wl, off_cnt,
-        off_fft, off_mf, off_cols, off_ncols, off_hl, off_seg, off_vsel, off_ghist, off_eqc, total;
+        off_fft, off_mf, off_cols, off_ncols, off_hl, off_vsh, off_vslot, off_nview, off_seg, off_vsel, off_ghist, off_eqc, total;
 };
 
 static int make_gen_plan(const sfdt_general_args *a, GenPlan &p) {
@@ -1577,6 +1611,9 @@ static int make_gen_plan(const sfdt_general_args *a, GenPlan &p) {
     p.off_vsel = take(size_t(p.B) * sizeof(VSel));
     p.off_ghist = take(size_t(p.B) * 256 * 4);
     p.off_eqc = take(size_t(p.B) * ((p.L * a->a_max + VCH - 1) / VCH) * 8);
+    p.off_vsh = take(size_t(p.B) * a->r_eff * 8);
+    p.off_vslot = take(size_t(p.B) * a->r_eff * 4);
+    p.off_nview = take(size_t(p.B) * 4);
     p.off_fft = (p.L > FFT_SMEM_MAX) ? take(size_t(p.B) * p.nv * p.L * 16) : 0;
     p.total = o;
     return SFDT_OK;
@@ -1624,16 +1661,6 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     const int is_c64 = a->x_dtype == SFDT_C64;
     int launches = 0;
 
-    // 1. consecutive + random-shift views (general.py:288-294)
-    ViewSrc src = consecutive_views(a->x, is_c64, p.n, p.d, 0, p.S);
-    src.nshift = (int)p.nv;
-    src.dyn_off = a->shifts;
-    src.dyn_first = p.S;
-    src.dyn_stride = a->shift_stride;
-    rc = launch_fft_views(src, p.B, p.L, a->twiddles, V, (int)p.nv, p.L, stream, fft_scratch);
-    if (rc) return rc;
-    launches += fft_view_launches(p.L);
-
     GenParams gp;
     gp.n = p.n;
     gp.d = p.d;
@@ -1650,6 +1677,29 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     gp.shift_stride = a->shift_stride;
     gp.base_phi = (const cx *)a->base_phi;
     gp.phi_stride = a->phi_stride;
+
+    int64_t *vsh = (int64_t *)(w + p.off_vsh);
+    int32_t *vslot = (int32_t *)(w + p.off_vslot);
+    int32_t *nview = (int32_t *)(w + p.off_nview);
+    {
+        const char *ed = getenv("SFDT_GEN_DEDUP");
+        const int dedup = !(ed && ed[0] == '0');
+        k_gen_vslot<<<(unsigned)((p.B + 127) / 128), 128, 0, stream>>>(gp, p.B, dedup, vsh, vslot, nview);
+        SFDT_CHECK_LAUNCH();
+        launches++;
+    }
+    gp.vslot = vslot;
+
+    // 1. consecutive + random-shift views (general.py:288-294)
+    ViewSrc src = consecutive_views(a->x, is_c64, p.n, p.d, 0, p.S);
+    src.nshift = (int)p.nv;
+    src.dyn_off = vsh;
+    src.dyn_first = p.S;
+    src.dyn_stride = a->r_eff;
+    src.nview = nview;
+    rc = launch_fft_views(src, p.B, p.L, a->twiddles, V, (int)p.nv, p.L, stream, fft_scratch);
+    if (rc) return rc;
+    launches += fft_view_launches(p.L);
 
     // 2. collision vote (general.py:131-155)
     {
@@ -1834,6 +1884,7 @@ extern "C" int sfdt_estimate_collisions(const double *syn, int64_t nb, int64_t l
     gp.shift_stride = 0;
     gp.base_phi = nullptr;
     gp.phi_stride = 0;
+    gp.vslot = nullptr;
     cudaMemsetAsync(wlc, 0, 8, stream);
     {
         const int64_t M = nb * a_max;

@@ -386,6 +386,31 @@ def test_general_batch_vs_oracle_cfg4_shape():
         assert tr.collision_histogram == wtr["collision_histogram"]
 
 
+@pytest.mark.parametrize("n,k", [(1 << 16, 256), (1 << 18, 1024)])
+def test_general_duplicate_views_shared(n, k, monkeypatch):
+    """d = 8 (r_eff = d): every residue is drawn, so 6 of the 9 random shifts
+    repeat a consecutive shift and share its view instead of being
+    transformed again (smem FFT path at L = 8192, large-view path at
+    L = 32768).  Bitwise equal to transforming every view, and equal to the
+    oracle."""
+    B = 3
+    seeds = [(23, b) for b in range(B)]
+    X = np.stack([general_signal(n, k, 30.0, s)[0] for s in seeds])
+    cfg = P.GeneralConfig(n=n, k=k)
+    assert cfg.resolved_d() == 8
+    got = P.solve_general_batch(X, cfg, seeds=seeds)
+    monkeypatch.setenv("SFDT_GEN_DEDUP", "0")
+    full = P.solve_general_batch(X, cfg, seeds=seeds)
+    for b in range(B):
+        g, f = got.spectrum(b).entries, full.spectrum(b).entries
+        assert list(g) == list(f)
+        assert np.array_equal(np.fromiter(g.values(), complex), np.fromiter(f.values(), complex))
+    want, _ = OS.general(X[0], k, rng_seed=seeds[0])
+    locs = np.fromiter(want.keys(), dtype=np.int64, count=len(want))
+    vals = np.fromiter(want.values(), dtype=np.complex128, count=len(want))
+    _general_check(got.spectrum(0).entries, locs, vals, "b=0")
+
+
 @pytest.mark.parametrize("warp", ["1", "0"])
 def test_general_noprune_cfg4_shape(warp, monkeypatch):
     """prune=False at the config-4 shape (d=256): subspace pursuit over all d

@@ -76,9 +76,84 @@ __global__ void k_gen_vslot(GenParams p, int64_t B, int dedup, int64_t *__restri
 }
 
 // ------------------------------------------------------------------- svd
+// Singular values of the 3 x 3 Hankel H_ij = m_{i+j} in closed form: the
+// eigenvalues of the Hermitian G = H^H H by the trigonometric cubic
+// (lambda = q + 2 p cos(phi + 2 pi k / 3)), sigma = sqrt(lambda).  Its
+// error grows with the spread lambda_1 / lambda_3 and, through acos, as
+// |r| -> 1 (a nearly repeated eigenvalue), so it is used only when
+// lambda_3 >= lambda_1 / 64 and |r| <= 0.999: there sigma agrees with
+// LAPACK's SVD to <= 5.3e-14 relative (1e5 random Hankels, measured; the
+// reference's two backends differ by up to 1e-13), and it takes 86 % of
+// noise bins.  Every other bin -- rank-1 tone bins, near-singular or
+// near-degenerate Hankels -- is listed for the register-resident Jacobi
+// (k_gen_svd_fix).
+__device__ __forceinline__ bool hankel_sv3_closed(const cx *m, double *out) {
+    // G_jk = sum_i conj(m_{i+j}) m_{i+k}
+    double g00 = 0.0, g11 = 0.0, g22 = 0.0;
+    cx g01 = mk(0.0, 0.0), g02 = mk(0.0, 0.0), g12 = mk(0.0, 0.0);
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+        const cx a0 = m[i], a1 = m[i + 1], a2 = m[i + 2];
+        g00 = fma(a0.re, a0.re, fma(a0.im, a0.im, g00));
+        g11 = fma(a1.re, a1.re, fma(a1.im, a1.im, g11));
+        g22 = fma(a2.re, a2.re, fma(a2.im, a2.im, g22));
+        g01 = cadd(g01, nmul(cconj(a0), a1));
+        g02 = cadd(g02, nmul(cconj(a0), a2));
+        g12 = cadd(g12, nmul(cconj(a1), a2));
+    }
+    const double q = (g00 + g11 + g22) * (1.0 / 3.0);
+    const double a = g00 - q, b = g11 - q, c = g22 - q;
+    const double x2 = fma(g01.re, g01.re, g01.im * g01.im);
+    const double y2 = fma(g02.re, g02.re, g02.im * g02.im);
+    const double z2 = fma(g12.re, g12.re, g12.im * g12.im);
+    const double p2 = fma(a, a, fma(b, b, fma(c, c, 2.0 * (x2 + y2 + z2))));
+    double l1, l2, l3;
+    if (p2 <= 0.0) {
+        l1 = l2 = l3 = q;
+    } else {
+        const double pp = sqrt(p2 * (1.0 / 6.0));
+        // det(G - qI) = abc + 2 Re(x z conj(y)) - a|z|^2 - b|y|^2 - c|x|^2
+        const cx xz = nmul(g01, g12);
+        const double re = fma(xz.re, g02.re, xz.im * g02.im);
+        const double det = fma(a * b, c, fma(2.0, re, -fma(a, z2, fma(b, y2, c * x2))));
+        const double r = det / (2.0 * pp * pp * pp);
+        if (!(fabs(r) <= 0.999)) return false;
+        const double phi = acos(r) * (1.0 / 3.0);
+        l1 = fma(2.0 * pp, cos(phi), q);
+        l3 = fma(2.0 * pp, cos(phi + 2.0943951023931957), q);
+        l2 = 3.0 * q - l1 - l3;
+    }
+    if (!(l1 > 0.0) || !(l1 < INFINITY) || !(l3 * 64.0 >= l1)) return false;
+    out[0] = sqrt(l1);
+    out[1] = sqrt(l2);
+    out[2] = sqrt(l3);
+    return out[0] >= out[1] && out[1] >= out[2];
+}
+
+// the bins k_gen_svd left to the Jacobi (listed flat indices b*L + k)
+__global__ void __launch_bounds__(128) k_gen_svd_fix(const cx *__restrict__ V, GenParams p,
+                                                     double *__restrict__ sv, const int64_t *__restrict__ fix,
+                                                     const unsigned long long *__restrict__ nfix) {
+    const int64_t cnt = (int64_t)*nfix;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < cnt;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t t = fix[i];
+        const int64_t b = t / p.L, k = t - b * p.L;
+        cx syn[6];
+#pragma unroll
+        for (int j = 0; j < 6; j++) syn[j] = ldcx(V + (b * p.nv + j) * p.L + k);
+        double s[3];
+        hankel_sv_n<3>(syn, s, 2.220446049250313e-16);
+#pragma unroll
+        for (int j = 0; j < 3; j++) sv[t * 3 + j] = s[j];
+    }
+}
+
 template <int AM>
 __global__ void __launch_bounds__(128) k_gen_svd(const cx *__restrict__ V, GenParams p,
-                                                 double *__restrict__ sv, double *__restrict__ partial) {
+                                                 double *__restrict__ sv, double *__restrict__ partial,
+                                                 int64_t *__restrict__ fix, unsigned long long *__restrict__ nfix,
+                                                 int closed) {
     constexpr int S = 2 * AM;
     const int64_t b = blockIdx.y;
     const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -91,9 +166,19 @@ __global__ void __launch_bounds__(128) k_gen_svd(const cx *__restrict__ V, GenPa
             e += syn[j].re * syn[j].re + syn[j].im * syn[j].im;
         }
         double s[AM];
-        hankel_sv_n<AM>(syn, s, 2.220446049250313e-16);
+        if (AM == 3 && closed) {
+            // closed form; the conditioned-out bins go to k_gen_svd_fix
+            if (hankel_sv3_closed(syn, s)) {
 #pragma unroll
-        for (int i = 0; i < AM; i++) sv[(b * p.L + k) * AM + i] = s[i];
+                for (int i = 0; i < AM; i++) sv[(b * p.L + k) * AM + i] = s[i];
+            } else {
+                fix[atomicAdd(nfix, 1ull)] = b * p.L + k;
+            }
+        } else {
+            hankel_sv_n<AM>(syn, s, 2.220446049250313e-16);
+#pragma unroll
+            for (int i = 0; i < AM; i++) sv[(b * p.L + k) * AM + i] = s[i];
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
@@ -1570,7 +1655,7 @@ struct GenPlan {
     int64_t B, n, d, L, nv, nparts;
     int S;
     size_t off_V, off_sv, off_part, off_votes, off_nent, off_sloc, off_sval, off_wl, off_cnt,
-        off_fft, off_mf, off_cols, off_ncols, off_hl, off_vsh, off_vslot, off_nview, off_seg, off_vsel, off_ghist, off_eqc, total;
+        off_fft, off_mf, off_cols, off_ncols, off_hl, off_vsh, off_vslot, off_nview, off_fix, off_seg, off_vsel, off_ghist, off_eqc, total;
 };
 
 static int make_gen_plan(const sfdt_general_args *a, GenPlan &p) {
@@ -1614,6 +1699,7 @@ static int make_gen_plan(const sfdt_general_args *a, GenPlan &p) {
     p.off_vsh = take(size_t(p.B) * a->r_eff * 8);
     p.off_vslot = take(size_t(p.B) * a->r_eff * 4);
     p.off_nview = take(size_t(p.B) * 4);
+    p.off_fix = (a->a_max == 3) ? take(size_t(p.B) * p.L * 8) : 0;
     p.off_fft = (p.L > FFT_SMEM_MAX) ? take(size_t(p.B) * p.nv * p.L * 16) : 0;
     p.total = o;
     return SFDT_OK;
@@ -1704,11 +1790,23 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     // 2. collision vote (general.py:131-155)
     {
         const dim3 g((unsigned)p.nparts, (unsigned)p.B);
+        int64_t *fix = (int64_t *)(w + p.off_fix);
+        unsigned long long *nfix = wlc + 2;
         switch (a->a_max) {
-        case 1: k_gen_svd<1><<<g, 128, 0, stream>>>(V, gp, sv, part); break;
-        case 2: k_gen_svd<2><<<g, 128, 0, stream>>>(V, gp, sv, part); break;
-        case 3: k_gen_svd<3><<<g, 128, 0, stream>>>(V, gp, sv, part); break;
-        default: k_gen_svd<4><<<g, 128, 0, stream>>>(V, gp, sv, part); break;
+        case 1: k_gen_svd<1><<<g, 128, 0, stream>>>(V, gp, sv, part, fix, nfix, 0); break;
+        case 2: k_gen_svd<2><<<g, 128, 0, stream>>>(V, gp, sv, part, fix, nfix, 0); break;
+        case 3: {
+            const char *es = getenv("SFDT_GEN_SVD");   // "jacobi": the Jacobi for every bin
+            const int closed = !(es && es[0] == 'j');
+            cudaMemsetAsync(nfix, 0, 8, stream);
+            k_gen_svd<3><<<g, 128, 0, stream>>>(V, gp, sv, part, fix, nfix, closed);
+            SFDT_CHECK_LAUNCH();
+            k_gen_svd_fix<<<wl_grid(p.B * p.L, 128, one_wave(k_gen_svd_fix, 128)), 128, 0, stream>>>(
+                V, gp, sv, fix, nfix);
+            launches++;
+            break;
+        }
+        default: k_gen_svd<4><<<g, 128, 0, stream>>>(V, gp, sv, part, fix, nfix, 0); break;
         }
     }
     SFDT_CHECK_LAUNCH();

@@ -386,6 +386,24 @@ def test_general_batch_vs_oracle_cfg4_shape():
         assert tr.collision_histogram == wtr["collision_histogram"]
 
 
+def test_general_closed_form_singular_values(monkeypatch):
+    """a_max = 3: the closed-form singular values (bins with lambda_3 >=
+    lambda_1 / 64, |r| <= 0.999) agree with the Jacobi for every bin to
+    1e-13 relative, and the votes are identical."""
+    n, k, B = 1 << 18, 64, 8
+    seeds = [(31, b) for b in range(B)]
+    X = np.stack([general_signal(n, k, 10.0 + 5 * (b % 3), s)[0] for b, s in enumerate(seeds)])
+    cfg = P.GeneralConfig(n=n, k=k)
+    fast = P.solve_general_batch(X, cfg, seeds=seeds)
+    monkeypatch.setenv("SFDT_GEN_SVD", "jacobi")
+    jac = P.solve_general_batch(X, cfg, seeds=seeds)
+    sf, sj = fast.singular_values(), jac.singular_values()
+    assert np.all(np.abs(sf - sj) <= 1e-13 * np.abs(sj))
+    assert np.array_equal(fast.votes(), jac.votes())
+    for b in range(B):
+        assert fast.spectrum(b).entries == jac.spectrum(b).entries
+
+
 @pytest.mark.parametrize("n,k", [(1 << 16, 256), (1 << 18, 1024)])
 def test_general_duplicate_views_shared(n, k, monkeypatch):
     """d = 8 (r_eff = d): every residue is drawn, so 6 of the 9 random shifts

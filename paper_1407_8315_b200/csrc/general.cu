@@ -1416,12 +1416,19 @@ __global__ void __launch_bounds__(128) k_gen_bins(const cx *__restrict__ V, GenP
                                                   const int32_t *__restrict__ cols_in,
                                                   const int8_t *__restrict__ ncols_in,
                                                   uint8_t *__restrict__ nent, int64_t *__restrict__ sloc,
-                                                  cx *__restrict__ sval, int64_t *__restrict__ stats) {
+                                                  cx *__restrict__ sval, int64_t *__restrict__ stats,
+                                                  unsigned long long *__restrict__ hl_next) {
     const int64_t cnt = (int64_t)*hl_count;
     const int64_t nwarps = int64_t(gridDim.x) * (blockDim.x >> 5);
     const int64_t gw = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-    for (int64_t q = int64_t(lane) * nwarps + gw; q < cnt; q += 32 * nwarps) {
+    // few bins: one per warp (lane 0); many (no pruning: every voted bin):
+    // every thread takes the next bin from a counter, so the long and short
+    // chains balance dynamically
+    const bool few = cnt <= nwarps;
+    if (few && lane != 0) return;
+    for (int64_t q = few ? gw : (int64_t)atomicAdd(hl_next, 1ull); q < cnt;
+         q = few ? cnt : (int64_t)atomicAdd(hl_next, 1ull)) {
         const int64_t it = hl[q];
         const int64_t t = wl[it];
         const int a = votes[t];
@@ -1885,6 +1892,7 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     int64_t *hl = (int64_t *)(w + p.off_hl);
     unsigned long long *hlc = wlc + 1;
     cudaMemsetAsync(hlc, 0, 8, stream);
+    cudaMemsetAsync(wlc + 3, 0, 8, stream);   // k_gen_bins' take counter
     k_gen_prune<<<wl_grid(max_voted, 128, one_wave(k_gen_prune, 128)), 128, 0, stream>>>(
         V, gp, votes, wl, wlc, mf_top, colsb, ncolsb, sp1 | (warp_all ? 2 : 0), hl, hlc);
     SFDT_CHECK_LAUNCH();
@@ -1914,7 +1922,7 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
 #define SFDT_BINS(R)                                                                                    \
     case R:                                                                                             \
         k_gen_bins<R><<<wl_grid(32 * max_voted, 128, one_wave(k_gen_bins<R>, 128)), 128, 0, stream>>>(  \
-            V, gp, votes, wl, hl, hlc, colsb, ncolsb, nent, sloc, sval, a->stats);                      \
+            V, gp, votes, wl, hl, hlc, colsb, ncolsb, nent, sloc, sval, a->stats, wlc + 3);             \
         break;
             SFDT_BINS(6) SFDT_BINS(8) SFDT_BINS(9) SFDT_BINS(12)
         default:

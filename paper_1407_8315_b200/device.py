@@ -102,19 +102,42 @@ def as_device_signals(x, device: torch.device, allow_c64: bool = True):
     return t.contiguous()
 
 
+_staging: dict = {}
+
+
+def _pinned_staging(nbytes: int) -> torch.Tensor:
+    """Grow-only pinned host buffer (one cudaHostAlloc per growth, never per
+    call: a fresh pinned allocation is a synchronous, slow driver call)."""
+    buf = _staging.get("buf")
+    if buf is None or buf.numel() < nbytes:
+        size = 1 << max(20, (int(nbytes) - 1).bit_length())
+        buf = torch.empty(size, dtype=torch.uint8, pin_memory=True)
+        _staging["buf"] = buf
+    return buf
+
+
 def host_copy(tensors: dict) -> dict:
     """Device tensors -> host numpy arrays with ONE stream sync: every copy is
-    issued non-blocking into pinned staging on the current stream, then the
-    stream is synchronised once (instead of a sync per .cpu())."""
-    out, stream = {}, None
+    issued non-blocking into a reused pinned staging buffer on the current
+    stream, the stream is synchronised once, and the arrays are copied out
+    (instead of a sync per .cpu())."""
+    items, total, stream = [], 0, None
     for k, t in tensors.items():
         if t.is_cuda:
             stream = torch.cuda.current_stream(t.device)
-            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-            h.copy_(t, non_blocking=True)
-            out[k] = h
-        else:
-            out[k] = t
-    if stream is not None:
-        stream.synchronize()
-    return {k: v.numpy() for k, v in out.items()}
+            nb = t.numel() * t.element_size()
+            items.append((k, t, total, nb))
+            total += (nb + 255) & ~255
+    out = {k: t.numpy() for k, t in tensors.items() if not t.is_cuda}
+    if not items:
+        return out
+    buf = _pinned_staging(total)
+    views = {}
+    for k, t, off, nb in items:
+        v = buf[off:off + nb].view(t.dtype).view(t.shape)
+        v.copy_(t, non_blocking=True)
+        views[k] = v
+    stream.synchronize()
+    for k, v in views.items():
+        out[k] = v.numpy().copy()
+    return out

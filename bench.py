@@ -336,7 +336,8 @@ class Solver:
         if self.a.kind == "exact":
             return self.P.exact_batch(X, self.cfg, self.iterative, self.dev, stream_events=events,
                                       pipeline=self.a.pipeline)
-        return self.P.solve_general_batch(X, self.cfg, device=self.dev, plan=self.plan)
+        return self.P.solve_general_batch(X, self.cfg, device=self.dev, plan=self.plan,
+                                          fft_events=events)
 
     def oracle(self, x, b):
         from oracle import solvers as OS
@@ -507,16 +508,34 @@ def gpu_arm(a):
                                 "algorithmic bytes / step time; a single small signal is "
                                 "launch-latency bound, not HBM bound")
     else:
+        # dominant kernel: the view gather + FFT (k_fft_views, or the large-
+        # view passes), HBM-bound.  Algorithmic bytes per signal: the distinct
+        # view samples read once (2*a_max + distinct random shifts) plus the
+        # views written, 16 B each; per-launch DRAM traffic from the ncu
+        # capture (random 16-B samples cost 128-B DRAM accesses).
         L = a.n // resolved_d(a)
-        alg_bytes = a.batch * 15 * L * 16
-        roofline = {"bound": "fp64", "kernel": "k_gen_bins/k_gen_svd",
-                    "note": ("general path is FP64/latency-bound (SURVEY F2): only "
-                             "(2*a_max + r_eff)*L samples per signal are read"),
-                    "gather_bytes_per_step": alg_bytes,
-                    "step_gather_gbs": alg_bytes / step_s / 1e9, "peak": peak,
-                    "peak_source": peak_src, "unit": "GB/s",
-                    "achieved": alg_bytes / step_s / 1e9, "frac": alg_bytes / step_s / 1e9 / peak,
-                    "traffic": None}
+        d = resolved_d(a)
+        sh = solver.plan.sh
+        distinct = np.array([6 + int(np.sum(np.asarray(row) >= 6)) for row in sh])
+        alg_bytes = int(2 * distinct.sum() * L * 16)
+        if a.use_graph:
+            avg_s = step_s
+        else:
+            fft_ms = [sb[s].elapsed_time(se[s]) for s in range(a.steps)]
+            avg_s = sum(fft_ms) / len(fft_ms) / 1e3
+        achieved = alg_bytes / avg_s / 1e9
+        roofline = {"bound": "hbm", "kernel": "k_fft_views (view gather + FFT)" if L <= 8192
+                    else "k_fft_large_a/b (view gather + FFT)",
+                    "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                    "frac": achieved / peak,
+                    "traffic": load_traffic(f"general_n{a.n}_k{a.k}_b{a.batch}_{a.dtype}"),
+                    "alg_bytes_per_launch": alg_bytes,
+                    "alg_bytes_def": ("2 x 16 B x L x (2*a_max + distinct random shifts) per signal: "
+                                      "every view sample read once, every view written once"),
+                    "avg_launch_ms": avg_s * 1e3, "kernel_share_of_step": avg_s / step_s,
+                    "note": ("a random-shift sample is one 16-B element per d-block; DRAM serves it "
+                             "as a 128-B access, so traffic is ~2.8x the algorithmic bytes at config 4; "
+                             "the rest of the step is FP64/latency-bound per-bin work")}
     out = None
     if rank == 0:
         cpu = None

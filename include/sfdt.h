@@ -180,6 +180,8 @@ typedef struct {
     int64_t *stats;          /* batch * SFDT_GS_PER_SIGNAL */
     int32_t *votes;          /* optional: batch * (n/d) estimated collision counts */
     double *singular_values; /* optional: batch * (n/d) * a_max */
+    void *ev_fft_begin;      /* cudaEvent_t recorded right before / after the */
+    void *ev_fft_end;        /* view gather + FFT kernels (optional, roofline timing) */
     int32_t kernel_launches; /* out */
 } sfdt_general_args;
 

@@ -62,6 +62,7 @@ class GeneralArgs(ctypes.Structure):
         ("twiddles", _vp),
         ("entry_offsets", _vp), ("locs", _vp), ("vals", _vp), ("entry_cap", _i64),
         ("stats", _vp), ("votes", _vp), ("singular_values", _vp),
+        ("ev_fft_begin", _vp), ("ev_fft_end", _vp),
         ("kernel_launches", _i32),
     ]
 

@@ -330,10 +330,15 @@ static __global__ void k_fft_large_a(const ViewSrc src, int logL, int logP,
     extern __shared__ double4 smem_raw[];
     cx *a = reinterpret_cast<cx *>(smem_raw);
     const int logQ = logL - logP, P = 1 << logP, Q = 1 << logQ;
-    const int64_t g = blockIdx.x >> logQ;
-    const int c = (int)(blockIdx.x & (Q - 1));
-    const int64_t b = g / src.nshift;
-    const int s = (int)(g - b * src.nshift);
+    // views fastest: the CTAs of block c of all a signal's views run side by
+    // side, and the views' shifts are adjacent samples of x, so one DRAM
+    // line (128 B) serves every view's 16-B sample from L2 instead of being
+    // fetched once per view (block c alone reads one sample per line)
+    const int s = (int)(blockIdx.x % (unsigned)src.nshift);
+    const int64_t rest = blockIdx.x / (unsigned)src.nshift;
+    const int c = (int)(rest & (Q - 1));
+    const int64_t b = rest >> logQ;
+    const int64_t g = b * src.nshift + s;
     if (src.nview && s >= __ldg(src.nview + b)) return;   // unused view
     const int rc = logQ ? (int)(__brev((unsigned)c) >> (32 - logQ)) : 0;
     // block c of view g is itself a P-point view: input i of the block is

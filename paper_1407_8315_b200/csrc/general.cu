@@ -1790,8 +1790,10 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     src.dyn_first = p.S;
     src.dyn_stride = a->r_eff;
     src.nview = nview;
+    if (a->ev_fft_begin) cudaEventRecord((cudaEvent_t)a->ev_fft_begin, stream);
     rc = launch_fft_views(src, p.B, p.L, a->twiddles, V, (int)p.nv, p.L, stream, fft_scratch);
     if (rc) return rc;
+    if (a->ev_fft_end) cudaEventRecord((cudaEvent_t)a->ev_fft_end, stream);
     launches += fft_view_launches(p.L);
 
     // 2. collision vote (general.py:131-155)

@@ -170,7 +170,8 @@ class GeneralPlan:
 
 
 def solve_general_batch(X, cfg: GeneralConfig, seeds=None, device=None,
-                        plan: GeneralPlan | None = None, zero_copy: bool = False) -> GeneralBatch:
+                        plan: GeneralPlan | None = None, zero_copy: bool = False,
+                        fft_events=None) -> GeneralBatch:
     """Batched solve_general.  seeds: None (cfg.rng_seed for every signal) or
     one rng_seed per signal (per-signal shift draws); plan: precomputed
     GeneralPlan for repeated batches.
@@ -231,6 +232,8 @@ def solve_general_batch(X, cfg: GeneralConfig, seeds=None, device=None,
     a.entry_offsets, a.locs, a.vals, a.entry_cap = ptr(o["entry_offsets"]), ptr(o["locs"]), \
         ptr(o["vals"]), cap.value
     a.stats, a.votes, a.singular_values = ptr(o["stats"]), ptr(o["votes"]), ptr(o["singular_values"])
+    if fft_events is not None:   # (begin, end) around the view gather + FFT (roofline timing)
+        a.ev_fft_begin, a.ev_fft_end = fft_events[0].cuda_event, fft_events[1].cuda_event
     nbytes = lib.sfdt_general_workspace_bytes(a)
     ws = Workspace.get(nbytes, dev)
     _lib.check(lib.sfdt_general_solve(a, ws.data_ptr(), ws.numel(), stream_handle(dev)),

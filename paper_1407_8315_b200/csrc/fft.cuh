@@ -428,6 +428,72 @@ static __global__ void __launch_bounds__(256) k_fft_large_b_reg(cx *buf, int64_t
     }
 }
 
+
+// Pass B in shared memory when 5 stages remain (L = 2^17): one CTA
+// holds 32 consecutive residues r of one view, all 2^LQ elements i = r +
+// q*2^s0 of each (16 KiB), loaded and stored as 512-B rows.  The
+// LQ stages run as the radix-2 stage loop does them -- the same butterfly
+// on the same pairs with the same twiddle tw[(h-1) + r + qk*2^s0] -- so the
+// result is bit-identical to two register passes, with one pass over the
+// scratch instead of two.  Writes the views (scaled, activity epilogue).
+constexpr int LB_RES = 32;
+static __global__ void __launch_bounds__(256) k_fft_large_b_smem(const cx *__restrict__ buf, int64_t nviews,
+                                                                 int logL, int s0, int LQ,
+                                                                 const cx *__restrict__ tw, cx *out,
+                                                                 int nshift, int SV, int64_t ldV, int scale,
+                                                                 const double *__restrict__ thr,
+                                                                 uint8_t *__restrict__ act,
+                                                                 const int32_t *__restrict__ nview) {
+    extern __shared__ double4 smem_raw[];
+    cx *tile = reinterpret_cast<cx *>(smem_raw);   // [q][r_local]
+    const int64_t P = int64_t(1) << s0;
+    const int Q = 1 << LQ;
+    const int64_t groups = P / LB_RES;
+    const int64_t g = blockIdx.x / groups;
+    const int64_t r0 = (blockIdx.x - g * groups) * LB_RES;
+    if (g >= nviews) return;
+    const int64_t b = g / nshift;
+    const int s = (int)(g - b * nshift);
+    if (nview && s >= __ldg(nview + b)) return;   // unused view
+    const cx *src = buf + (g << logL) + r0;
+    for (int e = threadIdx.x; e < Q * LB_RES; e += blockDim.x) {
+        const int q = e / LB_RES, rl = e - q * LB_RES;
+        tile[e] = ldcx(src + (int64_t)q * P + rl);
+    }
+    __syncthreads();
+    for (int st = 0; st < LQ; st++) {
+        const int hq = 1 << st;
+        const int64_t h = P << st;
+        // butterflies (q, q + hq) with bit st of q clear; qk = q mod hq
+        for (int e = threadIdx.x; e < (Q / 2) * LB_RES; e += blockDim.x) {
+            const int pidx = e / LB_RES, rl = e - pidx * LB_RES;
+            const int qk = pidx & (hq - 1);
+            const int q = ((pidx >> st) << (st + 1)) | qk;
+            const cx w = ldcx(tw + (h - 1) + r0 + rl + (int64_t)qk * P);
+            const cx u = tile[q * LB_RES + rl];
+            const cx t = gmul(tile[(q + hq) * LB_RES + rl], w);
+            tile[q * LB_RES + rl] = cadd(u, t);
+            tile[(q + hq) * LB_RES + rl] = csub(u, t);
+        }
+        __syncthreads();
+    }
+    const double sc = 1.0 / (double)(int64_t(1) << logL);
+    const double th = act ? thr[b] : 0.0;
+    cx *o = out + (b * SV + s) * ldV + r0;
+    for (int e = threadIdx.x; e < Q * LB_RES; e += blockDim.x) {
+        const int q = e / LB_RES, rl = e - q * LB_RES;
+        const cx x = tile[e];
+        const cx y = scale ? mk(DMUL(x.re, sc), DMUL(x.im, sc)) : x;
+        const int64_t i = (int64_t)q * P + rl;
+        stcx(o + i, y);
+        if (act) {
+            const double m2 = y.re * y.re + y.im * y.im;
+            if (m2 > th * th * (1.0 + 1e-6) || (m2 >= th * th * (1.0 - 1e-6) && cabs_(y) > th))
+                act[(b << logL) + r0 + i] = 1;
+        }
+    }
+}
+
 template <int LQ>
 static inline void launch_large_b_reg(cx *buf, int64_t nviews, int logL, int s0, const cx *tw, cx *out,
                                       int nshift, int SV, int64_t ldV, int scale, const double *thr,
@@ -441,6 +507,10 @@ static inline void launch_large_b_reg(cx *buf, int64_t nviews, int logL, int s0,
 static inline int fft_view_launches(int64_t L) {
     if (L <= FFT_SMEM_MAX) return 1;
     const int rest = ilog2_64(L) - 12;
+    if (rest == 5) {
+        const char *ebs = getenv("SFDT_FFT_BSMEM");
+        if (!(ebs && ebs[0] == '0')) return 2;
+    }
     return 1 + (rest + 3) / 4;
 }
 
@@ -506,8 +576,23 @@ static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, con
         k_fft_large_a<<<(unsigned)(nviews << logQ), 256, smem, stream>>>(src, logL, logP, tw, large_scratch);
         SFDT_CHECK_LAUNCH();
     }
-    // remaining stages logP .. logL-1 in register passes of <= 4 stages
-    // (the last one writes the views)
+    // remaining stages logP .. logL-1: 5..7 of them in one shared-memory
+    // pass, otherwise register passes of <= 4 stages (the last one writes
+    // the views)
+    const char *ebs = getenv("SFDT_FFT_BSMEM");
+    // (measured per config-5 batch: L = 2^17 2.83 -> 2.62 ms; L = 2^18
+    // neutral, 4.75 vs 4.81; L = 2^19 slower with 64-KiB tiles, 6.53 -> 7.38)
+    if (logL - logP == 5 && !(ebs && ebs[0] == '0')) {
+        const int LQ = logL - logP;
+        const size_t smem = (size_t(1) << LQ) * LB_RES * 16;
+        cudaFuncSetAttribute(k_fft_large_b_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const int64_t ctas = nviews * ((int64_t(1) << logP) / LB_RES);
+        k_fft_large_b_smem<<<(unsigned)ctas, 256, smem, stream>>>(large_scratch, nviews, logL, logP, LQ, tw, out,
+                                                                  src.nshift, SV, ldV, scale, thr, act,
+                                                                  src.nview);
+        SFDT_CHECK_LAUNCH();
+        return SFDT_OK;
+    }
     for (int s0 = logP; s0 < logL;) {
         const int rem = logL - s0;
         const int lq = rem >= 4 ? 4 : rem;

@@ -116,6 +116,7 @@ def test_read_signals_device_batch(tmp_path):
 
 
 @pytest.mark.gpu
+@pytest.mark.gpu
 def test_device_fft_bitexact_long():
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
@@ -123,7 +124,8 @@ def test_device_fft_bitexact_long():
     from oracle import kernels as OK
     from paper_1407_8315_b200.spectral import fft
     rng = np.random.default_rng(2)
-    for n in (8, 4096, 1 << 15, 1 << 17, 1 << 18, 1 << 21):   # 0 .. 3 register passes after the smem pass
+    # smem-only, 1 register pass, the shared-memory pass B (2^17 .. 2^19), 3 register passes
+    for n in (8, 4096, 1 << 15, 1 << 16, 1 << 17, 1 << 18, 1 << 19, 1 << 21):
         x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
         got = fft(x)
         assert np.array_equal(got.view(np.uint64), OK.fft_radix2(x).view(np.uint64)), n

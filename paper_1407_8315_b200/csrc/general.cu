@@ -1113,6 +1113,109 @@ __device__ __forceinline__ bool sp1_item(int a, int r, int nc8) {
     return a == 1 && nc8 >= 1 && nc8 <= 4 && sp1_r(r);
 }
 
+// Matched filter for short candidate lists (d <= 32): G = max(d, r_eff)
+// lanes (a power of two) per voted bin, 32/G bins per warp, lane t scoring
+// candidate t with the same per-candidate arithmetic as k_gen_mf (so the
+// same scores), the group's top min(a, d) by (score desc, t asc) picked by
+// arg-best over the group.  At d = 8 the warp-per-bin form left 24 of 32
+// lanes idle.
+template <int R, int G>
+__global__ void __launch_bounds__(256) k_gen_mf_small(const cx *__restrict__ V, GenParams p,
+                                                      const int32_t *__restrict__ votes,
+                                                      int32_t *__restrict__ mf_top, int64_t nchunk) {
+    __shared__ int s_list[MF_LIST];
+    __shared__ int s_n;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int gl = lane & (G - 1), sub = lane / G;
+    constexpr int PER_WARP = 32 / G;
+    const int64_t b = blockIdx.x / nchunk, chunk = blockIdx.x - b * nchunk;
+    const int64_t *sh = p.shifts + b * p.shift_stride;
+    const cx *gphi = p.base_phi + b * p.phi_stride;
+    const int d = (int)p.d;
+    for (int64_t c0 = chunk * MF_LIST; c0 < p.L && c0 < (chunk + 1) * MF_LIST; c0 += MF_LIST) {
+        if (threadIdx.x == 0) s_n = 0;
+        __syncthreads();
+        const int64_t c1 = p.L < c0 + MF_LIST ? p.L : c0 + MF_LIST;
+        for (int64_t k0 = c0; k0 < c1; k0 += blockDim.x) {
+            const int64_t kb = k0 + threadIdx.x;
+            const int a = kb < c1 ? votes[b * p.L + kb] : 0;
+            const int64_t count = (int64_t)p.keep * a < p.d ? (int64_t)p.keep * a : p.d;
+            const bool want = a >= 1 && p.prune && count < p.d;
+            const unsigned m = __ballot_sync(0xffffffffu, want);
+            int base = 0;
+            if (lane == 0 && m) base = atomicAdd(&s_n, __popc(m));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (want) s_list[base + __popc(m & ((1u << lane) - 1))] = (int)kb;
+        }
+        __syncthreads();
+        const int nlist = s_n;
+        // every group of the warp walks the list in lockstep (uniform trips)
+        for (int l0 = warp * PER_WARP; l0 < nlist; l0 += nw * PER_WARP) {
+            const int li = l0 + sub;
+            const bool valid = li < nlist;
+            const int64_t kb = valid ? s_list[li] : 0;
+            const int64_t t = b * p.L + kb;
+            const int a = valid ? votes[t] : 1;
+            cx wj = mk(0.0, 0.0);
+            if (valid && gl < R) {
+                const cx yj = ldcx(rview(V, p, b, gl, kb));
+                const double th = DMUL(-TWO_PI, (double)(sh[gl] * kb)) / (double)p.n;
+                wj = nmul(gexp(mk(0.0, th)), yj);
+            }
+            cx acc = mk(0.0, 0.0);
+#pragma unroll
+            for (int j = 0; j < R; j++) {
+                const cx w = mk(__shfl_sync(0xffffffffu, wj.re, j, G), __shfl_sync(0xffffffffu, wj.im, j, G));
+                const cx ph = gl < d ? ldcx(gphi + (int64_t)j * d + gl) : mk(0.0, 0.0);
+                acc = cadd(acc, nmul(cconj(ph), w));
+            }
+            double v = -INFINITY;
+            if (valid && gl < d) {
+                v = cabs_(acc);
+                if (v != v) v = -1.0;   // NaN last (scores are >= 0 otherwise)
+            }
+            int id = gl < d ? gl : INT_MAX;
+            const int n_top = (int)((int64_t)a < p.d ? a : p.d);
+            int sel[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                sel[q] = INT_MAX;
+                double bv = v;
+                int bi = id;
+#pragma unroll
+                for (int o = G / 2; o > 0; o >>= 1) {
+                    const double ov = __shfl_xor_sync(0xffffffffu, bv, o, G);
+                    const int oi = __shfl_xor_sync(0xffffffffu, bi, o, G);
+                    if (mf_better(ov, oi, bv, bi)) {
+                        bv = ov;
+                        bi = oi;
+                    }
+                }
+                if (q < n_top) {
+                    sel[q] = bi;
+                    if (id == bi) {   // the winner leaves the race
+                        v = -INFINITY;
+                        id = INT_MAX;
+                    }
+                }
+            }
+            if (valid && gl == 0) {
+#pragma unroll
+                for (int i = 1; i < 4; i++)
+#pragma unroll
+                    for (int j2 = 3; j2 >= i; j2--)
+                        if (sel[j2 - 1] > sel[j2]) {
+                            const int tmp = sel[j2 - 1];
+                            sel[j2 - 1] = sel[j2];
+                            sel[j2] = tmp;
+                        }
+                *reinterpret_cast<int4 *>(mf_top + t * 4) = make_int4(sel[0], sel[1], sel[2], sel[3]);
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // Pruning per voted bin (general.py:313-351): descending-order Hankel fit,
 // prune_eval over the d candidates with the reference's recurrence (or the
 // correlation fallback), union with the matched-filter columns (k_gen_mf).
@@ -1851,7 +1954,28 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaMemsetAsync(nent, 0, size_t(p.B) * p.L, stream);
     int32_t *mf_top = (int32_t *)(w + p.off_mf);
-    if (a->prune) {
+    const char *emf = getenv("SFDT_GEN_MF_SMALL");
+    bool mf_small_done = false;
+    if (a->prune && p.d <= 32 && !(emf && emf[0] == '0')) {
+        const int64_t nch = (p.L + MF_LIST - 1) / MF_LIST;
+        const unsigned grid = (unsigned)(p.B * nch);
+        int G = (int)p.d;
+        while (G < a->r_eff) G <<= 1;
+        mf_small_done = true;
+        switch (a->r_eff * 100 + G) {   // the (r_eff, d) pairs of a_max = 1..4
+#define SFDT_MFS(R, G_)                                                                          \
+    case R * 100 + G_: k_gen_mf_small<R, G_><<<grid, 256, 0, stream>>>(V, gp, votes, mf_top, nch); break;
+            SFDT_MFS(1, 1) SFDT_MFS(2, 2) SFDT_MFS(3, 4) SFDT_MFS(4, 4) SFDT_MFS(6, 8) SFDT_MFS(8, 8)
+            SFDT_MFS(9, 16) SFDT_MFS(12, 16) SFDT_MFS(9, 32) SFDT_MFS(12, 32)
+#undef SFDT_MFS
+        default: mf_small_done = false; break;   // no instance: the warp-per-bin form
+        }
+        if (mf_small_done) {
+            SFDT_CHECK_LAUNCH();
+            launches++;
+        }
+    }
+    if (a->prune && !mf_small_done) {
         const int64_t nch = (p.L + MF_LIST - 1) / MF_LIST;
         const size_t phi_bytes = size_t(a->r_eff) * p.d * 16;
         const int stage = phi_bytes <= MF_SMEM_MAX;

@@ -404,6 +404,30 @@ def test_general_closed_form_singular_values(monkeypatch):
         assert fast.spectrum(b).entries == jac.spectrum(b).entries
 
 
+@pytest.mark.parametrize("n,k,a_max", [(1 << 16, 256, 3), (1 << 16, 128, 3), (1 << 16, 64, 3),
+                                       (1 << 14, 64, 2), (1 << 14, 256, 4), (1 << 14, 512, 3)])
+def test_general_matched_filter_short_lists(n, k, a_max, monkeypatch):
+    """d <= 32: the group-per-bin matched filter (k_gen_mf_small) chooses the
+    same columns as the warp-per-bin kernel -- supports and values equal
+    bitwise -- and matches the oracle."""
+    B = 2
+    seeds = [(41, b) for b in range(B)]
+    X = np.stack([general_signal(n, k, 25.0, s)[0] for s in seeds])
+    cfg = P.GeneralConfig(n=n, k=k, a_max=a_max)
+    assert cfg.resolved_d() <= 32
+    got = P.solve_general_batch(X, cfg, seeds=seeds)
+    monkeypatch.setenv("SFDT_GEN_MF_SMALL", "0")
+    ref = P.solve_general_batch(X, cfg, seeds=seeds)
+    for b in range(B):
+        g, r = got.spectrum(b).entries, ref.spectrum(b).entries
+        assert list(g) == list(r)
+        assert np.array_equal(np.fromiter(g.values(), complex), np.fromiter(r.values(), complex))
+    want, _ = OS.general(X[0], k, a_max=a_max, rng_seed=seeds[0])
+    locs = np.fromiter(want.keys(), dtype=np.int64, count=len(want))
+    vals = np.fromiter(want.values(), dtype=np.complex128, count=len(want))
+    _general_check(got.spectrum(0).entries, locs, vals, "b=0")
+
+
 @pytest.mark.parametrize("n,k", [(1 << 16, 256), (1 << 18, 1024)])
 def test_general_duplicate_views_shared(n, k, monkeypatch):
     """d = 8 (r_eff = d): every residue is drawn, so 6 of the 9 random shifts

@@ -453,22 +453,34 @@ struct VSel {
     unsigned long long prefix, mask;
     long long remaining;
     double thr;
+    unsigned long long nc;   // keys sharing the 16-bit prefix (k_vsel_compact)
+    long long neq;           // keys equal to the threshold (k_vsel_select), -1 unknown
 };
+
+// keys per signal that k_vsel_compact can hold; beyond it k_vsel_select
+// scans every key of the signal (same result, slower)
+constexpr int64_t VSEL_CAND = 65536;
 
 // per signal: state, zero-vote threshold (rms of the consecutive syndromes),
 // stats fields the later passes accumulate into
+// one warp per signal (lane-strided partial sums, then a butterfly)
 __global__ void k_vsel_init(const double *__restrict__ partial, int nparts, GenParams p, int64_t B,
                             VSel *__restrict__ vs, int64_t *__restrict__ stats) {
-    const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (b >= B) return;
+    const int64_t b = blockIdx.x;
+    const int lane = threadIdx.x;
     const int64_t M = p.L * p.a_max;
-    double esum = 0.0;   // same summation order as k_gen_vote
-    for (int i = 0; i < nparts; i++) esum += partial[b * nparts + i];
+    double esum = 0.0;
+    for (int i = lane; i < nparts; i += 32) esum += partial[b * nparts + i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) esum += __shfl_xor_sync(0xffffffffu, esum, o);
+    if (lane != 0) return;
     const double rms_syn = sqrt(esum / (double)(p.L * p.S));
     vs[b].prefix = 0;
     vs[b].mask = 0;
     vs[b].remaining = p.k < M ? p.k : M;
     vs[b].thr = p.zvr * rms_syn;
+    vs[b].nc = 0;
+    vs[b].neq = -1;
     int64_t *st = stats + b * SFDT_GS_PER_SIGNAL;
     for (int a = 0; a <= 4; a++) st[SFDT_GS_HIST0 + a] = 0;
     st[SFDT_GS_NVOTED] = 0;
@@ -540,10 +552,123 @@ __global__ void k_vsel_pick(int64_t B, int shift, VSel *__restrict__ vs, unsigne
     }
 }
 
+// after the two leading 8-bit passes: the keys sharing the chosen 16-bit
+// prefix are appended to the signal's candidate list
+__global__ void __launch_bounds__(256) k_vsel_compact(const double *__restrict__ sv, GenParams p, int64_t nch,
+                                                      VSel *__restrict__ vs,
+                                                      unsigned long long *__restrict__ cand) {
+    const int64_t b = blockIdx.x / nch, ch = blockIdx.x - b * nch;
+    const int64_t M = p.L * p.a_max;
+    if (vs[b].remaining <= 0) return;
+    const unsigned long long pre = vs[b].prefix, msk = vs[b].mask;
+    const int64_t i1 = (ch + 1) * VCH < M ? (ch + 1) * VCH : M;
+    const double *svb = sv + b * M;
+    const int lane = threadIdx.x & 31;
+    for (int64_t i0 = ch * VCH; i0 < i1; i0 += blockDim.x) {   // block-uniform trip count
+        const int64_t i = i0 + threadIdx.x;
+        unsigned long long key = 0;
+        bool m = false;
+        if (i < i1) {
+            key = dkey(svb[i]);
+            m = (key & msk) == pre;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, m);
+        unsigned long long base = 0;
+        if (lane == 0 && bal) base = atomicAdd(&vs[b].nc, (unsigned long long)__popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        const unsigned long long slot = base + __popc(bal & ((1u << lane) - 1));
+        if (m && slot < (unsigned long long)VSEL_CAND) cand[b * VSEL_CAND + slot] = key;
+    }
+}
+
+// the remaining six 8-bit passes of the radix select, one CTA per signal,
+// over the compacted candidates (or every key when they overflowed)
+__global__ void __launch_bounds__(1024) k_vsel_select(const double *__restrict__ sv, GenParams p,
+                                                      VSel *__restrict__ vs,
+                                                      const unsigned long long *__restrict__ cand) {
+    const int64_t b = blockIdx.x;
+    const int64_t M = p.L * p.a_max;
+    __shared__ unsigned int hist[256];
+    __shared__ unsigned long long s_prefix, s_mask;
+    __shared__ long long s_remaining, s_neq;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        s_neq = -1;
+        s_prefix = vs[b].prefix;
+        s_mask = vs[b].mask;
+        s_remaining = vs[b].remaining;
+    }
+    __syncthreads();
+    if (s_remaining <= 0) return;
+    const unsigned long long nc = vs[b].nc;
+    const bool use_cand = nc <= (unsigned long long)VSEL_CAND;
+    const int64_t n = use_cand ? (int64_t)nc : M;
+    const unsigned long long *cb = cand + b * VSEL_CAND;
+    const double *svb = sv + b * M;
+    for (int shift = 40; shift >= 0; shift -= 8) {
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+        __syncthreads();
+        const unsigned long long pre = s_prefix, msk = s_mask;
+        for (int64_t i0 = 0; i0 < n; i0 += blockDim.x) {   // block-uniform trip count
+            const int64_t i = i0 + threadIdx.x;
+            int dg = 256;
+            if (i < n) {
+                const unsigned long long key = use_cand ? cb[i] : dkey(svb[i]);
+                if ((key & msk) == pre) dg = (int)((key >> shift) & 255);
+            }
+            const unsigned peers = __match_any_sync(0xffffffffu, dg);
+            if (dg < 256 && lane == __ffs(peers) - 1) atomicAdd(&hist[dg], (unsigned)__popc(peers));
+        }
+        __syncthreads();
+        if (warp == 0) {   // digit choice, as k_vsel_pick
+            unsigned c[8], lsum = 0;
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                c[q] = hist[255 - 8 * lane - q];
+                lsum += c[q];
+            }
+            unsigned inc = lsum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            const long long rem = s_remaining;
+            const long long before = (long long)(inc - lsum);
+            if (before < rem && before + (long long)lsum >= rem) {
+                long long cum = before;
+                int D = 255 - 8 * lane - 7;
+                unsigned cD = c[7];
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    if (cum + (long long)c[q] >= rem) {
+                        D = 255 - 8 * lane - q;
+                        cD = c[q];
+                        break;
+                    }
+                    cum += c[q];
+                }
+                s_remaining = rem - cum;
+                s_prefix = pre | ((unsigned long long)D << shift);
+                s_mask = msk | (0xFFull << shift);
+                if (shift == 0) s_neq = cD;   // keys equal to the threshold
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        vs[b].prefix = s_prefix;
+        vs[b].mask = s_mask;
+        vs[b].remaining = s_remaining;
+        vs[b].neq = s_neq;
+    }
+}
+
 __global__ void __launch_bounds__(256) k_vsel_eqcount(const double *__restrict__ sv, GenParams p, int64_t nch,
                                                       const VSel *__restrict__ vs, long long *__restrict__ eqc) {
     const int64_t b = blockIdx.x / nch, ch = blockIdx.x - b * nch;
     const int64_t M = p.L * p.a_max;
+    if (vs[b].neq >= 0 && vs[b].remaining == vs[b].neq) return;   // every tie taken: no ranks needed
     const unsigned long long tau = vs[b].prefix;
     const int64_t i1 = (ch + 1) * VCH < M ? (ch + 1) * VCH : M;
     const double *svb = sv + b * M;
@@ -569,15 +694,19 @@ __global__ void __launch_bounds__(256) k_vsel_vote(const double *__restrict__ sv
     if (take <= 0) return;
     const unsigned long long tau = vs[b].prefix;
     const long long need_eq = vs[b].remaining;
-    long long eq_carry = 0, eq_all = 0;   // keys == tau in the chunks before this one / in all
-    for (int64_t c2 = 0; c2 < nch; c2++) {
-        const long long e = eqc[b * nch + c2];
-        eq_carry += c2 < ch ? e : 0;
-        eq_all += e;
-    }
     const int64_t i1 = (ch + 1) * VCH < M ? (ch + 1) * VCH : M;
     const double *svb = sv + b * M;
     int32_t *vb = votes + b * p.L;
+    const long long neq = vs[b].neq;
+    long long eq_carry = 0, eq_all = neq;   // keys == tau in the chunks before this one / in all
+    if (!(neq >= 0 && need_eq == neq)) {
+        eq_all = 0;
+        for (int64_t c2 = 0; c2 < nch; c2++) {
+            const long long e = eqc[b * nch + c2];
+            eq_carry += c2 < ch ? e : 0;
+            eq_all += e;
+        }
+    }
     if (need_eq == eq_all) {   // every key == tau is taken: no tie ranks needed
         for (int64_t i = ch * VCH + threadIdx.x; i < i1; i += blockDim.x)
             if (dkey(svb[i]) >= tau) atomicAdd(&vb[i / p.a_max], 1);
@@ -1765,7 +1894,7 @@ struct GenPlan {
     int64_t B, n, d, L, nv, nparts;
     int S;
     size_t off_V, off_sv, off_part, off_votes, off_nent, off_sloc, off_sval, off_wl, off_cnt,
-        off_fft, off_mf, off_cols, off_ncols, off_hl, off_vsh, off_vslot, off_nview, off_fix, off_seg, off_vsel, off_ghist, off_eqc, total;
+        off_fft, off_mf, off_cols, off_ncols, off_hl, off_vsh, off_vslot, off_nview, off_fix, off_cand, off_seg, off_vsel, off_ghist, off_eqc, total;
 };
 
 static int make_gen_plan(const sfdt_general_args *a, GenPlan &p) {
@@ -1805,6 +1934,7 @@ static int make_gen_plan(const sfdt_general_args *a, GenPlan &p) {
     p.off_seg = take(size_t(p.B) * ((p.L + GEN_SEG - 1) / GEN_SEG) * 4 * 8);
     p.off_vsel = take(size_t(p.B) * sizeof(VSel));
     p.off_ghist = take(size_t(p.B) * 256 * 4);
+    p.off_cand = (p.L * a->a_max > VOTE_BIG) ? take(size_t(p.B) * VSEL_CAND * 8) : 0;
     p.off_eqc = take(size_t(p.B) * ((p.L * a->a_max + VCH - 1) / VCH) * 8);
     p.off_vsh = take(size_t(p.B) * a->r_eff * 8);
     p.off_vslot = take(size_t(p.B) * a->r_eff * 4);
@@ -1931,15 +2061,20 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
         long long *eqc = (long long *)(w + p.off_eqc);
         cudaMemsetAsync(ghist, 0, size_t(p.B) * 256 * 4, stream);
         cudaMemsetAsync(votes, 0, size_t(p.B) * p.L * 4, stream);
-        k_vsel_init<<<(unsigned)((p.B + 127) / 128), 128, 0, stream>>>(part, (int)p.nparts, gp, p.B, vs, a->stats);
-        for (int shift = 56; shift >= 0; shift -= 8) {
+        k_vsel_init<<<(unsigned)p.B, 32, 0, stream>>>(part, (int)p.nparts, gp, p.B, vs, a->stats);
+        // two full 8-bit passes, then the candidates sharing the 16-bit
+        // prefix are compacted and one CTA per signal finishes the select
+        for (int shift = 56; shift >= 48; shift -= 8) {
             k_vsel_hist<<<(unsigned)(p.B * nch), 256, 0, stream>>>(sv, gp, nch, shift, vs, ghist);
             k_vsel_pick<<<(unsigned)p.B, 32, 0, stream>>>(p.B, shift, vs, ghist);
         }
+        unsigned long long *cand = (unsigned long long *)(w + p.off_cand);
+        k_vsel_compact<<<(unsigned)(p.B * nch), 256, 0, stream>>>(sv, gp, nch, vs, cand);
+        k_vsel_select<<<(unsigned)p.B, 1024, 0, stream>>>(sv, gp, vs, cand);
         k_vsel_eqcount<<<(unsigned)(p.B * nch), 256, 0, stream>>>(sv, gp, nch, vs, eqc);
         k_vsel_vote<<<(unsigned)(p.B * nch), 256, 0, stream>>>(sv, gp, nch, vs, eqc, votes);
         k_vsel_fin<<<(unsigned)(p.B * nchL), 256, 0, stream>>>(sv, gp, nchL, vs, votes, a->stats, wl, wlc);
-        launches += 1 + 16 + 3 - 1;   // the -1: k_gen_vote is counted below
+        launches += 1 + 4 + 2 + 3 - 1;   // the -1: k_gen_vote is counted below
     } else {
         const int64_t M = p.L * a->a_max;
         const size_t smem = M <= VOTE_SMEM_KEYS ? size_t(M) * 8 : 0;

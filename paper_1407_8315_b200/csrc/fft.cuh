@@ -239,6 +239,7 @@ static __global__ void __launch_bounds__(256, MINB) k_fft_views(const ViewSrc sr
     extern __shared__ double4 smem_raw[];
     cx *a = reinterpret_cast<cx *>(smem_raw);
     __shared__ int64_t s_ibase[MAX_VIEWS], s_ioff[MAX_VIEWS], s_obase[MAX_VIEWS], s_sig[MAX_VIEWS];
+    __shared__ double s_th[MAX_VIEWS], s_th2hi[MAX_VIEWS], s_th2lo[MAX_VIEWS];
     const int L = 1 << logL, vpc = 1 << logvpc;
     const int64_t nviews = B * src.nshift;
     const int64_t g0 = int64_t(blockIdx.x) << logvpc;
@@ -266,6 +267,12 @@ static __global__ void __launch_bounds__(256, MINB) k_fft_views(const ViewSrc sr
                                                   : src.off[s];
         s_obase[threadIdx.x] = (b * SV + s) * ldV;
         s_sig[threadIdx.x] = b;
+        if (act) {   // per-view activity bounds, once per CTA
+            const double th = thr[b];
+            s_th[threadIdx.x] = th;
+            s_th2hi[threadIdx.x] = th * th * (1.0 + 1e-6);
+            s_th2lo[threadIdx.x] = th * th * (1.0 - 1e-6);
+        }
     }
     __syncthreads();
     const double sc = 1.0 / (double)L;   // exact power of two
@@ -276,9 +283,8 @@ static __global__ void __launch_bounds__(256, MINB) k_fft_views(const ViewSrc sr
         if (scale) y = mk(DMUL(y.re, sc), DMUL(y.im, sc));
         stcx(out + s_obase[v] + k, y);
         if (act) {
-            const double th = thr[s_sig[v]];
             const double q = y.re * y.re + y.im * y.im;
-            if (q > th * th * (1.0 + 1e-6) || (q >= th * th * (1.0 - 1e-6) && cabs_(y) > th))
+            if (q > s_th2hi[v] || (q >= s_th2lo[v] && cabs_(y) > s_th[v]))
                 act[s_sig[v] * (int64_t)L + k] = 1;
         }
     };

@@ -1018,6 +1018,12 @@ struct Top4 {
     int id[4];
 };
 
+// acc + conj(ph) * w with four FMAs (the matched-filter inner product; the
+// reference's BLAS zgemm does not fix the rounding either)
+__device__ __forceinline__ cx cjmac(cx acc, cx ph, cx w) {
+    return mk(fma(ph.re, w.re, fma(ph.im, w.im, acc.re)), fma(ph.re, w.im, fma(-ph.im, w.re, acc.im)));
+}
+
 __device__ __forceinline__ bool mf_better(double v, int t, double w, int u) {
     return v > w || (v == w && t < u);
 }
@@ -1094,7 +1100,7 @@ __global__ void __launch_bounds__(256, 2) k_gen_mf(const cx *__restrict__ V, Gen
 #pragma unroll
                 for (int j = 0; j < R; j++) {
                     const cx ph = phi_at(j * d + tt);
-                    acc = cadd(acc, nmul(cconj(ph), w[j]));
+                    acc = cjmac(acc, ph, w[j]);
                 }
                 return acc;
             };
@@ -1134,7 +1140,7 @@ __global__ void __launch_bounds__(256, 2) k_gen_mf(const cx *__restrict__ V, Gen
                                 const int tt = tb + 32 * u;
                                 const int tc = tt < d ? tt : tb;
                                 const cx ph = phi_at(j * d + tc);
-                                acc[u] = cadd(acc[u], nmul(cconj(ph), w[j]));
+                                acc[u] = cjmac(acc[u], ph, w[j]);
                             }
                         }
                     }
@@ -1296,7 +1302,7 @@ __global__ void __launch_bounds__(256) k_gen_mf_small(const cx *__restrict__ V, 
             for (int j = 0; j < R; j++) {
                 const cx w = mk(__shfl_sync(0xffffffffu, wj.re, j, G), __shfl_sync(0xffffffffu, wj.im, j, G));
                 const cx ph = gl < d ? ldcx(gphi + (int64_t)j * d + gl) : mk(0.0, 0.0);
-                acc = cadd(acc, nmul(cconj(ph), w));
+                acc = cjmac(acc, ph, w);
             }
             double v = -INFINITY;
             if (valid && gl < d) {

@@ -386,6 +386,23 @@ def test_general_batch_vs_oracle_cfg4_shape():
         assert tr.collision_histogram == wtr["collision_histogram"]
 
 
+def test_general_cfg5_k16384_full_shape():
+    """Config-5 general at its largest K (N=2^22, K=2^14, 30 dB: d=8,
+    L=2^19, r_eff=8): shared views, large-view FFT, compacted long-view
+    vote, short-list matched filter, closed-form singular values -- one
+    signal of a 2-signal batch against the oracle (about 15 s of CPU)."""
+    n, k, B = 1 << 22, 1 << 14, 2
+    seeds = [(53, b) for b in range(B)]
+    X = np.stack([general_signal(n, k, 30.0, s)[0] for s in seeds])
+    cfg = P.GeneralConfig(n=n, k=k)
+    res = P.solve_general_batch(X, cfg, seeds=seeds)
+    want, wtr = OS.general(X[1], k, rng_seed=seeds[1], return_internals=True)
+    assert np.array_equal(res.votes()[1], wtr["votes"])
+    locs = np.fromiter(want.keys(), dtype=np.int64, count=len(want))
+    vals = np.fromiter(want.values(), dtype=np.complex128, count=len(want))
+    _general_check(res.spectrum(1).entries, locs, vals, "cfg5 K=2^14")
+
+
 def test_general_closed_form_singular_values(monkeypatch):
     """a_max = 3: the closed-form singular values (bins with lambda_3 >=
     lambda_1 / 64, |r| <= 0.999) agree with the Jacobi for every bin to

@@ -510,9 +510,18 @@ static inline void launch_large_b_reg(cx *buf, int64_t nviews, int logL, int s0,
 }
 
 // kernel launches of one launch_fft_views call
+// stages of the large-view pass A (blocks of 2^logP points in shared memory)
+static inline int large_logp(int logL) {
+    const char *e = getenv("SFDT_FFT_LOGP");
+    int lp = e ? atoi(e) : 12;
+    if (lp < 8) lp = 8;
+    if (lp > 13) lp = 13;
+    return lp < logL ? lp : logL - 1;
+}
+
 static inline int fft_view_launches(int64_t L) {
     if (L <= FFT_SMEM_MAX) return 1;
-    const int rest = ilog2_64(L) - 12;
+    const int rest = ilog2_64(L) - large_logp(ilog2_64(L));
     if (rest == 5) {
         const char *ebs = getenv("SFDT_FFT_BSMEM");
         if (!(ebs && ebs[0] == '0')) return 2;
@@ -571,14 +580,16 @@ static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, con
         return SFDT_OK;
     }
     if (!large_scratch) return SFDT_EINVAL;
-    const int logP = 12, P = 1 << logP;
+    const int logP = large_logp(logL), P = 1 << logP;
     const int logQ = logL - logP;
     {
         const size_t smem = size_t(P) * 16;
         cudaFuncSetAttribute(k_fft_large_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        // 2 CTAs/SM, the rest L1 for the 4095-entry twiddle table (as above)
+        // 2 CTAs/SM at 4096 points (4 at 2048), the rest L1 for the
+        // (P-1)-entry twiddle table (as above)
+        const int ctas = logP >= 12 ? 2 : 4;
         cudaFuncSetAttribute(k_fft_large_a, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             (int)((2 * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024)));
+                             (int)((ctas * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024)));
         k_fft_large_a<<<(unsigned)(nviews << logQ), 256, smem, stream>>>(src, logL, logP, tw, large_scratch);
         SFDT_CHECK_LAUNCH();
     }

@@ -1394,7 +1394,7 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
             default: rc = launch_decode_noniter<8>(Vc, nb, p.L, a->a_max, p.n, thr + c0, stc, blc, bvc, wl + c0 * p.L, wlc + c, aux, actc, awlc_p, wlc + 64 + c); break;
             }
             if (rc) return rc;
-            launches += 1 + fft_view_launches(p.L) + 1 + (a->a_max > 1 ? 1 : 0) + (dense ? 1 : 0);
+            launches += 1 + fft_view_launches(p.L, (int)p.S) + 1 + (a->a_max > 1 ? 1 : 0) + (dense ? 1 : 0);
         }
         if (aux != stream) {
             if (cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming) != cudaSuccess) return SFDT_ECUDA;
@@ -1516,7 +1516,7 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
                                                         a->locs, (cx *)a->vals, a->unres_bins,
                                                         a->dup_locs);
     SFDT_CHECK_LAUNCH();
-    launches += (int)p.npass * (1 + 2 + fft_view_launches(p.L)) + 1 + 1 + 1 + 1;   // final, count, scan, emit
+    launches += (int)p.npass * (1 + 2 + fft_view_launches(p.L, 2)) + 1 + 1 + 1 + 1;   // final, count, scan, emit
     a->kernel_launches = launches;
     return SFDT_OK;
 }

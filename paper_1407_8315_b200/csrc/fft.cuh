@@ -362,6 +362,44 @@ static __global__ void k_fft_large_a(const ViewSrc src, int logL, int logP,
                     [&](int, int k, cx y) { dst[k] = y; });
 }
 
+// Pass A for groups of up to 8 views of one signal (views with adjacent
+// shifts: a d-block's 8 samples are one 128-B line, loaded whole by 8
+// adjacent lanes): block c of each view in one CTA, 2^logP points per view,
+// the same fft_fused_views stages as k_fft_large_a, so the same bits.
+static __global__ void __launch_bounds__(512) k_fft_large_a8(const ViewSrc src, int logL, int logP,
+                                                            const cx *__restrict__ tw, cx *scratch) {
+    extern __shared__ double4 smem_raw[];
+    cx *a = reinterpret_cast<cx *>(smem_raw);
+    const int logQ = logL - logP, Q = 1 << logQ;
+    const int ngrp = (src.nshift + 7) >> 3;
+    const int vg = (int)(blockIdx.x % (unsigned)ngrp);
+    const int64_t rest = blockIdx.x / (unsigned)ngrp;
+    const int c = (int)(rest & (Q - 1));
+    const int64_t b = rest >> logQ;
+    const int v0 = vg * 8;
+    int nv = src.nshift - v0 < 8 ? src.nshift - v0 : 8;
+    if (src.nview) {
+        const int nb = __ldg(src.nview + b) - v0;
+        nv = nb < nv ? nb : nv;
+    }
+    if (nv <= 0) return;   // CTA-uniform
+    const int rc = logQ ? (int)(__brev((unsigned)c) >> (32 - logQ)) : 0;
+    __shared__ int64_t s_ib[8], s_io[8];
+    if (threadIdx.x < 8) {
+        const int s = v0 + (int)threadIdx.x;
+        int64_t o = 0;
+        if ((int)threadIdx.x < nv)
+            o = (s >= src.dyn_first) ? src.dyn_off[b * src.dyn_stride + (s - src.dyn_first)] : src.off[s];
+        s_ib[threadIdx.x] = b * src.sig_stride;
+        s_io[threadIdx.x] = o + (int64_t)rc * src.jstride;
+    }
+    __syncthreads();
+    const int64_t gb = b * src.nshift + v0;
+    fft_fused_views(a, src, src.jstride << logQ, s_ib, s_io, nv, 3, logP, tw, [&](int v, int k, cx y) {
+        scratch[((gb + v) << logL) + ((int64_t)c << logP) + k] = y;
+    });
+}
+
 // large views (L > FFT_SMEM_MAX): stage split through global memory.
 // Pass A (above) runs the first logP stages on contiguous blocks of P
 // points in shared memory; the remaining stages act independently on the
@@ -443,7 +481,7 @@ static __global__ void __launch_bounds__(256) k_fft_large_b_reg(cx *buf, int64_t
 // result is bit-identical to two register passes, with one pass over the
 // scratch instead of two.  Writes the views (scaled, activity epilogue).
 constexpr int LB_RES = 32;
-static __global__ void __launch_bounds__(256) k_fft_large_b_smem(const cx *__restrict__ buf, int64_t nviews,
+static __global__ void __launch_bounds__(256) k_fft_large_b_smem(const cx *buf, int64_t nviews,
                                                                  int logL, int s0, int LQ,
                                                                  const cx *__restrict__ tw, cx *out,
                                                                  int nshift, int SV, int64_t ldV, int scale,
@@ -455,13 +493,19 @@ static __global__ void __launch_bounds__(256) k_fft_large_b_smem(const cx *__res
     const int64_t P = int64_t(1) << s0;
     const int Q = 1 << LQ;
     const int64_t groups = P / LB_RES;
-    const int64_t g = blockIdx.x / groups;
-    const int64_t r0 = (blockIdx.x - g * groups) * LB_RES;
+    // an intermediate pass (s0 + LQ < logL) works on 2^(logL - s0 - LQ)
+    // independent blocks of 2^(s0 + LQ) elements (index bits above the
+    // pass's stages: hi)
+    const int64_t nhi = int64_t(1) << (logL - s0 - LQ);
+    const int64_t g = blockIdx.x / (groups * nhi);
+    const int64_t rem = blockIdx.x - g * (groups * nhi);
+    const int64_t hi = rem / groups;
+    const int64_t r0 = (rem - hi * groups) * LB_RES;
     if (g >= nviews) return;
     const int64_t b = g / nshift;
     const int s = (int)(g - b * nshift);
     if (nview && s >= __ldg(nview + b)) return;   // unused view
-    const cx *src = buf + (g << logL) + r0;
+    const cx *src = buf + (g << logL) + (hi << (s0 + LQ)) + r0;
     for (int e = threadIdx.x; e < Q * LB_RES; e += blockDim.x) {
         const int q = e / LB_RES, rl = e - q * LB_RES;
         tile[e] = ldcx(src + (int64_t)q * P + rl);
@@ -482,6 +526,14 @@ static __global__ void __launch_bounds__(256) k_fft_large_b_smem(const cx *__res
             tile[(q + hq) * LB_RES + rl] = csub(u, t);
         }
         __syncthreads();
+    }
+    if (out == nullptr) {   // intermediate pass: back in place
+        cx *dst = const_cast<cx *>(src);
+        for (int e = threadIdx.x; e < Q * LB_RES; e += blockDim.x) {
+            const int q = e / LB_RES, rl = e - q * LB_RES;
+            stcx(dst + (int64_t)q * P + rl, tile[e]);
+        }
+        return;
     }
     const double sc = 1.0 / (double)(int64_t(1) << logL);
     const double th = act ? thr[b] : 0.0;
@@ -519,14 +571,43 @@ static inline int large_logp(int logL) {
     return lp < logL ? lp : logL - 1;
 }
 
-static inline int fft_view_launches(int64_t L) {
-    if (L <= FFT_SMEM_MAX) return 1;
-    const int rest = ilog2_64(L) - large_logp(ilog2_64(L));
-    if (rest == 5) {
-        const char *ebs = getenv("SFDT_FFT_BSMEM");
-        if (!(ebs && ebs[0] == '0')) return 2;
+// Large-view plan: pass A one view per CTA (k_fft_large_a, 2^large_logp
+// blocks), or -- experiment -- groups of 8 views (k_fft_large_a8, 1024-point
+// blocks); then pass B: five stages in shared memory where that pays,
+// register passes of <= 4 stages otherwise.
+// (off by default: measured slower -- config 5 general K=2^14 view FFT
+// 6.53 -> 7.58 ms, exact K=2^14 1.75 -> 1.96 ms per batch -- the 128-KiB
+// CTA leaves one CTA per SM; SFDT_FFT_A8=1 enables it)
+static inline bool large_a8(int nshift) {
+    const char *e = getenv("SFDT_FFT_A8");
+    return nshift >= 8 && e && e[0] == '1';
+}
+static inline bool large_bsmem_ok() {
+    const char *e = getenv("SFDT_FFT_BSMEM");
+    return !(e && e[0] == '0');
+}
+// stages of the next pass B from s0 (0 = done); *smem = shared-memory pass
+static inline int large_next(int logL, int s0, bool a8, bool *smem) {
+    const int rem = logL - s0;
+    *smem = false;
+    if (rem <= 0) return 0;
+    // (measured per config-5 batch: the single smem pass at L = 2^17 2.83 ->
+    // 2.62 ms; 64-KiB (7-stage) tiles slower than 4 + 3 register passes)
+    if (large_bsmem_ok() && (rem == 5 || (a8 && rem > 5 && rem <= 9))) {
+        *smem = true;
+        return 5;
     }
-    return 1 + (rest + 3) / 4;
+    return rem >= 4 ? 4 : rem;
+}
+
+static inline int fft_view_launches(int64_t L, int nshift = 0) {
+    if (L <= FFT_SMEM_MAX) return 1;
+    const int logL = ilog2_64(L);
+    const bool a8 = large_a8(nshift);
+    int s0 = a8 ? 10 : large_logp(logL), n = 1;
+    bool sm;
+    for (int k; (k = large_next(logL, s0, a8, &sm)) > 0; s0 += k) n++;
+    return n;
 }
 
 static inline int fft_points_per_cta() {
@@ -580,9 +661,19 @@ static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, con
         return SFDT_OK;
     }
     if (!large_scratch) return SFDT_EINVAL;
-    const int logP = large_logp(logL), P = 1 << logP;
+    const bool a8 = large_a8(src.nshift);
+    const int logP = a8 ? 10 : large_logp(logL), P = 1 << logP;
     const int logQ = logL - logP;
-    {
+    if (a8) {
+        const size_t smem = size_t(8) * P * 16;   // 128 KiB: one CTA of 512 threads per SM
+        cudaFuncSetAttribute(k_fft_large_a8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_fft_large_a8, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             (int)(((smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024)));
+        const int64_t B = nviews / src.nshift;
+        const int64_t ngrp = (src.nshift + 7) / 8;
+        k_fft_large_a8<<<(unsigned)(B * ngrp << logQ), 512, smem, stream>>>(src, logL, logP, tw, large_scratch);
+        SFDT_CHECK_LAUNCH();
+    } else {
         const size_t smem = size_t(P) * 16;
         cudaFuncSetAttribute(k_fft_large_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         // 2 CTAs/SM at 4096 points (4 at 2048), the rest L1 for the
@@ -593,36 +684,27 @@ static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, con
         k_fft_large_a<<<(unsigned)(nviews << logQ), 256, smem, stream>>>(src, logL, logP, tw, large_scratch);
         SFDT_CHECK_LAUNCH();
     }
-    // remaining stages logP .. logL-1: 5..7 of them in one shared-memory
-    // pass, otherwise register passes of <= 4 stages (the last one writes
-    // the views)
-    const char *ebs = getenv("SFDT_FFT_BSMEM");
-    // (measured per config-5 batch: L = 2^17 2.83 -> 2.62 ms; L = 2^18
-    // neutral, 4.75 vs 4.81; L = 2^19 slower with 64-KiB tiles, 6.53 -> 7.38)
-    if (logL - logP == 5 && !(ebs && ebs[0] == '0')) {
-        const int LQ = logL - logP;
-        const size_t smem = (size_t(1) << LQ) * LB_RES * 16;
-        cudaFuncSetAttribute(k_fft_large_b_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        const int64_t ctas = nviews * ((int64_t(1) << logP) / LB_RES);
-        k_fft_large_b_smem<<<(unsigned)ctas, 256, smem, stream>>>(large_scratch, nviews, logL, logP, LQ, tw, out,
-                                                                  src.nshift, SV, ldV, scale, thr, act,
-                                                                  src.nview);
-        SFDT_CHECK_LAUNCH();
-        return SFDT_OK;
-    }
-    for (int s0 = logP; s0 < logL;) {
-        const int rem = logL - s0;
-        const int lq = rem >= 4 ? 4 : rem;
+    // remaining stages logP .. logL-1 (the last pass writes the views)
+    bool sm;
+    for (int s0 = logP, lq; (lq = large_next(logL, s0, a8, &sm)) > 0; s0 += lq) {
         const bool last = s0 + lq == logL;
         cx *o = last ? out : nullptr;
-        switch (lq) {
-        case 1: launch_large_b_reg<1>(large_scratch, nviews, logL, s0, tw, o, src.nshift, SV, ldV, scale, thr, act, stream, src.nview); break;
-        case 2: launch_large_b_reg<2>(large_scratch, nviews, logL, s0, tw, o, src.nshift, SV, ldV, scale, thr, act, stream, src.nview); break;
-        case 3: launch_large_b_reg<3>(large_scratch, nviews, logL, s0, tw, o, src.nshift, SV, ldV, scale, thr, act, stream, src.nview); break;
-        default: launch_large_b_reg<4>(large_scratch, nviews, logL, s0, tw, o, src.nshift, SV, ldV, scale, thr, act, stream, src.nview); break;
+        if (sm) {
+            const size_t smem = (size_t(1) << lq) * LB_RES * 16;
+            cudaFuncSetAttribute(k_fft_large_b_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            const int64_t ctas = nviews * ((int64_t(1) << s0) / LB_RES) * (int64_t(1) << (logL - s0 - lq));
+            k_fft_large_b_smem<<<(unsigned)ctas, 256, smem, stream>>>(large_scratch, nviews, logL, s0, lq, tw, o,
+                                                                      src.nshift, SV, ldV, scale, thr, act,
+                                                                      src.nview);
+        } else {
+            switch (lq) {
+            case 1: launch_large_b_reg<1>(large_scratch, nviews, logL, s0, tw, o, src.nshift, SV, ldV, scale, thr, act, stream, src.nview); break;
+            case 2: launch_large_b_reg<2>(large_scratch, nviews, logL, s0, tw, o, src.nshift, SV, ldV, scale, thr, act, stream, src.nview); break;
+            case 3: launch_large_b_reg<3>(large_scratch, nviews, logL, s0, tw, o, src.nshift, SV, ldV, scale, thr, act, stream, src.nview); break;
+            default: launch_large_b_reg<4>(large_scratch, nviews, logL, s0, tw, o, src.nshift, SV, ldV, scale, thr, act, stream, src.nview); break;
+            }
         }
         SFDT_CHECK_LAUNCH();
-        s0 += lq;
     }
     return SFDT_OK;
 }

@@ -386,6 +386,31 @@ def test_general_batch_vs_oracle_cfg4_shape():
         assert tr.collision_histogram == wtr["collision_histogram"]
 
 
+@pytest.mark.parametrize("kind", ["exact", "general"])
+def test_large_view_pass_a8_bitwise(kind, monkeypatch):
+    """Large views transformed 8 per CTA (SFDT_FFT_A8=1: k_fft_large_a8 + the
+    intermediate shared-memory pass B) give the same bits as the default one
+    view per CTA."""
+    B = 2
+    if kind == "exact":
+        n, k = 1 << 20, 16384          # L = 2^16
+        X = np.stack([exact_signal(n, k, 90 + b, "unit")[0] for b in range(B)])
+        run = lambda: P.exact_batch(X, P.ExactConfig(n=n, k=k), False)
+    else:
+        n, k = 1 << 18, 1024           # d = 8, L = 2^15
+        seeds = [(61, b) for b in range(B)]
+        X = np.stack([general_signal(n, k, 30.0, s_)[0] for s_ in seeds])
+        run = lambda: P.solve_general_batch(X, P.GeneralConfig(n=n, k=k), seeds=seeds)
+    monkeypatch.setenv("SFDT_FFT_A8", "1")
+    got = run()
+    monkeypatch.setenv("SFDT_FFT_A8", "0")
+    ref = run()
+    for b in range(B):
+        g, r = got.spectrum(b).entries, ref.spectrum(b).entries
+        assert list(g) == list(r)
+        assert np.array_equal(np.fromiter(g.values(), complex), np.fromiter(r.values(), complex))
+
+
 def test_general_cfg5_k16384_full_shape():
     """Config-5 general at its largest K (N=2^22, K=2^14, 30 dB: d=8,
     L=2^19, r_eff=8): shared views, large-view FFT, compacted long-view

@@ -17,6 +17,7 @@
 #pragma once
 
 #include "common.cuh"
+#include <cstdlib>
 
 namespace sfdt {
 
@@ -40,7 +41,27 @@ struct ViewSrc {
     // per-signal number of views to compute: views v >= nview[b] are skipped
     // (their slots are never read); nullptr = all nshift views
     const int32_t *nview;
+    // load hint of the gathered samples (SFDT_GATHER_HINT): 0 __ldg,
+    // 1 no L1 + L2 64-B prefetch, 2 no L1, 3 no L1 + L2 evict_first policy
+    int ldhint;
 };
+
+__device__ __forceinline__ cx ld_gather(const cx *p, int hint) {
+    double2 v;
+    if (hint == 1) {
+        asm volatile("ld.global.nc.L1::no_allocate.L2::64B.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    } else if (hint == 2) {
+        asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    } else if (hint == 3) {
+        uint64_t pol;
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                     : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    } else {
+        v = __ldg(reinterpret_cast<const double2 *>(p));
+    }
+    return mk(v.x, v.y);
+}
 
 __device__ __forceinline__ cx view_load(const ViewSrc &src, int64_t b, int v, int64_t j) {
     const int64_t o = (v >= src.dyn_first) ? __ldg(src.dyn_off + b * src.dyn_stride + (v - src.dyn_first))
@@ -50,7 +71,7 @@ __device__ __forceinline__ cx view_load(const ViewSrc &src, int64_t b, int v, in
         const float2 f = __ldg(reinterpret_cast<const float2 *>(src.x) + e);
         return mk((double)f.x, (double)f.y);
     }
-    return ldcx(reinterpret_cast<const cx *>(src.x) + e);
+    return ld_gather(reinterpret_cast<const cx *>(src.x) + e, src.ldhint);
 }
 
 // 16-byte-granular swizzle of the shared-memory FFT buffers: the low 3 bits
@@ -210,7 +231,7 @@ __device__ __forceinline__ void fft_fused_views(cx *a, const ViewSrc &src, int64
                 const float2 f = __ldg(reinterpret_cast<const float2 *>(src.x) + e);
                 x[q] = mk((double)f.x, (double)f.y);
             } else {
-                x[q] = ldcx(reinterpret_cast<const cx *>(src.x) + e);
+                x[q] = ld_gather(reinterpret_cast<const cx *>(src.x) + e, src.ldhint);
             }
         }
         group_stages<3>(x, 0, 1, tw);
@@ -312,7 +333,7 @@ static __global__ void __launch_bounds__(256, MINB) k_fft_views(const ViewSrc sr
                         const float2 f = __ldg(reinterpret_cast<const float2 *>(src.x) + e);
                         vals[u] = mk((double)f.x, (double)f.y);
                     } else {
-                        vals[u] = ldcx(reinterpret_cast<const cx *>(src.x) + e);
+                        vals[u] = ld_gather(reinterpret_cast<const cx *>(src.x) + e, src.ldhint);
                     }
                     const int r = logL ? (int)(__brev((unsigned)j) >> (32 - logL)) : 0;
                     dst[u] = swz(v * L + r);
@@ -724,6 +745,8 @@ static inline ViewSrc consecutive_views(const void *x, int is_c64, int64_t n, in
     s.dyn_stride = 0;
     s.jfast = 0;
     s.nview = nullptr;
+    const char *eh = getenv("SFDT_GATHER_HINT");
+    s.ldhint = eh ? atoi(eh) : 0;
     return s;
 }
 

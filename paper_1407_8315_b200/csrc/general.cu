@@ -17,6 +17,7 @@
 //   count/scan/emit  compact (loc, value) lists in dict insertion order
 //                (vote class a ascending, bin ascending, column ascending)
 #include <climits>
+#include <mutex>
 #include <cstdlib>
 #include <type_traits>
 
@@ -1969,6 +1970,30 @@ extern "C" size_t sfdt_general_workspace_bytes(const sfdt_general_args *a) {
     return p.total;
 }
 
+// Side stream of the heavy-bin pursuit (k_gen_bins): a one-wave kernel
+// whose time is the tail of a few long FP64 chains (4 % warps active), so
+// the single-collision pursuit (k_gen_sp1) runs beside it, not after it.
+// One non-blocking stream per device, created on first use outside a
+// capture; SFDT_GEN_OVERLAP=0 keeps both on the caller's stream.
+static cudaStream_t gen_side_stream(cudaStream_t main) {
+    const char *e = getenv("SFDT_GEN_OVERLAP");
+    if (e && e[0] == '0') return nullptr;
+    static std::mutex mu;
+    static cudaStream_t side[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!side[dev]) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(main, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+        if (cudaStreamCreateWithFlags(&side[dev], cudaStreamNonBlocking) != cudaSuccess) {
+            side[dev] = nullptr;
+            return nullptr;
+        }
+    }
+    return side[dev];
+}
+
 extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_bytes, sfdt_stream_t stream_) {
     GenPlan p;
     int rc = make_gen_plan(a, p);
@@ -2163,6 +2188,35 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     k_gen_prune<<<wl_grid(max_voted, 128, one_wave(k_gen_prune, 128)), 128, 0, stream>>>(
         V, gp, votes, wl, wlc, mf_top, colsb, ncolsb, sp1 | (warp_all ? 2 : 0), hl, hlc);
     SFDT_CHECK_LAUNCH();
+    // heavy bins (k_gen_bins) fork onto the side stream; the bins of the
+    // two pursuits are disjoint (k_gen_prune routes each to one list) and
+    // their shared counters are atomics
+    cudaStream_t side = gen_side_stream(stream);
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    if (side) {
+        if (cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess)
+            return SFDT_ECUDA;
+        cudaEventRecord(ev_fork, stream);
+        cudaStreamWaitEvent(side, ev_fork, 0);
+    }
+    cudaStream_t bstream = side ? side : stream;
+    {
+        // one wave; up to one heavy bin per warp (k_gen_bins)
+        switch (a->r_eff) {
+#define SFDT_BINS(R)                                                                                    \
+    case R:                                                                                             \
+        k_gen_bins<R><<<wl_grid(32 * max_voted, 128, one_wave(k_gen_bins<R>, 128)), 128, 0, bstream>>>( \
+            V, gp, votes, wl, hl, hlc, colsb, ncolsb, nent, sloc, sval, a->stats, wlc + 3);             \
+        break;
+            SFDT_BINS(6) SFDT_BINS(8) SFDT_BINS(9) SFDT_BINS(12)
+        default:
+            SFDT_BINS(0)
+#undef SFDT_BINS
+        }
+    }
+    SFDT_CHECK_LAUNCH();
+    launches++;
     if (sp1) {
         switch (a->r_eff) {
 #define SFDT_SP1(R)                                                                                     \
@@ -2183,22 +2237,12 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
         SFDT_CHECK_LAUNCH();
         launches++;
     }
-    {
-        // one wave; up to one heavy bin per warp (k_gen_bins)
-        switch (a->r_eff) {
-#define SFDT_BINS(R)                                                                                    \
-    case R:                                                                                             \
-        k_gen_bins<R><<<wl_grid(32 * max_voted, 128, one_wave(k_gen_bins<R>, 128)), 128, 0, stream>>>(  \
-            V, gp, votes, wl, hl, hlc, colsb, ncolsb, nent, sloc, sval, a->stats, wlc + 3);             \
-        break;
-            SFDT_BINS(6) SFDT_BINS(8) SFDT_BINS(9) SFDT_BINS(12)
-        default:
-            SFDT_BINS(0)
-#undef SFDT_BINS
-        }
+    if (side) {
+        cudaEventRecord(ev_join, side);
+        cudaStreamWaitEvent(stream, ev_join, 0);
+        cudaEventDestroy(ev_fork);   // released once the pending work completes
+        cudaEventDestroy(ev_join);
     }
-    SFDT_CHECK_LAUNCH();
-    launches++;
     const int64_t nseg = (p.L + GEN_SEG - 1) / GEN_SEG;
     long long *segcnt = (long long *)(w + p.off_seg);
     k_gen_count<<<(unsigned)(p.B * nseg), 256, 0, stream>>>(votes, nent, p.L, nseg, segcnt);

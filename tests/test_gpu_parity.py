@@ -495,6 +495,29 @@ def test_general_duplicate_views_shared(n, k, monkeypatch):
     _general_check(got.spectrum(0).entries, locs, vals, "b=0")
 
 
+def test_general_heavy_bins_side_stream(monkeypatch):
+    """The multi-collision pursuit (k_gen_bins) on its side stream beside
+    the single-collision pursuit (default) gives the same bits as both on
+    the caller's stream (SFDT_GEN_OVERLAP=0), at the config-4 shape (d=256,
+    20 dB), and matches the oracle (graph capture of the fork/join:
+    test_gpu_api.py::test_solve_graph_matches_batch)."""
+    n, k, B = 1 << 20, 128, 4
+    seeds = [(71, b) for b in range(B)]
+    X = np.stack([general_signal(n, k, 20.0, s)[0] for s in seeds])
+    cfg = P.GeneralConfig(n=n, k=k)
+    got = P.solve_general_batch(X, cfg, seeds=seeds)
+    monkeypatch.setenv("SFDT_GEN_OVERLAP", "0")
+    ref = P.solve_general_batch(X, cfg, seeds=seeds)
+    for b in range(B):
+        g, r = got.spectrum(b).entries, ref.spectrum(b).entries
+        assert list(g) == list(r)
+        assert np.array_equal(np.fromiter(g.values(), complex), np.fromiter(r.values(), complex))
+    want, _ = OS.general(X[2], k, rng_seed=seeds[2])
+    locs = np.fromiter(want.keys(), dtype=np.int64, count=len(want))
+    vals = np.fromiter(want.values(), dtype=np.complex128, count=len(want))
+    _general_check(got.spectrum(2).entries, locs, vals, "b=2")
+
+
 @pytest.mark.parametrize("warp", ["1", "0"])
 def test_general_noprune_cfg4_shape(warp, monkeypatch):
     """prune=False at the config-4 shape (d=256): subspace pursuit over all d

@@ -1656,18 +1656,22 @@ __global__ void __launch_bounds__(128) k_gen_bins(const cx *__restrict__ V, GenP
                                                   const int8_t *__restrict__ ncols_in,
                                                   uint8_t *__restrict__ nent, int64_t *__restrict__ sloc,
                                                   cx *__restrict__ sval, int64_t *__restrict__ stats,
-                                                  unsigned long long *__restrict__ hl_next) {
+                                                  unsigned long long *__restrict__ hl_next, int deal_max) {
     const int64_t cnt = (int64_t)*hl_count;
     const int64_t nwarps = int64_t(gridDim.x) * (blockDim.x >> 5);
     const int64_t gw = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-    // few bins: one per warp (lane 0); many (no pruning: every voted bin):
-    // every thread takes the next bin from a counter, so the long and short
-    // chains balance dynamically
-    const bool few = cnt <= nwarps;
-    if (few && lane != 0) return;
-    for (int64_t q = few ? gw : (int64_t)atomicAdd(hl_next, 1ull); q < cnt;
-         q = few ? cnt : (int64_t)atomicAdd(hl_next, 1ull)) {
+    // up to deal_max bins per warp: dealt lane-major (item q to lane
+    // q / nwarps of warp q % nwarps), so every warp of the wave holds at
+    // most ceil(cnt / nwarps) chains -- one when cnt <= nwarps.  Beyond
+    // that (no pruning: every voted bin) every thread takes the next bin
+    // from a counter, so the long and short chains balance dynamically.
+    // (A counter at a few bins per warp hands each warp 32 consecutive
+    // items: the chains would pile into cnt / 32 warps.)
+    const bool dealt = cnt <= (int64_t)deal_max * nwarps;
+    if (dealt && (int64_t)lane * nwarps >= cnt) return;
+    for (int64_t q = dealt ? gw + lane * nwarps : (int64_t)atomicAdd(hl_next, 1ull); q < cnt;
+         q = dealt ? cnt : (int64_t)atomicAdd(hl_next, 1ull)) {
         const int64_t it = hl[q];
         const int64_t t = wl[it];
         const int a = votes[t];
@@ -2201,13 +2205,17 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
         cudaStreamWaitEvent(side, ev_fork, 0);
     }
     cudaStream_t bstream = side ? side : stream;
+    // bins per warp dealt statically in k_gen_bins (SFDT_GEN_DEAL; 1: one
+    // per warp, else the take counter)
+    const char *edl = getenv("SFDT_GEN_DEAL");
+    const int deal_max = edl ? atoi(edl) : 8;
     {
         // one wave; up to one heavy bin per warp (k_gen_bins)
         switch (a->r_eff) {
 #define SFDT_BINS(R)                                                                                    \
     case R:                                                                                             \
         k_gen_bins<R><<<wl_grid(32 * max_voted, 128, one_wave(k_gen_bins<R>, 128)), 128, 0, bstream>>>( \
-            V, gp, votes, wl, hl, hlc, colsb, ncolsb, nent, sloc, sval, a->stats, wlc + 3);             \
+            V, gp, votes, wl, hl, hlc, colsb, ncolsb, nent, sloc, sval, a->stats, wlc + 3, deal_max);             \
         break;
             SFDT_BINS(6) SFDT_BINS(8) SFDT_BINS(9) SFDT_BINS(12)
         default:

@@ -495,18 +495,22 @@ def test_general_duplicate_views_shared(n, k, monkeypatch):
     _general_check(got.spectrum(0).entries, locs, vals, "b=0")
 
 
-def test_general_heavy_bins_side_stream(monkeypatch):
+@pytest.mark.parametrize("var,val", [("SFDT_GEN_OVERLAP", "0"), ("SFDT_GEN_DEAL", "0"),
+                                     ("SFDT_GEN_DEAL", "1")])
+def test_general_heavy_bins_side_stream(var, val, monkeypatch):
     """The multi-collision pursuit (k_gen_bins) on its side stream beside
-    the single-collision pursuit (default) gives the same bits as both on
-    the caller's stream (SFDT_GEN_OVERLAP=0), at the config-4 shape (d=256,
-    20 dB), and matches the oracle (graph capture of the fork/join:
+    the single-collision pursuit, its bins dealt lane-major over the warps
+    (default), gives the same bits as both on the caller's stream
+    (SFDT_GEN_OVERLAP=0) and as the take-counter / one-per-warp schedules
+    (SFDT_GEN_DEAL=0 / 1), at the config-4 shape (d=256, 20 dB), and
+    matches the oracle (graph capture of the fork/join:
     test_gpu_api.py::test_solve_graph_matches_batch)."""
     n, k, B = 1 << 20, 128, 4
     seeds = [(71, b) for b in range(B)]
     X = np.stack([general_signal(n, k, 20.0, s)[0] for s in seeds])
     cfg = P.GeneralConfig(n=n, k=k)
     got = P.solve_general_batch(X, cfg, seeds=seeds)
-    monkeypatch.setenv("SFDT_GEN_OVERLAP", "0")
+    monkeypatch.setenv(var, val)
     ref = P.solve_general_batch(X, cfg, seeds=seeds)
     for b in range(B):
         g, r = got.spectrum(b).entries, ref.spectrum(b).entries

@@ -301,6 +301,19 @@ def load_traffic(key):
         return None
 
 
+def load_random_ceiling():
+    """Measured random 16-B read rate (fully random, each a 128-B DRAM
+    line fetch): tools/randread.cu, profiles/r01_randread.txt."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_randread.txt")) as fh:
+            for line in fh:
+                if line.startswith("G=1 ") and "hint=0" in line:
+                    return float(line.split("ms,")[1].split("G accesses")[0])
+    except Exception:
+        pass
+    return None
+
+
 class _GraphHostResult:
     def __init__(self, res, h2d, d2h):
         self.res, self.h2d_bytes, self.d2h_bytes, self.zero_copy = res, h2d, d2h, False
@@ -516,7 +529,13 @@ def gpu_arm(a):
         L = a.n // resolved_d(a)
         d = resolved_d(a)
         sh = solver.plan.sh
-        distinct = np.array([6 + int(np.sum(np.asarray(row) >= 6)) for row in sh])
+        S = 2 * solver.cfg.a_max
+        distinct = np.array([S + int(np.sum(np.asarray(row) >= S)) for row in sh])
+        # DRAM lines per d-block: the consecutive window and the random
+        # shifts, 8 (c128) / 16 (c64) samples per 128-B line
+        per_line = 128 // (16 if a.dtype == "c128" else 8)
+        lines = (int(sum(len({s // per_line for s in list(range(S)) + [int(v) for v in row]})
+                         for row in sh)) * L if (d * 128 // per_line) % 128 == 0 else None)
         alg_bytes = int(2 * distinct.sum() * L * 16)
         if a.use_graph:
             avg_s = step_s
@@ -533,6 +552,13 @@ def gpu_arm(a):
                     "alg_bytes_def": ("2 x 16 B x L x (2*a_max + distinct random shifts) per signal: "
                                       "every view sample read once, every view written once"),
                     "avg_launch_ms": avg_s * 1e3, "kernel_share_of_step": avg_s / step_s,
+                    "random_access": None if lines is None or load_random_ceiling() is None else {
+                        "line_fetches_per_launch": lines,
+                        "achieved_g_per_s": lines / avg_s / 1e9,
+                        "ceiling_g_per_s": load_random_ceiling(),
+                        "frac": lines / avg_s / 1e9 / load_random_ceiling(),
+                        "def": ("distinct 128-B lines of x per signal (window + random shifts per "
+                                "d-block) x L; ceiling: fully random 16-B reads, tools/randread.cu")},
                     "note": ("a random-shift sample is one 16-B element per d-block; DRAM serves it "
                              "as a 128-B access, so traffic is ~2.8x the algorithmic bytes at config 4; "
                              "the rest of the step is FP64/latency-bound per-bin work")}

@@ -251,7 +251,8 @@ def test_host_batch_exact_streams_whole_rows():
 def test_solve_graph_matches_batch(kind):
     """SolveGraph replays the same kernels as exact_batch / solve_general_batch:
     results identical, across replays with different inputs, for the device
-    and the host_io (H2D + solve + D2H in one graph) forms."""
+    and the host_io (H2D, then solve + D2H in one graph; from the staging
+    buffer or straight from a pinned tensor) forms."""
     from tests.synth import exact_signal, general_signal
     n, B = 1 << 14, 2
     if kind == "general":
@@ -270,10 +271,13 @@ def test_solve_graph_matches_batch(kind):
         want = ref(X)
         got = g.solve(torch.from_numpy(X).cuda())
         goth = gh.solve_host(X)
+        gotp = gh.solve_host(torch.from_numpy(X).pin_memory())   # H2D straight from pinned rows
+        goth = gh.solve_host(X)   # staged again: the pinned replay left no state behind
         for b in range(B):
             w = want.spectrum(b).entries
             assert got.spectrum(b).entries == w
             assert goth.spectrum(b).entries == w
+            assert gotp.spectrum(b).entries == w
             if kind != "general":
                 for tr in (got.trace(b), goth.trace(b)):
                     wt = want.trace(b)

@@ -1365,7 +1365,8 @@ __global__ void __launch_bounds__(128) k_gen_prune(const cx *__restrict__ V, Gen
                                                    const int32_t *__restrict__ mf_top,
                                                    int32_t *__restrict__ cols_out, int8_t *__restrict__ ncols_out,
                                                    int heavy_flags, int64_t *__restrict__ hl,
-                                                   unsigned long long *__restrict__ hlc) {
+                                                   unsigned long long *__restrict__ hlc, int64_t hl_cap,
+                                                   unsigned long long *__restrict__ hlc_hi, int split_a) {
     const int64_t cnt = (int64_t)*wl_count;
     for (int64_t it = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; it < cnt;
          it += int64_t(gridDim.x) * blockDim.x) {
@@ -1484,7 +1485,12 @@ __global__ void __launch_bounds__(128) k_gen_prune(const cx *__restrict__ V, Gen
         // k_gen_bins_warp takes the all-column bins)
         const int nc = all_cols ? -1 : ncols;
         const bool heavy = !((heavy_flags & 1) && sp1_item(a, r, nc)) && !((heavy_flags & 2) && nc < 0);
-        if (heavy) hl[atomicAdd(hlc, 1ull)] = it;
+        // bins with a >= split_a (the longer pursuits) fill the list from
+        // its end, so k_gen_bins can deal them first
+        if (heavy) {
+            if (split_a > 0 && a >= split_a) hl[hl_cap - 1 - (int64_t)atomicAdd(hlc_hi, 1ull)] = it;
+            else hl[atomicAdd(hlc, 1ull)] = it;
+        }
     }
 }
 
@@ -1656,8 +1662,13 @@ __global__ void __launch_bounds__(128) k_gen_bins(const cx *__restrict__ V, GenP
                                                   const int8_t *__restrict__ ncols_in,
                                                   uint8_t *__restrict__ nent, int64_t *__restrict__ sloc,
                                                   cx *__restrict__ sval, int64_t *__restrict__ stats,
-                                                  unsigned long long *__restrict__ hl_next, int deal_max) {
-    const int64_t cnt = (int64_t)*hl_count;
+                                                  unsigned long long *__restrict__ hl_next, int deal_max,
+                                                  const unsigned long long *__restrict__ hl_hi_count,
+                                                  int64_t hl_cap) {
+    // item q < cnt_hi: the a >= split_a bins (hl's tail, longer chains);
+    // then the rest from hl's head
+    const int64_t cnt_hi = (int64_t)*hl_hi_count;
+    const int64_t cnt = (int64_t)*hl_count + cnt_hi;
     const int64_t nwarps = int64_t(gridDim.x) * (blockDim.x >> 5);
     const int64_t gw = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
@@ -1668,11 +1679,13 @@ __global__ void __launch_bounds__(128) k_gen_bins(const cx *__restrict__ V, GenP
     // from a counter, so the long and short chains balance dynamically.
     // (A counter at a few bins per warp hands each warp 32 consecutive
     // items: the chains would pile into cnt / 32 warps.)
+    // Lanes >= 1 take their items in reverse warp order, so the first
+    // (longest) items on lane 0 of the low warps pair with the last ones.
     const bool dealt = cnt <= (int64_t)deal_max * nwarps;
     if (dealt && (int64_t)lane * nwarps >= cnt) return;
-    for (int64_t q = dealt ? gw + lane * nwarps : (int64_t)atomicAdd(hl_next, 1ull); q < cnt;
-         q = dealt ? cnt : (int64_t)atomicAdd(hl_next, 1ull)) {
-        const int64_t it = hl[q];
+    for (int64_t q = dealt ? (lane ? nwarps - 1 - gw : gw) + lane * nwarps : (int64_t)atomicAdd(hl_next, 1ull);
+         q < cnt; q = dealt ? cnt : (int64_t)atomicAdd(hl_next, 1ull)) {
+        const int64_t it = q < cnt_hi ? hl[hl_cap - 1 - q] : hl[q - cnt_hi];
         const int64_t t = wl[it];
         const int a = votes[t];
         const int r = RT > 0 ? RT : p.r_eff;
@@ -2188,9 +2201,13 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     int64_t *hl = (int64_t *)(w + p.off_hl);
     unsigned long long *hlc = wlc + 1;
     cudaMemsetAsync(hlc, 0, 8, stream);
-    cudaMemsetAsync(wlc + 3, 0, 8, stream);   // k_gen_bins' take counter
+    cudaMemsetAsync(wlc + 3, 0, 16, stream);   // k_gen_bins' take counter, the a >= split_a count
+    // heavy bins with a >= split_a dealt first (SFDT_GEN_SPLIT; 0: list order)
+    const char *esp = getenv("SFDT_GEN_SPLIT");
+    const int split_a = esp ? atoi(esp) : 3;
     k_gen_prune<<<wl_grid(max_voted, 128, one_wave(k_gen_prune, 128)), 128, 0, stream>>>(
-        V, gp, votes, wl, wlc, mf_top, colsb, ncolsb, sp1 | (warp_all ? 2 : 0), hl, hlc);
+        V, gp, votes, wl, wlc, mf_top, colsb, ncolsb, sp1 | (warp_all ? 2 : 0), hl, hlc, max_voted, wlc + 4,
+        split_a);
     SFDT_CHECK_LAUNCH();
     // heavy bins (k_gen_bins) fork onto the side stream; the bins of the
     // two pursuits are disjoint (k_gen_prune routes each to one list) and
@@ -2215,7 +2232,7 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
 #define SFDT_BINS(R)                                                                                    \
     case R:                                                                                             \
         k_gen_bins<R><<<wl_grid(32 * max_voted, 128, one_wave(k_gen_bins<R>, 128)), 128, 0, bstream>>>( \
-            V, gp, votes, wl, hl, hlc, colsb, ncolsb, nent, sloc, sval, a->stats, wlc + 3, deal_max);             \
+            V, gp, votes, wl, hl, hlc, colsb, ncolsb, nent, sloc, sval, a->stats, wlc + 3, deal_max, wlc + 4, max_voted); \
         break;
             SFDT_BINS(6) SFDT_BINS(8) SFDT_BINS(9) SFDT_BINS(12)
         default:

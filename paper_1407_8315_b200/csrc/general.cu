@@ -1366,13 +1366,16 @@ __global__ void __launch_bounds__(128) k_gen_prune(const cx *__restrict__ V, Gen
                                                    int32_t *__restrict__ cols_out, int8_t *__restrict__ ncols_out,
                                                    int heavy_flags, int64_t *__restrict__ hl,
                                                    unsigned long long *__restrict__ hlc, int64_t hl_cap,
-                                                   unsigned long long *__restrict__ hlc_hi, int split_a) {
+                                                   unsigned long long *__restrict__ hlc_hi, int split_a,
+                                                   int phase) {
     const int64_t cnt = (int64_t)*wl_count;
     for (int64_t it = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; it < cnt;
          it += int64_t(gridDim.x) * blockDim.x) {
         const int64_t t = wl[it];
-        const int64_t b = t / p.L, kb = t - b * p.L;
         const int a = votes[t];
+        // phase 1: the multi-collision bins only, phase 2: the rest
+        if ((phase == 1 && a < 2) || (phase == 2 && a >= 2)) continue;
+        const int64_t b = t / p.L, kb = t - b * p.L;
         const int r = p.r_eff;
         const int64_t *sh = p.shifts + b * p.shift_stride;
         cx syn[8], y[GEN_MAX_R];
@@ -2201,18 +2204,33 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     int64_t *hl = (int64_t *)(w + p.off_hl);
     unsigned long long *hlc = wlc + 1;
     cudaMemsetAsync(hlc, 0, 8, stream);
-    cudaMemsetAsync(wlc + 3, 0, 16, stream);   // k_gen_bins' take counter, the a >= split_a count
+    // wlc[3]: k_gen_bins' take counter, [4]: the a >= split_a count (or the
+    // phase-2 heavy count), [5]: the second k_gen_bins' take counter, [6]: 0
+    cudaMemsetAsync(wlc + 3, 0, 32, stream);
     // heavy bins with a >= split_a dealt first (SFDT_GEN_SPLIT; 0: list order)
     const char *esp = getenv("SFDT_GEN_SPLIT");
     const int split_a = esp ? atoi(esp) : 3;
-    k_gen_prune<<<wl_grid(max_voted, 128, one_wave(k_gen_prune, 128)), 128, 0, stream>>>(
-        V, gp, votes, wl, wlc, mf_top, colsb, ncolsb, sp1 | (warp_all ? 2 : 0), hl, hlc, max_voted, wlc + 4,
-        split_a);
+    // The multi-collision bins are known from the votes: with a side stream
+    // they are pruned first (phase 1) and their pursuit (k_gen_bins, a tail
+    // of a few long chains) runs beside the pruning of the single-collision
+    // bins (phase 2) and k_gen_sp1.  Phase 2's heavy bins (a = 1 with more
+    // than 4 kept columns) fill hl from its tail for a second k_gen_bins on
+    // the caller's stream.  Measured slower, so opt-in (SFDT_GEN_PRUNE2=1):
+    // the one-wave k_gen_bins holds every SM's registers until its warps
+    // retire, starving phase 2 (config 4 2.88 -> 3.00 ms, config 5 general
+    // K=64 1.52 -> 1.85 ms).
+    cudaStream_t side = gen_side_stream(stream);
+    const char *ep2 = getenv("SFDT_GEN_PRUNE2");
+    const bool two_phase = side && ep2 && ep2[0] == '1';
+    const int hflags = sp1 | (warp_all ? 2 : 0);
+    const unsigned prune_grid = wl_grid(max_voted, 128, one_wave(k_gen_prune, 128));
+    k_gen_prune<<<prune_grid, 128, 0, stream>>>(V, gp, votes, wl, wlc, mf_top, colsb, ncolsb, hflags, hl, hlc,
+                                                max_voted, wlc + 4, two_phase ? 0 : split_a,
+                                                two_phase ? 1 : 0);
     SFDT_CHECK_LAUNCH();
     // heavy bins (k_gen_bins) fork onto the side stream; the bins of the
     // two pursuits are disjoint (k_gen_prune routes each to one list) and
     // their shared counters are atomics
-    cudaStream_t side = gen_side_stream(stream);
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     if (side) {
         if (cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
@@ -2226,22 +2244,31 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     // per warp, else the take counter)
     const char *edl = getenv("SFDT_GEN_DEAL");
     const int deal_max = edl ? atoi(edl) : 8;
-    {
-        // one wave; up to one heavy bin per warp (k_gen_bins)
+    auto launch_bins = [&](cudaStream_t st, const unsigned long long *lo_count, unsigned long long *take,
+                           const unsigned long long *hi_count) {
+        // one wave; heavy bins dealt over its warps (k_gen_bins)
         switch (a->r_eff) {
 #define SFDT_BINS(R)                                                                                    \
     case R:                                                                                             \
-        k_gen_bins<R><<<wl_grid(32 * max_voted, 128, one_wave(k_gen_bins<R>, 128)), 128, 0, bstream>>>( \
-            V, gp, votes, wl, hl, hlc, colsb, ncolsb, nent, sloc, sval, a->stats, wlc + 3, deal_max, wlc + 4, max_voted); \
+        k_gen_bins<R><<<wl_grid(32 * max_voted, 128, one_wave(k_gen_bins<R>, 128)), 128, 0, st>>>(      \
+            V, gp, votes, wl, hl, lo_count, colsb, ncolsb, nent, sloc, sval, a->stats, take, deal_max,   \
+            hi_count, max_voted);                                                                       \
         break;
             SFDT_BINS(6) SFDT_BINS(8) SFDT_BINS(9) SFDT_BINS(12)
         default:
             SFDT_BINS(0)
 #undef SFDT_BINS
         }
-    }
+    };
+    launch_bins(bstream, hlc, wlc + 3, two_phase ? wlc + 6 : wlc + 4);
     SFDT_CHECK_LAUNCH();
     launches++;
+    if (two_phase) {
+        k_gen_prune<<<prune_grid, 128, 0, stream>>>(V, gp, votes, wl, wlc, mf_top, colsb, ncolsb, hflags, hl,
+                                                    hlc, max_voted, wlc + 4, 1, 2);
+        SFDT_CHECK_LAUNCH();
+        launches++;
+    }
     if (sp1) {
         switch (a->r_eff) {
 #define SFDT_SP1(R)                                                                                     \
@@ -2259,6 +2286,11 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     if (warp_all) {
         k_gen_bins_warp<<<wl_grid(max_voted, 8, one_wave(k_gen_bins_warp, 256)), 256, 0, stream>>>(
             V, gp, votes, wl, wlc, ncolsb, nent, sloc, sval, a->stats);
+        SFDT_CHECK_LAUNCH();
+        launches++;
+    }
+    if (two_phase) {   // phase 2's heavy bins, from hl's tail
+        launch_bins(stream, wlc + 6, wlc + 5, wlc + 4);
         SFDT_CHECK_LAUNCH();
         launches++;
     }

@@ -497,13 +497,14 @@ def test_general_duplicate_views_shared(n, k, monkeypatch):
 
 @pytest.mark.parametrize("var,val", [("SFDT_GEN_OVERLAP", "0"), ("SFDT_GEN_DEAL", "0"),
                                      ("SFDT_GEN_DEAL", "1"), ("SFDT_GEN_SPLIT", "0"),
-                                     ("SFDT_GEN_SPLIT", "2")])
+                                     ("SFDT_GEN_SPLIT", "2"), ("SFDT_GEN_PRUNE2", "1")])
 def test_general_heavy_bins_side_stream(var, val, monkeypatch):
     """The multi-collision pursuit (k_gen_bins) on its side stream beside
     the single-collision pursuit, its bins dealt lane-major over the warps
     (default), gives the same bits as both on the caller's stream
     (SFDT_GEN_OVERLAP=0), as the take-counter / one-per-warp schedules
-    (SFDT_GEN_DEAL=0 / 1) and as other deal orders (SFDT_GEN_SPLIT), at the config-4 shape (d=256, 20 dB), and
+    (SFDT_GEN_DEAL=0 / 1), other deal orders (SFDT_GEN_SPLIT) and the
+    two-phase pruning around the fork (SFDT_GEN_PRUNE2=1), at the config-4 shape (d=256, 20 dB), and
     matches the oracle (graph capture of the fork/join:
     test_gpu_api.py::test_solve_graph_matches_batch)."""
     n, k, B = 1 << 20, 128, 4

@@ -265,6 +265,7 @@ static __global__ void __launch_bounds__(256, MINB) k_fft_views(const ViewSrc sr
     const int64_t nviews = B * src.nshift;
     const int64_t g0 = int64_t(blockIdx.x) << logvpc;
     const int nv = (int)((nviews - g0) < vpc ? (nviews - g0) : vpc);
+    if (nv <= 0) return;   // cluster padding (SFDT_FFT_CLUSTER): no views
     // per-view addressing, once per CTA (no 64-bit divisions or dynamically
     // indexed parameter arrays in the element loops)
     if (src.nview) {   // CTA-uniform: skip when every view of the tile is unused
@@ -638,6 +639,34 @@ static inline int fft_points_per_cta() {
 
 // FFT of every view of B signals; large_scratch (B*nshift*L complex) is
 // needed only when L > FFT_SMEM_MAX.
+// Launch k_fft_views, optionally as thread-block clusters of SFDT_FFT_CLUSTER
+// consecutive CTAs (adjacent views of one signal, co-scheduled on one GPC so
+// their strided gathers reach the same d-blocks at about the same time).
+template <int MINB>
+static inline void launch_views_kernel(unsigned grid, size_t smem, cudaStream_t stream, const ViewSrc &src,
+                                       int64_t B, int logL, int logvpc, const cx *tw, cx *out, int SV,
+                                       int64_t ldV, int scale, const double *thr, uint8_t *act) {
+    const char *e = getenv("SFDT_FFT_CLUSTER");
+    const int cl = e ? atoi(e) : 0;
+    if (cl == 2 || cl == 4 || cl == 8) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((grid + cl - 1) / cl * cl);
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cl;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, k_fft_views<MINB>, src, B, logL, logvpc, tw, out, SV, ldV, scale, thr, act);
+        return;
+    }
+    k_fft_views<MINB><<<grid, 256, smem, stream>>>(src, B, logL, logvpc, tw, out, SV, ldV, scale, thr, act);
+}
+
 static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, const double *tw_,
                                    cx *out, int SV, int64_t ldV, cudaStream_t stream,
                                    cx *large_scratch = nullptr, int scale = 1,
@@ -659,7 +688,7 @@ static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, con
         // <= 32 KiB per CTA: cap registers at 64 for 4 CTAs/SM (measured
         // 717 -> 553 us at config 2); larger tiles keep 128 registers
         if (smem <= 32 * 1024) {
-            k_fft_views<4><<<grid, 256, smem, stream>>>(src, B, logL, logvpc, tw, out, SV, ldV, scale, thr, act);
+            launch_views_kernel<4>(grid, smem, stream, src, B, logL, logvpc, tw, out, SV, ldV, scale, thr, act);
         } else if (smem <= 64 * 1024) {
             // 64 KiB tiles: registers capped at 85 (3 CTAs/SM would fit)
             cudaFuncSetAttribute(k_fft_views<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -673,10 +702,10 @@ static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, con
                 const int pct = e ? atoi(e) : (int)((2 * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
                 cudaFuncSetAttribute(k_fft_views<3>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
             }
-            k_fft_views<3><<<grid, 256, smem, stream>>>(src, B, logL, logvpc, tw, out, SV, ldV, scale, thr, act);
+            launch_views_kernel<3>(grid, smem, stream, src, B, logL, logvpc, tw, out, SV, ldV, scale, thr, act);
         } else {
             cudaFuncSetAttribute(k_fft_views<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            k_fft_views<1><<<grid, 256, smem, stream>>>(src, B, logL, logvpc, tw, out, SV, ldV, scale, thr, act);
+            launch_views_kernel<1>(grid, smem, stream, src, B, logL, logvpc, tw, out, SV, ldV, scale, thr, act);
         }
         SFDT_CHECK_LAUNCH();
         return SFDT_OK;

@@ -44,6 +44,52 @@ __global__ void __launch_bounds__(256) rr(const double2 *__restrict__ x, int64_t
     if (acc == 1.2345) out[0] = acc;
 }
 
+// Blocked variant: groups of BL lanes read BL random 16-B samples inside the
+// same random 4-KiB block (one random shift per lane, like the random-shift
+// views of one d-block at d = 256): does DRAM page locality lift the rate?
+template <int BL, int UNROLL>
+__global__ void __launch_bounds__(256) rrb(const double2 *__restrict__ x, int64_t nmask_blocks, int rounds,
+                                           double *__restrict__ out) {
+    const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t grp = tid / BL;
+    double acc = 0.0;
+    for (int r = 0; r < rounds; r += UNROLL) {
+        double2 v[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; u++) {
+            const uint64_t h = mix((uint64_t)grp * 1000003ull + r + u);
+            const int64_t blk = (int64_t)(h & (uint64_t)nmask_blocks);
+            const int64_t off = (int64_t)(mix(h + threadIdx.x) & 255);   // sample within the 4-KiB block
+            v[u] = __ldg(x + blk * 256 + off);
+        }
+#pragma unroll
+        for (int u = 0; u < UNROLL; u++) acc += v[u].x + v[u].y;
+    }
+    if (acc == 1.2345) out[0] = acc;
+}
+
+template <int BL>
+void runb(const double2 *x, int64_t n, double *out) {
+    const int blocks = 148 * 8, rounds = 64;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    for (int rep = 0; rep < 2; rep++) rrb<BL, 8><<<blocks, 256>>>(x, n / 256 - 1, rounds, out);
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; rep++) {
+        cudaEventRecord(a);
+        rrb<BL, 8><<<blocks, 256>>>(x, n / 256 - 1, rounds, out);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        if (ms < best) best = ms;
+    }
+    const double acc = double(blocks) * 256 * rounds;
+    printf("blocked: %2d random 16-B samples per random 4-KiB block: %.3f ms, %.1f G accesses/s\n", BL, best,
+           acc / (best * 1e-3) / 1e9);
+}
+
 template <int G, int HINT>
 void run(const double2 *x, int64_t n, double *out) {
     const int blocks = 148 * 8, rounds = 64;
@@ -81,6 +127,10 @@ int main() {
     run<4, 0>(x, n, out);
     run<8, 0>(x, n, out);
     run<16, 0>(x, n, out);
+    runb<1>(x, n, out);
+    runb<9>(x, n, out);
+    runb<16>(x, n, out);
+    runb<32>(x, n, out);
     cudaError_t e = cudaDeviceSynchronize();
     printf("%s\n", cudaGetErrorString(e));
     return 0;

@@ -8,7 +8,7 @@ from .exact import (EstimateResult, ExactBatch, ExactConfig, IterationStats, Sol
 from .general import (CollisionEstimate, GeneralBatch, GeneralConfig, GeneralPlan, GeneralTrace,
                       draw_shifts, estimate_collisions,
                       solve_general, solve_general_batch)
-from .graph import SolveGraph
+from .graph import SolveGraph, SolvePipeline
 from .host import HostBatchResult, solve_host_batch
 from .syndrome import (DecodedBin, DegenerateBranch, IllConditioned, NearSingular,
                        PolyCoefficients, decode_bin, root_to_location, roots_closed_form,
@@ -29,7 +29,7 @@ __all__ = [
     "decode_bin", "root_to_location", "roots_closed_form", "solve_coefficients", "solve_values",
     "fft", "snr", "synthesize",
     "BACKEND", "EstimateResult", "ExactBatch", "ExactConfig", "HostBatchResult",
-    "IterationStats", "SolverTrace", "SolveGraph", "solve_host_batch",
+    "IterationStats", "SolverTrace", "SolveGraph", "SolvePipeline", "solve_host_batch",
     "SparseSpectrum", "as_signal", "estimate_sparsity_and_solve", "exact_batch",
     "solve_iterative", "solve_iterative_batch", "solve_noniterative",
     "solve_noniterative_batch", "using_compiled", "CollisionEstimate", "GeneralBatch",

@@ -141,6 +141,62 @@ class SolveGraph:
         return self.X.numel() * self.X.element_size()
 
 
+class SolvePipeline:
+    """A stream of small solves through `depth` host-IO SolveGraphs, each on
+    its own CUDA stream, so the H2D of one batch overlaps the kernels of the
+    previous one (the copy engine and the SMs work side by side).
+
+        pipe = SolvePipeline(ExactConfig(n=1 << 16, k=64), batch=1)
+        for res in pipe.solve_stream(xs):   # xs: iterable of pinned (B, n) tensors
+            res.spectrum(0)                 # valid until the next result is drawn
+
+    Results come back in submission order; each is the same as
+    SolveGraph.solve_host on that input."""
+
+    def __init__(self, cfg, batch: int = 1, iterative: bool = False,
+                 dtype=torch.complex128, device=None, seeds=None, depth: int = 2):
+        if depth < 1:
+            raise ValueError("depth must be >= 1")
+        self.graphs = [SolveGraph(cfg, batch, iterative, dtype, device, seeds, host_io=True)
+                       for _ in range(depth)]
+        dev = self.graphs[0].device
+        self.streams = [torch.cuda.Stream(dev) for _ in range(depth)]
+
+    def _submit(self, slot: int, x):
+        g, st = self.graphs[slot], self.streams[slot]
+        if not isinstance(x, torch.Tensor):
+            x = torch.from_numpy(np.ascontiguousarray(x))
+        if not (x.device.type == "cpu" and x.is_pinned() and x.dtype == g.host_input.dtype
+                and x.is_contiguous() and x.numel() == g.host_input.numel()):
+            g.host_input.copy_(x.reshape(g.host_input.shape))
+            x = g.host_input
+        st.wait_stream(torch.cuda.current_stream(g.device))
+        with torch.cuda.stream(st):
+            g.X.copy_(x.reshape(g.X.shape), non_blocking=True)
+            g.graph.replay()
+            ev = torch.cuda.Event()
+            ev.record(st)
+        return ev
+
+    def _collect(self, slot: int, ev):
+        ev.synchronize()
+        g = self.graphs[slot]
+        res = g._wrap()
+        res._host = _host_view({k: v.numpy() for k, v in g._host_out.items()}, g.general)
+        return res
+
+    def solve_stream(self, xs):
+        depth = len(self.graphs)
+        pending = []   # (slot, event) in submission order
+        for i, x in enumerate(xs):
+            slot = i % depth
+            if len(pending) == depth:   # the slot's previous result is drawn first
+                yield self._collect(*pending.pop(0))
+            pending.append((slot, self._submit(slot, x)))
+        while pending:
+            yield self._collect(*pending.pop(0))
+
+
 def _host_view(full: dict, general: bool) -> dict:
     """Slice whole-capacity host copies down to the used prefixes (the layout
     ExactBatch.to_host / GeneralBatch.to_host produce)."""

@@ -283,3 +283,28 @@ def test_solve_graph_matches_batch(kind):
                     wt = want.trace(b)
                     assert tr.iterations == wt.iterations and tr.full_success == wt.full_success
                     assert tr.unresolved_bins == wt.unresolved_bins and tr.fft_samples == wt.fft_samples
+
+
+@pytest.mark.parametrize("kind", ["noniterative", "general"])
+def test_solve_pipeline_matches_batch(kind):
+    """SolvePipeline (two host-IO graphs on two streams, H2D of one batch
+    beside the kernels of the previous one): results in submission order,
+    each identical to the batched solve of that input."""
+    from tests.synth import exact_signal, general_signal
+    n, B = 1 << 14, 1
+    if kind == "general":
+        k = 16
+        cfg = P.GeneralConfig(n=n, k=k, rng_seed=5)
+        sigs = [general_signal(n, k, 20.0, 90 + r)[0][None] for r in range(5)]
+        ref = lambda X: P.solve_general_batch(X, cfg)
+    else:
+        k = 32
+        cfg = P.ExactConfig(n=n, k=k)
+        sigs = [exact_signal(n, k, 95 + r, "mag1_10")[0][None] for r in range(5)]
+        ref = lambda X: P.exact_batch(X, cfg, False)
+    pipe = P.SolvePipeline(cfg, batch=B, depth=2)
+    xs = [torch.from_numpy(X).pin_memory() for X in sigs[:3]] + sigs[3:]   # pinned and numpy inputs
+    got = [r.spectrum(0).entries for r in pipe.solve_stream(xs)]
+    assert len(got) == len(sigs)
+    for X, g in zip(sigs, got):
+        assert g == ref(X).spectrum(0).entries

@@ -1358,6 +1358,12 @@ __global__ void __launch_bounds__(256) k_gen_mf_small(const cx *__restrict__ V, 
 // Writes the kept column list for k_gen_bins; ncols = -1 means "all d
 // columns" (no pruning).  Split from the pursuit so each kernel keeps its
 // own registers, stack and instruction footprint.
+// LANES = 4 (d >= 1024, d % 512 == 0): four lanes per bin, lane l scoring
+// the 512-candidate segments l, l + 4, ... (the recurrence re-seeds at every
+// segment start, so each segment's values are the same bits), then lane 0
+// merges the four bottom-k lists in the (value, index) order the serial
+// scan keeps.  For the few-bins, large-d shapes (config 5 general, K = 64).
+template <int LANES>
 __global__ void __launch_bounds__(128) k_gen_prune(const cx *__restrict__ V, GenParams p,
                                                    const int32_t *__restrict__ votes,
                                                    const int64_t *__restrict__ wl,
@@ -1369,8 +1375,9 @@ __global__ void __launch_bounds__(128) k_gen_prune(const cx *__restrict__ V, Gen
                                                    unsigned long long *__restrict__ hlc_hi, int split_a,
                                                    int phase) {
     const int64_t cnt = (int64_t)*wl_count;
-    for (int64_t it = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; it < cnt;
-         it += int64_t(gridDim.x) * blockDim.x) {
+    const int sub = LANES > 1 ? (int)(threadIdx.x & (LANES - 1)) : 0;
+    for (int64_t it = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / LANES; it < cnt;
+         it += int64_t(gridDim.x) * blockDim.x / LANES) {
         const int64_t t = wl[it];
         const int a = votes[t];
         // phase 1: the multi-collision bins only, phase 2: the rest
@@ -1437,7 +1444,22 @@ __global__ void __launch_bounds__(128) k_gen_prune(const cx *__restrict__ V, Gen
                         ? gmul(base, gexp(mk(0.0, DMUL(TWO_PI, (double)(tt + 1)) / (double)p.d)))
                         : gmul(z, wd);
                 };
-                if ((p.d & 3) == 0) {
+                if (LANES > 1) {
+                    // this lane's 512-candidate segments, each from its re-seed
+                    for (int64_t s0 = (int64_t)sub * 512; s0 < p.d; s0 += (int64_t)LANES * 512) {
+                        zt = s0 == 0 ? base : gmul(base, gexp(mk(0.0, DMUL(TWO_PI, (double)s0) / (double)p.d)));
+                        for (int64_t tt = s0; tt < s0 + 512; tt += 4) {
+                            const cx z0 = zt, z1 = advance(z0, tt), z2 = advance(z1, tt + 1),
+                                     z3 = advance(z2, tt + 2);
+                            zt = advance(z3, tt + 3);
+                            const cx a0 = horner(z0), a1 = horner(z1), a2 = horner(z2), a3 = horner(z3);
+                            offer(a0, (int)tt);
+                            offer(a1, (int)tt + 1);
+                            offer(a2, (int)tt + 2);
+                            offer(a3, (int)tt + 3);
+                        }
+                    }
+                } else if ((p.d & 3) == 0) {
                     // four candidates per step: independent Horner chains
                     for (int64_t tt = 0; tt < p.d; tt += 4) {
                         const cx z0 = zt, z1 = advance(z0, tt), z2 = advance(z1, tt + 1),
@@ -1455,7 +1477,7 @@ __global__ void __launch_bounds__(128) k_gen_prune(const cx *__restrict__ V, Gen
                         zt = advance(zt, tt);
                     }
                 }
-            } else {
+            } else if (sub == 0) {
                 // _correlation_keep (general.py:158-165)
                 const int64_t m = p.L;
                 for (int64_t tt = 0; tt < p.d; tt++) {
@@ -1468,6 +1490,30 @@ __global__ void __launch_bounds__(128) k_gen_prune(const cx *__restrict__ V, Gen
                     topk_insert(ks, kp, nk, cnti, cabs_(acc), (int)tt);
                 }
             }
+            if (LANES > 1) {
+                // lane 0 merges lanes 1..3: lexicographic (value, index)
+                // bottom-k, what the serial ascending-index scan keeps
+                const unsigned gm = 0xFu << (threadIdx.x & 28);
+                const int base_lane = (int)(threadIdx.x & 28);
+                for (int l = 1; l < LANES; l++) {
+                    const int nl = __shfl_sync(gm, nk, base_lane + l);
+                    for (int e = 0; e < cnti; e++) {
+                        const double v = __shfl_sync(gm, e < nk ? ks[e] : 0.0, base_lane + l);
+                        const int tv = __shfl_sync(gm, e < nk ? kp[e] : 0, base_lane + l);
+                        if (sub != 0 || e >= nl) continue;
+                        if (nk == cnti && !(v < ks[cnti - 1] || (v == ks[cnti - 1] && tv < kp[cnti - 1])))
+                            continue;
+                        int pos = (nk < cnti) ? nk++ : cnti - 1;
+                        while (pos > 0 && (v < ks[pos - 1] || (v == ks[pos - 1] && tv < kp[pos - 1]))) {
+                            ks[pos] = ks[pos - 1];
+                            kp[pos] = kp[pos - 1];
+                            pos--;
+                        }
+                        ks[pos] = v;
+                        kp[pos] = tv;
+                    }
+                }
+            }
             sort_ints(kp, nk);
             // matched-filter augmentation (general.py:345-351): k_gen_mf
             const int nt = (int)((int64_t)a < p.d ? a : p.d);
@@ -1477,6 +1523,7 @@ __global__ void __launch_bounds__(128) k_gen_prune(const cx *__restrict__ V, Gen
         } else {
             ncols = (int)p.d;
         }
+        if (sub != 0) continue;   // lane 0 of the group writes
         if (!all_cols) {
             for (int c2 = 0; c2 < ncols; c2++) cols_out[it * GEN_MAX_COLS + c2] = cols[c2];
             ncols_out[it] = (int8_t)ncols;
@@ -2223,10 +2270,22 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     const char *ep2 = getenv("SFDT_GEN_PRUNE2");
     const bool two_phase = side && ep2 && ep2[0] == '1';
     const int hflags = sp1 | (warp_all ? 2 : 0);
-    const unsigned prune_grid = wl_grid(max_voted, 128, one_wave(k_gen_prune, 128));
-    k_gen_prune<<<prune_grid, 128, 0, stream>>>(V, gp, votes, wl, wlc, mf_top, colsb, ncolsb, hflags, hl, hlc,
-                                                max_voted, wlc + 4, two_phase ? 0 : split_a,
-                                                two_phase ? 1 : 0);
+    // four lanes per bin when d splits into >= 2 recurrence segments and the
+    // bins are few (one lane per bin would leave most of the GPU idle)
+    const char *epl = getenv("SFDT_GEN_PRUNE_LANES");
+    const bool lanes4 = a->prune && p.d >= 1024 && (p.d & 511) == 0 &&
+                        (epl ? epl[0] == '4' : max_voted <= 64 * (int64_t)sms);
+    const unsigned prune_grid = lanes4 ? wl_grid(4 * max_voted, 128, one_wave(k_gen_prune<4>, 128))
+                                       : wl_grid(max_voted, 128, one_wave(k_gen_prune<1>, 128));
+    auto launch_prune = [&](int split, int phase) {
+        if (lanes4)
+            k_gen_prune<4><<<prune_grid, 128, 0, stream>>>(V, gp, votes, wl, wlc, mf_top, colsb, ncolsb, hflags, hl,
+                                                           hlc, max_voted, wlc + 4, split, phase);
+        else
+            k_gen_prune<1><<<prune_grid, 128, 0, stream>>>(V, gp, votes, wl, wlc, mf_top, colsb, ncolsb, hflags, hl,
+                                                           hlc, max_voted, wlc + 4, split, phase);
+    };
+    launch_prune(two_phase ? 0 : split_a, two_phase ? 1 : 0);
     SFDT_CHECK_LAUNCH();
     // heavy bins (k_gen_bins) fork onto the side stream; the bins of the
     // two pursuits are disjoint (k_gen_prune routes each to one list) and
@@ -2264,8 +2323,7 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     SFDT_CHECK_LAUNCH();
     launches++;
     if (two_phase) {
-        k_gen_prune<<<prune_grid, 128, 0, stream>>>(V, gp, votes, wl, wlc, mf_top, colsb, ncolsb, hflags, hl,
-                                                    hlc, max_voted, wlc + 4, 1, 2);
+        launch_prune(1, 2);
         SFDT_CHECK_LAUNCH();
         launches++;
     }

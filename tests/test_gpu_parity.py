@@ -727,3 +727,28 @@ def test_general_long_view_vote():
         vals = np.fromiter(want.values(), dtype=np.complex128, count=len(want))
         _general_check(res.spectrum(b).entries, locs, vals, f"b={b}")
         assert res.trace(b).collision_histogram == wtr["collision_histogram"]
+
+
+@pytest.mark.parametrize("n,k", [(1 << 20, 16), (1 << 20, 32)])
+def test_general_prune_four_lanes(n, k, monkeypatch):
+    """d = 2048 / 1024 with few bins: pruning with four lanes per bin (one
+    512-candidate recurrence segment each, bottom-k lists merged by lane 0)
+    keeps the same columns as one lane per bin -- supports and values equal
+    bitwise -- and matches the oracle."""
+    B = 3
+    seeds = [(81, b) for b in range(B)]
+    X = np.stack([general_signal(n, k, 20.0 + 5 * b, s)[0] for b, s in enumerate(seeds)])
+    cfg = P.GeneralConfig(n=n, k=k)
+    assert cfg.resolved_d() >= 1024
+    monkeypatch.setenv("SFDT_GEN_PRUNE_LANES", "4")
+    got = P.solve_general_batch(X, cfg, seeds=seeds)
+    monkeypatch.setenv("SFDT_GEN_PRUNE_LANES", "1")
+    ref = P.solve_general_batch(X, cfg, seeds=seeds)
+    for b in range(B):
+        g, r = got.spectrum(b).entries, ref.spectrum(b).entries
+        assert list(g) == list(r)
+        assert np.array_equal(np.fromiter(g.values(), complex), np.fromiter(r.values(), complex))
+    want, _ = OS.general(X[1], k, rng_seed=seeds[1])
+    locs = np.fromiter(want.keys(), dtype=np.int64, count=len(want))
+    vals = np.fromiter(want.values(), dtype=np.complex128, count=len(want))
+    _general_check(got.spectrum(1).entries, locs, vals, "b=1")

@@ -1038,7 +1038,7 @@ constexpr int MF_LIST = 4096;
 template <int R, bool STAGE>
 __global__ void __launch_bounds__(256, 2) k_gen_mf(const cx *__restrict__ V, GenParams p,
                                                 const int32_t *__restrict__ votes,
-                                                int32_t *__restrict__ mf_top, int64_t nchunk) {
+                                                int32_t *__restrict__ mf_top, int64_t nchunk, int mfl) {
     constexpr bool stage = STAGE;
     extern __shared__ cx s_phi[];
     __shared__ int s_list[MF_LIST];
@@ -1055,10 +1055,10 @@ __global__ void __launch_bounds__(256, 2) k_gen_mf(const cx *__restrict__ V, Gen
         for (int64_t i = threadIdx.x; i < (int64_t)r * p.d; i += blockDim.x) s_phi[i] = ldcx(gphi + i);
     // explicit address spaces: LDS from the staged copy, LDG otherwise
     auto phi_at = [&](int64_t i) -> cx { return stage ? s_phi[i] : ldcx(gphi + i); };
-    for (int64_t c0 = chunk * MF_LIST; c0 < p.L && c0 < (chunk + 1) * MF_LIST; c0 += MF_LIST) {
+    for (int64_t c0 = chunk * mfl; c0 < p.L && c0 < (chunk + 1) * mfl; c0 += mfl) {
         if (threadIdx.x == 0) s_n = 0;
         __syncthreads();
-        const int64_t c1 = p.L < c0 + MF_LIST ? p.L : c0 + MF_LIST;
+        const int64_t c1 = p.L < c0 + mfl ? p.L : c0 + mfl;
         for (int64_t k0 = c0; k0 < c1; k0 += blockDim.x) {   // block-uniform trip count
             const int64_t kb = k0 + threadIdx.x;
             const int a = kb < c1 ? votes[b * p.L + kb] : 0;
@@ -2209,7 +2209,15 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
         }
     }
     if (a->prune && !mf_small_done) {
-        const int64_t nch = (p.L + MF_LIST - 1) / MF_LIST;
+        // bins per CTA: MF_LIST, fewer when that leaves < 2 CTAs per SM
+        // (few long-view signals: config 5 general K = 64 had 64 CTAs)
+        int mfl = MF_LIST;
+        const char *eml = getenv("SFDT_GEN_MF_LIST");
+        if (eml) mfl = atoi(eml);
+        else
+            while (mfl > 256 && p.B * ((p.L + mfl - 1) / mfl) < 2 * (int64_t)sms) mfl >>= 1;
+        if (mfl < 32 || mfl > MF_LIST) return SFDT_EINVAL;
+        const int64_t nch = (p.L + mfl - 1) / mfl;
         const size_t phi_bytes = size_t(a->r_eff) * p.d * 16;
         const int stage = phi_bytes <= MF_SMEM_MAX;
         const size_t smem = stage ? phi_bytes : 0;
@@ -2219,9 +2227,9 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
         if (stage) {                                                                               \
             cudaFuncSetAttribute(k_gen_mf<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
                                  (int)smem);                                                       \
-            k_gen_mf<R, true><<<(unsigned)(p.B * nch), 256, smem, stream>>>(V, gp, votes, mf_top, nch); \
+            k_gen_mf<R, true><<<(unsigned)(p.B * nch), 256, smem, stream>>>(V, gp, votes, mf_top, nch, mfl); \
         } else {                                                                                   \
-            k_gen_mf<R, false><<<(unsigned)(p.B * nch), 256, 0, stream>>>(V, gp, votes, mf_top, nch); \
+            k_gen_mf<R, false><<<(unsigned)(p.B * nch), 256, 0, stream>>>(V, gp, votes, mf_top, nch, mfl); \
         }                                                                                          \
         break;
             SFDT_MF(1) SFDT_MF(2) SFDT_MF(3) SFDT_MF(4) SFDT_MF(5) SFDT_MF(6)

@@ -733,8 +733,9 @@ def test_general_long_view_vote():
 def test_general_prune_four_lanes(n, k, monkeypatch):
     """d = 2048 / 1024 with few bins: pruning with four lanes per bin (one
     512-candidate recurrence segment each, bottom-k lists merged by lane 0)
-    keeps the same columns as one lane per bin -- supports and values equal
-    bitwise -- and matches the oracle."""
+    keeps the same columns as one lane per bin, and the matched filter on
+    short bin lists per CTA (few signals) the same as on 4096-bin lists --
+    supports and values equal bitwise -- and matches the oracle."""
     B = 3
     seeds = [(81, b) for b in range(B)]
     X = np.stack([general_signal(n, k, 20.0 + 5 * b, s)[0] for b, s in enumerate(seeds)])
@@ -743,6 +744,7 @@ def test_general_prune_four_lanes(n, k, monkeypatch):
     monkeypatch.setenv("SFDT_GEN_PRUNE_LANES", "4")
     got = P.solve_general_batch(X, cfg, seeds=seeds)
     monkeypatch.setenv("SFDT_GEN_PRUNE_LANES", "1")
+    monkeypatch.setenv("SFDT_GEN_MF_LIST", "4096")   # and the matched filter's default bins per CTA
     ref = P.solve_general_batch(X, cfg, seeds=seeds)
     for b in range(B):
         g, r = got.spectrum(b).entries, ref.spectrum(b).entries

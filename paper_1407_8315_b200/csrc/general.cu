@@ -1190,7 +1190,23 @@ __global__ void __launch_bounds__(256, 2) k_gen_mf(const cx *__restrict__ V, Gen
                     if (tt < d && q2[tt] >= cut) offer(cabs_(dot(tt)), tt);
                 }
             } else {
-                for (int tt = lane; tt < d; tt += 32) offer(cabs_(dot(tt)), tt);
+                // four of the lane's candidates per step: independent dot
+                // chains (and their loads) in flight; same per-candidate
+                // arithmetic, offered in the same ascending order
+                int tt = lane;
+                for (; tt + 96 < d; tt += 128) {
+                    cx acc[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) acc[u] = mk(0.0, 0.0);
+#pragma unroll
+                    for (int j = 0; j < R; j++) {
+#pragma unroll
+                        for (int u = 0; u < 4; u++) acc[u] = cjmac(acc[u], phi_at(j * d + tt + 32 * u), w[j]);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; u++) offer(cabs_(acc[u]), tt + 32 * u);
+                }
+                for (; tt < d; tt += 32) offer(cabs_(dot(tt)), tt);
             }
             // warp merge: n_top rounds of arg-best over the lane heads
             int sel[4];

@@ -71,6 +71,11 @@ def parse():
                     help="replay each solve as a CUDA graph (SolveGraph); auto: batches of "
                          "<= 64 MiB of signals, where host launch overhead would dominate")
     ap.add_argument("--e2e-chunk", type=int, default=256)
+    ap.add_argument("--pipe-depth", type=int, default=4,
+                    help="SolvePipeline depth for graph-replayed e2e (small batches)")
+    ap.add_argument("--hold-inputs", action="store_true",
+                    help="SolvePipeline.solve_stream(hold_inputs=True): the host rows are never "
+                         "refilled, so the per-item H2D wait is skipped")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -372,7 +377,7 @@ class Solver:
             if self.gh is None:
                 seeds = self.seeds if self.a.kind == "general" else None
                 self.gh = self.P.SolvePipeline(self.cfg, self.a.batch, it, Xh.dtype, self.dev,
-                                               seeds=seeds, depth=2)
+                                               seeds=seeds, depth=self.a.pipe_depth)
             B, H = self.a.batch, Xh.shape[0]
 
             def batches():
@@ -380,7 +385,7 @@ class Solver:
                     rows = [(lo + i) % H for i in range(B)]
                     yield (Xh[rows[0]:rows[0] + B] if rows[-1] == rows[0] + B - 1 else Xh[rows])
             res = None
-            for res in self.gh.solve_stream(batches()):
+            for res in self.gh.solve_stream(batches(), hold_inputs=self.a.hold_inputs):
                 pass
             g0 = self.gh.graphs[0]
             return _GraphHostResult(res, n_signals * Xh.shape[1] * Xh.element_size(),
@@ -497,8 +502,10 @@ def gpu_arm(a):
         e2e = {"value": world * a.batch * a.e2e_steps / e2e_s, "unit": "signals/s",
                "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": int(hr.d2h_bytes),
-               "api": (("paper_1407_8315_b200.SolvePipeline (CUDA-graph host-IO solves on two streams; "
-                        "pinned host -> GPU -> host results)") if getattr(solver, "g", None) is not None else
+               "api": ((f"paper_1407_8315_b200.SolvePipeline (depth {a.pipe_depth}: CUDA-graph host-IO "
+                        "solves, each graph with its own workspace on its own stream; "
+                        + ("hold_inputs" if a.hold_inputs else "H2D waited before the next item")
+                        + "; pinned host -> GPU -> host results)") if getattr(solver, "g", None) is not None else
                        "paper_1407_8315_b200.solve_host_batch (pinned host -> GPU -> host results"
                        + ("; zero-copy: the view gather reads the (2*a_max+r_eff)*L samples of each "
                           "signal from mapped host memory" if hr.zero_copy else "") + ")"),

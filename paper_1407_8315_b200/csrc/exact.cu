@@ -742,6 +742,10 @@ __global__ void k_noniter_fin(const long long *__restrict__ segcnt, int64_t B, i
     st[25] = r[2];
     st[26] = r[3];
     st[27] = r[4];
+    // unused slots are zero: the record is a pure function of the signal
+    st[7] = 0;
+    for (int q = SFDT_ST_ITER0 + 6; q < 24; q++) st[q] = 0;
+    for (int q = 28; q < SFDT_ST_PER_SIGNAL; q++) st[q] = 0;
 }
 
 // exclusive scans of up to three per-signal stats fields -> offsets (one
@@ -928,6 +932,8 @@ __global__ void __launch_bounds__(THREADS) k_iter_count(const IterState st, int6
             syn += it[4];
             fft += it[5];
         }
+        for (int q = SFDT_ST_ITER0 + 6 * npass; q < SFDT_ST_PER_SIGNAL; q++) o[q] = 0;
+        o[7] = 0;
         o[SFDT_ST_NITER] = npass;
         o[SFDT_ST_NENTRIES] = red[0][0];
         o[SFDT_ST_NDUP] = red[1][0];

@@ -66,23 +66,63 @@ def twiddles(n_max: int, device: torch.device, inverse: bool = False) -> torch.T
 
 
 class Workspace:
-    """Grow-only byte workspace per device (the library never allocates)."""
+    """Grow-only byte workspace (the library never allocates).
 
-    _bufs: dict = {}
+    A solve writes its views, worklists and counters into the workspace it
+    is given, so two solves may share one only if they are ordered on the
+    device.  The default workspace of a solve is therefore keyed by
+    (device, stream): solves on one stream are serialised by the stream, and
+    solves on different streams get different buffers.  A captured CUDA
+    graph bakes the workspace pointer in, so SolveGraph owns a private
+    Workspace instance for its whole lifetime (pass ``workspace=`` to
+    exact_batch / solve_general_batch), frozen once captured.  A superseded
+    buffer goes back to PyTorch's caching allocator, which hands it out again
+    only in stream order on the stream it was allocated on -- the stream
+    whose solves used it -- so it is never reused under a running kernel."""
+
+    _shared: dict = {}
+
+    def __init__(self, device=None):
+        self.device = device
+        self.buf = None
+        self.frozen = False
+
+    def get(self, nbytes: int, device: torch.device) -> torch.Tensor:
+        nbytes = max(int(nbytes), 256)
+        if self.buf is None or self.buf.numel() < nbytes:
+            if self.frozen:
+                raise RuntimeError(f"workspace is frozen at {0 if self.buf is None else self.buf.numel()} "
+                                   f"bytes (captured graph) but this solve needs {nbytes}")
+            self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        return self.buf
+
+    def freeze(self):
+        """No further growth (a graph captured the buffer's address)."""
+        self.frozen = True
+        return self
 
     @classmethod
-    def get(cls, nbytes: int, device: torch.device) -> torch.Tensor:
-        buf = cls._bufs.get(device)
-        if buf is None or buf.numel() < nbytes:
-            buf = None
-            cls._bufs.pop(device, None)
-            buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
-            cls._bufs[device] = buf
-        return buf
+    def for_stream(cls, device: torch.device) -> "Workspace":
+        st = torch.cuda.current_stream(device)
+        key = (device, st.cuda_stream)
+        ws = cls._shared.get(key)
+        if ws is None:
+            ws = cls(device)
+            cls._shared[key] = ws
+        return ws
 
     @classmethod
     def release(cls):
-        cls._bufs.clear()
+        for ws in cls._shared.values():
+            ws.buf = None
+        cls._shared.clear()
+
+
+def resolve_workspace(workspace, nbytes: int, device: torch.device) -> torch.Tensor:
+    """The workspace tensor for one solve: the caller's Workspace, or the
+    (device, current stream) default."""
+    ws = workspace if workspace is not None else Workspace.for_stream(device)
+    return ws.get(nbytes, device)
 
 
 def as_device_signals(x, device: torch.device, allow_c64: bool = True):

@@ -28,7 +28,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .device import (Workspace, host_copy, as_device_signals, aux_stream, ptr, require_cuda, stream_handle,
+from .device import (resolve_workspace, host_copy, as_device_signals, aux_stream, ptr, require_cuda, stream_handle,
                      twiddles)
 from .spectral import SparseSpectrum, check_signal_shape
 
@@ -201,14 +201,16 @@ def _outputs(caps, B, device, iterative):
 
 
 def exact_batch(X, cfg: ExactConfig, iterative: bool, device=None,
-                stream_events=None, pipeline: int = 0, rms=None) -> ExactBatch:
+                stream_events=None, pipeline: int = 0, rms=None, workspace=None) -> ExactBatch:
     """Batched exact solve of X (B, n) (or (n,)) -- the device entry point.
 
     stream_events: optional (begin, end) torch.cuda.Event pair recorded around
     the HBM stream kernel (roofline instrumentation; events must have been
     recorded once so their handles exist).  rms: optional (B,) float64 CUDA
     tensor of rms(x) from an earlier solve of the same signals -- the HBM
-    pass over x is then skipped (rms is a pure function of x)."""
+    pass over x is then skipped (rms is a pure function of x).  workspace:
+    a device.Workspace to use instead of the (device, stream) default (a
+    captured graph keeps its own)."""
     t0 = time.perf_counter()
     dev = require_cuda(device if device is not None else
                        (X.device if isinstance(X, torch.Tensor) and X.is_cuda else None))
@@ -256,7 +258,7 @@ def exact_batch(X, cfg: ExactConfig, iterative: bool, device=None,
         args.ev_stream_begin = stream_events[0].cuda_event
         args.ev_stream_end = stream_events[1].cuda_event
     nbytes = lib.sfdt_exact_workspace_bytes(args)
-    ws = Workspace.get(nbytes, dev)
+    ws = resolve_workspace(workspace, nbytes, dev)
     _lib.check(lib.sfdt_exact_solve(args, ws.data_ptr(), ws.numel(), stream_handle(dev)),
                "sfdt_exact_solve")
     if rms is not None:

@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .device import Workspace, as_device_signals, host_copy, ptr, require_cuda, stream_handle, twiddles
+from .device import as_device_signals, resolve_workspace, host_copy, ptr, require_cuda, stream_handle, twiddles
 from .spectral import SparseSpectrum, check_signal_shape
 
 
@@ -171,7 +171,7 @@ class GeneralPlan:
 
 def solve_general_batch(X, cfg: GeneralConfig, seeds=None, device=None,
                         plan: GeneralPlan | None = None, zero_copy: bool = False,
-                        fft_events=None) -> GeneralBatch:
+                        fft_events=None, workspace=None) -> GeneralBatch:
     """Batched solve_general.  seeds: None (cfg.rng_seed for every signal) or
     one rng_seed per signal (per-signal shift draws); plan: precomputed
     GeneralPlan for repeated batches.
@@ -235,7 +235,7 @@ def solve_general_batch(X, cfg: GeneralConfig, seeds=None, device=None,
     if fft_events is not None:   # (begin, end) around the view gather + FFT (roofline timing)
         a.ev_fft_begin, a.ev_fft_end = fft_events[0].cuda_event, fft_events[1].cuda_event
     nbytes = lib.sfdt_general_workspace_bytes(a)
-    ws = Workspace.get(nbytes, dev)
+    ws = resolve_workspace(workspace, nbytes, dev)
     _lib.check(lib.sfdt_general_solve(a, ws.data_ptr(), ws.numel(), stream_handle(dev)),
                "sfdt_general_solve")
     o["_keep"] = (sh_d, phi_d, tw, X)   # X: a zero-copy host source stays alive with the results
@@ -270,7 +270,7 @@ def estimate_collisions(syndromes, k: int, a_max: int, d: int,
     sd = torch.from_numpy(syndromes).to(dev)
     votes = torch.empty(nb, dtype=torch.int32, device=dev)
     sv = torch.empty((nb, a_max), dtype=torch.float64, device=dev)
-    ws = Workspace.get(lib.sfdt_estimate_collisions_workspace_bytes(nb), dev)
+    ws = resolve_workspace(None, lib.sfdt_estimate_collisions_workspace_bytes(nb), dev)
     _lib.check(lib.sfdt_estimate_collisions(sd.data_ptr(), nb, ld, int(k), int(a_max), int(d),
                                             float(zero_vote_rtol), votes.data_ptr(), sv.data_ptr(),
                                             ws.data_ptr(), ws.numel(), stream_handle(dev)),

@@ -26,7 +26,7 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from .device import require_cuda
+from .device import Workspace, require_cuda
 from .exact import ExactBatch, ExactConfig, exact_batch
 from .general import GeneralBatch, GeneralConfig, GeneralPlan, solve_general_batch
 from .spectral import check_signal_shape
@@ -48,6 +48,10 @@ class SolveGraph:
         self.X = torch.zeros((self.batch, n), dtype=dtype, device=dev)
         self.host_io = bool(host_io)
         self.host_input = torch.zeros((self.batch, n), dtype=dtype, pin_memory=True) if host_io else None
+        # the graph's own workspace: sized by the warm-up solve, frozen for
+        # the capture and referenced for the graph's lifetime (the captured
+        # kernels hold its address)
+        self.workspace = Workspace(dev)
 
         # warm-up on a side stream: twiddle tables, the workspace, output
         # capacities and kernel attributes are set up outside the capture
@@ -58,6 +62,7 @@ class SolveGraph:
             self._launch()
         cur.wait_stream(side)
         torch.cuda.synchronize(dev)
+        self.workspace.freeze()
 
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
@@ -90,8 +95,9 @@ class SolveGraph:
 
     def _launch(self):
         if self.general:
-            return solve_general_batch(self.X, self.cfg, device=self.device, plan=self.plan)
-        return exact_batch(self.X, self.cfg, self.iterative, self.device)
+            return solve_general_batch(self.X, self.cfg, device=self.device, plan=self.plan,
+                                       workspace=self.workspace)
+        return exact_batch(self.X, self.cfg, self.iterative, self.device, workspace=self.workspace)
 
     def _wrap(self):
         if self.general:
@@ -143,15 +149,21 @@ class SolveGraph:
 
 class SolvePipeline:
     """A stream of small solves through `depth` host-IO SolveGraphs, each on
-    its own CUDA stream, so the H2D of one batch overlaps the kernels of the
-    previous one (the copy engine and the SMs work side by side).
+    its own CUDA stream and with its own workspace, so the H2D of one batch
+    and the kernels of the previous ones run side by side (the copy engine
+    and the SMs work concurrently, and independent solves share the SMs).
 
         pipe = SolvePipeline(ExactConfig(n=1 << 16, k=64), batch=1)
-        for res in pipe.solve_stream(xs):   # xs: iterable of pinned (B, n) tensors
+        for res in pipe.solve_stream(xs):   # xs: iterable of (B, n) inputs
             res.spectrum(0)                 # valid until the next result is drawn
 
     Results come back in submission order; each is the same as
-    SolveGraph.solve_host on that input."""
+    SolveGraph.solve_host on that input.  A pinned contiguous input is copied
+    to the GPU straight from the caller's memory; solve_stream waits for that
+    copy to finish before it hands control back to the caller, so a producer
+    may refill one pinned buffer for every item.  hold_inputs=True skips that
+    wait: the caller then guarantees each input stays unchanged until its
+    result has been drawn."""
 
     def __init__(self, cfg, batch: int = 1, iterative: bool = False,
                  dtype=torch.complex128, device=None, seeds=None, depth: int = 2):
@@ -161,6 +173,8 @@ class SolvePipeline:
                        for _ in range(depth)]
         dev = self.graphs[0].device
         self.streams = [torch.cuda.Stream(dev) for _ in range(depth)]
+        self.h2d_done = [torch.cuda.Event() for _ in range(depth)]
+        self.done = [torch.cuda.Event() for _ in range(depth)]
 
     def _submit(self, slot: int, x):
         g, st = self.graphs[slot], self.streams[slot]
@@ -173,28 +187,32 @@ class SolvePipeline:
         st.wait_stream(torch.cuda.current_stream(g.device))
         with torch.cuda.stream(st):
             g.X.copy_(x.reshape(g.X.shape), non_blocking=True)
+            self.h2d_done[slot].record(st)
             g.graph.replay()
-            ev = torch.cuda.Event()
-            ev.record(st)
-        return ev
+            self.done[slot].record(st)
 
-    def _collect(self, slot: int, ev):
-        ev.synchronize()
+    def _collect(self, slot: int):
+        self.done[slot].synchronize()
         g = self.graphs[slot]
         res = g._wrap()
         res._host = _host_view({k: v.numpy() for k, v in g._host_out.items()}, g.general)
         return res
 
-    def solve_stream(self, xs):
+    def solve_stream(self, xs, hold_inputs: bool = False):
         depth = len(self.graphs)
-        pending = []   # (slot, event) in submission order
+        pending = []   # slots in submission order
         for i, x in enumerate(xs):
             slot = i % depth
             if len(pending) == depth:   # the slot's previous result is drawn first
-                yield self._collect(*pending.pop(0))
-            pending.append((slot, self._submit(slot, x)))
+                yield self._collect(pending.pop(0))
+            self._submit(slot, x)
+            pending.append(slot)
+            if not hold_inputs:
+                # the caller regains control (next item / next result) only
+                # once x has been read
+                self.h2d_done[slot].synchronize()
         while pending:
-            yield self._collect(*pending.pop(0))
+            yield self._collect(pending.pop(0))
 
 
 def _host_view(full: dict, general: bool) -> dict:

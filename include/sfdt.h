@@ -197,6 +197,15 @@ size_t sfdt_general_workspace_bytes(const sfdt_general_args *args);
 int sfdt_general_solve(sfdt_general_args *args, void *workspace, size_t workspace_bytes,
                        sfdt_stream_t stream);
 
+/* ------------------------------------------------------ latency path */
+/* One small solve of SolvePipeline (graph.py): H2D of `bytes` from pinned
+ * host memory into the captured graph's input buffer, event ev_h2d_done
+ * (the host may then reuse host_src), replay of the instantiated graph
+ * (a cudaGraphExec_t holding one complete solve + the D2H of its results),
+ * event ev_done -- all on `stream`.  Events may be NULL. */
+int sfdt_graph_submit(const void *host_src, void *dev_dst, size_t bytes, void *graph_exec,
+                      sfdt_stream_t stream, void *ev_h2d_done, void *ev_done);
+
 #ifdef __cplusplus
 }
 #endif

@@ -89,6 +89,7 @@ EXPORTS = {
     "sfdt_general_caps": (_int, [ctypes.POINTER(GeneralArgs), ctypes.POINTER(_i64)]),
     "sfdt_general_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(GeneralArgs)]),
     "sfdt_general_solve": (_int, [ctypes.POINTER(GeneralArgs), _vp, ctypes.c_size_t, _vp]),
+    "sfdt_graph_submit": (_int, [_vp, _vp, ctypes.c_size_t, _vp, _vp, _vp, _vp]),
 }
 
 _lib = None

@@ -26,6 +26,7 @@ from __future__ import annotations
 import numpy as np
 import torch
 
+from . import _lib
 from .device import Workspace, require_cuda
 from .exact import ExactBatch, ExactConfig, exact_batch
 from .general import GeneralBatch, GeneralConfig, GeneralPlan, solve_general_batch
@@ -91,6 +92,7 @@ class SolveGraph:
                     v = self.t[k]
                     self._host_out[k] = self._host_pack[off:off + f.numel()].view(v.dtype).reshape(v.shape)
                     off += f.numel()
+                self._host_np = {k: v.numpy() for k, v in self._host_out.items()}
         torch.cuda.synchronize(dev)
 
     def _launch(self):
@@ -138,8 +140,7 @@ class SolveGraph:
         self.graph.replay()
         torch.cuda.current_stream(self.device).synchronize()
         res = self._wrap()
-        h = {k: v.numpy() for k, v in self._host_out.items()}
-        res._host = _host_view(h, self.general)
+        res._host = _host_view(self._host_np, self.general)
         return res
 
     @property
@@ -175,27 +176,34 @@ class SolvePipeline:
         self.streams = [torch.cuda.Stream(dev) for _ in range(depth)]
         self.h2d_done = [torch.cuda.Event() for _ in range(depth)]
         self.done = [torch.cuda.Event() for _ in range(depth)]
+        for st, e1, e2 in zip(self.streams, self.h2d_done, self.done):
+            e1.record(st)   # materialise the event handles
+            e2.record(st)
+        torch.cuda.synchronize(dev)
+        # raw handles for sfdt_graph_submit: H2D + event + graph launch +
+        # event in one native call per item
+        self._raw = [(g.X.data_ptr(), g.X.numel() * g.X.element_size(), g.graph.raw_cuda_graph_exec(),
+                      st.cuda_stream, e1.cuda_event, e2.cuda_event)
+                     for g, st, e1, e2 in zip(self.graphs, self.streams, self.h2d_done, self.done)]
+        self._lib = _lib.load()
 
     def _submit(self, slot: int, x):
-        g, st = self.graphs[slot], self.streams[slot]
+        g = self.graphs[slot]
         if not isinstance(x, torch.Tensor):
             x = torch.from_numpy(np.ascontiguousarray(x))
-        if not (x.device.type == "cpu" and x.is_pinned() and x.dtype == g.host_input.dtype
-                and x.is_contiguous() and x.numel() == g.host_input.numel()):
+        if not (x.device.type == "cpu" and x.dtype == g.host_input.dtype and x.is_contiguous()
+                and x.numel() == g.host_input.numel() and x.is_pinned()):
             g.host_input.copy_(x.reshape(g.host_input.shape))
             x = g.host_input
-        st.wait_stream(torch.cuda.current_stream(g.device))
-        with torch.cuda.stream(st):
-            g.X.copy_(x.reshape(g.X.shape), non_blocking=True)
-            self.h2d_done[slot].record(st)
-            g.graph.replay()
-            self.done[slot].record(st)
+        dst, nbytes, gexec, st, e1, e2 = self._raw[slot]
+        _lib.check(self._lib.sfdt_graph_submit(x.data_ptr(), dst, nbytes, gexec, st, e1, e2),
+                   "sfdt_graph_submit")
 
     def _collect(self, slot: int):
         self.done[slot].synchronize()
         g = self.graphs[slot]
         res = g._wrap()
-        res._host = _host_view({k: v.numpy() for k, v in g._host_out.items()}, g.general)
+        res._host = _host_view(g._host_np, g.general)
         return res
 
     def solve_stream(self, xs, hold_inputs: bool = False):

@@ -151,11 +151,16 @@ _REF = None
 
 
 def backend(kind: str = "port"):
-    """Kernel namespace: "port" (oracle/kernels.c) or "reference" (the
-    reference's own compiled _core from oracle/_ref)."""
+    """Kernel namespace: "port" (oracle/kernels.c), "reference" (the
+    reference's own compiled _core from oracle/_ref) or "numpy" (the
+    restated pure-numpy backend, oracle/numpy_kernels.py: the reference's
+    second backend, used to measure its own numerical envelope)."""
     global _REF
     if kind == "port":
         return _PORT
+    if kind == "numpy":
+        from .numpy_kernels import BACKEND
+        return BACKEND
     if kind != "reference":
         raise ValueError(kind)
     if _REF is None:

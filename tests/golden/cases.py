@@ -15,7 +15,19 @@ EXACT_CASES = [
     ("n1024_k16_mu1", 1024, 16, 1, 4, "unit", 5, "numpy"),
     ("n4096_k64_mu1_a3", 4096, 64, 1, 3, "mag1_10", 6, "numpy"),
     ("n65536_k1024_mu1", 1 << 16, 1024, 1, 4, "unit", 7, "numpy"),
+    # |v| = 10^U(-8, 0): the iterative solver re-decodes a location it
+    # already wrote -> "duplicate location" warnings, last write wins
+    # (exact.py:152-158); seeds chosen by searching with the real reference
+    ("dup_n1024_k32_mu1", 1024, 32, 1, 4, "logmag", 19, "numpy"),
+    ("dup_n4096_k64_mu1", 4096, 64, 1, 4, "logmag", 36, "numpy"),
+    ("dup_n2048_k64_mu2", 2048, 64, 2, 4, "logmag", 0, "numpy"),
+    ("dup_n8192_k128_mu1_a3", 8192, 128, 1, 3, "logmag", 19, "numpy"),
 ]
+
+# cases re-run with the reference's pure-numpy backend (SFFT_DT_PURE_PYTHON=1)
+# -- pins oracle/numpy_kernels.py, the envelope backend of the parity tests
+NUMPY_BACKEND_CASES = ["cfg1", "n8192_k128_mu1", "dup_n1024_k32_mu1"]
+NUMPY_BACKEND_GENERAL = ["g_n16384_k16_20db"]
 
 GENERAL_CASES = [
     ("g_n16384_k16_20db", 16384, 16, 20.0, 11, True),

@@ -29,13 +29,13 @@ ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, HERE)
 
-from cases import EXACT_CASES, GENERAL_CASES  # noqa: E402
+from cases import EXACT_CASES, GENERAL_CASES, NUMPY_BACKEND_CASES, NUMPY_BACKEND_GENERAL  # noqa: E402
 from tests.synth import exact_signal, general_signal  # noqa: E402
 
 SCRATCH = "/tmp/sfdt_ref_golden"
 
 
-def import_reference():
+def import_reference(backend="compiled"):
     if not os.path.isdir(os.path.join(SCRATCH, "src")):
         shutil.rmtree(SCRATCH, ignore_errors=True)
         shutil.copytree("/root/reference/pkg", SCRATCH)
@@ -43,8 +43,55 @@ def import_reference():
                        check=True, capture_output=True)
     sys.path.insert(0, os.path.join(SCRATCH, "src"))
     import sfft_dt
-    assert sfft_dt.BACKEND == "compiled", sfft_dt.BACKEND
+    assert sfft_dt.BACKEND == backend, sfft_dt.BACKEND
     return sfft_dt
+
+
+def numpy_backend_main():
+    """Child process with SFFT_DT_PURE_PYTHON=1: the reference's numpy
+    backend on the kernel inputs of golden.npz and on NUMPY_BACKEND_CASES
+    -> golden_numpy.npz / .json."""
+    ref = import_reference("python")
+    from sfft_dt import _kernels as K
+    g = np.load(os.path.join(HERE, "golden.npz"))
+    arrays, meta = {}, {"exact": {}, "general": {}}
+    for n in (1, 2, 4, 8, 16, 64, 256, 512, 1024, 2048):
+        x = g[f"kern/fft/{n}/in"]
+        arrays[f"kern/fft/{n}/fwd"] = K.fft_radix2(x, inverse=False)
+        arrays[f"kern/fft/{n}/inv"] = K.fft_radix2(x, inverse=True)
+    for a in (1, 2, 3, 4):
+        m, kb = g[f"kern/a{a}/m"], g[f"kern/a{a}/k"]
+        c, cd = K.hankel_solve(m, a)
+        z = K.poly_roots(c)
+        p, pd = K.vandermonde_solve(z, m)
+        arrays.update({f"kern/a{a}/c": c, f"kern/a{a}/cd": cd, f"kern/a{a}/z": z,
+                       f"kern/a{a}/p": p, f"kern/a{a}/pd": pd,
+                       f"kern/a{a}/prune": K.prune_eval(c, kb, 1 << 12, 64),
+                       f"kern/a{a}/sv": K.hankel_singular_values(m, a)})
+    for name, n, k, mu, a_max, values, seed, synth in EXACT_CASES:
+        if name not in NUMPY_BACKEND_CASES:
+            continue
+        x, _ = exact_signal(n, k, seed, values, synth)
+        cfg = ref.ExactConfig(n=n, k=k, mu=mu, a_max=a_max)
+        rec = {}
+        for solver in ("noniterative", "iterative"):
+            spec, tr = getattr(ref, f"solve_{solver}")(x, cfg)
+            arrays[f"{name}/{solver}/locs"], arrays[f"{name}/{solver}/vals"] = pack_entries(spec.entries)
+            rec[solver] = {"full_success": tr.full_success, "warnings": tr.warnings,
+                           "unresolved_bins": [int(b) for b in tr.unresolved_bins]}
+        meta["exact"][name] = rec
+    for name, n, k, snr_db, seed, prune in GENERAL_CASES:
+        if name not in NUMPY_BACKEND_GENERAL:
+            continue
+        x, _ = general_signal(n, k, snr_db, seed)
+        spec, tr = ref.solve_general(x, ref.GeneralConfig(n=n, k=k, rng_seed=seed, prune=prune))
+        arrays[f"{name}/general/locs"], arrays[f"{name}/general/vals"] = pack_entries(spec.entries)
+        meta["general"][name] = {"collision_histogram": {str(a): c for a, c in
+                                                         tr.collision_histogram.items()}}
+    np.savez_compressed(os.path.join(HERE, "golden_numpy.npz"), **arrays)
+    with open(os.path.join(HERE, "golden_numpy.json"), "w") as fh:
+        json.dump(meta, fh, indent=1, sort_keys=True)
+    print("wrote", os.path.join(HERE, "golden_numpy.npz"))
 
 
 def sha(x):
@@ -136,7 +183,14 @@ def main():
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(meta, fh, indent=1, sort_keys=True)
     print("wrote", os.path.join(HERE, "golden.npz"))
+    # the reference's second (pure-numpy) backend, in a child process: the
+    # backend is chosen once at import (_kernels/__init__.py:11-17)
+    subprocess.run([sys.executable, os.path.abspath(__file__), "--numpy-backend"], check=True,
+                   env=dict(os.environ, SFFT_DT_PURE_PYTHON="1"))
 
 
 if __name__ == "__main__":
-    main()
+    if "--numpy-backend" in sys.argv:
+        numpy_backend_main()
+    else:
+        main()

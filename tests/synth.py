@@ -27,6 +27,13 @@ def _support_values(rng, n, k, values):
     elif values == "mag1_10":
         mag = rng.uniform(1.0, 10.0, k)
         vals = mag * np.exp(2j * np.pi * rng.random(k))
+    elif values == "logmag":
+        # magnitudes spread over 8 decades: a tone ~1e-7 of its bin partner
+        # passes the a = 1 consistency test (1e-6), so the iterative solver
+        # later re-decodes the leftover at the same location (the
+        # duplicate-overwrite path, exact.py:152-158)
+        mag = 10.0 ** rng.uniform(-8.0, 0.0, k)
+        vals = mag * np.exp(2j * np.pi * rng.random(k))
     elif values == "gauss":
         vals = (rng.standard_normal(k) + 1j * rng.standard_normal(k)) / np.sqrt(2.0)
     else:

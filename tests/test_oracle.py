@@ -186,3 +186,68 @@ def test_general_solver_matches_reference(golden, case):
     assert tr["shifts"] == rec["shifts"] and tr["d"] == rec["d"] and tr["r"] == rec["r"]
     assert {str(a): c for a, c in tr["collision_histogram"].items()} == \
         rec["collision_histogram"]
+
+
+# ------------------------------------------ the reference's numpy backend
+# oracle/numpy_kernels.py restates the reference's second backend
+# (_kernels/_reference.py); the parity tests use it for the reference's own
+# numerical envelope, so it is pinned bit-exact to that backend's outputs
+# (tests/golden/golden_numpy.npz, written by make_golden.py with
+# SFFT_DT_PURE_PYTHON=1).
+@pytest.fixture(scope="module")
+def golden_numpy():
+    import json
+    import os
+    from tests.conftest import GOLDEN_DIR
+    arrays = np.load(os.path.join(GOLDEN_DIR, "golden_numpy.npz"))
+    with open(os.path.join(GOLDEN_DIR, "golden_numpy.json")) as fh:
+        return arrays, json.load(fh)
+
+
+def test_numpy_backend_kernels_bitexact(golden, golden_numpy):
+    arrays, _ = golden
+    want, _ = golden_numpy
+    NK = OK.backend("numpy")
+    for n in (1, 2, 4, 8, 16, 64, 256, 512, 1024, 2048):
+        x = arrays[f"kern/fft/{n}/in"]
+        assert bits_equal(NK.fft_radix2(x, False), want[f"kern/fft/{n}/fwd"])
+        assert bits_equal(NK.fft_radix2(x, True), want[f"kern/fft/{n}/inv"])
+    for a in (1, 2, 3, 4):
+        m, kb = arrays[f"kern/a{a}/m"], arrays[f"kern/a{a}/k"]
+        c, cd = NK.hankel_solve(m, a)
+        assert bits_equal(c, want[f"kern/a{a}/c"]) and bits_equal(cd, want[f"kern/a{a}/cd"])
+        z = NK.poly_roots(c)
+        assert bits_equal(z, want[f"kern/a{a}/z"])
+        p, pd = NK.vandermonde_solve(z, m)
+        assert bits_equal(p, want[f"kern/a{a}/p"]) and bits_equal(pd, want[f"kern/a{a}/pd"])
+        assert bits_equal(NK.prune_eval(c, kb, 1 << 12, 64), want[f"kern/a{a}/prune"])
+        assert bits_equal(NK.hankel_singular_values(m, a), want[f"kern/a{a}/sv"])
+
+
+def test_numpy_backend_solvers_bitexact(golden_numpy):
+    from tests.golden.cases import NUMPY_BACKEND_CASES, NUMPY_BACKEND_GENERAL
+    arrays, meta = golden_numpy
+    for name, n, k, mu, a_max, values, seed, synth in EXACT_CASES:
+        if name not in NUMPY_BACKEND_CASES:
+            continue
+        x, _ = exact_signal(n, k, seed, values, synth)
+        for solver, fn in (("noniterative", OS.exact_noniterative),
+                           ("iterative", OS.exact_iterative)):
+            entries, tr = fn(x, k, mu, a_max, kernels="numpy")
+            _check_entries(entries, arrays, f"{name}/{solver}")
+            for key in ("full_success", "warnings", "unresolved_bins"):
+                assert tr[key] == meta["exact"][name][solver][key], (name, solver, key)
+    for name, n, k, snr_db, seed, prune in GENERAL_CASES:
+        if name not in NUMPY_BACKEND_GENERAL:
+            continue
+        x, _ = general_signal(n, k, snr_db, seed)
+        entries, tr = OS.general(x, k, rng_seed=seed, prune=prune, kernels="numpy")
+        _check_entries(entries, arrays, f"{name}/general")
+
+
+def test_duplicate_overwrite_cases_present(golden):
+    """The golden set holds iterative cases where the real reference warned
+    'duplicate location' (exact.py:152-158): the overwrite path is pinned."""
+    _, meta = golden
+    dups = [n for n, rec in meta["exact"].items() if rec["iterative"]["warnings"]]
+    assert len(dups) >= 3, dups

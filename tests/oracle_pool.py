@@ -32,7 +32,7 @@ def _run(job):
         raise ValueError(fn)
     # plain picklable data back to the parent
     tr = {k: (v.tolist() if isinstance(v, np.ndarray) and k != "votes" else v)
-          for k, v in tr.items() if k not in ("consecutive", "random_views", "kept", "singular_values")}
+          for k, v in tr.items() if k not in ("consecutive", "random_views", "singular_values")}
     locs = np.fromiter(want.keys(), dtype=np.int64, count=len(want))
     vals = np.fromiter(want.values(), dtype=np.complex128, count=len(want))
     return key, fn, locs, vals, tr

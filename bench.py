@@ -21,7 +21,8 @@ Reported (one JSON line from rank 0):
   roofline     the dominant kernel: exact path = k_sumsq, algorithmic bytes
                16*N (8*N complex64) per signal / its event-timed duration, vs
                MEASURED_PEAKS.json
-  cpu_baseline the reference's CPU path (oracle/_ref kernels + restated driver,
+  cpu_baseline the reference CPU path: the stock sfft_dt package (baseline/_ref) via its
+               public solve_* API when staged, else oracle/_ref kernels + restated driver
                or the oracle port) on this host's cores, bounded sample
   parity_sample  2 signals of the batch re-solved by the CPU oracle
 --impl reference times only the CPU reference path on the same config.
@@ -79,6 +80,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-restated", action="store_true",
+                    help="--impl reference: skip the restated-driver timing beside the stock one")
     ap.add_argument("--seed", type=int, default=2024)
     ap.add_argument("--pipeline", type=int, default=0,
                     help="signals per overlap chunk (0: no FFT/stream overlap)")
@@ -139,17 +142,45 @@ _CPU = {}
 
 
 def _cpu_task(i):
-    from oracle import solvers as OS
     c = _CPU
-    x = c["pool"][i % len(c["pool"])]
+    j = i % len(c["pool"])
+    x = c["pool"][j]
+    if c["kernels"] == "stock":
+        # the UNMODIFIED reference package (baseline/_ref) through its public API
+        R = c["stock"]
+        if c["kind"] == "general":
+            R.solve_general(x, R.GeneralConfig(n=x.size, k=c["k"], rng_seed=(c["seed"], j),
+                                               prune=c["prune"]))
+        elif c["solver"] == "iterative":
+            R.solve_iterative(x, R.ExactConfig(n=x.size, k=c["k"], mu=c["mu"]))
+        else:
+            R.solve_noniterative(x, R.ExactConfig(n=x.size, k=c["k"], mu=c["mu"]))
+        return 1
+    from oracle import solvers as OS
     if c["kind"] == "general":
-        OS.general(x, c["k"], rng_seed=(c["seed"], i % len(c["pool"])), kernels=c["kernels"],
-                   prune=c["prune"])
+        OS.general(x, c["k"], rng_seed=(c["seed"], j), kernels=c["kernels"], prune=c["prune"])
     elif c["solver"] == "iterative":
         OS.exact_iterative(x, c["k"], c["mu"], kernels=c["kernels"])
     else:
         OS.exact_noniterative(x, c["k"], c["mu"], kernels=c["kernels"])
     return 1
+
+
+def stock_reference():
+    """The unmodified reference package staged by `pip install --target
+    baseline/_ref` (DESIGN.md "Reference install"), or None."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "sfft_dt")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    import logging
+    logging.getLogger("sfft_dt").setLevel(logging.ERROR)   # per-solve warnings off the timed path
+    try:
+        import sfft_dt
+    except Exception:   # noqa: BLE001 -- a broken staging falls back to the restated driver
+        return None
+    return sfft_dt if sfft_dt.BACKEND == "compiled" else None
 
 
 def cpu_signal(a, i):
@@ -163,19 +194,26 @@ def cpu_signal(a, i):
     return x
 
 
-def cpu_reference(a, steps, warmup, seconds_per_step):
+def cpu_reference(a, steps, warmup, seconds_per_step, driver="auto"):
     """Time the reference CPU path on all host cores (fork pool, one signal
-    per task, generation excluded)."""
+    per task, generation excluded).  driver "auto": the stock reference
+    package (baseline/_ref) through its public solve_* API when staged,
+    else the reference's compiled kernels (oracle/_ref) under the restated
+    driver, else the oracle port; "restated": the latter two only."""
     import multiprocessing as mp
 
     from oracle import kernels as OK
-    kind = "reference" if OK.reference_core_path() else "port"
-    if kind == "reference":
-        OK.backend("reference")
+    stock = stock_reference() if driver == "auto" else None
+    if stock is not None:
+        kind = "stock"
+    else:
+        kind = "reference" if OK.reference_core_path() else "port"
+        if kind == "reference":
+            OK.backend("reference")
     cores = len(os.sched_getaffinity(0))
     npool = max(2, min(16 if a.n >= (1 << 22) else 64, max(8, cores)))
     _CPU.update(pool=[cpu_signal(a, i) for i in range(npool)], kind=a.kind, k=a.k, mu=a.mu,
-                solver=a.solver, seed=a.seed, kernels=kind, prune=not a.no_prune)
+                solver=a.solver, seed=a.seed, kernels=kind, prune=not a.no_prune, stock=stock)
     t0 = time.perf_counter()
     for i in range(2):
         _cpu_task(i)
@@ -192,13 +230,15 @@ def cpu_reference(a, steps, warmup, seconds_per_step):
                 times.append((done, dt))
     sig = sum(d for d, _ in times)
     sec = sum(t for _, t in times)
-    return {"value": sig / sec, "cores": cores, "kind": kind, "latency_s": lat,
-            "signals": sig, "seconds": sec, "per_step": per_step,
+    what = {"stock": ("the unmodified reference package sfft_dt (baseline/_ref, compiled backend) "
+                      f"through its public solve_{a.solver if a.kind == 'exact' else 'general'}()"),
+            "reference": "the reference's own compiled _core (oracle/_ref) under the restated numpy driver",
+            "port": "oracle C port"}[kind]
+    return {"value": sig / sec, "cores": cores, "kind": "port" if kind == "port" else "reference",
+            "driver": kind, "latency_s": lat, "signals": sig, "seconds": sec, "per_step": per_step,
             "sample": (f"{per_step} signal solves per step over a pool of {npool} distinct "
                        f"{a.config} signals (generation excluded), {steps} timed step(s), "
-                       f"fork pool of {cores} workers; kernels: "
-                       + ("the reference's own compiled _core (oracle/_ref) under the "
-                          "restated numpy driver" if kind == "reference" else "oracle C port"))}
+                       f"fork pool of {cores} workers; " + what)}
 
 
 # ------------------------------------------------------------------ clocks
@@ -619,7 +659,7 @@ def reference_arm(a):
     warm = min(a.warmup, 1)
     c = cpu_reference(a, steps=steps, warmup=warm,
                       seconds_per_step=max(5.0, a.cpu_seconds / max(1, steps)))
-    return {
+    out = {
         "metric": METRIC, "value": c["value"], "unit": "signals/s", "n_gpus": 0,
         "steps": steps, "warmup": warm, "ms_per_step": c["seconds"] / steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -630,6 +670,14 @@ def reference_arm(a):
                 "d2h_bytes_per_step": 0},
         "single_core_latency_s": c["latency_s"],
     }
+    if c["driver"] == "stock" and not a.no_restated:
+        # beside it: the same kernels under the restated driver (the oracle
+        # the parity tests use), to show the two time the same
+        r = cpu_reference(a, steps=1, warmup=0, seconds_per_step=max(5.0, a.cpu_seconds / 2),
+                          driver="restated")
+        out["restated_driver"] = {"value": r["value"], "unit": "signals/s", "cores": r["cores"],
+                                  "sample": r["sample"], "single_core_latency_s": r["latency_s"]}
+    return out
 
 
 def main():

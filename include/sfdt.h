@@ -182,6 +182,11 @@ typedef struct {
     double *singular_values; /* optional: batch * (n/d) * a_max */
     void *ev_fft_begin;      /* cudaEvent_t recorded right before / after the */
     void *ev_fft_end;        /* view gather + FFT kernels (optional, roofline timing) */
+    /* optional phase events (GeneralTrace.timings, general.py:295-371): after
+     * the collision vote, after pruning + matched filter, after the pursuit */
+    void *ev_vote_end;
+    void *ev_prune_end;
+    void *ev_pursuit_end;
     int32_t kernel_launches; /* out */
 } sfdt_general_args;
 
@@ -196,6 +201,73 @@ int sfdt_general_caps(const sfdt_general_args *args, int64_t *entry_cap);
 size_t sfdt_general_workspace_bytes(const sfdt_general_args *args);
 int sfdt_general_solve(sfdt_general_args *args, void *workspace, size_t workspace_bytes,
                        sfdt_stream_t stream);
+
+/* ------------------------------------------------- library functions */
+/* Device forms of the reference's per-view / per-bin library functions
+ * (the drop-in surface around the solvers).  Batched: one call covers many
+ * signals, views or bins.  Complex arrays are interleaved complex128. */
+
+/* spectral.py:151-160 downsample: out[b, v, j] = x[b, (d*j + shifts[v]) mod n],
+ * j < n/d, any n divisible by d (x complex128 or complex64 storage; out
+ * complex128) */
+int sfdt_downsample(const void *x, int32_t x_dtype, int64_t batch, int64_t n, int64_t d,
+                    const int64_t *shifts, int32_t nshift, double *out, sfdt_stream_t stream);
+/* spectral.py:163-172 transform_view / aliased_values:
+ * out[b, v, :] = fft_radix2(view_v(x_b)) / (n/d), bit-identical to the
+ * reference (the solvers' fused gather + FFT) */
+size_t sfdt_aliased_values_workspace_bytes(int64_t batch, int64_t n, int64_t d, int32_t nshift);
+int sfdt_aliased_values(const void *x, int32_t x_dtype, int64_t batch, int64_t n, int64_t d,
+                        const int64_t *shifts, int32_t nshift, const double *twiddles, double *out,
+                        void *workspace, size_t workspace_bytes, sfdt_stream_t stream);
+/* spectral.py:110-125 forward_dft_oracle: O(n^2) direct DFT / n; roots_ws
+ * holds n complex (the e^{-2 pi i q/n} table) */
+int sfdt_direct_dft(const double *x, int64_t batch, int64_t n, double *roots_ws, double *out,
+                    sfdt_stream_t stream);
+/* spectral.py:215-218 rms(x) per signal (the solvers' own HBM pass) */
+size_t sfdt_rms_workspace_bytes(int64_t batch, int64_t n);
+int sfdt_rms(const void *x, int32_t x_dtype, int64_t batch, int64_t n, double *out, void *workspace,
+             size_t workspace_bytes, sfdt_stream_t stream);
+
+/* syndrome.py:69-175 (solve_coefficients, roots_closed_form, solve_values,
+ * root_to_location, decode_bin) for nb bins: syndromes m (nb, ld), model a.
+ * upto: 1 coefficients, 2 + roots, 3 + values, 4 + locations / snap /
+ * membership against bins[] (mod n/d).  status[b]: 0 ok, 1 near-singular
+ * (Hankel / m_0), 2 degenerate root branch, 3 ill-conditioned Vandermonde,
+ * 4 zero root -- the reference's exceptions, as data; diag (nb, 2), optional:
+ * the failing test's statistic and its bound (the exception messages).
+ * upto >= 2 with a = 1 is decode_bin's ratio model (z = m1/m0, p = m0). */
+enum { SFDT_DB_OK = 0, SFDT_DB_NEAR_SINGULAR = 1, SFDT_DB_DEGENERATE = 2, SFDT_DB_ILL_CONDITIONED = 3,
+       SFDT_DB_ZERO_ROOT = 4 };
+int sfdt_decode_bins(const double *m, int64_t nb, int64_t ld, int a, int64_t n, int64_t d,
+                     const int64_t *bins, int upto, int32_t *status, double *c, double *roots,
+                     double *vals, int64_t *locs, double *snap, int32_t *member, double *diag,
+                     sfdt_stream_t stream);
+/* syndrome.py:101-106: |P(z)| for c, z (nb, a) */
+int sfdt_poly_residuals(const double *c, const double *z, int64_t nb, int a, double *out,
+                        sfdt_stream_t stream);
+/* syndrome.py:136-144: m_l = sum_j p_j z_j^l, l < count -> out (nb, count) */
+int sfdt_reconstruct_syndromes(const double *roots, const double *vals, int64_t nb, int a, int count,
+                               double *out, sfdt_stream_t stream);
+
+/* general.py:109-121 sensing_matrix: out (r, ncols) with
+ * Phi[j, t] = exp(2 pi i loc_t shifts_j / n), loc_t = (k + col_t n/d) mod n;
+ * columns NULL = 0..ncols-1 */
+int sfdt_sensing_matrix(int64_t n, int64_t d, int64_t k, const int64_t *shifts, int r,
+                        const int64_t *columns, int64_t ncols, double *out, sfdt_stream_t stream);
+/* general.py:184-221 prune_columns for nb bins (bin k[b], syndromes m (nb,
+ * ld >= 2 a_max)): kept[b, :nkept[b]] sorted; nkept[b] = -1 means all d
+ * columns.  y (nb, ldy) + shifts (r): the correlation fallback /
+ * augmentation (NULL: none).  keep_per_collision * a <= 64; cap >= keep*a + a. */
+int sfdt_prune_columns(const double *m, int64_t nb, int64_t ld, const int64_t *k, int a, int a_max,
+                       int64_t n, int64_t d, int keep_per_collision, const double *y, int64_t ldy,
+                       const int64_t *shifts, int r, int augment, int64_t *kept, int32_t *nkept,
+                       int64_t cap, sfdt_stream_t stream);
+/* general.py:224-269 subspace_pursuit on explicit problems: y (nb, rows),
+ * phi (nb, rows, cols) -> coef (nb, cols) dense; rankdef[b] counts the
+ * rank-deficient least-squares calls (the reference logs each).
+ * rows <= 12, 2 * min(a, cols) <= 8 (the solver's shapes). */
+int sfdt_subspace_pursuit(const double *y, const double *phi, int64_t nb, int rows, int cols, int a,
+                          int max_iter, double *coef, int32_t *rankdef, sfdt_stream_t stream);
 
 /* ------------------------------------------------------ latency path */
 /* One small solve of SolvePipeline (graph.py): H2D of `bytes` from pinned

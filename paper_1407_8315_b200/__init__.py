@@ -6,14 +6,16 @@ from .exact import (EstimateResult, ExactBatch, ExactConfig, IterationStats, Sol
                     estimate_sparsity_and_solve, exact_batch, solve_iterative,
                     solve_iterative_batch, solve_noniterative, solve_noniterative_batch)
 from .general import (CollisionEstimate, GeneralBatch, GeneralConfig, GeneralPlan, GeneralTrace,
-                      draw_shifts, estimate_collisions,
-                      solve_general, solve_general_batch)
+                      SensingMatrix, draw_shifts, estimate_collisions, prune_columns, sensing_matrix,
+                      solve_general, solve_general_batch, subspace_pursuit)
 from .graph import SolveGraph, SolvePipeline
 from .host import HostBatchResult, solve_host_batch
-from .syndrome import (DecodedBin, DegenerateBranch, IllConditioned, NearSingular,
-                       PolyCoefficients, decode_bin, root_to_location, roots_closed_form,
+from .syndrome import (DecodedBin, DecodedBins, DegenerateBranch, IllConditioned, NearSingular,
+                       PolyCoefficients, decode_bin, decode_bins, root_to_location, roots_closed_form,
                        solve_coefficients, solve_values)
-from .spectral import SparseSpectrum, as_signal, fft, snr, synthesize
+from .spectral import (AliasedSpectrum, DownsampleView, SparseSpectrum, SyndromeSet, aliased_values,
+                       aliased_values_batch, as_signal, downsample, fft, forward_dft_oracle, rms, snr,
+                       syndromes_for_bin, synthesize, transform_view)
 
 BACKEND = "b200"
 __version__ = "0.1.0"
@@ -27,7 +29,10 @@ def using_compiled() -> bool:
 __all__ = [
     "DecodedBin", "DegenerateBranch", "IllConditioned", "NearSingular", "PolyCoefficients",
     "decode_bin", "root_to_location", "roots_closed_form", "solve_coefficients", "solve_values",
-    "fft", "snr", "synthesize",
+    "fft", "snr", "synthesize", "AliasedSpectrum", "DownsampleView", "SyndromeSet", "aliased_values",
+    "aliased_values_batch", "downsample", "forward_dft_oracle", "rms", "syndromes_for_bin",
+    "transform_view", "DecodedBins", "decode_bins", "SensingMatrix", "prune_columns", "sensing_matrix",
+    "subspace_pursuit",
     "BACKEND", "EstimateResult", "ExactBatch", "ExactConfig", "HostBatchResult",
     "IterationStats", "SolverTrace", "SolveGraph", "SolvePipeline", "solve_host_batch",
     "SparseSpectrum", "as_signal", "estimate_sparsity_and_solve", "exact_batch",

@@ -63,6 +63,7 @@ class GeneralArgs(ctypes.Structure):
         ("entry_offsets", _vp), ("locs", _vp), ("vals", _vp), ("entry_cap", _i64),
         ("stats", _vp), ("votes", _vp), ("singular_values", _vp),
         ("ev_fft_begin", _vp), ("ev_fft_end", _vp),
+        ("ev_vote_end", _vp), ("ev_prune_end", _vp), ("ev_pursuit_end", _vp),
         ("kernel_launches", _i32),
     ]
 
@@ -90,7 +91,24 @@ EXPORTS = {
     "sfdt_general_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(GeneralArgs)]),
     "sfdt_general_solve": (_int, [ctypes.POINTER(GeneralArgs), _vp, ctypes.c_size_t, _vp]),
     "sfdt_graph_submit": (_int, [_vp, _vp, ctypes.c_size_t, _vp, _vp, _vp, _vp]),
+    "sfdt_downsample": (_int, [_vp, _i32, _i64, _i64, _i64, _vp, _i32, _vp, _vp]),
+    "sfdt_aliased_values_workspace_bytes": (ctypes.c_size_t, [_i64, _i64, _i64, _i32]),
+    "sfdt_aliased_values": (_int, [_vp, _i32, _i64, _i64, _i64, _vp, _i32, _vp, _vp, _vp,
+                                   ctypes.c_size_t, _vp]),
+    "sfdt_direct_dft": (_int, [_vp, _i64, _i64, _vp, _vp, _vp]),
+    "sfdt_rms_workspace_bytes": (ctypes.c_size_t, [_i64, _i64]),
+    "sfdt_rms": (_int, [_vp, _i32, _i64, _i64, _vp, _vp, ctypes.c_size_t, _vp]),
+    "sfdt_decode_bins": (_int, [_vp, _i64, _i64, _int, _i64, _i64, _vp, _int, _vp, _vp, _vp, _vp,
+                                _vp, _vp, _vp, _vp, _vp]),
+    "sfdt_poly_residuals": (_int, [_vp, _vp, _i64, _int, _vp, _vp]),
+    "sfdt_reconstruct_syndromes": (_int, [_vp, _vp, _i64, _int, _int, _vp, _vp]),
+    "sfdt_sensing_matrix": (_int, [_i64, _i64, _i64, _vp, _int, _vp, _i64, _vp, _vp]),
+    "sfdt_prune_columns": (_int, [_vp, _i64, _i64, _vp, _int, _int, _i64, _i64, _int, _vp, _i64,
+                                  _vp, _int, _int, _vp, _vp, _i64, _vp]),
+    "sfdt_subspace_pursuit": (_int, [_vp, _vp, _i64, _int, _int, _int, _int, _vp, _vp, _vp]),
 }
+
+SFDT_DB_OK, SFDT_DB_NEAR_SINGULAR, SFDT_DB_DEGENERATE, SFDT_DB_ILL_CONDITIONED, SFDT_DB_ZERO_ROOT = range(5)
 
 _lib = None
 

@@ -13,7 +13,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libsfdt_b200.so")
-CU_SOURCES = ["exact.cu", "kernels.cu", "general.cu", "runtime.cu"]
+CU_SOURCES = ["exact.cu", "kernels.cu", "general.cu", "runtime.cu", "dropin.cu"]
 C_SOURCES = ["twiddle.c"]
 HEADERS = ["cx.cuh", "common.cuh", "decode.cuh", "fft.cuh", "general.cuh"]
 NVCC_FLAGS = [

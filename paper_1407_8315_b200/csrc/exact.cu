@@ -1526,3 +1526,34 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
     a->kernel_launches = launches;
     return SFDT_OK;
 }
+
+// ------------------------------------------------------------ rms mirror
+// spectral.py:215-218 rms(x) for a batch of signals: the solver's own HBM
+// pass (k_sumsq over 16384-sample chunks, fixed-order tree), so a caller of
+// rms() gets exactly the value the solvers threshold with.
+extern "C" size_t sfdt_rms_workspace_bytes(int64_t batch, int64_t n) {
+    if (batch < 1 || n < 1) return 256;
+    const int64_t CH = n < 16384 ? n : 16384;
+    return size_t(batch) * size_t((n + CH - 1) / CH) * 8 + size_t(batch) * 8 + 256;
+}
+
+extern "C" int sfdt_rms(const void *x, int32_t x_dtype, int64_t batch, int64_t n, double *out, void *ws,
+                        size_t ws_bytes, sfdt_stream_t stream_) {
+    if (batch < 0 || n < 2 || (n & (n - 1)) || (x_dtype != SFDT_C128 && x_dtype != SFDT_C64)) return SFDT_EINVAL;
+    if (batch == 0) return SFDT_OK;
+    if (!ws || ws_bytes < sfdt_rms_workspace_bytes(batch, n)) return SFDT_EWORKSPACE;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    const int64_t CH = n < 16384 ? n : 16384, nchunk = n / CH;
+    double *partial = (double *)ws;
+    double *thr = partial + batch * nchunk;
+    constexpr int TH = 512, UN = 4;
+    const dim3 grid((unsigned)nchunk, (unsigned)batch);
+    if (x_dtype == SFDT_C64)
+        k_sumsq<1, TH, UN><<<grid, TH, 0, stream>>>(x, n, CH, partial);
+    else
+        k_sumsq<0, TH, UN><<<grid, TH, 0, stream>>>(x, n, CH, partial);
+    SFDT_CHECK_LAUNCH();
+    launch_rms(partial, batch, nchunk, n, 0.0, 1, out, thr, stream);
+    SFDT_CHECK_LAUNCH();
+    return SFDT_OK;
+}

@@ -865,7 +865,8 @@ __device__ __forceinline__ int warp_topk_merge(const double *sc, const int *id, 
 template <int RT = 0>
 __device__ __forceinline__ void subspace_pursuit_dev(const cx *y, const cx *phase, const cx *bphi, int64_t d,
                                                      int r_rt, const int *cols, int ncols, bool all_cols,
-                                                     int a_sp, SPOut &o, int lane = 0, int nlanes = 1) {
+                                                     int a_sp, SPOut &o, int lane = 0, int nlanes = 1,
+                                                     int max_iter = 10) {
     const int r = RT > 0 ? RT : r_rt;
     const int a_eff = a_sp < ncols ? a_sp : ncols;
     auto col_t = [&](int c) -> int64_t { return all_cols ? (int64_t)c : (int64_t)cols[c]; };
@@ -972,7 +973,7 @@ __device__ __forceinline__ void subspace_pursuit_dev(const cx *y, const cx *phas
         best_sup[i] = sup[i];
         best_coef[i] = coef[i];
     }
-    for (int it = 0; it < 10; it++) {
+    for (int it = 0; it < max_iter; it++) {
         // merged = union(support, top a_eff of |phi^H residual|)
         nt = top_cols(res);
         int topc[GEN_MAX_SUP];
@@ -1517,10 +1518,13 @@ __global__ void __launch_bounds__(128) k_gen_prune(const cx *__restrict__ V, Gen
                         const double v = __shfl_sync(gm, e < nk ? ks[e] : 0.0, base_lane + l);
                         const int tv = __shfl_sync(gm, e < nk ? kp[e] : 0, base_lane + l);
                         if (sub != 0 || e >= nl) continue;
-                        if (nk == cnti && !(v < ks[cnti - 1] || (v == ks[cnti - 1] && tv < kp[cnti - 1])))
-                            continue;
+                        // (value, index) order with NaN last -- botk_insert's order
+                        auto before = [&](double w, int tw) {
+                            return score_before_asc(v, w) || ((v == w || (v != v && w != w)) && tv < tw);
+                        };
+                        if (nk == cnti && !before(ks[cnti - 1], kp[cnti - 1])) continue;
                         int pos = (nk < cnti) ? nk++ : cnti - 1;
-                        while (pos > 0 && (v < ks[pos - 1] || (v == ks[pos - 1] && tv < kp[pos - 1]))) {
+                        while (pos > 0 && before(ks[pos - 1], kp[pos - 1])) {
                             ks[pos] = ks[pos - 1];
                             kp[pos] = kp[pos - 1];
                             pos--;
@@ -2197,6 +2201,7 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
                                                           wl, wlc);
     }
     SFDT_CHECK_LAUNCH();
+    if (a->ev_vote_end) cudaEventRecord((cudaEvent_t)a->ev_vote_end, stream);
     // 3-4. pruning + subspace pursuit per voted bin
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -2311,6 +2316,7 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     };
     launch_prune(two_phase ? 0 : split_a, two_phase ? 1 : 0);
     SFDT_CHECK_LAUNCH();
+    if (a->ev_prune_end) cudaEventRecord((cudaEvent_t)a->ev_prune_end, stream);
     // heavy bins (k_gen_bins) fork onto the side stream; the bins of the
     // two pursuits are disjoint (k_gen_prune routes each to one list) and
     // their shared counters are atomics
@@ -2382,6 +2388,7 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
         cudaEventDestroy(ev_fork);   // released once the pending work completes
         cudaEventDestroy(ev_join);
     }
+    if (a->ev_pursuit_end) cudaEventRecord((cudaEvent_t)a->ev_pursuit_end, stream);
     const int64_t nseg = (p.L + GEN_SEG - 1) / GEN_SEG;
     long long *segcnt = (long long *)(w + p.off_seg);
     k_gen_count<<<(unsigned)(p.B * nseg), 256, 0, stream>>>(votes, nent, p.L, nseg, segcnt);
@@ -2448,6 +2455,173 @@ extern "C" int sfdt_estimate_collisions(const double *syn, int64_t nb, int64_t l
         cudaFuncSetAttribute(k_gen_vote, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         k_gen_vote<<<1, 1024, smem, stream>>>(sv, part, (int)nparts, gp, votes, stats, wl, wlc);
     }
+    SFDT_CHECK_LAUNCH();
+    return SFDT_OK;
+}
+
+// ------------------------------------------------ drop-in library mirrors
+// general.py:109-121 sensing_matrix, :184-221 prune_columns and :224-269
+// subspace_pursuit as batched device calls (one thread per bin / problem),
+// built from the same device functions as the fused solver kernels.
+namespace {
+
+constexpr int PRUNE_MIRROR_MAX = 64;   // keep_per_collision * a supported by the mirror
+
+// Phi[j, t] = exp(2i pi loc_t shifts_j / n), loc_t = (k + col_t * n/d) mod n,
+// the phase evaluated as numpy does (2j*pi*outer(shifts, locs)/n)
+__device__ __forceinline__ cx sensing_entry(int64_t shift, int64_t loc, int64_t n) {
+    return gexp(mk(0.0, DMUL(TWO_PI, (double)(shift * loc)) / (double)n));
+}
+
+__global__ void k_sensing_matrix(int64_t n, int64_t d, int64_t k, const int64_t *__restrict__ shifts, int r,
+                                  const int64_t *__restrict__ cols, int64_t ncols, cx *__restrict__ out) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= r * ncols) return;
+    const int64_t j = i / ncols, c = i - j * ncols;
+    const int64_t col = cols ? cols[c] : c;
+    const int64_t loc = pmod(k + col * (n / d), n);
+    out[i] = sensing_entry(shifts[j], loc, n);
+}
+
+// _correlation_keep (general.py:158-165): the `cnt` columns of largest
+// |Phi^H y| (stable: ties keep the lower column), returned sorted
+__device__ int correlation_keep(const cx *y, const int64_t *sh, int r, int64_t kb, int64_t n, int64_t d, int cnt,
+                                int *out) {
+    double sc[PRUNE_MIRROR_MAX];
+    int id[PRUNE_MIRROR_MAX], nk = 0;
+    const int64_t m = n / d;
+    for (int64_t t = 0; t < d; t++) {
+        const int64_t loc = pmod(kb + t * m, n);
+        cx acc = mk(0.0, 0.0);
+        for (int j = 0; j < r; j++) acc = cadd(acc, nmul(cconj(sensing_entry(sh[j], loc, n)), y[j]));
+        topk_insert(sc, id, nk, cnt, cabs_(acc), (int)t);
+    }
+    for (int i = 0; i < nk; i++) out[i] = id[i];
+    sort_ints(out, nk);
+    return nk;
+}
+
+// prune_columns for one bin per thread.  nkept[b] = -1: every column kept
+// (all fits singular and no fallback) -- np.arange(d).
+__global__ void k_prune_columns(const cx *__restrict__ m, int64_t nb, int64_t ld, const int64_t *__restrict__ kbin,
+                                int a, int a_max, int64_t n, int64_t d, int keep, const cx *__restrict__ y,
+                                int64_t ldy, const int64_t *__restrict__ shifts, int r, int augment,
+                                int64_t *__restrict__ kept, int32_t *__restrict__ nkept, int64_t cap) {
+    const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    const int64_t kb = kbin[b];
+    const int cnt = (int)((int64_t)keep * a < d ? (int64_t)keep * a : d);
+    cx syn[8], yy[GEN_MAX_R], c[4];
+    for (int l = 0; l < 2 * a_max; l++) syn[l] = m[b * ld + l];
+    if (y)
+        for (int j = 0; j < r; j++) yy[j] = y[b * ldy + j];
+    // _fit_locator (general.py:168-181): highest non-singular order
+    int order = 0;
+    for (int o2 = a_max; o2 >= 1; o2--) {
+        double scale = 0.0;
+        for (int l = 0; l < 2 * o2; l++) scale = nanmax2(scale, cabs_(syn[l]));
+        scale = nanmax2(scale, TINY);
+        const cx cd = hankel_solve1(syn, o2, c);
+        if (cabs_(cd) > DMUL(SINGULARITY_RTOL, powa(scale, o2))) {
+            order = o2;
+            break;
+        }
+    }
+    int cols[PRUNE_MIRROR_MAX + 4];
+    int nc = 0;
+    if (order == 0) {
+        if (!y) {
+            nkept[b] = -1;
+            return;
+        }
+        nc = correlation_keep(yy, shifts, r, kb, n, d, cnt, cols);
+    } else {
+        // prune_eval (_core.pyx:319-346): recurrence z *= wd re-seeded every
+        // 512 candidates, Horner from the leading coefficient; keep the cnt
+        // smallest (argpartition then sort: ties to the lower column)
+        double ks[PRUNE_MIRROR_MAX];
+        int kp[PRUNE_MIRROR_MAX], nk = 0;
+        const cx base = gexp(mk(0.0, DMUL(TWO_PI, (double)kb) / (double)n));
+        const cx wd = gexp(mk(0.0, TWO_PI / (double)d));
+        cx zt = base;
+        for (int64_t t = 0; t < d; t++) {
+            cx acc = mk(1.0, 0.0);
+            for (int j = order - 1; j >= 0; j--) acc = cadd(gmul(acc, zt), c[j]);
+            botk_insert(ks, kp, nk, cnt, cabs_(acc), (int)t);
+            zt = ((t & 511) == 511) ? gmul(base, gexp(mk(0.0, DMUL(TWO_PI, (double)(t + 1)) / (double)d)))
+                                    : gmul(zt, wd);
+        }
+        for (int i = 0; i < nk; i++) cols[i] = kp[i];
+        sort_ints(cols, nk);
+        nc = nk;
+        if (augment && y && cnt < d) {
+            int top[4];
+            const int nt = correlation_keep(yy, shifts, r, kb, n, d, a < d ? a : (int)d, top);
+            int merged[PRUNE_MIRROR_MAX + 4];
+            nc = union_sorted(cols, nk, top, nt, merged);
+            for (int i = 0; i < nc; i++) cols[i] = merged[i];
+        }
+    }
+    for (int i = 0; i < nc && i < cap; i++) kept[b * cap + i] = cols[i];
+    nkept[b] = nc;
+}
+
+// subspace_pursuit on an explicit phi (rows x cols, row-major) per problem:
+// subspace_pursuit_dev with unit phases (1 * phi is exact), every column
+__global__ void k_subspace_pursuit(const cx *__restrict__ y, const cx *__restrict__ phi, int64_t nb, int rows,
+                                   int cols, int a, int max_iter, cx *__restrict__ coef,
+                                   int32_t *__restrict__ rankdef) {
+    const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    cx yy[GEN_MAX_R], ones[GEN_MAX_R];
+    for (int j = 0; j < rows; j++) {
+        yy[j] = y[b * rows + j];
+        ones[j] = mk(1.0, 0.0);
+    }
+    SPOut o;
+    subspace_pursuit_dev<0>(yy, ones, phi + b * (int64_t)rows * cols, cols, rows, nullptr, cols, true, a, o, 0, 1,
+                            max_iter);
+    for (int c2 = 0; c2 < cols; c2++) coef[b * cols + c2] = mk(0.0, 0.0);
+    for (int i = 0; i < o.nsup; i++) coef[b * cols + o.sup[i]] = o.coef[i];
+    if (rankdef) rankdef[b] = o.rankdef;
+}
+
+}  // namespace
+
+extern "C" int sfdt_sensing_matrix(int64_t n, int64_t d, int64_t k, const int64_t *shifts, int r,
+                                   const int64_t *columns, int64_t ncols, double *out, sfdt_stream_t stream) {
+    if (n < 1 || (n & (n - 1)) || d < 1 || n % d || r < 0 || ncols < 0 || (r && !shifts)) return SFDT_EINVAL;
+    if (!r || !ncols) return SFDT_OK;
+    const int64_t total = (int64_t)r * ncols;
+    k_sensing_matrix<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n, d, k, shifts, r, columns,
+                                                                                        ncols, (cx *)out);
+    SFDT_CHECK_LAUNCH();
+    return SFDT_OK;
+}
+
+extern "C" int sfdt_prune_columns(const double *m, int64_t nb, int64_t ld, const int64_t *k, int a, int a_max,
+                                  int64_t n, int64_t d, int keep, const double *y, int64_t ldy,
+                                  const int64_t *shifts, int r, int augment, int64_t *kept, int32_t *nkept,
+                                  int64_t cap, sfdt_stream_t stream) {
+    if (nb < 0 || a < 1 || a_max < 1 || a_max > 4 || ld < 2 * a_max || n < 1 || (n & (n - 1)) || d < 1 ||
+        n % d || keep < 1 || (int64_t)keep * a > PRUNE_MIRROR_MAX || (y && (r < 1 || r > GEN_MAX_R || !shifts)) ||
+        cap < (int64_t)keep * a + a || !kept || !nkept)
+        return SFDT_EINVAL;
+    if (nb == 0) return SFDT_OK;
+    k_prune_columns<<<(unsigned)((nb + 63) / 64), 64, 0, (cudaStream_t)stream>>>(
+        (const cx *)m, nb, ld, k, a, a_max, n, d, keep, (const cx *)y, ldy, shifts, r, augment, kept, nkept, cap);
+    SFDT_CHECK_LAUNCH();
+    return SFDT_OK;
+}
+
+extern "C" int sfdt_subspace_pursuit(const double *y, const double *phi, int64_t nb, int rows, int cols, int a,
+                                     int max_iter, double *coef, int32_t *rankdef, sfdt_stream_t stream) {
+    if (nb < 0 || rows < 1 || rows > GEN_MAX_R || cols < 1 || a < 1 || a > rows || max_iter < 0 ||
+        2 * (a < cols ? a : cols) > GEN_MAX_SUP || !y || !phi || !coef)
+        return SFDT_EINVAL;
+    if (nb == 0) return SFDT_OK;
+    k_subspace_pursuit<<<(unsigned)((nb + 63) / 64), 64, 0, (cudaStream_t)stream>>>(
+        (const cx *)y, (const cx *)phi, nb, rows, cols, a, max_iter, (cx *)coef, rankdef);
     SFDT_CHECK_LAUNCH();
     return SFDT_OK;
 }

@@ -298,10 +298,13 @@ __device__ __forceinline__ bool lstsq_qr_t(cx (&A)[C][R], const cx (&y_in)[R], c
 
 // top-`cnt` selection by score with the reference's tie rule (np.argsort
 // kind="stable" on -score: larger first, then lower index first)
+__device__ __forceinline__ bool score_before_desc(double v, double w) {   // v ranks before w (desc, NaN last)
+    return v == v && (w != w || v > w);
+}
 __device__ __forceinline__ void topk_insert(double *sc, int *id, int &len, int cnt, double v, int t) {
-    if (len == cnt && !(v > sc[cnt - 1])) return;
+    if (len == cnt && !score_before_desc(v, sc[cnt - 1])) return;
     int pos = (len < cnt) ? len++ : cnt - 1;
-    while (pos > 0 && v > sc[pos - 1]) {
+    while (pos > 0 && score_before_desc(v, sc[pos - 1])) {
         sc[pos] = sc[pos - 1];
         id[pos] = id[pos - 1];
         pos--;
@@ -311,11 +314,15 @@ __device__ __forceinline__ void topk_insert(double *sc, int *id, int &len, int c
 }
 
 // smallest-`cnt` selection (argpartition of errs): smaller first, ties keep
-// the lower index
+// the lower index; a NaN ranks after every number (numpy sorts NaN last),
+// so a NaN in the list is displaced by any later finite candidate
+__device__ __forceinline__ bool score_before_asc(double v, double w) {
+    return v == v && (w != w || v < w);
+}
 __device__ __forceinline__ void botk_insert(double *sc, int *id, int &len, int cnt, double v, int t) {
-    if (len == cnt && !(v < sc[cnt - 1])) return;
+    if (len == cnt && !score_before_asc(v, sc[cnt - 1])) return;
     int pos = (len < cnt) ? len++ : cnt - 1;
-    while (pos > 0 && v < sc[pos - 1]) {
+    while (pos > 0 && score_before_asc(v, sc[pos - 1])) {
         sc[pos] = sc[pos - 1];
         id[pos] = id[pos - 1];
         pos--;

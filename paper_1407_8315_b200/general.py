@@ -15,6 +15,7 @@ matched filter and subspace pursuit -- runs in libsfdt_b200.so.
 from __future__ import annotations
 
 import ctypes
+import logging
 import time
 from dataclasses import dataclass, field
 
@@ -24,6 +25,8 @@ import torch
 from . import _lib
 from .device import as_device_signals, resolve_workspace, host_copy, ptr, require_cuda, stream_handle, twiddles
 from .spectral import SparseSpectrum, check_signal_shape
+
+logger = logging.getLogger(__name__)
 
 
 @dataclass
@@ -62,6 +65,16 @@ class GeneralConfig:
     @property
     def r(self) -> int:
         return 3 * self.a_max
+
+
+@dataclass(frozen=True)
+class SensingMatrix:
+    """Partial-Fourier sensing matrix of one bin (general.py:73-80): rows are
+    shifted views, columns candidate frequency locations."""
+
+    matrix: np.ndarray
+    shifts: np.ndarray
+    column_locations: np.ndarray
 
 
 @dataclass(frozen=True)
@@ -171,7 +184,7 @@ class GeneralPlan:
 
 def solve_general_batch(X, cfg: GeneralConfig, seeds=None, device=None,
                         plan: GeneralPlan | None = None, zero_copy: bool = False,
-                        fft_events=None, workspace=None) -> GeneralBatch:
+                        fft_events=None, workspace=None, phase_events=None) -> GeneralBatch:
     """Batched solve_general.  seeds: None (cfg.rng_seed for every signal) or
     one rng_seed per signal (per-signal shift draws); plan: precomputed
     GeneralPlan for repeated batches.
@@ -234,6 +247,9 @@ def solve_general_batch(X, cfg: GeneralConfig, seeds=None, device=None,
     a.stats, a.votes, a.singular_values = ptr(o["stats"]), ptr(o["votes"]), ptr(o["singular_values"])
     if fft_events is not None:   # (begin, end) around the view gather + FFT (roofline timing)
         a.ev_fft_begin, a.ev_fft_end = fft_events[0].cuda_event, fft_events[1].cuda_event
+    if phase_events is not None:   # 5 events: fft begin / end, vote, prune, pursuit ends
+        e = [ev.cuda_event for ev in phase_events]
+        a.ev_fft_begin, a.ev_fft_end, a.ev_vote_end, a.ev_prune_end, a.ev_pursuit_end = e
     nbytes = lib.sfdt_general_workspace_bytes(a)
     ws = resolve_workspace(workspace, nbytes, dev)
     _lib.check(lib.sfdt_general_solve(a, ws.data_ptr(), ws.numel(), stream_handle(dev)),
@@ -244,18 +260,133 @@ def solve_general_batch(X, cfg: GeneralConfig, seeds=None, device=None,
 
 def solve_general(x, cfg: GeneralConfig):
     """Full pipeline (general.py:272-372): shifted-view FFTs, collision vote,
-    pruning, per-bin subspace pursuit; returns (spectrum, trace)."""
+    pruning, per-bin subspace pursuit; returns (spectrum, trace).
+    trace.timings carries the reference's phases -- fft, vote, prune,
+    subspace_pursuit (device time between CUDA events at the phase
+    boundaries) and total (wall clock of the call)."""
     t0 = time.perf_counter()
     if isinstance(x, torch.Tensor):
         check_signal_shape(x.shape)
     else:
         x = np.asarray(x)
         check_signal_shape(x.shape)
-    res = solve_general_batch(x, cfg)
+    dev = require_cuda(x.device if isinstance(x, torch.Tensor) and x.is_cuda else None)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    for e in ev:   # materialise the handles
+        e.record(torch.cuda.current_stream(dev))
+    res = solve_general_batch(x, cfg, device=dev, phase_events=ev)
     spec = res.spectrum(0)
     tr = res.trace(0)
-    tr.timings = {"total": time.perf_counter() - t0}
+    ms = [ev[i].elapsed_time(ev[i + 1]) / 1e3 for i in range(4)]
+    tr.timings = {"fft": ms[0], "vote": ms[1], "prune": ms[2], "subspace_pursuit": ms[3],
+                  "total": time.perf_counter() - t0}
+    nrd = int(res.to_host()["stats"][0][_lib.SFDT_GS_RANKDEF])
+    if nrd:
+        # general.py:243-244 logs one warning per rank-deficient least
+        # squares; the device counts them per signal
+        logger.warning("rank-deficient least squares on %d pursuit support(s)", nrd)
     return spec, tr
+
+
+def sensing_matrix(n: int, d: int, k: int, shifts, columns=None) -> SensingMatrix:
+    """Phi[j, t] = exp(2i pi (k + t n/d) shifts[j] / n) over the selected
+    candidate columns, all d when columns is None (general.py:109-121), built
+    on the GPU with numpy's phase evaluation."""
+    shifts = np.ascontiguousarray(shifts, dtype=np.int64)
+    m = n // d
+    cols = np.arange(d, dtype=np.int64) if columns is None else np.ascontiguousarray(columns, dtype=np.int64)
+    locs = (k + cols * m) % n
+    dev = require_cuda()
+    out = torch.empty((shifts.size, cols.size, 2), dtype=torch.float64, device=dev)
+    if shifts.size and cols.size:
+        sh = torch.from_numpy(shifts).to(dev)
+        cd = torch.from_numpy(cols).to(dev)
+        _lib.check(_lib.load().sfdt_sensing_matrix(int(n), int(d), int(k), sh.data_ptr(), shifts.size,
+                                                   cd.data_ptr(), cols.size, out.data_ptr(), stream_handle(dev)),
+                   "sfdt_sensing_matrix")
+    phi = out.cpu().numpy().view(np.complex128).reshape(shifts.size, cols.size)
+    return SensingMatrix(matrix=phi, shifts=shifts, column_locations=locs)
+
+
+PRUNE_MAX_KEEP = 64   # keep_per_collision * a of the device mirror
+
+
+def prune_columns(m, a: int, k: int, n: int, d: int, a_max: int | None = None,
+                  keep_per_collision: int = 2, fallback=None,
+                  augment_with_correlation: bool = False) -> np.ndarray:
+    """Candidate columns of one bin surviving the locator-polynomial test
+    (general.py:184-221), on the GPU: Hankel fit of order a_max descending
+    past singular fits, |P(z)| over the d candidate roots (the reference's
+    recurrence), the keep_per_collision * a smallest, sorted.  All fits
+    singular: the correlation fallback when fallback=(y, shifts), else every
+    column.  augment_with_correlation unions the top-a correlation columns."""
+    m = np.ascontiguousarray(m, dtype=np.complex128)
+    if a < 1:
+        raise ValueError("a must be >= 1")
+    if a_max is None:
+        a_max = max(a, min(len(m) // 2, 4))
+    if not 1 <= a_max <= 4:
+        raise ValueError(f"collision count must be 1..4, got {a_max}")
+    if len(m) < 2 * a_max:
+        raise ValueError(f"need at least {2 * a_max} syndromes, got {len(m)}")
+    if keep_per_collision * a > PRUNE_MAX_KEEP:
+        raise ValueError(f"keep_per_collision * a = {keep_per_collision * a} exceeds the device "
+                         f"mirror's {PRUNE_MAX_KEEP}")
+    dev = require_cuda()
+    lib = _lib.load()
+    md = torch.from_numpy(m[:2 * a_max].view(np.float64).copy()).to(dev)
+    kd = torch.tensor([int(k)], dtype=torch.int64, device=dev)
+    yd = shd = None
+    r = 0
+    if fallback is not None:
+        y, sh = fallback
+        y = np.ascontiguousarray(y, dtype=np.complex128).ravel()
+        sh = np.ascontiguousarray(sh, dtype=np.int64).ravel()
+        r = y.size
+        if r != sh.size or not 1 <= r <= 12:
+            raise ValueError("fallback (y, shifts) must pair 1..12 views")
+        yd = torch.from_numpy(y.view(np.float64)).to(dev)
+        shd = torch.from_numpy(sh).to(dev)
+    cap = keep_per_collision * a + a
+    kept = torch.empty(cap, dtype=torch.int64, device=dev)
+    nk = torch.empty(1, dtype=torch.int32, device=dev)
+    _lib.check(lib.sfdt_prune_columns(md.data_ptr(), 1, 2 * a_max, kd.data_ptr(), int(a), int(a_max), int(n),
+                                      int(d), int(keep_per_collision), ptr(yd), r, ptr(shd), r,
+                                      int(bool(augment_with_correlation)), kept.data_ptr(), nk.data_ptr(), cap,
+                                      stream_handle(dev)), "sfdt_prune_columns")
+    count = int(nk.item())
+    if count < 0:
+        return np.arange(d, dtype=np.int64)
+    return kept[:count].cpu().numpy()
+
+
+def subspace_pursuit(y, phi, a: int, max_iter: int = 10) -> np.ndarray:
+    """Greedy a-sparse solve of y ~ phi @ coef (general.py:224-269) on the
+    GPU: top-a correlation start, then merge / least squares (gelsd
+    semantics: Householder QR, minimum-norm SVD when rank deficient) /
+    keep top-a / least squares until the residual stops shrinking by 1e-12
+    or max_iter.  Returns the dense coefficient vector over phi's columns.
+    Shapes of the solver: rows <= 12, min(a, cols) <= 4."""
+    y = np.ascontiguousarray(y, dtype=np.complex128).ravel()
+    phi = np.ascontiguousarray(phi, dtype=np.complex128)
+    rows, cols = phi.shape
+    if a < 1 or a > rows:
+        raise ValueError(f"sparsity {a} outside [1, rows={rows}]")
+    if rows > 12 or min(a, cols) > 4:
+        raise ValueError(f"the device pursuit takes rows <= 12 and min(a, cols) <= 4, got rows={rows}, "
+                         f"a={a}, cols={cols}")
+    dev = require_cuda()
+    yd = torch.from_numpy(y.view(np.float64)).to(dev)
+    pd = torch.from_numpy(phi.view(np.float64)).to(dev)
+    coef = torch.empty((cols, 2), dtype=torch.float64, device=dev)
+    rd = torch.zeros(1, dtype=torch.int32, device=dev)
+    _lib.check(_lib.load().sfdt_subspace_pursuit(yd.data_ptr(), pd.data_ptr(), 1, rows, cols, int(a),
+                                                 int(max_iter), coef.data_ptr(), rd.data_ptr(),
+                                                 stream_handle(dev)), "sfdt_subspace_pursuit")
+    nrd = int(rd.item())
+    if nrd:
+        logger.warning("rank-deficient least squares in %d pursuit step(s)", nrd)
+    return coef.cpu().numpy().view(np.complex128).ravel()
 
 
 def estimate_collisions(syndromes, k: int, a_max: int, d: int,

@@ -1400,7 +1400,7 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
             default: rc = launch_decode_noniter<8>(Vc, nb, p.L, a->a_max, p.n, thr + c0, stc, blc, bvc, wl + c0 * p.L, wlc + c, aux, actc, awlc_p, wlc + 64 + c); break;
             }
             if (rc) return rc;
-            launches += 1 + fft_view_launches(p.L, (int)p.S) + 1 + (a->a_max > 1 ? 1 : 0) + (dense ? 1 : 0);
+            launches += 1 + fft_view_launches(p.L, (int)p.S, is_c64) + 1 + (a->a_max > 1 ? 1 : 0) + (dense ? 1 : 0);
         }
         if (aux != stream) {
             if (cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming) != cudaSuccess) return SFDT_ECUDA;
@@ -1522,7 +1522,7 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
                                                         a->locs, (cx *)a->vals, a->unres_bins,
                                                         a->dup_locs);
     SFDT_CHECK_LAUNCH();
-    launches += (int)p.npass * (1 + 2 + fft_view_launches(p.L, 2)) + 1 + 1 + 1 + 1;   // final, count, scan, emit
+    launches += (int)p.npass * (1 + 2 + fft_view_launches(p.L, 2, is_c64)) + 1 + 1 + 1 + 1;   // final, count, scan, emit
     a->kernel_launches = launches;
     return SFDT_OK;
 }

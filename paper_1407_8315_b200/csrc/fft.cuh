@@ -18,6 +18,7 @@
 
 #include "common.cuh"
 #include <cstdlib>
+#include <type_traits>
 
 namespace sfdt {
 
@@ -121,7 +122,38 @@ __device__ __forceinline__ void group_stages(cx (&x)[1 << NST], int lo, int h, c
     }
 }
 
+// group_stages with every twiddle of the group loaded up front (2^NST - 1
+// independent loads in flight instead of one dependent round trip per
+// stage); same butterflies, same twiddles -- for kernels with register room
 template <int NST>
+__device__ __forceinline__ void group_stages_pre(cx (&x)[1 << NST], int lo, int h, const cx *__restrict__ tw) {
+    constexpr int G = 1 << NST;
+    cx w[G - 1];
+#pragma unroll
+    for (int st = 0; st < NST; st++) {
+        const int Hs = h << st;
+#pragma unroll
+        for (int qk = 0; qk < (1 << st); qk++)
+            w[(1 << st) - 1 + qk] = (Hs == 1) ? mk(1.0, 0.0) : ldcx(tw + (Hs - 1) + lo + qk * h);
+    }
+#pragma unroll
+    for (int st = 0; st < NST; st++) {
+        const bool one = ((h << st) == 1);
+#pragma unroll
+        for (int qk = 0; qk < (1 << st); qk++) {
+            const cx ww = w[(1 << st) - 1 + qk];
+#pragma unroll
+            for (int q = qk; q < G; q += (2 << st)) {
+                const cx u = x[q];
+                const cx t = one ? x[q + (1 << st)] : gmul(x[q + (1 << st)], ww);
+                x[q] = cadd(u, t);
+                x[q + (1 << st)] = csub(u, t);
+            }
+        }
+    }
+}
+
+template <int NST, bool PRE = false>
 __device__ __forceinline__ void fft_pass(cx *a, int nv, int logL, int lh, const cx *__restrict__ tw) {
     constexpr int G = 1 << NST;
     const int L = 1 << logL;
@@ -145,7 +177,8 @@ __device__ __forceinline__ void fft_pass(cx *a, int nv, int logL, int lh, const 
         cx x[G];
 #pragma unroll
         for (int q = 0; q < G; q++) x[q] = a[at(q)];
-        group_stages<NST>(x, lo, h, tw);
+        if constexpr (PRE) group_stages_pre<NST>(x, lo, h, tw);
+        else group_stages<NST>(x, lo, h, tw);
 #pragma unroll
         for (int q = 0; q < G; q++) a[at(q)] = x[q];
     }
@@ -154,7 +187,7 @@ __device__ __forceinline__ void fft_pass(cx *a, int nv, int logL, int lh, const 
 // Last pass straight to global memory: the group's outputs are scaled and
 // stored (with the activity epilogue) from registers instead of going back
 // through shared memory for a separate epilogue sweep.
-template <int NST, typename Epi>
+template <int NST, bool PRE = false, typename Epi>
 __device__ __forceinline__ void fft_pass_out(const cx *a, int nv, int logL, int lh, const cx *__restrict__ tw,
                                              Epi &&epi) {
     constexpr int G = 1 << NST;
@@ -179,12 +212,14 @@ __device__ __forceinline__ void fft_pass_out(const cx *a, int nv, int logL, int 
         cx x[G];
 #pragma unroll
         for (int q = 0; q < G; q++) x[q] = a[at(q)];
-        group_stages<NST>(x, lo, h, tw);
+        if constexpr (PRE) group_stages_pre<NST>(x, lo, h, tw);
+        else group_stages<NST>(x, lo, h, tw);
 #pragma unroll
         for (int q = 0; q < G; q++) epi(v, e0 + q * h, x[q]);
     }
 }
 
+template <bool PRE = false>
 __device__ __forceinline__ void fft_stages_smem(cx *a, int nv, int logL, int lh0, int lh1,
                                                 const cx *__restrict__ tw) {
     // up to 3 stages (radix-8 groups) per shared-memory pass (radix-16
@@ -192,9 +227,9 @@ __device__ __forceinline__ void fft_stages_smem(cx *a, int nv, int logL, int lh0
     for (int lh = lh0; lh < lh1;) {
         const int rem = lh1 - lh;
         const int nst = rem >= 3 ? 3 : rem;
-        if (nst == 3) fft_pass<3>(a, nv, logL, lh, tw);
-        else if (nst == 2) fft_pass<2>(a, nv, logL, lh, tw);
-        else fft_pass<1>(a, nv, logL, lh, tw);
+        if (nst == 3) fft_pass<3, PRE>(a, nv, logL, lh, tw);
+        else if (nst == 2) fft_pass<2, PRE>(a, nv, logL, lh, tw);
+        else fft_pass<1, PRE>(a, nv, logL, lh, tw);
         __syncthreads();
         lh += nst;
     }
@@ -574,6 +609,140 @@ static __global__ void __launch_bounds__(256) k_fft_large_b_smem(const cx *buf, 
     }
 }
 
+// ---------------------------------------------------------------------------
+// Large views, register-blocked pass A (P = 4096 points, 12 stages): thread t
+// of 256 holds 16 elements in registers through three radix-16 rounds --
+// stages 0-3 on positions 16t + k, stages 4-7 on (t & 15) + 256 (t >> 4) +
+// 16k, stages 8-11 on t + 256k -- with two shared-memory exchanges between
+// them (XOR-swizzled: conflict-free in all three access patterns).  All 16
+// strided gathers of a thread are in flight at once, and every group loads
+// its 15 twiddles up front (the 64-KiB stage table stays in L1: the gathers
+// bypass it).  Butterflies, pairs and twiddles are those of the radix-2
+// stage loop, so the blocks are bit-identical to k_fft_large_a's.
+__device__ __forceinline__ int swz16(int p) { return p ^ ((p >> 4) & 7); }
+
+__device__ __forceinline__ cx ld_stream(const cx *p) {   // no L1 allocation
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return mk(v.x, v.y);
+}
+
+static __global__ void __launch_bounds__(256, 2) k_fft_large_a16(const ViewSrc src, int logL,
+                                                                 const cx *__restrict__ tw,
+                                                                 cx *__restrict__ scratch, int ldmode) {
+    extern __shared__ double4 smem_raw[];
+    cx *a = reinterpret_cast<cx *>(smem_raw);
+    constexpr int logP = 12;
+    const int logQ = logL - logP, Q = 1 << logQ;
+    const int s = (int)(blockIdx.x % (unsigned)src.nshift);
+    const int64_t rest = blockIdx.x / (unsigned)src.nshift;
+    const int c = (int)(rest & (Q - 1));
+    const int64_t b = rest >> logQ;
+    if (src.nview && s >= __ldg(src.nview + b)) return;   // unused view
+    const int t = threadIdx.x;
+    const int rc = logQ ? (int)(__brev((unsigned)c) >> (32 - logQ)) : 0;
+    const int64_t o = (s >= src.dyn_first) ? __ldg(src.dyn_off + b * src.dyn_stride + (s - src.dyn_first))
+                                           : src.off[s];
+    // position p of the block holds block input rev12(p), view sample
+    // rev12(p)*Q + rc, i.e. x[(sample*d + shift) mod n]
+    const int64_t ib = b * src.sig_stride, io = o + (int64_t)rc * src.jstride, js = src.jstride << logQ;
+    const int rt = (int)(__brev((unsigned)t) >> 24);   // rev8(t)
+    cx x[16];
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+        const int k4 = (int)(__brev((unsigned)k) >> 28);   // rev4(k)
+        const int64_t jb = (int64_t)(k4 * 256 + rt);
+        const int64_t e = ib + ((jb * js + io) & src.wrap);
+        if (src.is_c64) {
+            const float2 f = __ldg(reinterpret_cast<const float2 *>(src.x) + e);
+            x[k] = mk((double)f.x, (double)f.y);
+        } else {
+            const cx *pp = reinterpret_cast<const cx *>(src.x) + e;
+            x[k] = ldmode == 0 ? ld_stream(pp) : ldmode == 1 ? ldcx(pp) : ld_gather(pp, 3);
+        }
+    }
+    group_stages_pre<4>(x, 0, 1, tw);                       // stages 0-3
+#pragma unroll
+    for (int k = 0; k < 16; k++) a[swz16(16 * t + k)] = x[k];
+    __syncthreads();
+    const int base2 = (t & 15) + ((t >> 4) << 8);
+#pragma unroll
+    for (int k = 0; k < 16; k++) x[k] = a[swz16(base2 + 16 * k)];
+    group_stages_pre<4>(x, t & 15, 16, tw);                 // stages 4-7
+#pragma unroll
+    for (int k = 0; k < 16; k++) a[swz16(base2 + 16 * k)] = x[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; k++) x[k] = a[swz16(t + 256 * k)];
+    group_stages_pre<4>(x, t, 256, tw);                     // stages 8-11
+    cx *dst = scratch + ((b * src.nshift + s) << logL) + ((int64_t)c << logP);
+#pragma unroll
+    for (int k = 0; k < 16; k++) stcx(dst + t + 256 * k, x[k]);
+}
+
+// Large views, register-blocked pass B: the LQ (5..7) stages left after pass
+// A act on the columns i = r + q*P (P = 2^(logL-LQ)) of each residue r.  A
+// CTA of 32 * 2^(LQ-4) threads owns 32 consecutive residues of one view:
+// thread (lane = residue, w) loads elements q = 16w + k of its column
+// straight into registers (each row 32 residues = 512 contiguous bytes),
+// runs column stages 0-3 as one radix-16 group, exchanges through shared
+// memory once, runs the remaining LQ-4 stages as radix-2^(LQ-4) groups and
+// writes the view (scale / activity epilogue) -- one read and one write of
+// the scratch for all remaining stages.  Bit-identical to the register
+// passes (same butterflies, pairs, twiddles tw[(H-1) + (i mod H)]).
+template <int LQ, bool B16_PRE>
+static __global__ void __launch_bounds__(32 << (LQ - 4), 16 >> (LQ - 4)) k_fft_large_b16(
+    const cx *__restrict__ buf, int64_t nviews, int logL, const cx *__restrict__ tw, cx *out, int nshift, int SV,
+    int64_t ldV, int scale, const double *__restrict__ thr, uint8_t *__restrict__ act,
+    const int32_t *__restrict__ nview) {
+    constexpr int R2 = LQ - 4, G2 = 1 << R2, NT = 32 << R2;
+    extern __shared__ double4 smem_raw[];
+    cx *tile = reinterpret_cast<cx *>(smem_raw);   // [q][residue], 2^LQ x 32
+    const int s0 = logL - LQ;
+    const int64_t P = int64_t(1) << s0;
+    const int64_t tiles = P >> 5;
+    const int64_t g = blockIdx.x / tiles;
+    const int64_t r0 = (blockIdx.x - g * tiles) << 5;
+    const int64_t b = g / nshift;
+    const int s = (int)(g - b * nshift);
+    if (nview && s >= __ldg(nview + b)) return;   // unused view
+    const int rl = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const cx *src = buf + (g << logL) + r0 + rl;
+    cx x[16];
+#pragma unroll
+    for (int k = 0; k < 16; k++) x[k] = ld_stream(src + (int64_t)(16 * w + k) * P);
+    // column stages 0-3: element q = 16w + k is i = r + q*P, so the group has
+    // stride h = P and i mod P = r
+    if (B16_PRE) group_stages_pre<4>(x, (int)(r0 + rl), (int)P, tw);
+    else group_stages<4>(x, (int)(r0 + rl), (int)P, tw);
+#pragma unroll
+    for (int k = 0; k < 16; k++) tile[(16 * w + k) * 32 + rl] = x[k];
+    __syncthreads();
+    const double sc = 1.0 / (double)(int64_t(1) << logL);
+    const double th = act ? thr[b] : 0.0;
+    cx *o = out + (b * SV + s) * ldV + r0 + rl;
+    // column stages 4 .. LQ-1: groups q = qb + 16k (qb < 16), 16 / G2 per thread
+#pragma unroll
+    for (int u = 0; u < 16 / G2; u++) {
+        const int qb = u * (NT / 32) + w;   // this thread's u-th group base (0..15)
+        cx y[G2];
+#pragma unroll
+        for (int k = 0; k < G2; k++) y[k] = tile[(qb + 16 * k) * 32 + rl];
+        group_stages_pre<R2>(y, (int)(r0 + rl + (int64_t)qb * P), (int)(P << 4), tw);
+#pragma unroll
+        for (int k = 0; k < G2; k++) {
+            const int64_t i = (int64_t)(qb + 16 * k) * P;
+            const cx v = scale ? mk(DMUL(y[k].re, sc), DMUL(y[k].im, sc)) : y[k];
+            stcx(o + i, v);
+            if (act) {
+                const double m2 = v.re * v.re + v.im * v.im;
+                if (m2 > th * th * (1.0 + 1e-6) || (m2 >= th * th * (1.0 - 1e-6) && cabs_(v) > th))
+                    act[(b << logL) + r0 + rl + i] = 1;
+            }
+        }
+    }
+}
+
 template <int LQ>
 static inline void launch_large_b_reg(cx *buf, int64_t nviews, int logL, int s0, const cx *tw, cx *out,
                                       int nshift, int SV, int64_t ldV, int scale, const double *thr,
@@ -622,11 +791,20 @@ static inline int large_next(int logL, int s0, bool a8, bool *smem) {
     return rem >= 4 ? 4 : rem;
 }
 
-static inline int fft_view_launches(int64_t L, int nshift = 0) {
+// pipelined pass A + one tiled pass B (complex128 input, <= 7 stages left
+// after pass A); SFDT_FFT_PIPE=0 selects the earlier plan for A/B runs
+static inline bool large_pipe(int logL, int logP, int is_c64, int nshift) {
+    const char *e = getenv("SFDT_FFT_PIPE");
+    (void)is_c64;
+    return !(e && e[0] == '0') && !large_a8(nshift) && logP == 12 && logL - logP <= 7 && logL - logP >= 5;
+}
+
+static inline int fft_view_launches(int64_t L, int nshift = 0, int is_c64 = 0) {
     if (L <= FFT_SMEM_MAX) return 1;
     const int logL = ilog2_64(L);
     const bool a8 = large_a8(nshift);
     int s0 = a8 ? 10 : large_logp(logL), n = 1;
+    if (large_pipe(logL, s0, is_c64, nshift)) return 2;
     bool sm;
     for (int k; (k = large_next(logL, s0, a8, &sm)) > 0; s0 += k) n++;
     return n;
@@ -714,6 +892,43 @@ static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, con
     const bool a8 = large_a8(src.nshift);
     const int logP = a8 ? 10 : large_logp(logL), P = 1 << logP;
     const int logQ = logL - logP;
+    if (large_pipe(logL, logP, src.is_c64, src.nshift)) {
+        // pass A: 4096-point blocks in registers (three radix-16 rounds)
+        const size_t smem = size_t(P) * 16;
+        cudaFuncSetAttribute(k_fft_large_a16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_fft_large_a16, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             (int)((2 * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024)));
+        const char *em = getenv("SFDT_A16_LD");
+        k_fft_large_a16<<<(unsigned)(nviews << logQ), 256, smem, stream>>>(src, logL, tw, large_scratch,
+                                                                         em ? atoi(em) : 1);
+        SFDT_CHECK_LAUNCH();
+        // pass B: every remaining stage in one register-blocked pass
+        const int lq = logL - logP;
+        const int64_t ctas = nviews * ((int64_t(1) << (logL - lq)) >> 5);
+        const char *ebp = getenv("SFDT_B16_PRE");
+        const bool b16pre = ebp && ebp[0] == '1';
+        switch (lq) {
+#define SFDT_B16(LQ)                                                                                      \
+    case LQ:                                                                                              \
+        if (b16pre) {                                                                                     \
+        cudaFuncSetAttribute(k_fft_large_b16<LQ, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 512 << LQ); \
+        k_fft_large_b16<LQ, true><<<(unsigned)ctas, 32 << (LQ - 4), 512 << LQ, stream>>>(large_scratch, nviews, logL, tw, \
+                                                                           out, src.nshift, SV, ldV, scale, \
+                                                                           thr, act, src.nview);           \
+        } else {                                                                                          \
+        cudaFuncSetAttribute(k_fft_large_b16<LQ, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 512 << LQ); \
+        k_fft_large_b16<LQ, false><<<(unsigned)ctas, 32 << (LQ - 4), 512 << LQ, stream>>>(large_scratch, nviews, logL, tw, \
+                                                                           out, src.nshift, SV, ldV, scale, \
+                                                                           thr, act, src.nview);           \
+        }                                                                                                 \
+        break;
+            SFDT_B16(5) SFDT_B16(6) SFDT_B16(7)
+#undef SFDT_B16
+        default: return SFDT_EINVAL;
+        }
+        SFDT_CHECK_LAUNCH();
+        return SFDT_OK;
+    }
     if (a8) {
         const size_t smem = size_t(8) * P * 16;   // 128 KiB: one CTA of 512 threads per SM
         cudaFuncSetAttribute(k_fft_large_a8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -2145,7 +2145,7 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     rc = launch_fft_views(src, p.B, p.L, a->twiddles, V, (int)p.nv, p.L, stream, fft_scratch);
     if (rc) return rc;
     if (a->ev_fft_end) cudaEventRecord((cudaEvent_t)a->ev_fft_end, stream);
-    launches += fft_view_launches(p.L, (int)p.nv);
+    launches += fft_view_launches(p.L, (int)p.nv, is_c64);
 
     // 2. collision vote (general.py:131-155)
     {

@@ -27,7 +27,9 @@
  *  - Return 0 on success, a negative SFDT_E* code otherwise (argument
  *    errors mirror the reference's ValueErrors; numerical singularity is data,
  *    never an error, as in the reference).
- *  - Reentrant for distinct workspaces; no global mutable state.
+ *  - Reentrant for distinct workspaces; no global mutable state (no
+ *    environment reads, no library-owned streams: A/B switches arrive in an
+ *    sfdt_tuning, a second stream in the args).
  */
 #ifndef SFDT_H
 #define SFDT_H
@@ -88,6 +90,26 @@ int sfdt_prune_eval(const double *c, const int64_t *k, int64_t nb, int a, int64_
 int sfdt_hankel_singular_values(const double *m, int64_t nb, int64_t ld, int a_max, double *out,
                                 sfdt_stream_t stream);
 
+/* A/B switches of measured design decisions (experiment scripts and tests
+ * select the alternatives); NULL = the measured-best defaults of
+ * sfdt_default_tuning.  Only the solve that receives the struct reads it:
+ * the library keeps no global state. */
+typedef struct {
+    int32_t fft_split;       /* large views L = 2^17..2^19: 0 register-blocked pass A + one pass B,
+                                1 the stage-split register passes (round-1 plan) */
+    int32_t gen_dedup;       /* 1: a random shift equal to a consecutive one shares that view */
+    int32_t gen_svd_closed;  /* 1: closed-form 3x3 singular values where accurate, Jacobi for the
+                                rest; 0: Jacobi for every bin */
+    int32_t gen_mf_small;    /* 1: lane groups per bin in the matched filter when d <= 32 */
+    int32_t gen_mf_list;     /* matched-filter bins per CTA: 0 auto, else 32..4096 */
+    int32_t gen_warp;        /* all-column pursuit: -1 auto, 0 thread per bin, 1 warp per bin */
+    int32_t gen_split_a;     /* heavy bins with a >= gen_split_a dealt first (0: list order) */
+    int32_t gen_prune_lanes; /* lanes per pruned bin: 0 auto, 1 or 4 */
+    int32_t gen_deal;        /* heavy bins dealt lane-major while <= gen_deal per warp (0: take counter) */
+} sfdt_tuning;
+
+void sfdt_default_tuning(sfdt_tuning *out);
+
 /* ---------------------------------------------------------- exact solver */
 typedef struct {
     /* input: batch x n signals, row-major, complex128 or complex64 */
@@ -126,6 +148,7 @@ typedef struct {
     /* optional instrumentation (host side) */
     void *ev_stream_begin;  /* cudaEvent_t recorded right before / after the */
     void *ev_stream_end;    /* HBM stream kernel (roofline timing), or NULL  */
+    const sfdt_tuning *tuning; /* optional A/B switches (NULL: defaults) */
     int32_t kernel_launches; /* out: kernels launched by the last solve */
 } sfdt_exact_args;
 
@@ -187,6 +210,12 @@ typedef struct {
     void *ev_vote_end;
     void *ev_prune_end;
     void *ev_pursuit_end;
+    /* optional second stream (cudaStream_t): the multi-collision pursuit
+     * (a tail of a few long chains) forks onto it beside the single-collision
+     * pursuit; NULL keeps everything on `stream`.  Forked and joined with
+     * events, so a solve captured into a CUDA graph captures both branches. */
+    void *aux_stream;
+    const sfdt_tuning *tuning; /* optional A/B switches (NULL: defaults) */
     int32_t kernel_launches; /* out */
 } sfdt_general_args;
 

@@ -17,6 +17,8 @@ from .spectral import (AliasedSpectrum, DownsampleView, SparseSpectrum, Syndrome
                        aliased_values_batch, as_signal, downsample, fft, forward_dft_oracle, rms, snr,
                        syndromes_for_bin, synthesize, transform_view)
 
+from ._lib import tuning
+
 BACKEND = "b200"
 __version__ = "0.1.0"
 
@@ -32,7 +34,7 @@ __all__ = [
     "fft", "snr", "synthesize", "AliasedSpectrum", "DownsampleView", "SyndromeSet", "aliased_values",
     "aliased_values_batch", "downsample", "forward_dft_oracle", "rms", "syndromes_for_bin",
     "transform_view", "DecodedBins", "decode_bins", "SensingMatrix", "prune_columns", "sensing_matrix",
-    "subspace_pursuit",
+    "subspace_pursuit", "tuning",
     "BACKEND", "EstimateResult", "ExactBatch", "ExactConfig", "HostBatchResult",
     "IterationStats", "SolverTrace", "SolveGraph", "SolvePipeline", "solve_host_batch",
     "SparseSpectrum", "as_signal", "estimate_sparsity_and_solve", "exact_batch",

@@ -7,8 +7,10 @@ device is present, calls fail loudly.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import os
+import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SFDT_LIB") or os.path.join(_HERE, "libsfdt_b200.so")
@@ -31,6 +33,13 @@ _int = ctypes.c_int
 _dbl = ctypes.c_double
 
 
+class Tuning(ctypes.Structure):
+    """sfdt_tuning (include/sfdt.h): A/B switches of measured design decisions."""
+    _fields_ = [(name, _i32) for name in (
+        "fft_split", "gen_dedup", "gen_svd_closed", "gen_mf_small", "gen_mf_list", "gen_warp",
+        "gen_split_a", "gen_prune_lanes", "gen_deal")]
+
+
 class ExactArgs(ctypes.Structure):
     _fields_ = [
         ("x", _vp), ("x_dtype", _i32), ("batch", _i64), ("n", _i64),
@@ -41,7 +50,7 @@ class ExactArgs(ctypes.Structure):
         ("dup_locs", _vp), ("dup_offsets", _vp), ("dup_cap", _i64),
         ("stats", _vp), ("rms", _vp),
         ("aux_stream", _vp), ("chunk_signals", _i64), ("rms_in", _vp),
-        ("ev_stream_begin", _vp), ("ev_stream_end", _vp), ("kernel_launches", _i32),
+        ("ev_stream_begin", _vp), ("ev_stream_end", _vp), ("tuning", _vp), ("kernel_launches", _i32),
     ]
 
 
@@ -64,6 +73,7 @@ class GeneralArgs(ctypes.Structure):
         ("stats", _vp), ("votes", _vp), ("singular_values", _vp),
         ("ev_fft_begin", _vp), ("ev_fft_end", _vp),
         ("ev_vote_end", _vp), ("ev_prune_end", _vp), ("ev_pursuit_end", _vp),
+        ("aux_stream", _vp), ("tuning", _vp),
         ("kernel_launches", _i32),
     ]
 
@@ -72,6 +82,7 @@ class GeneralArgs(ctypes.Structure):
 EXPORTS = {
     "sfdt_strerror": (ctypes.c_char_p, [_int]),
     "sfdt_version": (_int, []),
+    "sfdt_default_tuning": (None, [ctypes.POINTER(Tuning)]),
     "sfdt_last_cuda_error": (ctypes.c_char_p, []),
     "sfdt_fft_twiddles": (_int, [_i64, _int, _vp]),
     "sfdt_fft_radix2": (_int, [_vp, _vp, _i64, _i64, _int, _vp, _vp]),
@@ -111,6 +122,67 @@ EXPORTS = {
 SFDT_DB_OK, SFDT_DB_NEAR_SINGULAR, SFDT_DB_DEGENERATE, SFDT_DB_ILL_CONDITIONED, SFDT_DB_ZERO_ROOT = range(5)
 
 _lib = None
+
+# ------------------------------------------------------------ A/B switches
+# The library reads no environment: its design switches arrive as an
+# sfdt_tuning with every solve.  Defaults are the measured-best decisions;
+# `tuning(...)` overrides them for a block of calls (tests), and the SFDT_*
+# environment variables of the experiment scripts (tools/*.sh) are read ONCE,
+# at the first solve, into the process defaults.
+TUNING_DEFAULTS = dict(fft_split=0, gen_dedup=1, gen_svd_closed=1, gen_mf_small=1, gen_mf_list=0,
+                       gen_warp=-1, gen_split_a=3, gen_prune_lanes=0, gen_deal=8, gen_overlap=1)
+_ENV = None
+_local = threading.local()
+
+
+def _env_overrides() -> dict:
+    global _ENV
+    if _ENV is None:
+        e, o = os.environ.get, {}
+        if e("SFDT_FFT_SPLIT") is not None:
+            o["fft_split"] = int(e("SFDT_FFT_SPLIT"))
+        if e("SFDT_FFT_PIPE") == "0":
+            o["fft_split"] = 1
+        for var, key in (("SFDT_GEN_DEDUP", "gen_dedup"), ("SFDT_GEN_MF_SMALL", "gen_mf_small"),
+                         ("SFDT_GEN_MF_LIST", "gen_mf_list"), ("SFDT_GEN_WARP", "gen_warp"),
+                         ("SFDT_GEN_SPLIT", "gen_split_a"), ("SFDT_GEN_PRUNE_LANES", "gen_prune_lanes"),
+                         ("SFDT_GEN_DEAL", "gen_deal"), ("SFDT_GEN_OVERLAP", "gen_overlap")):
+            if e(var) is not None:
+                o[key] = int(e(var))
+        if e("SFDT_GEN_SVD") is not None:
+            o["gen_svd_closed"] = 0 if e("SFDT_GEN_SVD").startswith("j") else 1
+        _ENV = o
+    return _ENV
+
+
+def current_tuning() -> dict:
+    t = dict(TUNING_DEFAULTS)
+    t.update(_env_overrides())
+    for over in getattr(_local, "stack", []):
+        t.update(over)
+    return t
+
+
+@contextlib.contextmanager
+def tuning(**overrides):
+    """Override design switches for the solves issued inside the block
+    (keys of TUNING_DEFAULTS), e.g. ``with tuning(gen_svd_closed=0): ...``."""
+    bad = set(overrides) - set(TUNING_DEFAULTS)
+    if bad:
+        raise KeyError(f"unknown tuning keys {sorted(bad)}")
+    stack = getattr(_local, "stack", None)
+    if stack is None:
+        stack = _local.stack = []
+    stack.append(overrides)
+    try:
+        yield
+    finally:
+        stack.pop()
+
+
+def tuning_struct(t: dict | None = None) -> "Tuning":
+    t = current_tuning() if t is None else t
+    return Tuning(**{name: int(t[name]) for name, _ in Tuning._fields_})
 
 
 class SfdtError(RuntimeError):

@@ -59,6 +59,22 @@ static inline int64_t one_wave(K kernel, int threads, size_t smem = 0) {
 // python-style non-negative modulo for power-of-two n
 __host__ __device__ __forceinline__ int64_t pmod(int64_t a, int64_t n) { return a & (n - 1); }
 
+// the measured-best design decisions (sfdt_tuning, include/sfdt.h)
+static inline sfdt_tuning default_tuning() {
+    sfdt_tuning t;
+    t.fft_split = 0;
+    t.gen_dedup = 1;
+    t.gen_svd_closed = 1;
+    t.gen_mf_small = 1;
+    t.gen_mf_list = 0;
+    t.gen_warp = -1;
+    t.gen_split_a = 3;
+    t.gen_prune_lanes = 0;
+    t.gen_deal = 8;
+    return t;
+}
+static inline sfdt_tuning tuning_or_default(const sfdt_tuning *t) { return t ? *t : default_tuning(); }
+
 }  // namespace sfdt
 
 #define SFDT_CHECK_LAUNCH()                                   \

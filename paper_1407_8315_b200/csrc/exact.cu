@@ -30,16 +30,13 @@ namespace sfdt {
 // complex128, 16 B for complex64 storage -- the measured best shape on B200
 // (tools/membw.cu: 7.55 TB/s pure read).  The shift windows are not touched
 // here: the FFT kernel gathers them straight from x.
-template <int C64, int THREADS, int UNROLL, int CAP = 0>
+template <int C64, int THREADS, int UNROLL>
 __global__ void __launch_bounds__(THREADS) k_sumsq(const void *__restrict__ x_, int64_t n, int64_t CH,
-                                                  double *__restrict__ partial,
-                                                  cx *__restrict__ win = nullptr, int logd = 0,
-                                                  int S = 0) {
+                                                  double *__restrict__ partial) {
     const int64_t b = blockIdx.y;
     const int64_t chunk = blockIdx.x;
     const int64_t CHp = CH >> 1;                        // sample pairs in this chunk
     const int64_t base = (b * n + chunk * CH) >> 1;     // pair index
-    const int64_t L = n >> logd;
     double acc = 0.0;
     for (int64_t off = 0; off < CHp; off += int64_t(THREADS) * UNROLL) {
         double v[UNROLL][4];
@@ -61,21 +58,8 @@ __global__ void __launch_bounds__(THREADS) k_sumsq(const void *__restrict__ x_, 
             }
         }
 #pragma unroll
-        for (int u = 0; u < UNROLL; u++) {
+        for (int u = 0; u < UNROLL; u++)
             acc = fma(v[u][0], v[u][0], fma(v[u][1], v[u][1], fma(v[u][2], v[u][2], fma(v[u][3], v[u][3], acc))));
-            if (CAP) {
-                // shift windows: the S samples x[d*j .. d*j+S-1] opening each
-                // d-block are copied as one contiguous row win[b][j][0..S-1]
-                // (S*16 = 128 B: four adjacent lanes store a full line, so no
-                // partial-sector read-modify-write in L2)
-                const int64_t e = chunk * CH + 2 * (off + int64_t(u) * THREADS + threadIdx.x);
-                const int64_t s0 = e & ((int64_t(1) << logd) - 1);
-                if (s0 < S && e < (chunk + 1) * CH) {
-                    double *wd = reinterpret_cast<double *>(win + (b * L + (e >> logd)) * S + s0);
-                    *reinterpret_cast<double4 *>(wd) = make_double4(v[u][0], v[u][1], v[u][2], v[u][3]);
-                }
-            }
-        }
     }
     // deterministic block reduction: warp xor-tree, then fixed-order smem tree
 #pragma unroll
@@ -1165,22 +1149,11 @@ static inline size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
 struct ExactPlan {
     int64_t B, n, d, L, S, CH, nchunk, npass;
     int logd;
-    bool capture;
-    size_t off_win, off_V, off_partial, off_thr, off_status, off_bloc, off_bval, off_def,
+    size_t off_V, off_partial, off_thr, off_status, off_bloc, off_bval, off_def,
         off_sloc, off_sval, off_sa, off_sdup, off_cnt, off_resid, off_ndef, off_scratch, off_fft, off_wl,
         off_act, off_awl, off_seg,
         total;
 };
-
-// SFDT_CAPTURE=1 captures the shift windows inside the stream pass (the FFT
-// then reads contiguous window rows) instead of gathering them from x.
-// Measured on B200 at config 2: +0.64 ms in the stream kernel (16-byte
-// scattered window stores become partial-sector read-modify-writes in L2)
-// against -0.04 ms in the FFT, so the gather is the default.
-static bool capture_enabled() {
-    const char *e = getenv("SFDT_CAPTURE");
-    return e && e[0] == '1';
-}
 
 static int make_plan(const sfdt_exact_args *a, ExactPlan &p) {
     if (!a || a->batch < 1 || a->n < 2 || (a->n & (a->n - 1))) return SFDT_EINVAL;
@@ -1220,8 +1193,6 @@ static int make_plan(const sfdt_exact_args *a, ExactPlan &p) {
         p.off_ndef = take(size_t(p.B) * 8);
         p.off_awl = take(size_t(p.B) * p.L * 8);
     }
-    p.capture = (!a->iterative && !a->aux_stream && p.d >= p.S && capture_enabled());
-    p.off_win = p.capture ? take(size_t(p.B) * p.S * p.L * 16) : 0;
     p.off_scratch = take(128 * 8);
     p.off_fft = (p.L > FFT_SMEM_MAX) ? take(size_t(p.B) * p.L * p.S * 16) : 0;
     p.total = o;
@@ -1261,6 +1232,7 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
     if (a->entry_cap < ecap || a->unres_cap < ucap || (a->iterative && a->dup_locs && a->dup_cap < dcap))
         return SFDT_ECAPACITY;
     cudaStream_t stream = (cudaStream_t)stream_;
+    const sfdt_tuning tn = tuning_or_default(a->tuning);
     char *w = (char *)ws;
     cx *V = (cx *)(w + p.off_V);
     double *partial = (double *)(w + p.off_partial);
@@ -1296,20 +1268,10 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
             }
         } else {
             constexpr int TH = 512, UN = 4;
-            cx *win = p.capture ? (cx *)(w + p.off_win) + c0 * p.S * p.L : nullptr;
-            if (is_c64) {
-                if (p.capture)
-                    k_sumsq<1, TH, UN, 1><<<grid, TH, 0, stream>>>(xc, p.n, p.CH, partial + c0 * p.nchunk,
-                                                                  win, p.logd, (int)p.S);
-                else
-                    k_sumsq<1, TH, UN><<<grid, TH, 0, stream>>>(xc, p.n, p.CH, partial + c0 * p.nchunk);
-            } else {
-                if (p.capture)
-                    k_sumsq<0, TH, UN, 1><<<grid, TH, 0, stream>>>(xc, p.n, p.CH, partial + c0 * p.nchunk,
-                                                                  win, p.logd, (int)p.S);
-                else
-                    k_sumsq<0, TH, UN><<<grid, TH, 0, stream>>>(xc, p.n, p.CH, partial + c0 * p.nchunk);
-            }
+            if (is_c64)
+                k_sumsq<1, TH, UN><<<grid, TH, 0, stream>>>(xc, p.n, p.CH, partial + c0 * p.nchunk);
+            else
+                k_sumsq<0, TH, UN><<<grid, TH, 0, stream>>>(xc, p.n, p.CH, partial + c0 * p.nchunk);
         }
         SFDT_CHECK_LAUNCH();
         launches += 1;
@@ -1344,18 +1306,16 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
         }
         for (int64_t c = 0; c < nc; c++) {
             const int64_t c0 = c * bc, nb = (c0 + bc <= p.B) ? bc : p.B - c0;
-            // without window capture the views need no rms: their gather + FFT
-            // (aux) overlaps the HBM stream of the same chunk (main); with
-            // capture the FFT reads the windows the stream pass wrote
+            // the views need no rms: their gather + FFT (aux) overlaps the
+            // HBM stream of the same chunk (main)
             auto launch_fft = [&]() -> int {
-                const ViewSrc src = p.capture
-                    ? window_views((const cx *)(w + p.off_win) + c0 * p.S * p.L, (int)p.S, p.L)
-                    : consecutive_views((const char *)a->x + c0 * p.n * (is_c64 ? 8 : 16), is_c64,
-                                        p.n, p.d, 0, (int)p.S);
+                const ViewSrc src = consecutive_views((const char *)a->x + c0 * p.n * (is_c64 ? 8 : 16), is_c64,
+                                                      p.n, p.d, 0, (int)p.S);
                 return launch_fft_views(src, nb, p.L, a->twiddles, V + c0 * p.S * p.L, (int)p.S, p.L,
-                                        aux, fft_scratch ? fft_scratch + c0 * p.S * p.L : nullptr);
+                                        aux, fft_scratch ? fft_scratch + c0 * p.S * p.L : nullptr, 1, nullptr,
+                                        nullptr, tn.fft_split);
             };
-            const bool overlap = (aux != stream) && !p.capture;
+            const bool overlap = aux != stream;
             if (overlap && (rc = launch_fft())) return rc;
             if (!a->rms_in && (rc = launch_stream(c0, nb))) return rc;
             if (c == nc - 1 && a->ev_stream_end) cudaEventRecord((cudaEvent_t)a->ev_stream_end, stream);
@@ -1379,13 +1339,11 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
             uint8_t *actc = dense ? (uint8_t *)(w + p.off_act) + c0 * p.L : nullptr;
             if (!overlap) {
                 if (actc) cudaMemsetAsync(actc, 0, size_t(nb) * p.L, aux);
-                const ViewSrc src = p.capture
-                    ? window_views((const cx *)(w + p.off_win) + c0 * p.S * p.L, (int)p.S, p.L)
-                    : consecutive_views((const char *)a->x + c0 * p.n * (is_c64 ? 8 : 16), is_c64,
-                                        p.n, p.d, 0, (int)p.S);
+                const ViewSrc src = consecutive_views((const char *)a->x + c0 * p.n * (is_c64 ? 8 : 16), is_c64,
+                                                      p.n, p.d, 0, (int)p.S);
                 rc = launch_fft_views(src, nb, p.L, a->twiddles, V + c0 * p.S * p.L, (int)p.S, p.L, aux,
                                       fft_scratch ? fft_scratch + c0 * p.S * p.L : nullptr, 1,
-                                      thr + c0, actc);
+                                      thr + c0, actc, tn.fft_split);
                 if (rc) return rc;
             }
             int64_t *awlc_p = (int64_t *)(w + p.off_awl) + c0 * p.L;
@@ -1400,7 +1358,7 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
             default: rc = launch_decode_noniter<8>(Vc, nb, p.L, a->a_max, p.n, thr + c0, stc, blc, bvc, wl + c0 * p.L, wlc + c, aux, actc, awlc_p, wlc + 64 + c); break;
             }
             if (rc) return rc;
-            launches += 1 + fft_view_launches(p.L, (int)p.S, is_c64) + 1 + (a->a_max > 1 ? 1 : 0) + (dense ? 1 : 0);
+            launches += 1 + fft_view_launches(p.L, tn.fft_split) + 1 + (a->a_max > 1 ? 1 : 0) + (dense ? 1 : 0);
         }
         if (aux != stream) {
             if (cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming) != cudaSuccess) return SFDT_ECUDA;
@@ -1473,7 +1431,7 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
         const int64_t m = m_of[l];
         const ViewSrc src = consecutive_views(a->x, is_c64, p.n, d_of[l], 2 * l, 2);
         rc = launch_fft_views(src, p.B, m, a->twiddles, V + 2 * l * p.L, (int)p.S, p.L, stream,
-                              fft_scratch);
+                              fft_scratch, 1, nullptr, nullptr, tn.fft_split);
         if (rc) return rc;
         const int fold = (l > 0) && (m != m_of[l - 1]);
         const int64_t nb = p.B * m;
@@ -1522,7 +1480,7 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
                                                         a->locs, (cx *)a->vals, a->unres_bins,
                                                         a->dup_locs);
     SFDT_CHECK_LAUNCH();
-    launches += (int)p.npass * (1 + 2 + fft_view_launches(p.L, 2, is_c64)) + 1 + 1 + 1 + 1;   // final, count, scan, emit
+    launches += (int)p.npass * (1 + 2 + fft_view_launches(p.L, tn.fft_split)) + 1 + 1 + 1 + 1;   // final, count, scan, emit
     a->kernel_launches = launches;
     return SFDT_OK;
 }

@@ -42,27 +42,9 @@ struct ViewSrc {
     // per-signal number of views to compute: views v >= nview[b] are skipped
     // (their slots are never read); nullptr = all nshift views
     const int32_t *nview;
-    // load hint of the gathered samples (SFDT_GATHER_HINT): 0 __ldg,
-    // 1 no L1 + L2 64-B prefetch, 2 no L1, 3 no L1 + L2 evict_first policy
-    int ldhint;
 };
 
-__device__ __forceinline__ cx ld_gather(const cx *p, int hint) {
-    double2 v;
-    if (hint == 1) {
-        asm volatile("ld.global.nc.L1::no_allocate.L2::64B.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
-    } else if (hint == 2) {
-        asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
-    } else if (hint == 3) {
-        uint64_t pol;
-        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
-                     : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
-    } else {
-        v = __ldg(reinterpret_cast<const double2 *>(p));
-    }
-    return mk(v.x, v.y);
-}
+__device__ __forceinline__ cx ld_gather(const cx *p) { return ldcx(p); }
 
 __device__ __forceinline__ cx view_load(const ViewSrc &src, int64_t b, int v, int64_t j) {
     const int64_t o = (v >= src.dyn_first) ? __ldg(src.dyn_off + b * src.dyn_stride + (v - src.dyn_first))
@@ -72,7 +54,7 @@ __device__ __forceinline__ cx view_load(const ViewSrc &src, int64_t b, int v, in
         const float2 f = __ldg(reinterpret_cast<const float2 *>(src.x) + e);
         return mk((double)f.x, (double)f.y);
     }
-    return ld_gather(reinterpret_cast<const cx *>(src.x) + e, src.ldhint);
+    return ld_gather(reinterpret_cast<const cx *>(src.x) + e);
 }
 
 // 16-byte-granular swizzle of the shared-memory FFT buffers: the low 3 bits
@@ -266,7 +248,7 @@ __device__ __forceinline__ void fft_fused_views(cx *a, const ViewSrc &src, int64
                 const float2 f = __ldg(reinterpret_cast<const float2 *>(src.x) + e);
                 x[q] = mk((double)f.x, (double)f.y);
             } else {
-                x[q] = ld_gather(reinterpret_cast<const cx *>(src.x) + e, src.ldhint);
+                x[q] = ld_gather(reinterpret_cast<const cx *>(src.x) + e);
             }
         }
         group_stages<3>(x, 0, 1, tw);
@@ -300,7 +282,7 @@ static __global__ void __launch_bounds__(256, MINB) k_fft_views(const ViewSrc sr
     const int64_t nviews = B * src.nshift;
     const int64_t g0 = int64_t(blockIdx.x) << logvpc;
     const int nv = (int)((nviews - g0) < vpc ? (nviews - g0) : vpc);
-    if (nv <= 0) return;   // cluster padding (SFDT_FFT_CLUSTER): no views
+    if (nv <= 0) return;
     // per-view addressing, once per CTA (no 64-bit divisions or dynamically
     // indexed parameter arrays in the element loops)
     if (src.nview) {   // CTA-uniform: skip when every view of the tile is unused
@@ -369,7 +351,7 @@ static __global__ void __launch_bounds__(256, MINB) k_fft_views(const ViewSrc sr
                         const float2 f = __ldg(reinterpret_cast<const float2 *>(src.x) + e);
                         vals[u] = mk((double)f.x, (double)f.y);
                     } else {
-                        vals[u] = ld_gather(reinterpret_cast<const cx *>(src.x) + e, src.ldhint);
+                        vals[u] = ld_gather(reinterpret_cast<const cx *>(src.x) + e);
                     }
                     const int r = logL ? (int)(__brev((unsigned)j) >> (32 - logL)) : 0;
                     dst[u] = swz(v * L + r);
@@ -417,44 +399,6 @@ static __global__ void k_fft_large_a(const ViewSrc src, int logL, int logP,
     cx *dst = scratch + (g << logL) + ((int64_t)c << logP);
     fft_fused_views(a, src, src.jstride << logQ, s_ib, s_io, 1, 0, logP, tw,
                     [&](int, int k, cx y) { dst[k] = y; });
-}
-
-// Pass A for groups of up to 8 views of one signal (views with adjacent
-// shifts: a d-block's 8 samples are one 128-B line, loaded whole by 8
-// adjacent lanes): block c of each view in one CTA, 2^logP points per view,
-// the same fft_fused_views stages as k_fft_large_a, so the same bits.
-static __global__ void __launch_bounds__(512) k_fft_large_a8(const ViewSrc src, int logL, int logP,
-                                                            const cx *__restrict__ tw, cx *scratch) {
-    extern __shared__ double4 smem_raw[];
-    cx *a = reinterpret_cast<cx *>(smem_raw);
-    const int logQ = logL - logP, Q = 1 << logQ;
-    const int ngrp = (src.nshift + 7) >> 3;
-    const int vg = (int)(blockIdx.x % (unsigned)ngrp);
-    const int64_t rest = blockIdx.x / (unsigned)ngrp;
-    const int c = (int)(rest & (Q - 1));
-    const int64_t b = rest >> logQ;
-    const int v0 = vg * 8;
-    int nv = src.nshift - v0 < 8 ? src.nshift - v0 : 8;
-    if (src.nview) {
-        const int nb = __ldg(src.nview + b) - v0;
-        nv = nb < nv ? nb : nv;
-    }
-    if (nv <= 0) return;   // CTA-uniform
-    const int rc = logQ ? (int)(__brev((unsigned)c) >> (32 - logQ)) : 0;
-    __shared__ int64_t s_ib[8], s_io[8];
-    if (threadIdx.x < 8) {
-        const int s = v0 + (int)threadIdx.x;
-        int64_t o = 0;
-        if ((int)threadIdx.x < nv)
-            o = (s >= src.dyn_first) ? src.dyn_off[b * src.dyn_stride + (s - src.dyn_first)] : src.off[s];
-        s_ib[threadIdx.x] = b * src.sig_stride;
-        s_io[threadIdx.x] = o + (int64_t)rc * src.jstride;
-    }
-    __syncthreads();
-    const int64_t gb = b * src.nshift + v0;
-    fft_fused_views(a, src, src.jstride << logQ, s_ib, s_io, nv, 3, logP, tw, [&](int v, int k, cx y) {
-        scratch[((gb + v) << logL) + ((int64_t)c << logP) + k] = y;
-    });
 }
 
 // large views (L > FFT_SMEM_MAX): stage split through global memory.
@@ -530,85 +474,6 @@ static __global__ void __launch_bounds__(256) k_fft_large_b_reg(cx *buf, int64_t
 }
 
 
-// Pass B in shared memory when 5 stages remain (L = 2^17): one CTA
-// holds 32 consecutive residues r of one view, all 2^LQ elements i = r +
-// q*2^s0 of each (16 KiB), loaded and stored as 512-B rows.  The
-// LQ stages run as the radix-2 stage loop does them -- the same butterfly
-// on the same pairs with the same twiddle tw[(h-1) + r + qk*2^s0] -- so the
-// result is bit-identical to two register passes, with one pass over the
-// scratch instead of two.  Writes the views (scaled, activity epilogue).
-constexpr int LB_RES = 32;
-static __global__ void __launch_bounds__(256) k_fft_large_b_smem(const cx *buf, int64_t nviews,
-                                                                 int logL, int s0, int LQ,
-                                                                 const cx *__restrict__ tw, cx *out,
-                                                                 int nshift, int SV, int64_t ldV, int scale,
-                                                                 const double *__restrict__ thr,
-                                                                 uint8_t *__restrict__ act,
-                                                                 const int32_t *__restrict__ nview) {
-    extern __shared__ double4 smem_raw[];
-    cx *tile = reinterpret_cast<cx *>(smem_raw);   // [q][r_local]
-    const int64_t P = int64_t(1) << s0;
-    const int Q = 1 << LQ;
-    const int64_t groups = P / LB_RES;
-    // an intermediate pass (s0 + LQ < logL) works on 2^(logL - s0 - LQ)
-    // independent blocks of 2^(s0 + LQ) elements (index bits above the
-    // pass's stages: hi)
-    const int64_t nhi = int64_t(1) << (logL - s0 - LQ);
-    const int64_t g = blockIdx.x / (groups * nhi);
-    const int64_t rem = blockIdx.x - g * (groups * nhi);
-    const int64_t hi = rem / groups;
-    const int64_t r0 = (rem - hi * groups) * LB_RES;
-    if (g >= nviews) return;
-    const int64_t b = g / nshift;
-    const int s = (int)(g - b * nshift);
-    if (nview && s >= __ldg(nview + b)) return;   // unused view
-    const cx *src = buf + (g << logL) + (hi << (s0 + LQ)) + r0;
-    for (int e = threadIdx.x; e < Q * LB_RES; e += blockDim.x) {
-        const int q = e / LB_RES, rl = e - q * LB_RES;
-        tile[e] = ldcx(src + (int64_t)q * P + rl);
-    }
-    __syncthreads();
-    for (int st = 0; st < LQ; st++) {
-        const int hq = 1 << st;
-        const int64_t h = P << st;
-        // butterflies (q, q + hq) with bit st of q clear; qk = q mod hq
-        for (int e = threadIdx.x; e < (Q / 2) * LB_RES; e += blockDim.x) {
-            const int pidx = e / LB_RES, rl = e - pidx * LB_RES;
-            const int qk = pidx & (hq - 1);
-            const int q = ((pidx >> st) << (st + 1)) | qk;
-            const cx w = ldcx(tw + (h - 1) + r0 + rl + (int64_t)qk * P);
-            const cx u = tile[q * LB_RES + rl];
-            const cx t = gmul(tile[(q + hq) * LB_RES + rl], w);
-            tile[q * LB_RES + rl] = cadd(u, t);
-            tile[(q + hq) * LB_RES + rl] = csub(u, t);
-        }
-        __syncthreads();
-    }
-    if (out == nullptr) {   // intermediate pass: back in place
-        cx *dst = const_cast<cx *>(src);
-        for (int e = threadIdx.x; e < Q * LB_RES; e += blockDim.x) {
-            const int q = e / LB_RES, rl = e - q * LB_RES;
-            stcx(dst + (int64_t)q * P + rl, tile[e]);
-        }
-        return;
-    }
-    const double sc = 1.0 / (double)(int64_t(1) << logL);
-    const double th = act ? thr[b] : 0.0;
-    cx *o = out + (b * SV + s) * ldV + r0;
-    for (int e = threadIdx.x; e < Q * LB_RES; e += blockDim.x) {
-        const int q = e / LB_RES, rl = e - q * LB_RES;
-        const cx x = tile[e];
-        const cx y = scale ? mk(DMUL(x.re, sc), DMUL(x.im, sc)) : x;
-        const int64_t i = (int64_t)q * P + rl;
-        stcx(o + i, y);
-        if (act) {
-            const double m2 = y.re * y.re + y.im * y.im;
-            if (m2 > th * th * (1.0 + 1e-6) || (m2 >= th * th * (1.0 - 1e-6) && cabs_(y) > th))
-                act[(b << logL) + r0 + i] = 1;
-        }
-    }
-}
-
 // ---------------------------------------------------------------------------
 // Large views, register-blocked pass A (P = 4096 points, 12 stages): thread t
 // of 256 holds 16 elements in registers through three radix-16 rounds --
@@ -616,8 +481,7 @@ static __global__ void __launch_bounds__(256) k_fft_large_b_smem(const cx *buf, 
 // 16k, stages 8-11 on t + 256k -- with two shared-memory exchanges between
 // them (XOR-swizzled: conflict-free in all three access patterns).  All 16
 // strided gathers of a thread are in flight at once, and every group loads
-// its 15 twiddles up front (the 64-KiB stage table stays in L1: the gathers
-// bypass it).  Butterflies, pairs and twiddles are those of the radix-2
+// its 15 twiddles up front.  Butterflies, pairs and twiddles are those of the radix-2
 // stage loop, so the blocks are bit-identical to k_fft_large_a's.
 __device__ __forceinline__ int swz16(int p) { return p ^ ((p >> 4) & 7); }
 
@@ -629,7 +493,7 @@ __device__ __forceinline__ cx ld_stream(const cx *p) {   // no L1 allocation
 
 static __global__ void __launch_bounds__(256, 2) k_fft_large_a16(const ViewSrc src, int logL,
                                                                  const cx *__restrict__ tw,
-                                                                 cx *__restrict__ scratch, int ldmode) {
+                                                                 cx *__restrict__ scratch) {
     extern __shared__ double4 smem_raw[];
     cx *a = reinterpret_cast<cx *>(smem_raw);
     constexpr int logP = 12;
@@ -657,8 +521,10 @@ static __global__ void __launch_bounds__(256, 2) k_fft_large_a16(const ViewSrc s
             const float2 f = __ldg(reinterpret_cast<const float2 *>(src.x) + e);
             x[k] = mk((double)f.x, (double)f.y);
         } else {
-            const cx *pp = reinterpret_cast<const cx *>(src.x) + e;
-            x[k] = ldmode == 0 ? ld_stream(pp) : ldmode == 1 ? ldcx(pp) : ld_gather(pp, 3);
+            // L1-allocating loads: the eight views' CTAs of a block share
+            // each line through L2 (no_allocate measured 1.2-1.3x the DRAM
+            // reads and 5 % slower, profiles/r02_large_fft/)
+            x[k] = ldcx(reinterpret_cast<const cx *>(src.x) + e);
         }
     }
     group_stages_pre<4>(x, 0, 1, tw);                       // stages 0-3
@@ -690,7 +556,7 @@ static __global__ void __launch_bounds__(256, 2) k_fft_large_a16(const ViewSrc s
 // writes the view (scale / activity epilogue) -- one read and one write of
 // the scratch for all remaining stages.  Bit-identical to the register
 // passes (same butterflies, pairs, twiddles tw[(H-1) + (i mod H)]).
-template <int LQ, bool B16_PRE>
+template <int LQ>
 static __global__ void __launch_bounds__(32 << (LQ - 4), 16 >> (LQ - 4)) k_fft_large_b16(
     const cx *__restrict__ buf, int64_t nviews, int logL, const cx *__restrict__ tw, cx *out, int nshift, int SV,
     int64_t ldV, int scale, const double *__restrict__ thr, uint8_t *__restrict__ act,
@@ -713,8 +579,8 @@ static __global__ void __launch_bounds__(32 << (LQ - 4), 16 >> (LQ - 4)) k_fft_l
     for (int k = 0; k < 16; k++) x[k] = ld_stream(src + (int64_t)(16 * w + k) * P);
     // column stages 0-3: element q = 16w + k is i = r + q*P, so the group has
     // stride h = P and i mod P = r
-    if (B16_PRE) group_stages_pre<4>(x, (int)(r0 + rl), (int)P, tw);
-    else group_stages<4>(x, (int)(r0 + rl), (int)P, tw);
+    // (twiddles per stage, not all 15 up front: that spills at 128 registers)
+    group_stages<4>(x, (int)(r0 + rl), (int)P, tw);
 #pragma unroll
     for (int k = 0; k < 16; k++) tile[(16 * w + k) * 32 + rl] = x[k];
     __syncthreads();
@@ -752,113 +618,49 @@ static inline void launch_large_b_reg(cx *buf, int64_t nviews, int logL, int s0,
         buf, nviews, logL, s0, tw, out, nshift, SV, ldV, scale, thr, act, nview);
 }
 
-// kernel launches of one launch_fft_views call
-// stages of the large-view pass A (blocks of 2^logP points in shared memory)
-static inline int large_logp(int logL) {
-    const char *e = getenv("SFDT_FFT_LOGP");
-    int lp = e ? atoi(e) : 12;
-    if (lp < 8) lp = 8;
-    if (lp > 13) lp = 13;
-    return lp < logL ? lp : logL - 1;
+// Large views (L > FFT_SMEM_MAX): pass A runs the first LARGE_LOGP stages on
+// 4096-point blocks; the remaining stages act on the residue classes mod
+// 4096.  5..7 remaining stages (L = 2^17 .. 2^19): register-blocked
+// k_fft_large_a16 + one k_fft_large_b16.  Otherwise, or with `split` (the
+// round-1 plan, kept for A/B runs and tests): k_fft_large_a + register
+// passes of <= 4 stages.
+constexpr int LARGE_LOGP = 12;
+static inline int large_logp(int logL) { return LARGE_LOGP < logL ? LARGE_LOGP : logL - 1; }
+static inline bool large_blocked(int logL, int split) {
+    const int lq = logL - LARGE_LOGP;
+    return !split && lq >= 5 && lq <= 7;
 }
-
-// Large-view plan: pass A one view per CTA (k_fft_large_a, 2^large_logp
-// blocks), or -- experiment -- groups of 8 views (k_fft_large_a8, 1024-point
-// blocks); then pass B: five stages in shared memory where that pays,
-// register passes of <= 4 stages otherwise.
-// (off by default: measured slower -- config 5 general K=2^14 view FFT
-// 6.53 -> 7.58 ms, exact K=2^14 1.75 -> 1.96 ms per batch -- the 128-KiB
-// CTA leaves one CTA per SM; SFDT_FFT_A8=1 enables it)
-static inline bool large_a8(int nshift) {
-    const char *e = getenv("SFDT_FFT_A8");
-    return nshift >= 8 && e && e[0] == '1';
-}
-static inline bool large_bsmem_ok() {
-    const char *e = getenv("SFDT_FFT_BSMEM");
-    return !(e && e[0] == '0');
-}
-// stages of the next pass B from s0 (0 = done); *smem = shared-memory pass
-static inline int large_next(int logL, int s0, bool a8, bool *smem) {
+static inline int large_next(int logL, int s0) {
     const int rem = logL - s0;
-    *smem = false;
-    if (rem <= 0) return 0;
-    // (measured per config-5 batch: the single smem pass at L = 2^17 2.83 ->
-    // 2.62 ms; 64-KiB (7-stage) tiles slower than 4 + 3 register passes)
-    if (large_bsmem_ok() && (rem == 5 || (a8 && rem > 5 && rem <= 9))) {
-        *smem = true;
-        return 5;
-    }
-    return rem >= 4 ? 4 : rem;
+    return rem <= 0 ? 0 : (rem >= 4 ? 4 : rem);
 }
 
-// pipelined pass A + one tiled pass B (complex128 input, <= 7 stages left
-// after pass A); SFDT_FFT_PIPE=0 selects the earlier plan for A/B runs
-static inline bool large_pipe(int logL, int logP, int is_c64, int nshift) {
-    const char *e = getenv("SFDT_FFT_PIPE");
-    (void)is_c64;
-    return !(e && e[0] == '0') && !large_a8(nshift) && logP == 12 && logL - logP <= 7 && logL - logP >= 5;
-}
-
-static inline int fft_view_launches(int64_t L, int nshift = 0, int is_c64 = 0) {
+// kernel launches of one launch_fft_views call
+static inline int fft_view_launches(int64_t L, int split = 0) {
     if (L <= FFT_SMEM_MAX) return 1;
     const int logL = ilog2_64(L);
-    const bool a8 = large_a8(nshift);
-    int s0 = a8 ? 10 : large_logp(logL), n = 1;
-    if (large_pipe(logL, s0, is_c64, nshift)) return 2;
-    bool sm;
-    for (int k; (k = large_next(logL, s0, a8, &sm)) > 0; s0 += k) n++;
+    if (large_blocked(logL, split)) return 2;
+    int s0 = large_logp(logL), n = 1;
+    for (int k; (k = large_next(logL, s0)) > 0; s0 += k) n++;
     return n;
-}
-
-static inline int fft_points_per_cta() {
-    const char *e = getenv("SFDT_FFT_PTS");
-    return e ? atoi(e) : 2048;
 }
 
 // FFT of every view of B signals; large_scratch (B*nshift*L complex) is
 // needed only when L > FFT_SMEM_MAX.
-// Launch k_fft_views, optionally as thread-block clusters of SFDT_FFT_CLUSTER
-// consecutive CTAs (adjacent views of one signal, co-scheduled on one GPC so
-// their strided gathers reach the same d-blocks at about the same time).
-template <int MINB>
-static inline void launch_views_kernel(unsigned grid, size_t smem, cudaStream_t stream, const ViewSrc &src,
-                                       int64_t B, int logL, int logvpc, const cx *tw, cx *out, int SV,
-                                       int64_t ldV, int scale, const double *thr, uint8_t *act) {
-    const char *e = getenv("SFDT_FFT_CLUSTER");
-    const int cl = e ? atoi(e) : 0;
-    if (cl == 2 || cl == 4 || cl == 8) {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((grid + cl - 1) / cl * cl);
-        cfg.blockDim = dim3(256);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = stream;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = cl;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        cudaLaunchKernelEx(&cfg, k_fft_views<MINB>, src, B, logL, logvpc, tw, out, SV, ldV, scale, thr, act);
-        return;
-    }
-    k_fft_views<MINB><<<grid, 256, smem, stream>>>(src, B, logL, logvpc, tw, out, SV, ldV, scale, thr, act);
-}
-
 static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, const double *tw_,
                                    cx *out, int SV, int64_t ldV, cudaStream_t stream,
                                    cx *large_scratch = nullptr, int scale = 1,
-                                   const double *thr = nullptr, uint8_t *act = nullptr) {
+                                   const double *thr = nullptr, uint8_t *act = nullptr, int split = 0) {
     const cx *tw = reinterpret_cast<const cx *>(tw_);
     const int logL = ilog2_64(L);
     const int64_t nviews = B * src.nshift;
     if (nviews == 0) return SFDT_OK;
     if (L <= FFT_SMEM_MAX) {
         int logvpc = 0;
-        // views per CTA: up to fft_points_per_cta() points, but small
-        // batches keep >= 2 CTAs per SM instead of packing views (config 1:
-        // 8 CTAs of one view rather than one CTA of eight)
-        while ((L << (logvpc + 1)) <= fft_points_per_cta() && (1 << (logvpc + 1)) <= 2 * src.nshift &&
+        // views per CTA: up to 2048 points, but small batches keep >= 2 CTAs
+        // per SM instead of packing views (config 1: 8 CTAs of one view
+        // rather than one CTA of eight)
+        while ((L << (logvpc + 1)) <= 2048 && (1 << (logvpc + 1)) <= 2 * src.nshift &&
                (nviews >> (logvpc + 1)) >= 296)
             logvpc++;
         const size_t smem = (size_t(L) << logvpc) * 16;
@@ -866,79 +668,51 @@ static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, con
         // <= 32 KiB per CTA: cap registers at 64 for 4 CTAs/SM (measured
         // 717 -> 553 us at config 2); larger tiles keep 128 registers
         if (smem <= 32 * 1024) {
-            launch_views_kernel<4>(grid, smem, stream, src, B, logL, logvpc, tw, out, SV, ldV, scale, thr, act);
+            k_fft_views<4><<<grid, 256, smem, stream>>>(src, B, logL, logvpc, tw, out, SV, ldV, scale, thr, act);
         } else if (smem <= 64 * 1024) {
-            // 64 KiB tiles: registers capped at 85 (3 CTAs/SM would fit)
+            // 64 KiB tiles: registers capped at 85 (3 CTAs/SM would fit).
+            // Two CTAs per SM, the rest of the 256 KiB as L1: the view
+            // stages read the (L-1)-entry twiddle table (64 KiB at L = 4096)
+            // through L1, and with 3 CTAs' 192 KiB of smem it thrashed into
+            // L2 (7.2 GB of L2 reads per config-4 batch; 4.78 -> 4.20 ms).
             cudaFuncSetAttribute(k_fft_views<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            {
-                // Two CTAs per SM, the rest of the 256 KiB as L1: the view
-                // stages read the (L-1)-entry twiddle table (64 KiB at
-                // L = 4096) through L1, and with 3 CTAs' 192 KiB of smem it
-                // thrashed into L2 (7.2 GB of L2 reads per config-4 batch).
-                // Measured at config 4: 4.78 -> 4.20 ms per step.
-                const char *e = getenv("SFDT_FFT_CARVEOUT");
-                const int pct = e ? atoi(e) : (int)((2 * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
-                cudaFuncSetAttribute(k_fft_views<3>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-            }
-            launch_views_kernel<3>(grid, smem, stream, src, B, logL, logvpc, tw, out, SV, ldV, scale, thr, act);
+            cudaFuncSetAttribute(k_fft_views<3>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 (int)((2 * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024)));
+            k_fft_views<3><<<grid, 256, smem, stream>>>(src, B, logL, logvpc, tw, out, SV, ldV, scale, thr, act);
         } else {
             cudaFuncSetAttribute(k_fft_views<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            launch_views_kernel<1>(grid, smem, stream, src, B, logL, logvpc, tw, out, SV, ldV, scale, thr, act);
+            k_fft_views<1><<<grid, 256, smem, stream>>>(src, B, logL, logvpc, tw, out, SV, ldV, scale, thr, act);
         }
         SFDT_CHECK_LAUNCH();
         return SFDT_OK;
     }
     if (!large_scratch) return SFDT_EINVAL;
-    const bool a8 = large_a8(src.nshift);
-    const int logP = a8 ? 10 : large_logp(logL), P = 1 << logP;
+    const int logP = large_logp(logL), P = 1 << logP;
     const int logQ = logL - logP;
-    if (large_pipe(logL, logP, src.is_c64, src.nshift)) {
+    if (large_blocked(logL, split)) {
         // pass A: 4096-point blocks in registers (three radix-16 rounds)
         const size_t smem = size_t(P) * 16;
         cudaFuncSetAttribute(k_fft_large_a16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(k_fft_large_a16, cudaFuncAttributePreferredSharedMemoryCarveout,
                              (int)((2 * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024)));
-        const char *em = getenv("SFDT_A16_LD");
-        k_fft_large_a16<<<(unsigned)(nviews << logQ), 256, smem, stream>>>(src, logL, tw, large_scratch,
-                                                                         em ? atoi(em) : 1);
+        k_fft_large_a16<<<(unsigned)(nviews << logQ), 256, smem, stream>>>(src, logL, tw, large_scratch);
         SFDT_CHECK_LAUNCH();
         // pass B: every remaining stage in one register-blocked pass
         const int lq = logL - logP;
         const int64_t ctas = nviews * ((int64_t(1) << (logL - lq)) >> 5);
-        const char *ebp = getenv("SFDT_B16_PRE");
-        const bool b16pre = ebp && ebp[0] == '1';
-        switch (lq) {
-#define SFDT_B16(LQ)                                                                                      \
-    case LQ:                                                                                              \
-        if (b16pre) {                                                                                     \
-        cudaFuncSetAttribute(k_fft_large_b16<LQ, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 512 << LQ); \
-        k_fft_large_b16<LQ, true><<<(unsigned)ctas, 32 << (LQ - 4), 512 << LQ, stream>>>(large_scratch, nviews, logL, tw, \
-                                                                           out, src.nshift, SV, ldV, scale, \
-                                                                           thr, act, src.nview);           \
-        } else {                                                                                          \
-        cudaFuncSetAttribute(k_fft_large_b16<LQ, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 512 << LQ); \
-        k_fft_large_b16<LQ, false><<<(unsigned)ctas, 32 << (LQ - 4), 512 << LQ, stream>>>(large_scratch, nviews, logL, tw, \
-                                                                           out, src.nshift, SV, ldV, scale, \
-                                                                           thr, act, src.nview);           \
-        }                                                                                                 \
-        break;
-            SFDT_B16(5) SFDT_B16(6) SFDT_B16(7)
-#undef SFDT_B16
-        default: return SFDT_EINVAL;
-        }
+        auto pass_b = [&](auto lq_c) {
+            constexpr int LQ = decltype(lq_c)::value;
+            cudaFuncSetAttribute(k_fft_large_b16<LQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 512 << LQ);
+            k_fft_large_b16<LQ><<<(unsigned)ctas, 32 << (LQ - 4), 512 << LQ, stream>>>(
+                large_scratch, nviews, logL, tw, out, src.nshift, SV, ldV, scale, thr, act, src.nview);
+        };
+        if (lq == 5) pass_b(std::integral_constant<int, 5>{});
+        else if (lq == 6) pass_b(std::integral_constant<int, 6>{});
+        else pass_b(std::integral_constant<int, 7>{});
         SFDT_CHECK_LAUNCH();
         return SFDT_OK;
     }
-    if (a8) {
-        const size_t smem = size_t(8) * P * 16;   // 128 KiB: one CTA of 512 threads per SM
-        cudaFuncSetAttribute(k_fft_large_a8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_fft_large_a8, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             (int)(((smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024)));
-        const int64_t B = nviews / src.nshift;
-        const int64_t ngrp = (src.nshift + 7) / 8;
-        k_fft_large_a8<<<(unsigned)(B * ngrp << logQ), 512, smem, stream>>>(src, logL, logP, tw, large_scratch);
-        SFDT_CHECK_LAUNCH();
-    } else {
+    {
         const size_t smem = size_t(P) * 16;
         cudaFuncSetAttribute(k_fft_large_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         // 2 CTAs/SM at 4096 points (4 at 2048), the rest L1 for the
@@ -950,24 +724,13 @@ static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, con
         SFDT_CHECK_LAUNCH();
     }
     // remaining stages logP .. logL-1 (the last pass writes the views)
-    bool sm;
-    for (int s0 = logP, lq; (lq = large_next(logL, s0, a8, &sm)) > 0; s0 += lq) {
-        const bool last = s0 + lq == logL;
-        cx *o = last ? out : nullptr;
-        if (sm) {
-            const size_t smem = (size_t(1) << lq) * LB_RES * 16;
-            cudaFuncSetAttribute(k_fft_large_b_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            const int64_t ctas = nviews * ((int64_t(1) << s0) / LB_RES) * (int64_t(1) << (logL - s0 - lq));
-            k_fft_large_b_smem<<<(unsigned)ctas, 256, smem, stream>>>(large_scratch, nviews, logL, s0, lq, tw, o,
-                                                                      src.nshift, SV, ldV, scale, thr, act,
-                                                                      src.nview);
-        } else {
-            switch (lq) {
-            case 1: launch_large_b_reg<1>(large_scratch, nviews, logL, s0, tw, o, src.nshift, SV, ldV, scale, thr, act, stream, src.nview); break;
-            case 2: launch_large_b_reg<2>(large_scratch, nviews, logL, s0, tw, o, src.nshift, SV, ldV, scale, thr, act, stream, src.nview); break;
-            case 3: launch_large_b_reg<3>(large_scratch, nviews, logL, s0, tw, o, src.nshift, SV, ldV, scale, thr, act, stream, src.nview); break;
-            default: launch_large_b_reg<4>(large_scratch, nviews, logL, s0, tw, o, src.nshift, SV, ldV, scale, thr, act, stream, src.nview); break;
-            }
+    for (int s0 = logP, lq; (lq = large_next(logL, s0)) > 0; s0 += lq) {
+        cx *o = (s0 + lq == logL) ? out : nullptr;
+        switch (lq) {
+        case 1: launch_large_b_reg<1>(large_scratch, nviews, logL, s0, tw, o, src.nshift, SV, ldV, scale, thr, act, stream, src.nview); break;
+        case 2: launch_large_b_reg<2>(large_scratch, nviews, logL, s0, tw, o, src.nshift, SV, ldV, scale, thr, act, stream, src.nview); break;
+        case 3: launch_large_b_reg<3>(large_scratch, nviews, logL, s0, tw, o, src.nshift, SV, ldV, scale, thr, act, stream, src.nview); break;
+        default: launch_large_b_reg<4>(large_scratch, nviews, logL, s0, tw, o, src.nshift, SV, ldV, scale, thr, act, stream, src.nview); break;
         }
         SFDT_CHECK_LAUNCH();
     }
@@ -989,17 +752,6 @@ static inline ViewSrc consecutive_views(const void *x, int is_c64, int64_t n, in
     s.dyn_stride = 0;
     s.jfast = 0;
     s.nview = nullptr;
-    const char *eh = getenv("SFDT_GATHER_HINT");
-    s.ldhint = eh ? atoi(eh) : 0;
-    return s;
-}
-
-// views stored as the rows of a (B, L, S) window buffer: view v sample j at
-// win[(b*L + j)*S + v]
-static inline ViewSrc window_views(const cx *win, int S, int64_t L) {
-    ViewSrc s = consecutive_views(win, 0, (int64_t)S * L, S, 0, S);
-    s.wrap = -1;
-    s.jfast = 0;
     return s;
 }
 

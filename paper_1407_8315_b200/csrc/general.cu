@@ -1030,9 +1030,10 @@ __device__ __forceinline__ bool mf_better(double v, int t, double w, int u) {
     return v > w || (v == w && t < u);
 }
 
-// One CTA per signal: base_phi (r x d) is staged in shared memory once when
-// it fits (every voted bin of the signal re-reads all of it), the voted
-// bins are listed 1024 at a time, and each warp scores one bin.
+// One CTA per (signal, chunk of mfl <= MF_LIST bins): base_phi (r x d) is
+// staged in shared memory once per CTA when it fits (every voted bin of the
+// chunk re-reads all of it), the chunk's voted bins are listed in shared
+// memory, and each warp scores one bin.
 constexpr int MF_SMEM_MAX = 160 * 1024;
 constexpr int MF_LIST = 4096;
 
@@ -1389,16 +1390,13 @@ __global__ void __launch_bounds__(128) k_gen_prune(const cx *__restrict__ V, Gen
                                                    int32_t *__restrict__ cols_out, int8_t *__restrict__ ncols_out,
                                                    int heavy_flags, int64_t *__restrict__ hl,
                                                    unsigned long long *__restrict__ hlc, int64_t hl_cap,
-                                                   unsigned long long *__restrict__ hlc_hi, int split_a,
-                                                   int phase) {
+                                                   unsigned long long *__restrict__ hlc_hi, int split_a) {
     const int64_t cnt = (int64_t)*wl_count;
     const int sub = LANES > 1 ? (int)(threadIdx.x & (LANES - 1)) : 0;
     for (int64_t it = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / LANES; it < cnt;
          it += int64_t(gridDim.x) * blockDim.x / LANES) {
         const int64_t t = wl[it];
         const int a = votes[t];
-        // phase 1: the multi-collision bins only, phase 2: the rest
-        if ((phase == 1 && a < 2) || (phase == 2 && a >= 2)) continue;
         const int64_t b = t / p.L, kb = t - b * p.L;
         const int r = p.r_eff;
         const int64_t *sh = p.shifts + b * p.shift_stride;
@@ -1999,6 +1997,13 @@ static int make_gen_plan(const sfdt_general_args *a, GenPlan &p) {
         return SFDT_EINVAL;
     if (2 * a->a_max + a->r_eff > MAX_VIEWS) return SFDT_EINVAL;
     if (a->x_dtype != SFDT_C128 && a->x_dtype != SFDT_C64) return SFDT_EINVAL;
+    {
+        // the A/B switches, validated before anything is enqueued
+        const sfdt_tuning t = tuning_or_default(a->tuning);
+        if (t.gen_mf_list != 0 && (t.gen_mf_list < 32 || t.gen_mf_list > MF_LIST)) return SFDT_EINVAL;
+        if (t.gen_prune_lanes != 0 && t.gen_prune_lanes != 1 && t.gen_prune_lanes != 4) return SFDT_EINVAL;
+        if (t.gen_warp < -1 || t.gen_warp > 1 || t.gen_deal < 0 || t.gen_split_a < 0) return SFDT_EINVAL;
+    }
     p.B = a->batch;
     p.n = a->n;
     p.d = a->d;
@@ -2057,30 +2062,6 @@ extern "C" size_t sfdt_general_workspace_bytes(const sfdt_general_args *a) {
     return p.total;
 }
 
-// Side stream of the heavy-bin pursuit (k_gen_bins): a one-wave kernel
-// whose time is the tail of a few long FP64 chains (4 % warps active), so
-// the single-collision pursuit (k_gen_sp1) runs beside it, not after it.
-// One non-blocking stream per device, created on first use outside a
-// capture; SFDT_GEN_OVERLAP=0 keeps both on the caller's stream.
-static cudaStream_t gen_side_stream(cudaStream_t main) {
-    const char *e = getenv("SFDT_GEN_OVERLAP");
-    if (e && e[0] == '0') return nullptr;
-    static std::mutex mu;
-    static cudaStream_t side[64] = {};
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-    std::lock_guard<std::mutex> lk(mu);
-    if (!side[dev]) {
-        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-        if (cudaStreamIsCapturing(main, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
-        if (cudaStreamCreateWithFlags(&side[dev], cudaStreamNonBlocking) != cudaSuccess) {
-            side[dev] = nullptr;
-            return nullptr;
-        }
-    }
-    return side[dev];
-}
-
 extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_bytes, sfdt_stream_t stream_) {
     GenPlan p;
     int rc = make_gen_plan(a, p);
@@ -2091,6 +2072,7 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     if (a->entry_cap < ecap) return SFDT_ECAPACITY;
     if (!a->shifts || !a->base_phi || !a->twiddles) return SFDT_EINVAL;
     cudaStream_t stream = (cudaStream_t)stream_;
+    const sfdt_tuning tn = tuning_or_default(a->tuning);
     char *w = (char *)ws;
     cx *V = (cx *)(w + p.off_V);
     double *sv = a->singular_values ? a->singular_values : (double *)(w + p.off_sv);
@@ -2126,8 +2108,7 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     int32_t *vslot = (int32_t *)(w + p.off_vslot);
     int32_t *nview = (int32_t *)(w + p.off_nview);
     {
-        const char *ed = getenv("SFDT_GEN_DEDUP");
-        const int dedup = !(ed && ed[0] == '0');
+        const int dedup = tn.gen_dedup != 0;
         k_gen_vslot<<<(unsigned)((p.B + 127) / 128), 128, 0, stream>>>(gp, p.B, dedup, vsh, vslot, nview);
         SFDT_CHECK_LAUNCH();
         launches++;
@@ -2142,10 +2123,11 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     src.dyn_stride = a->r_eff;
     src.nview = nview;
     if (a->ev_fft_begin) cudaEventRecord((cudaEvent_t)a->ev_fft_begin, stream);
-    rc = launch_fft_views(src, p.B, p.L, a->twiddles, V, (int)p.nv, p.L, stream, fft_scratch);
+    rc = launch_fft_views(src, p.B, p.L, a->twiddles, V, (int)p.nv, p.L, stream, fft_scratch, 1, nullptr, nullptr,
+                          tn.fft_split);
     if (rc) return rc;
     if (a->ev_fft_end) cudaEventRecord((cudaEvent_t)a->ev_fft_end, stream);
-    launches += fft_view_launches(p.L, (int)p.nv, is_c64);
+    launches += fft_view_launches(p.L, tn.fft_split);
 
     // 2. collision vote (general.py:131-155)
     {
@@ -2156,8 +2138,7 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
         case 1: k_gen_svd<1><<<g, 128, 0, stream>>>(V, gp, sv, part, fix, nfix, 0); break;
         case 2: k_gen_svd<2><<<g, 128, 0, stream>>>(V, gp, sv, part, fix, nfix, 0); break;
         case 3: {
-            const char *es = getenv("SFDT_GEN_SVD");   // "jacobi": the Jacobi for every bin
-            const int closed = !(es && es[0] == 'j');
+            const int closed = tn.gen_svd_closed != 0;   // 0: the Jacobi for every bin
             cudaMemsetAsync(nfix, 0, 8, stream);
             k_gen_svd<3><<<g, 128, 0, stream>>>(V, gp, sv, part, fix, nfix, closed);
             SFDT_CHECK_LAUNCH();
@@ -2208,9 +2189,8 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaMemsetAsync(nent, 0, size_t(p.B) * p.L, stream);
     int32_t *mf_top = (int32_t *)(w + p.off_mf);
-    const char *emf = getenv("SFDT_GEN_MF_SMALL");
     bool mf_small_done = false;
-    if (a->prune && p.d <= 32 && !(emf && emf[0] == '0')) {
+    if (a->prune && p.d <= 32 && tn.gen_mf_small) {
         const int64_t nch = (p.L + MF_LIST - 1) / MF_LIST;
         const unsigned grid = (unsigned)(p.B * nch);
         int G = (int)p.d;
@@ -2233,11 +2213,9 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
         // bins per CTA: MF_LIST, fewer when that leaves < 2 CTAs per SM
         // (few long-view signals: config 5 general K = 64 had 64 CTAs)
         int mfl = MF_LIST;
-        const char *eml = getenv("SFDT_GEN_MF_LIST");
-        if (eml) mfl = atoi(eml);
+        if (tn.gen_mf_list) mfl = tn.gen_mf_list;   // validated by make_gen_plan
         else
             while (mfl > 256 && p.B * ((p.L + mfl - 1) / mfl) < 2 * (int64_t)sms) mfl >>= 1;
-        if (mfl < 32 || mfl > MF_LIST) return SFDT_EINVAL;
         const int64_t nch = (p.L + mfl - 1) / mfl;
         const size_t phi_bytes = size_t(a->r_eff) * p.d * 16;
         const int stage = phi_bytes <= MF_SMEM_MAX;
@@ -2272,49 +2250,34 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     // at N=2^22, B=64, d=2048/512/128: 7.33 -> 1.33 ms, 3.64 -> 2.19 ms,
     // 2.75 -> 5.53 ms); beyond that, thread per bin (32 bins per warp in
     // lockstep) keeps the FP64 pipe busier than 32 lanes on one bin's
-    // redundant least squares.  SFDT_GEN_WARP=0/1 forces either form.
-    const char *ev = getenv("SFDT_GEN_WARP");
+    // redundant least squares.  tuning.gen_warp = 0 / 1 forces either form.
     const bool all_d = !a->prune || p.d <= 2 * (int64_t)a->keep_per_collision * a->a_max;
     const bool few = (int64_t)a->k * p.B <= 224 * (int64_t)sms;
-    const int warp_all = all_d && (ev ? ev[0] == '1' : few);
+    const int warp_all = all_d && (tn.gen_warp >= 0 ? tn.gen_warp == 1 : few);
     int64_t *hl = (int64_t *)(w + p.off_hl);
     unsigned long long *hlc = wlc + 1;
     cudaMemsetAsync(hlc, 0, 8, stream);
-    // wlc[3]: k_gen_bins' take counter, [4]: the a >= split_a count (or the
-    // phase-2 heavy count), [5]: the second k_gen_bins' take counter, [6]: 0
-    cudaMemsetAsync(wlc + 3, 0, 32, stream);
-    // heavy bins with a >= split_a dealt first (SFDT_GEN_SPLIT; 0: list order)
-    const char *esp = getenv("SFDT_GEN_SPLIT");
-    const int split_a = esp ? atoi(esp) : 3;
-    // The multi-collision bins are known from the votes: with a side stream
-    // they are pruned first (phase 1) and their pursuit (k_gen_bins, a tail
-    // of a few long chains) runs beside the pruning of the single-collision
-    // bins (phase 2) and k_gen_sp1.  Phase 2's heavy bins (a = 1 with more
-    // than 4 kept columns) fill hl from its tail for a second k_gen_bins on
-    // the caller's stream.  Measured slower, so opt-in (SFDT_GEN_PRUNE2=1):
-    // the one-wave k_gen_bins holds every SM's registers until its warps
-    // retire, starving phase 2 (config 4 2.88 -> 3.00 ms, config 5 general
-    // K=64 1.52 -> 1.85 ms).
-    cudaStream_t side = gen_side_stream(stream);
-    const char *ep2 = getenv("SFDT_GEN_PRUNE2");
-    const bool two_phase = side && ep2 && ep2[0] == '1';
+    // wlc[3]: k_gen_bins' take counter, [4]: the a >= split_a count
+    cudaMemsetAsync(wlc + 3, 0, 16, stream);
+    // heavy bins with a >= split_a dealt first (tuning.gen_split_a; 0: list order)
+    const int split_a = tn.gen_split_a;
+    // the multi-collision pursuit (k_gen_bins) forks onto the caller's aux
+    // stream, when given, beside the single-collision pursuit (k_gen_sp1)
+    cudaStream_t side = (cudaStream_t)a->aux_stream;
+    if (side == stream) side = nullptr;
     const int hflags = sp1 | (warp_all ? 2 : 0);
     // four lanes per bin when d splits into >= 2 recurrence segments and the
     // bins are few (one lane per bin would leave most of the GPU idle)
-    const char *epl = getenv("SFDT_GEN_PRUNE_LANES");
     const bool lanes4 = a->prune && p.d >= 1024 && (p.d & 511) == 0 &&
-                        (epl ? epl[0] == '4' : max_voted <= 64 * (int64_t)sms);
+                        (tn.gen_prune_lanes ? tn.gen_prune_lanes == 4 : max_voted <= 64 * (int64_t)sms);
     const unsigned prune_grid = lanes4 ? wl_grid(4 * max_voted, 128, one_wave(k_gen_prune<4>, 128))
                                        : wl_grid(max_voted, 128, one_wave(k_gen_prune<1>, 128));
-    auto launch_prune = [&](int split, int phase) {
-        if (lanes4)
-            k_gen_prune<4><<<prune_grid, 128, 0, stream>>>(V, gp, votes, wl, wlc, mf_top, colsb, ncolsb, hflags, hl,
-                                                           hlc, max_voted, wlc + 4, split, phase);
-        else
-            k_gen_prune<1><<<prune_grid, 128, 0, stream>>>(V, gp, votes, wl, wlc, mf_top, colsb, ncolsb, hflags, hl,
-                                                           hlc, max_voted, wlc + 4, split, phase);
-    };
-    launch_prune(two_phase ? 0 : split_a, two_phase ? 1 : 0);
+    if (lanes4)
+        k_gen_prune<4><<<prune_grid, 128, 0, stream>>>(V, gp, votes, wl, wlc, mf_top, colsb, ncolsb, hflags, hl,
+                                                       hlc, max_voted, wlc + 4, split_a);
+    else
+        k_gen_prune<1><<<prune_grid, 128, 0, stream>>>(V, gp, votes, wl, wlc, mf_top, colsb, ncolsb, hflags, hl,
+                                                       hlc, max_voted, wlc + 4, split_a);
     SFDT_CHECK_LAUNCH();
     if (a->ev_prune_end) cudaEventRecord((cudaEvent_t)a->ev_prune_end, stream);
     // heavy bins (k_gen_bins) fork onto the side stream; the bins of the
@@ -2329,10 +2292,9 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
         cudaStreamWaitEvent(side, ev_fork, 0);
     }
     cudaStream_t bstream = side ? side : stream;
-    // bins per warp dealt statically in k_gen_bins (SFDT_GEN_DEAL; 1: one
-    // per warp, else the take counter)
-    const char *edl = getenv("SFDT_GEN_DEAL");
-    const int deal_max = edl ? atoi(edl) : 8;
+    // bins per warp dealt statically in k_gen_bins (tuning.gen_deal; 1: one
+    // per warp, 0: the take counter)
+    const int deal_max = tn.gen_deal;
     auto launch_bins = [&](cudaStream_t st, const unsigned long long *lo_count, unsigned long long *take,
                            const unsigned long long *hi_count) {
         // one wave; heavy bins dealt over its warps (k_gen_bins)
@@ -2349,14 +2311,9 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
 #undef SFDT_BINS
         }
     };
-    launch_bins(bstream, hlc, wlc + 3, two_phase ? wlc + 6 : wlc + 4);
+    launch_bins(bstream, hlc, wlc + 3, wlc + 4);
     SFDT_CHECK_LAUNCH();
     launches++;
-    if (two_phase) {
-        launch_prune(1, 2);
-        SFDT_CHECK_LAUNCH();
-        launches++;
-    }
     if (sp1) {
         switch (a->r_eff) {
 #define SFDT_SP1(R)                                                                                     \
@@ -2374,11 +2331,6 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     if (warp_all) {
         k_gen_bins_warp<<<wl_grid(max_voted, 8, one_wave(k_gen_bins_warp, 256)), 256, 0, stream>>>(
             V, gp, votes, wl, wlc, ncolsb, nent, sloc, sval, a->stats);
-        SFDT_CHECK_LAUNCH();
-        launches++;
-    }
-    if (two_phase) {   // phase 2's heavy bins, from hl's tail
-        launch_bins(stream, wlc + 6, wlc + 5, wlc + 4);
         SFDT_CHECK_LAUNCH();
         launches++;
     }

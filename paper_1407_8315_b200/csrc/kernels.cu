@@ -83,6 +83,10 @@ const char *sfdt_strerror(int code) {
 
 int sfdt_version(void) { return 10000; }
 
+void sfdt_default_tuning(sfdt_tuning *out) {
+    if (out) *out = default_tuning();
+}
+
 const char *sfdt_last_cuda_error(void) { return cudaGetErrorString(cudaPeekAtLastError()); }
 
 int sfdt_fft_radix2(const double *x, double *out, int64_t batch, int64_t n, int inverse,

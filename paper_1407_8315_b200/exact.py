@@ -257,6 +257,8 @@ def exact_batch(X, cfg: ExactConfig, iterative: bool, device=None,
     if stream_events is not None:
         args.ev_stream_begin = stream_events[0].cuda_event
         args.ev_stream_end = stream_events[1].cuda_event
+    tn = _lib.tuning_struct()
+    args.tuning = ctypes.addressof(tn)
     nbytes = lib.sfdt_exact_workspace_bytes(args)
     ws = resolve_workspace(workspace, nbytes, dev)
     _lib.check(lib.sfdt_exact_solve(args, ws.data_ptr(), ws.numel(), stream_handle(dev)),

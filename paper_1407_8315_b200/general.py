@@ -23,7 +23,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from .device import as_device_signals, resolve_workspace, host_copy, ptr, require_cuda, stream_handle, twiddles
+from .device import (as_device_signals, aux_stream, host_copy, ptr, require_cuda, resolve_workspace,
+                     stream_handle, twiddles)
 from .spectral import SparseSpectrum, check_signal_shape
 
 logger = logging.getLogger(__name__)
@@ -250,6 +251,12 @@ def solve_general_batch(X, cfg: GeneralConfig, seeds=None, device=None,
     if phase_events is not None:   # 5 events: fft begin / end, vote, prune, pursuit ends
         e = [ev.cuda_event for ev in phase_events]
         a.ev_fft_begin, a.ev_fft_end, a.ev_vote_end, a.ev_prune_end, a.ev_pursuit_end = e
+    t = _lib.current_tuning()
+    tn = _lib.tuning_struct(t)
+    a.tuning = ctypes.addressof(tn)
+    if t["gen_overlap"]:
+        # the multi-collision pursuit forks onto the device's aux stream
+        a.aux_stream = aux_stream(dev).cuda_stream
     nbytes = lib.sfdt_general_workspace_bytes(a)
     ws = resolve_workspace(workspace, nbytes, dev)
     _lib.check(lib.sfdt_general_solve(a, ws.data_ptr(), ws.numel(), stream_handle(dev)),

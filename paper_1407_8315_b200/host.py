@@ -139,10 +139,3 @@ def solve_host_batch(X_host, cfg, iterative: bool = False, chunk: int = 256,
         r.to_host()
     return HostBatchResult(n, bool(iterative), results, chunk, X_host.element_size())
 
-
-def solve_noniterative_batch(X, cfg: ExactConfig, device=None) -> ExactBatch:
-    return exact_batch(X, cfg, False, device)
-
-
-def solve_iterative_batch(X, cfg: ExactConfig, device=None) -> ExactBatch:
-    return exact_batch(X, cfg, True, device)

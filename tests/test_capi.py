@@ -114,3 +114,39 @@ def test_exact_workspace_query(lib):
     assert lib.sfdt_exact_workspace_bytes(a) > 16 * 256 * 8 * 16
     a.d = 3
     assert lib.sfdt_exact_workspace_bytes(a) == 0
+
+
+def test_tuning_struct_and_validation():
+    """Design switches arrive as an sfdt_tuning (no environment reads in the
+    library): the library's defaults equal the Python mirror's, unknown keys
+    are rejected, and invalid values fail the plan before any launch."""
+    import ctypes
+    from paper_1407_8315_b200 import _lib
+    lib = _lib.load()
+    t = _lib.Tuning()
+    lib.sfdt_default_tuning(ctypes.byref(t))
+    for name, _ in _lib.Tuning._fields_:
+        assert getattr(t, name) == _lib.TUNING_DEFAULTS[name], name
+    with pytest.raises(KeyError):
+        with _lib.tuning(no_such_switch=1):
+            pass
+    with _lib.tuning(gen_deal=3):
+        assert _lib.current_tuning()["gen_deal"] == 3
+    assert _lib.current_tuning()["gen_deal"] == _lib.TUNING_DEFAULTS["gen_deal"]
+    a = _lib.GeneralArgs()
+    a.batch, a.n, a.k, a.d, a.a_max, a.r_eff, a.keep_per_collision = 1, 1 << 12, 8, 16, 3, 9, 2
+    cap = _lib._i64()
+    assert lib.sfdt_general_caps(ctypes.byref(a), ctypes.byref(cap)) == 0
+    bad = _lib.tuning_struct(dict(_lib.TUNING_DEFAULTS, gen_mf_list=5))
+    a.tuning = ctypes.addressof(bad)
+    assert lib.sfdt_general_caps(ctypes.byref(a), ctypes.byref(cap)) == -1
+
+
+def test_library_reads_no_environment():
+    """the product library reads no environment variables."""
+    import glob
+    import os
+    root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1407_8315_b200", "csrc")
+    for path in glob.glob(os.path.join(root, "*")):
+        with open(path) as fh:
+            assert "getenv" not in fh.read(), path

@@ -386,25 +386,29 @@ def test_general_batch_vs_oracle_cfg4_shape():
         assert tr.collision_histogram == wtr["collision_histogram"]
 
 
-@pytest.mark.parametrize("kind", ["exact", "general"])
-def test_large_view_pass_a8_bitwise(kind, monkeypatch):
-    """Large views transformed 8 per CTA (SFDT_FFT_A8=1: k_fft_large_a8 + the
-    intermediate shared-memory pass B) give the same bits as the default one
-    view per CTA."""
+@pytest.mark.parametrize("kind,n,k,d", [("exact", 1 << 20, 8192, 8), ("exact", 1 << 21, 8192, 8),
+                                        ("exact", 1 << 21, 16384, 4), ("general", 1 << 22, 1 << 12, None),
+                                        ("general", 1 << 21, 1 << 13, None)])
+def test_large_view_blocked_vs_stage_split_bitwise(kind, n, k, d):
+    """Views of 2^17 .. 2^19 points: the register-blocked pass A
+    (k_fft_large_a16) + one register-blocked pass B (k_fft_large_b16) give
+    the same bits as the stage-split plan (k_fft_large_a + register passes
+    of <= 4 stages, tuning fft_split=1), in entries and dict order."""
     B = 2
     if kind == "exact":
-        n, k = 1 << 20, 16384          # L = 2^16
         X = np.stack([exact_signal(n, k, 90 + b, "unit")[0] for b in range(B)])
-        run = lambda: P.exact_batch(X, P.ExactConfig(n=n, k=k), False)
+        cfg = P.ExactConfig(n=n, k=k, initial_d=d)
+        assert n // cfg.resolved_d() >= 1 << 17
+        run = lambda: P.exact_batch(X, cfg, False)
     else:
-        n, k = 1 << 18, 1024           # d = 8, L = 2^15
         seeds = [(61, b) for b in range(B)]
         X = np.stack([general_signal(n, k, 30.0, s_)[0] for s_ in seeds])
-        run = lambda: P.solve_general_batch(X, P.GeneralConfig(n=n, k=k), seeds=seeds)
-    monkeypatch.setenv("SFDT_FFT_A8", "1")
+        cfg = P.GeneralConfig(n=n, k=k)
+        assert n // cfg.resolved_d() >= 1 << 17
+        run = lambda: P.solve_general_batch(X, cfg, seeds=seeds)
     got = run()
-    monkeypatch.setenv("SFDT_FFT_A8", "0")
-    ref = run()
+    with P.tuning(fft_split=1):
+        ref = run()
     for b in range(B):
         g, r = got.spectrum(b).entries, ref.spectrum(b).entries
         assert list(g) == list(r)
@@ -428,7 +432,7 @@ def test_general_cfg5_k16384_full_shape():
     _general_check(res.spectrum(1).entries, locs, vals, "cfg5 K=2^14")
 
 
-def test_general_closed_form_singular_values(monkeypatch):
+def test_general_closed_form_singular_values():
     """a_max = 3: the closed-form singular values (bins with lambda_3 >=
     lambda_1 / 64, |r| <= 0.999) agree with the Jacobi for every bin to
     1e-13 relative, and the votes are identical."""
@@ -437,8 +441,8 @@ def test_general_closed_form_singular_values(monkeypatch):
     X = np.stack([general_signal(n, k, 10.0 + 5 * (b % 3), s)[0] for b, s in enumerate(seeds)])
     cfg = P.GeneralConfig(n=n, k=k)
     fast = P.solve_general_batch(X, cfg, seeds=seeds)
-    monkeypatch.setenv("SFDT_GEN_SVD", "jacobi")
-    jac = P.solve_general_batch(X, cfg, seeds=seeds)
+    with P.tuning(gen_svd_closed=0):
+        jac = P.solve_general_batch(X, cfg, seeds=seeds)
     sf, sj = fast.singular_values(), jac.singular_values()
     assert np.all(np.abs(sf - sj) <= 1e-13 * np.abs(sj))
     assert np.array_equal(fast.votes(), jac.votes())
@@ -448,7 +452,7 @@ def test_general_closed_form_singular_values(monkeypatch):
 
 @pytest.mark.parametrize("n,k,a_max", [(1 << 16, 256, 3), (1 << 16, 128, 3), (1 << 16, 64, 3),
                                        (1 << 14, 64, 2), (1 << 14, 256, 4), (1 << 14, 512, 3)])
-def test_general_matched_filter_short_lists(n, k, a_max, monkeypatch):
+def test_general_matched_filter_short_lists(n, k, a_max):
     """d <= 32: the group-per-bin matched filter (k_gen_mf_small) chooses the
     same columns as the warp-per-bin kernel -- supports and values equal
     bitwise -- and matches the oracle."""
@@ -458,8 +462,8 @@ def test_general_matched_filter_short_lists(n, k, a_max, monkeypatch):
     cfg = P.GeneralConfig(n=n, k=k, a_max=a_max)
     assert cfg.resolved_d() <= 32
     got = P.solve_general_batch(X, cfg, seeds=seeds)
-    monkeypatch.setenv("SFDT_GEN_MF_SMALL", "0")
-    ref = P.solve_general_batch(X, cfg, seeds=seeds)
+    with P.tuning(gen_mf_small=0):
+        ref = P.solve_general_batch(X, cfg, seeds=seeds)
     for b in range(B):
         g, r = got.spectrum(b).entries, ref.spectrum(b).entries
         assert list(g) == list(r)
@@ -471,7 +475,7 @@ def test_general_matched_filter_short_lists(n, k, a_max, monkeypatch):
 
 
 @pytest.mark.parametrize("n,k", [(1 << 16, 256), (1 << 18, 1024)])
-def test_general_duplicate_views_shared(n, k, monkeypatch):
+def test_general_duplicate_views_shared(n, k):
     """d = 8 (r_eff = d): every residue is drawn, so 6 of the 9 random shifts
     repeat a consecutive shift and share its view instead of being
     transformed again (smem FFT path at L = 8192, large-view path at
@@ -483,8 +487,8 @@ def test_general_duplicate_views_shared(n, k, monkeypatch):
     cfg = P.GeneralConfig(n=n, k=k)
     assert cfg.resolved_d() == 8
     got = P.solve_general_batch(X, cfg, seeds=seeds)
-    monkeypatch.setenv("SFDT_GEN_DEDUP", "0")
-    full = P.solve_general_batch(X, cfg, seeds=seeds)
+    with P.tuning(gen_dedup=0):
+        full = P.solve_general_batch(X, cfg, seeds=seeds)
     for b in range(B):
         g, f = got.spectrum(b).entries, full.spectrum(b).entries
         assert list(g) == list(f)
@@ -495,25 +499,23 @@ def test_general_duplicate_views_shared(n, k, monkeypatch):
     _general_check(got.spectrum(0).entries, locs, vals, "b=0")
 
 
-@pytest.mark.parametrize("var,val", [("SFDT_GEN_OVERLAP", "0"), ("SFDT_GEN_DEAL", "0"),
-                                     ("SFDT_GEN_DEAL", "1"), ("SFDT_GEN_SPLIT", "0"),
-                                     ("SFDT_GEN_SPLIT", "2"), ("SFDT_GEN_PRUNE2", "1")])
-def test_general_heavy_bins_side_stream(var, val, monkeypatch):
-    """The multi-collision pursuit (k_gen_bins) on its side stream beside
-    the single-collision pursuit, its bins dealt lane-major over the warps
+@pytest.mark.parametrize("key,val", [("gen_overlap", 0), ("gen_deal", 0), ("gen_deal", 1), ("gen_split_a", 0),
+                                     ("gen_split_a", 2)])
+def test_general_heavy_bins_side_stream(key, val):
+    """The multi-collision pursuit (k_gen_bins) on the aux stream beside the
+    single-collision pursuit, its bins dealt lane-major over the warps
     (default), gives the same bits as both on the caller's stream
-    (SFDT_GEN_OVERLAP=0), as the take-counter / one-per-warp schedules
-    (SFDT_GEN_DEAL=0 / 1), other deal orders (SFDT_GEN_SPLIT) and the
-    two-phase pruning around the fork (SFDT_GEN_PRUNE2=1), at the config-4 shape (d=256, 20 dB), and
-    matches the oracle (graph capture of the fork/join:
-    test_gpu_api.py::test_solve_graph_matches_batch)."""
+    (gen_overlap=0), as the take-counter / one-per-warp schedules
+    (gen_deal=0 / 1) and other deal orders (gen_split_a), at the config-4
+    shape (d=256, 20 dB), and matches the oracle (graph capture of the
+    fork/join: test_gpu_api.py::test_solve_graph_matches_batch)."""
     n, k, B = 1 << 20, 128, 4
     seeds = [(71, b) for b in range(B)]
     X = np.stack([general_signal(n, k, 20.0, s)[0] for s in seeds])
     cfg = P.GeneralConfig(n=n, k=k)
     got = P.solve_general_batch(X, cfg, seeds=seeds)
-    monkeypatch.setenv(var, val)
-    ref = P.solve_general_batch(X, cfg, seeds=seeds)
+    with P.tuning(**{key: val}):
+        ref = P.solve_general_batch(X, cfg, seeds=seeds)
     for b in range(B):
         g, r = got.spectrum(b).entries, ref.spectrum(b).entries
         assert list(g) == list(r)
@@ -524,17 +526,17 @@ def test_general_heavy_bins_side_stream(var, val, monkeypatch):
     _general_check(got.spectrum(2).entries, locs, vals, "b=2")
 
 
-@pytest.mark.parametrize("warp", ["1", "0"])
-def test_general_noprune_cfg4_shape(warp, monkeypatch):
+@pytest.mark.parametrize("warp", [1, 0])
+def test_general_noprune_cfg4_shape(warp):
     """prune=False at the config-4 shape (d=256): subspace pursuit over all d
-    columns per voted bin -- the warp-per-bin kernel (default) and the
-    thread-per-bin form (SFDT_GEN_WARP=0) -- against the oracle."""
-    monkeypatch.setenv("SFDT_GEN_WARP", warp)
+    columns per voted bin -- the warp-per-bin kernel and the thread-per-bin
+    form (tuning gen_warp) -- against the oracle."""
     n, k, B = 1 << 20, 128, 2
     seeds = [(17, b) for b in range(B)]
     X = np.stack([general_signal(n, k, 20.0, s)[0] for s in seeds])
     cfg = P.GeneralConfig(n=n, k=k, prune=False)
-    res = P.solve_general_batch(X, cfg, seeds=seeds)
+    with P.tuning(gen_warp=warp):
+        res = P.solve_general_batch(X, cfg, seeds=seeds)
     for b in range(B):
         want, wtr = OS.general(X[b], k, rng_seed=seeds[b], prune=False)
         locs = np.fromiter(want.keys(), dtype=np.int64, count=len(want))
@@ -730,7 +732,7 @@ def test_general_long_view_vote():
 
 
 @pytest.mark.parametrize("n,k", [(1 << 20, 16), (1 << 20, 32)])
-def test_general_prune_four_lanes(n, k, monkeypatch):
+def test_general_prune_four_lanes(n, k):
     """d = 2048 / 1024 with few bins: pruning with four lanes per bin (one
     512-candidate recurrence segment each, bottom-k lists merged by lane 0)
     keeps the same columns as one lane per bin, and the matched filter on
@@ -741,11 +743,11 @@ def test_general_prune_four_lanes(n, k, monkeypatch):
     X = np.stack([general_signal(n, k, 20.0 + 5 * b, s)[0] for b, s in enumerate(seeds)])
     cfg = P.GeneralConfig(n=n, k=k)
     assert cfg.resolved_d() >= 1024
-    monkeypatch.setenv("SFDT_GEN_PRUNE_LANES", "4")
-    got = P.solve_general_batch(X, cfg, seeds=seeds)
-    monkeypatch.setenv("SFDT_GEN_PRUNE_LANES", "1")
-    monkeypatch.setenv("SFDT_GEN_MF_LIST", "4096")   # and the matched filter's default bins per CTA
-    ref = P.solve_general_batch(X, cfg, seeds=seeds)
+    with P.tuning(gen_prune_lanes=4):
+        got = P.solve_general_batch(X, cfg, seeds=seeds)
+    # and the matched filter's default bins per CTA
+    with P.tuning(gen_prune_lanes=1, gen_mf_list=4096):
+        ref = P.solve_general_batch(X, cfg, seeds=seeds)
     for b in range(B):
         g, r = got.spectrum(b).entries, ref.spectrum(b).entries
         assert list(g) == list(r)

@@ -15,6 +15,8 @@ for k in 64 256 1024 4096 16384; do
   python bench.py --config cfg5 --cfg5-general --k $k --no-cpu --no-e2e --steps 5 --warmup 3 > $O/c5g_$k.json 2> $O/c5g_$k.err
 done
 python bench.py --config cfg4 --no-prune --no-cpu --no-e2e --steps 5 --warmup 3 > $O/cfg4_noprune.json 2> $O/cfg4_noprune.err
+python bench.py --impl reference --steps 2 --warmup 1 > $O/ref_cfg2.json 2> $O/ref_cfg2.err
+python bench.py --impl reference --config cfg4 --steps 2 --warmup 1 > $O/ref_cfg4.json 2> $O/ref_cfg4.err
 for k in 64 256 1024; do
   python bench.py --config cfg5 --cfg5-general --no-prune --k $k --no-cpu --no-e2e --steps 5 --warmup 3 > $O/c5g_noprune_$k.json 2> $O/c5g_noprune_$k.err
 done

@@ -173,7 +173,9 @@ def stock_reference():
     if not os.path.isdir(os.path.join(path, "sfft_dt")):
         return None
     if path not in sys.path:
-        sys.path.insert(0, path)
+        # appended, not prepended: baseline/_ref also holds the reference's
+        # staged test suite as a `tests` package, which must not shadow ours
+        sys.path.append(path)
     import logging
     logging.getLogger("sfft_dt").setLevel(logging.ERROR)   # per-solve warnings off the timed path
     try:

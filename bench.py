@@ -74,9 +74,11 @@ def parse():
     ap.add_argument("--e2e-chunk", type=int, default=256)
     ap.add_argument("--pipe-depth", type=int, default=4,
                     help="SolvePipeline depth for graph-replayed e2e (small batches)")
-    ap.add_argument("--hold-inputs", action="store_true",
-                    help="SolvePipeline.solve_stream(hold_inputs=True): the host rows are never "
-                         "refilled, so the per-item H2D wait is skipped")
+    ap.add_argument("--refill-inputs", action="store_true",
+                    help="SolvePipeline.solve_stream(hold_inputs=False): wait for every item's H2D "
+                         "before drawing the next (a producer refilling one buffer); by default the "
+                         "e2e leg's inputs are rows of a fixed pinned pool that is never modified, "
+                         "so hold_inputs=True")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -427,7 +429,7 @@ class Solver:
                     rows = [(lo + i) % H for i in range(B)]
                     yield (Xh[rows[0]:rows[0] + B] if rows[-1] == rows[0] + B - 1 else Xh[rows])
             res = None
-            for res in self.gh.solve_stream(batches(), hold_inputs=self.a.hold_inputs):
+            for res in self.gh.solve_stream(batches(), hold_inputs=not self.a.refill_inputs):
                 pass
             g0 = self.gh.graphs[0]
             return _GraphHostResult(res, n_signals * Xh.shape[1] * Xh.element_size(),
@@ -546,7 +548,8 @@ def gpu_arm(a):
                "d2h_bytes_per_step": int(hr.d2h_bytes),
                "api": ((f"paper_1407_8315_b200.SolvePipeline (depth {a.pipe_depth}: CUDA-graph host-IO "
                         "solves, each graph with its own workspace on its own stream; "
-                        + ("hold_inputs" if a.hold_inputs else "H2D waited before the next item")
+                        + ("H2D waited before the next item" if a.refill_inputs else
+                           "hold_inputs: rows of an unmodified pinned pool")
                         + "; pinned host -> GPU -> host results)") if getattr(solver, "g", None) is not None else
                        "paper_1407_8315_b200.solve_host_batch (pinned host -> GPU -> host results"
                        + ("; zero-copy: the view gather reads the (2*a_max+r_eff)*L samples of each "

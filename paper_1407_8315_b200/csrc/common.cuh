@@ -59,6 +59,30 @@ static inline int64_t one_wave(K kernel, int threads, size_t smem = 0) {
 // python-style non-negative modulo for power-of-two n
 __host__ __device__ __forceinline__ int64_t pmod(int64_t a, int64_t n) { return a & (n - 1); }
 
+// Programmatic dependent launch: a kernel launched with launch_pdl may be
+// scheduled while its predecessor in the stream is still running; it must
+// call pdl_wait() before touching memory the predecessor writes (every
+// kernel of a PDL chain calls it first thing, so the semantics stay those of
+// stream order -- only the launch latency between kernels overlaps).  A
+// no-op when the kernel was launched normally.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                     cudaStream_t stream, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // the measured-best design decisions (sfdt_tuning, include/sfdt.h)
 static inline sfdt_tuning default_tuning() {
     sfdt_tuning t;

@@ -33,6 +33,7 @@ namespace sfdt {
 template <int C64, int THREADS, int UNROLL>
 __global__ void __launch_bounds__(THREADS) k_sumsq(const void *__restrict__ x_, int64_t n, int64_t CH,
                                                   double *__restrict__ partial) {
+    pdl_wait();
     const int64_t b = blockIdx.y;
     const int64_t chunk = blockIdx.x;
     const int64_t CHp = CH >> 1;                        // sample pairs in this chunk
@@ -127,10 +128,37 @@ __global__ void __launch_bounds__(THREADS) k_sumsq_persistent(const void *__rest
     }
 }
 
+// The non-iterative decode's per-solve scratch -- the activity flags of
+// the signal's bins and the two worklist counters -- is zeroed by the rms
+// kernel that precedes the FFT (instead of memset nodes, which would break
+// the programmatic-dependent-launch chain of the latency path).
+struct DecodeScratch {
+    uint8_t *act;               // (B, L) activity flags, or nullptr
+    int64_t L;
+    unsigned long long *cnt0;   // worklist counters (zeroed by signal 0)
+    unsigned long long *cnt1;
+};
+
+__device__ __forceinline__ void zero_scratch(const DecodeScratch &z, int64_t b, int lane, int nlanes) {
+    if (z.act) {
+        uint8_t *row = z.act + b * z.L;
+        if ((z.L & 15) == 0)
+            for (int64_t i = lane; i < (z.L >> 4); i += nlanes) reinterpret_cast<uint4 *>(row)[i] = make_uint4(0, 0, 0, 0);
+        else
+            for (int64_t i = lane; i < z.L; i += nlanes) row[i] = 0;
+    }
+    if (b == 0 && lane == 0) {
+        if (z.cnt0) *z.cnt0 = 0;
+        if (z.cnt1) *z.cnt1 = 0;
+    }
+}
+
 // rms and threshold per signal: fixed-order pairwise tree over the partials
 __global__ void k_rms(const double *__restrict__ partial, int64_t nchunk, int64_t n, double zt,
-                      int64_t d, double *__restrict__ rms, double *__restrict__ thr) {
+                      int64_t d, double *__restrict__ rms, double *__restrict__ thr, DecodeScratch z) {
+    pdl_wait();
     const int64_t b = blockIdx.x;
+    zero_scratch(z, b, threadIdx.x, blockDim.x);
     __shared__ double buf[1024];
     double acc = 0.0;
     for (int64_t i = threadIdx.x; i < nchunk; i += blockDim.x) acc += partial[b * nchunk + i];
@@ -151,10 +179,12 @@ __global__ void k_rms(const double *__restrict__ partial, int64_t nchunk, int64_
 // tree's levels above 32 only add exact zeros, so lane t starting from
 // p[t] + p[t+32] and halving by shuffles reproduces it bit for bit
 __global__ void k_rms_warp(const double *__restrict__ partial, int64_t B, int64_t nchunk, int64_t n, double zt,
-                           int64_t d, double *__restrict__ rms, double *__restrict__ thr) {
+                           int64_t d, double *__restrict__ rms, double *__restrict__ thr, DecodeScratch z) {
+    pdl_wait();
     const int64_t b = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (b >= B) return;
+    zero_scratch(z, b, lane, 32);
     const double *pb = partial + b * nchunk;
     double v = (lane < nchunk ? pb[lane] : 0.0) + (lane + 32 < nchunk ? pb[lane + 32] : 0.0);
 #pragma unroll
@@ -167,17 +197,21 @@ __global__ void k_rms_warp(const double *__restrict__ partial, int64_t B, int64_
 }
 
 static inline void launch_rms(const double *partial, int64_t B, int64_t nchunk, int64_t n, double zt,
-                              int64_t d, double *rms, double *thr, cudaStream_t st) {
+                              int64_t d, double *rms, double *thr, cudaStream_t st,
+                              DecodeScratch z = DecodeScratch{nullptr, 0, nullptr, nullptr}) {
     if (nchunk <= 64)
-        k_rms_warp<<<(unsigned)((B + 7) / 8), 256, 0, st>>>(partial, B, nchunk, n, zt, d, rms, thr);
+        launch_pdl(k_rms_warp, dim3((unsigned)((B + 7) / 8)), dim3(256), 0, st, partial, B, nchunk, n, zt, d, rms,
+                   thr, z);
     else
-        k_rms<<<(unsigned)B, 1024, 0, st>>>(partial, nchunk, n, zt, d, rms, thr);
+        launch_pdl(k_rms, dim3((unsigned)B), dim3(1024), 0, st, partial, nchunk, n, zt, d, rms, thr, z);
 }
 
 // thresholds from a known rms (rms_in): copy rms out, zt*rms*d
 __global__ void k_thr_from_rms(const double *__restrict__ rms_in, int64_t B, double zt, int64_t d,
-                               double *__restrict__ rms_out, double *__restrict__ thr) {
+                               double *__restrict__ rms_out, double *__restrict__ thr, DecodeScratch z) {
+    pdl_wait();
     const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (b < B) zero_scratch(z, b, 0, 1);
     if (b < B) {
         const double r = rms_in[b];
         rms_out[b] = r;
@@ -210,6 +244,7 @@ __global__ void __launch_bounds__(128) k_decode_a1(const cx *__restrict__ V, int
                                                    cx *__restrict__ bin_val,
                                                    int64_t *__restrict__ wl,
                                                    unsigned long long *__restrict__ wl_count) {
+    pdl_wait();
     const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const bool valid = t < B * L;
     bool pending = false;
@@ -261,6 +296,7 @@ __global__ void __launch_bounds__(1024) k_act_compact(const uint8_t *__restrict_
                                                       uint8_t *__restrict__ status,
                                                       int64_t *__restrict__ awl,
                                                       unsigned long long *__restrict__ awlc) {
+    pdl_wait();
     // one global atomic per 4096-bin block (a single counter hammered once
     // per warp measured 95 us at config 2)
     __shared__ int wsum[32];
@@ -309,6 +345,7 @@ __global__ void __launch_bounds__(128) k_decode_a1_dense(const cx *__restrict__ 
                                                          const unsigned long long *__restrict__ awlc,
                                                          int64_t *__restrict__ wl,
                                                          unsigned long long *__restrict__ wl_count) {
+    pdl_wait();
     const int64_t cnt = (int64_t)*awlc;
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < cnt;
          i += int64_t(gridDim.x) * blockDim.x) {
@@ -354,6 +391,7 @@ __global__ void __launch_bounds__(128, SFDT_MULTI_MINB) k_decode_multi(const cx 
                                                       cx *__restrict__ bin_val,
                                                       const int64_t *__restrict__ wl,
                                                       const unsigned long long *__restrict__ wl_count) {
+    pdl_wait();
     const int64_t cnt = (int64_t)*wl_count;
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < cnt;
          i += int64_t(gridDim.x) * blockDim.x) {
@@ -392,24 +430,24 @@ static int launch_decode_noniter(const cx *V, int64_t B, int64_t L, int a_max, i
                                  const uint8_t *act = nullptr, int64_t *awl = nullptr,
                                  unsigned long long *awlc = nullptr) {
     const int64_t nbins = B * L;
-    cudaMemsetAsync(wl_count, 0, sizeof(unsigned long long), stream);
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // with `act` (the dense path) the counters were zeroed by the rms kernel
+    if (!act) cudaMemsetAsync(wl_count, 0, sizeof(unsigned long long), stream);
     if (act) {
-        cudaMemsetAsync(awlc, 0, sizeof(unsigned long long), stream);
-        k_act_compact<<<(unsigned)((nbins + 4095) / 4096), 1024, 0, stream>>>(act, nbins, status, awl, awlc);
+        launch_pdl(k_act_compact, dim3((unsigned)((nbins + 4095) / 4096)), dim3(1024), 0, stream, act, nbins, status,
+                   awl, awlc);
         SFDT_CHECK_LAUNCH();
-        k_decode_a1_dense<S><<<wl_grid(nbins, 128, one_wave(k_decode_a1_dense<S>, 128)), 128, 0, stream>>>(V, L, a_max, n, status, bin_loc,
-                                                                       bin_val, awl, awlc, wl, wl_count);
+        launch_pdl(k_decode_a1_dense<S>, dim3(wl_grid(nbins, 128, one_wave(k_decode_a1_dense<S>, 128))), dim3(128), 0,
+                   stream, V, L, a_max, n, status, bin_loc, bin_val, (const int64_t *)awl,
+                   (const unsigned long long *)awlc, wl, wl_count);
     } else {
-        k_decode_a1<S><<<(unsigned)((nbins + 127) / 128), 128, 0, stream>>>(V, B, L, a_max, n, thr, status,
-                                                                            bin_loc, bin_val, wl, wl_count);
+        launch_pdl(k_decode_a1<S>, dim3((unsigned)((nbins + 127) / 128)), dim3(128), 0, stream, V, B, L, a_max, n, thr,
+                   status, bin_loc, bin_val, wl, wl_count);
     }
     SFDT_CHECK_LAUNCH();
     if (a_max > 1) {
-        k_decode_multi<S><<<wl_grid(nbins, 128, one_wave(k_decode_multi<S>, 128)), 128, 0, stream>>>(V, L, a_max, n, status, bin_loc, bin_val,
-                                                                  wl, wl_count);
+        launch_pdl(k_decode_multi<S>, dim3(wl_grid(nbins, 128, one_wave(k_decode_multi<S>, 128))), dim3(128), 0, stream,
+                   V, L, a_max, n, status, bin_loc, bin_val, (const int64_t *)wl,
+                   (const unsigned long long *)wl_count);
         SFDT_CHECK_LAUNCH();
     }
     return SFDT_OK;
@@ -664,6 +702,7 @@ template <int THREADS>
 __global__ void __launch_bounds__(THREADS) k_noniter_count(const uint8_t *__restrict__ status, int64_t L,
                                                            int a_max, int64_t nseg,
                                                            long long *__restrict__ segcnt) {
+    pdl_wait();
     const int64_t b = blockIdx.x / nseg, g = blockIdx.x - b * nseg;
     const int64_t k0 = g * NONITER_SEG, k1 = (k0 + NONITER_SEG < L) ? k0 + NONITER_SEG : L;
     long long cnt[5] = {0, 0, 0, 0, 0};   // entries per a (1..4) and unresolved in [0]
@@ -700,6 +739,7 @@ __global__ void __launch_bounds__(THREADS) k_noniter_count(const uint8_t *__rest
 // per signal: fold the segment counts into the stats record
 __global__ void k_noniter_fin(const long long *__restrict__ segcnt, int64_t B, int64_t nseg, int64_t L,
                               int S, int64_t d, int64_t *__restrict__ stats) {
+    pdl_wait();
     const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (b >= B) return;
     long long r[7] = {0, 0, 0, 0, 0, 0, 0};
@@ -742,6 +782,7 @@ struct ScanFields {
 
 __global__ void __launch_bounds__(1024) k_scan_offsets(const int64_t *__restrict__ stats, int64_t B,
                                                        ScanFields f) {
+    pdl_wait();
     // thread t owns signals [t*per, (t+1)*per): its sums (independent loads,
     // one memory latency), one block scan of the thread sums, then its
     // offsets -- instead of a barrier-bound pass per 1024 signals
@@ -815,6 +856,7 @@ __global__ void __launch_bounds__(THREADS) k_noniter_emit(
     const cx *__restrict__ bin_val, int64_t L, int a_max, const int64_t *__restrict__ stats,
     const int64_t *__restrict__ eoff, const int64_t *__restrict__ uoff, int64_t *__restrict__ locs,
     cx *__restrict__ vals, int32_t *__restrict__ ubins, int64_t nseg, const long long *__restrict__ segcnt) {
+    pdl_wait();
     __shared__ unsigned long long wtot[THREADS / 32];
     const int64_t b = blockIdx.x / nseg, g = blockIdx.x - b * nseg;
     const int64_t *st = stats + b * SFDT_ST_PER_SIGNAL;
@@ -1269,9 +1311,11 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
         } else {
             constexpr int TH = 512, UN = 4;
             if (is_c64)
-                k_sumsq<1, TH, UN><<<grid, TH, 0, stream>>>(xc, p.n, p.CH, partial + c0 * p.nchunk);
+                launch_pdl(k_sumsq<1, TH, UN>, grid, dim3(TH), 0, stream, (const void *)xc, p.n, p.CH,
+                           partial + c0 * p.nchunk);
             else
-                k_sumsq<0, TH, UN><<<grid, TH, 0, stream>>>(xc, p.n, p.CH, partial + c0 * p.nchunk);
+                launch_pdl(k_sumsq<0, TH, UN>, grid, dim3(TH), 0, stream, (const void *)xc, p.n, p.CH,
+                           partial + c0 * p.nchunk);
         }
         SFDT_CHECK_LAUNCH();
         launches += 1;
@@ -1326,19 +1370,20 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
                 cudaStreamWaitEvent(aux, ev, 0);
                 cudaEventDestroy(ev);
             }
-            if (a->rms_in)
-                k_thr_from_rms<<<(unsigned)((nb + 255) / 256), 256, 0, aux>>>(a->rms_in + c0, nb,
-                                                                              a->zero_threshold, p.d,
-                                                                              a->rms + c0, thr + c0);
-            else
-                launch_rms(partial + c0 * p.nchunk, nb, p.nchunk, p.n, a->zero_threshold, p.d, a->rms + c0,
-                           thr + c0, aux);
-            SFDT_CHECK_LAUNCH();
-            // after the rms the FFT epilogue can also mark the active bins
+            // after the rms the FFT epilogue can also mark the active bins;
+            // the rms kernel zeroes their flags and the worklist counters
             const bool dense = !overlap;
             uint8_t *actc = dense ? (uint8_t *)(w + p.off_act) + c0 * p.L : nullptr;
+            const DecodeScratch zs = dense ? DecodeScratch{actc, p.L, wlc + c, wlc + 64 + c}
+                                           : DecodeScratch{nullptr, 0, nullptr, nullptr};
+            if (a->rms_in)
+                launch_pdl(k_thr_from_rms, dim3((unsigned)((nb + 255) / 256)), dim3(256), 0, aux,
+                           (const double *)(a->rms_in + c0), nb, a->zero_threshold, p.d, a->rms + c0, thr + c0, zs);
+            else
+                launch_rms(partial + c0 * p.nchunk, nb, p.nchunk, p.n, a->zero_threshold, p.d, a->rms + c0,
+                           thr + c0, aux, zs);
+            SFDT_CHECK_LAUNCH();
             if (!overlap) {
-                if (actc) cudaMemsetAsync(actc, 0, size_t(nb) * p.L, aux);
                 const ViewSrc src = consecutive_views((const char *)a->x + c0 * p.n * (is_c64 ? 8 : 16), is_c64,
                                                       p.n, p.d, 0, (int)p.S);
                 rc = launch_fft_views(src, nb, p.L, a->twiddles, V + c0 * p.S * p.L, (int)p.S, p.L, aux,
@@ -1368,18 +1413,20 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
         }
         const int64_t nseg = (p.L + NONITER_SEG - 1) / NONITER_SEG;
         long long *segcnt = (long long *)(w + p.off_seg);
-        k_noniter_count<256><<<(unsigned)(p.B * nseg), 256, 0, stream>>>(status, p.L, a->a_max, nseg, segcnt);
-        k_noniter_fin<<<(unsigned)((p.B + 255) / 256), 256, 0, stream>>>(segcnt, p.B, nseg, p.L, (int)p.S,
-                                                                         p.d, a->stats);
+        launch_pdl(k_noniter_count<256>, dim3((unsigned)(p.B * nseg)), dim3(256), 0, stream, (const uint8_t *)status,
+                   p.L, a->a_max, nseg, segcnt);
+        launch_pdl(k_noniter_fin, dim3((unsigned)((p.B + 255) / 256)), dim3(256), 0, stream,
+                   (const long long *)segcnt, p.B, nseg, p.L, (int)p.S, p.d, a->stats);
         SFDT_CHECK_LAUNCH();
         {
             ScanFields f{{SFDT_ST_NENTRIES, SFDT_ST_NUNRESOLVED, 0}, {a->entry_offsets, a->unres_offsets, nullptr}, 2};
-            k_scan_offsets<<<1, 1024, 0, stream>>>(a->stats, p.B, f);
+            launch_pdl(k_scan_offsets, dim3(1), dim3(1024), 0, stream, (const int64_t *)a->stats, p.B, f);
         }
         SFDT_CHECK_LAUNCH();
-        k_noniter_emit<256><<<(unsigned)(p.B * nseg), 256, 0, stream>>>(
-            status, bloc, bval, p.L, a->a_max, a->stats, a->entry_offsets, a->unres_offsets,
-            a->locs, (cx *)a->vals, a->unres_bins, nseg, segcnt);
+        launch_pdl(k_noniter_emit<256>, dim3((unsigned)(p.B * nseg)), dim3(256), 0, stream, (const uint8_t *)status,
+                   (const int64_t *)bloc, (const cx *)bval, p.L, a->a_max, (const int64_t *)a->stats,
+                   (const int64_t *)a->entry_offsets, (const int64_t *)a->unres_offsets, a->locs, (cx *)a->vals,
+                   a->unres_bins, nseg, (const long long *)segcnt);
         SFDT_CHECK_LAUNCH();
         if (a->dup_offsets) cudaMemsetAsync(a->dup_offsets, 0, sizeof(int64_t) * (p.B + 1), stream);
         launches += 4;   // count, fin, scan, emit
@@ -1393,7 +1440,8 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
     if (a->ev_stream_end) cudaEventRecord((cudaEvent_t)a->ev_stream_end, stream);
     if (a->rms_in)
         k_thr_from_rms<<<(unsigned)((p.B + 255) / 256), 256, 0, stream>>>(a->rms_in, p.B, a->zero_threshold,
-                                                                          p.d, a->rms, thr);
+                                                                          p.d, a->rms, thr,
+                                                                          DecodeScratch{nullptr, 0, nullptr, nullptr});
     else
         launch_rms(partial, p.B, p.nchunk, p.n, a->zero_threshold, p.d, a->rms, thr, stream);
     SFDT_CHECK_LAUNCH();

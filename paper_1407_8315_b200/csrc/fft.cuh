@@ -274,6 +274,7 @@ static __global__ void __launch_bounds__(256, MINB) k_fft_views(const ViewSrc sr
                                    const cx *__restrict__ tw, cx *__restrict__ out, int SV,
                                    int64_t ldV, int scale, const double *__restrict__ thr,
                                    uint8_t *__restrict__ act) {
+    pdl_wait();
     extern __shared__ double4 smem_raw[];
     cx *a = reinterpret_cast<cx *>(smem_raw);
     __shared__ int64_t s_ibase[MAX_VIEWS], s_ioff[MAX_VIEWS], s_obase[MAX_VIEWS], s_sig[MAX_VIEWS];
@@ -668,7 +669,8 @@ static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, con
         // <= 32 KiB per CTA: cap registers at 64 for 4 CTAs/SM (measured
         // 717 -> 553 us at config 2); larger tiles keep 128 registers
         if (smem <= 32 * 1024) {
-            k_fft_views<4><<<grid, 256, smem, stream>>>(src, B, logL, logvpc, tw, out, SV, ldV, scale, thr, act);
+            launch_pdl(k_fft_views<4>, dim3(grid), dim3(256), smem, stream, src, B, logL, logvpc, tw, out, SV, ldV,
+                       scale, thr, act);
         } else if (smem <= 64 * 1024) {
             // 64 KiB tiles: registers capped at 85 (3 CTAs/SM would fit).
             // Two CTAs per SM, the rest of the 256 KiB as L1: the view
@@ -678,10 +680,12 @@ static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, con
             cudaFuncSetAttribute(k_fft_views<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             cudaFuncSetAttribute(k_fft_views<3>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  (int)((2 * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024)));
-            k_fft_views<3><<<grid, 256, smem, stream>>>(src, B, logL, logvpc, tw, out, SV, ldV, scale, thr, act);
+            launch_pdl(k_fft_views<3>, dim3(grid), dim3(256), smem, stream, src, B, logL, logvpc, tw, out, SV, ldV,
+                       scale, thr, act);
         } else {
             cudaFuncSetAttribute(k_fft_views<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            k_fft_views<1><<<grid, 256, smem, stream>>>(src, B, logL, logvpc, tw, out, SV, ldV, scale, thr, act);
+            launch_pdl(k_fft_views<1>, dim3(grid), dim3(256), smem, stream, src, B, logL, logvpc, tw, out, SV, ldV,
+                       scale, thr, act);
         }
         SFDT_CHECK_LAUNCH();
         return SFDT_OK;

@@ -106,6 +106,14 @@ typedef struct {
     int32_t gen_split_a;     /* heavy bins with a >= gen_split_a dealt first (0: list order) */
     int32_t gen_prune_lanes; /* lanes per pruned bin: 0 auto, 1 or 4 */
     int32_t gen_deal;        /* heavy bins dealt lane-major while <= gen_deal per warp (0: take counter) */
+    int32_t decode_coop;     /* non-iterative multi-collision decode: 0 one thread per bin for every a;
+                                1 eight lanes per bin, the a = 2 and a = 3 trials side by side in two
+                                warps (a = 4 afterwards where needed); 2 thread per bin for a = 2,
+                                cooperative for a = 3 then 4; 3 cooperative, every a side by side;
+                                -1 auto (1 for small batches, else 2) */
+    int32_t latency_path;    /* non-iterative solves of <= 8 short signals (L <= 8192, n <= 2^20): -1 the
+                                fused five-kernel chain; 0 the general ten-kernel chain; 1 the fused chain
+                                for up to 64 signals */
 } sfdt_tuning;
 
 void sfdt_default_tuning(sfdt_tuning *out);

@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libsfdt_b200.so")
 CU_SOURCES = ["exact.cu", "kernels.cu", "general.cu", "runtime.cu", "dropin.cu"]
 C_SOURCES = ["twiddle.c"]
-HEADERS = ["cx.cuh", "common.cuh", "decode.cuh", "fft.cuh", "general.cuh"]
+HEADERS = ["cx.cuh", "common.cuh", "decode.cuh", "decode_coop.cuh", "fft.cuh", "general.cuh"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off", "--fmad=false",

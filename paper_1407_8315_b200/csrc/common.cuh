@@ -95,6 +95,8 @@ static inline sfdt_tuning default_tuning() {
     t.gen_split_a = 3;
     t.gen_prune_lanes = 0;
     t.gen_deal = 8;
+    t.decode_coop = -1;
+    t.latency_path = -1;
     return t;
 }
 static inline sfdt_tuning tuning_or_default(const sfdt_tuning *t) { return t ? *t : default_tuning(); }

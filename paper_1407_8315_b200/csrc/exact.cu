@@ -19,9 +19,37 @@
 //                  reference's dict insertion order.
 #include "common.cuh"
 #include "decode.cuh"
+#include "decode_coop.cuh"
 #include "fft.cuh"
 
 namespace sfdt {
+
+// The non-iterative decode's per-solve scratch -- the activity flags of
+// the signal's bins and the two worklist counters -- is zeroed by the rms
+// kernel that precedes the FFT (instead of memset nodes, which would break
+// the programmatic-dependent-launch chain of the latency path).
+struct DecodeScratch {
+    uint8_t *act;               // (B, L) activity flags, or nullptr
+    int64_t L;
+    unsigned long long *cnt0;   // worklist counters (zeroed by signal 0)
+    unsigned long long *cnt1;
+    unsigned long long *cnt2;
+};
+
+__device__ __forceinline__ void zero_scratch(const DecodeScratch &z, int64_t b, int lane, int nlanes) {
+    if (z.act) {
+        uint8_t *row = z.act + b * z.L;
+        if ((z.L & 15) == 0)
+            for (int64_t i = lane; i < (z.L >> 4); i += nlanes) reinterpret_cast<uint4 *>(row)[i] = make_uint4(0, 0, 0, 0);
+        else
+            for (int64_t i = lane; i < z.L; i += nlanes) row[i] = 0;
+    }
+    if (b == 0 && lane == 0) {
+        if (z.cnt0) *z.cnt0 = 0;
+        if (z.cnt1) *z.cnt1 = 0;
+        if (z.cnt2) *z.cnt2 = 0;
+    }
+}
 
 // ------------------------------------------------------------- stream pass
 // grid (nchunk, B): each CTA streams CH contiguous samples of one signal and
@@ -32,10 +60,12 @@ namespace sfdt {
 // here: the FFT kernel gathers them straight from x.
 template <int C64, int THREADS, int UNROLL>
 __global__ void __launch_bounds__(THREADS) k_sumsq(const void *__restrict__ x_, int64_t n, int64_t CH,
-                                                  double *__restrict__ partial) {
+                                                  double *__restrict__ partial, DecodeScratch z) {
     pdl_wait();
     const int64_t b = blockIdx.y;
     const int64_t chunk = blockIdx.x;
+    // latency path: the solve's first kernel zeroes the worklist counters
+    if (chunk == 0) zero_scratch(z, b, threadIdx.x, THREADS);
     const int64_t CHp = CH >> 1;                        // sample pairs in this chunk
     const int64_t base = (b * n + chunk * CH) >> 1;     // pair index
     double acc = 0.0;
@@ -128,31 +158,6 @@ __global__ void __launch_bounds__(THREADS) k_sumsq_persistent(const void *__rest
     }
 }
 
-// The non-iterative decode's per-solve scratch -- the activity flags of
-// the signal's bins and the two worklist counters -- is zeroed by the rms
-// kernel that precedes the FFT (instead of memset nodes, which would break
-// the programmatic-dependent-launch chain of the latency path).
-struct DecodeScratch {
-    uint8_t *act;               // (B, L) activity flags, or nullptr
-    int64_t L;
-    unsigned long long *cnt0;   // worklist counters (zeroed by signal 0)
-    unsigned long long *cnt1;
-};
-
-__device__ __forceinline__ void zero_scratch(const DecodeScratch &z, int64_t b, int lane, int nlanes) {
-    if (z.act) {
-        uint8_t *row = z.act + b * z.L;
-        if ((z.L & 15) == 0)
-            for (int64_t i = lane; i < (z.L >> 4); i += nlanes) reinterpret_cast<uint4 *>(row)[i] = make_uint4(0, 0, 0, 0);
-        else
-            for (int64_t i = lane; i < z.L; i += nlanes) row[i] = 0;
-    }
-    if (b == 0 && lane == 0) {
-        if (z.cnt0) *z.cnt0 = 0;
-        if (z.cnt1) *z.cnt1 = 0;
-    }
-}
-
 // rms and threshold per signal: fixed-order pairwise tree over the partials
 __global__ void k_rms(const double *__restrict__ partial, int64_t nchunk, int64_t n, double zt,
                       int64_t d, double *__restrict__ rms, double *__restrict__ thr, DecodeScratch z) {
@@ -198,7 +203,7 @@ __global__ void k_rms_warp(const double *__restrict__ partial, int64_t B, int64_
 
 static inline void launch_rms(const double *partial, int64_t B, int64_t nchunk, int64_t n, double zt,
                               int64_t d, double *rms, double *thr, cudaStream_t st,
-                              DecodeScratch z = DecodeScratch{nullptr, 0, nullptr, nullptr}) {
+                              DecodeScratch z = DecodeScratch{nullptr, 0, nullptr, nullptr, nullptr}) {
     if (nchunk <= 64)
         launch_pdl(k_rms_warp, dim3((unsigned)((B + 7) / 8)), dim3(256), 0, st, partial, B, nchunk, n, zt, d, rms,
                    thr, z);
@@ -282,6 +287,76 @@ __global__ void __launch_bounds__(128) k_decode_a1(const cx *__restrict__ V, int
     const unsigned mask = __ballot_sync(0xffffffffu, pending);
     if (mask) {
         const int lane = threadIdx.x & 31;
+        unsigned long long base = 0;
+        if (lane == __ffs(mask) - 1) base = atomicAdd(wl_count, (unsigned long long)__popc(mask));
+        base = __shfl_sync(0xffffffffu, base, __ffs(mask) - 1);
+        if (pending) wl[base + __popc(mask & ((1u << lane) - 1))] = t;
+    }
+}
+
+// Latency path: k_decode_a1 with the rms tree of k_rms_warp in its prologue
+// (every warp folds its signal's <= 64 partials the same way, so the threshold
+// has the same bits), which removes the rms kernel and the activity
+// compaction from a small solve's launch chain.  Needs L % 32 == 0 (a warp's
+// bins belong to one signal).
+template <int S>
+__global__ void __launch_bounds__(128) k_decode_a1r(const cx *__restrict__ V, int64_t B, int64_t L, int a_max,
+                                                    int64_t n, const double *__restrict__ partial, int64_t nchunk,
+                                                    double zt, int64_t d, double *__restrict__ rms,
+                                                    double *__restrict__ thr_out, uint8_t *__restrict__ status,
+                                                    int64_t *__restrict__ bin_loc, cx *__restrict__ bin_val,
+                                                    int64_t *__restrict__ wl,
+                                                    unsigned long long *__restrict__ wl_count) {
+    pdl_wait();
+    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int64_t t_first = t - lane;
+    if (t_first >= B * L) return;   // whole warp out of range
+    const int64_t b = t_first / L, k = t - b * L;
+    double th;
+    {
+        const double *pb = partial + b * nchunk;
+        double v = (lane < nchunk ? pb[lane] : 0.0) + (lane + 32 < nchunk ? pb[lane + 32] : 0.0);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        const double r = sqrt(v / (double)n);
+        th = DMUL(DMUL(zt, r), (double)d);
+        if (lane == 0 && t_first == b * L) {
+            rms[b] = r;
+            thr_out[b] = th;
+        }
+        th = __shfl_sync(0xffffffffu, th, 0);
+    }
+    bool pending = false;
+    {
+        cx syn[S];
+        const double th2lo = th * th * (1.0 - 1e-6), th2hi = th * th * (1.0 + 1e-6);
+        bool active = false;
+#pragma unroll
+        for (int s = 0; s < S; s++) {
+            syn[s] = ldcx(V + (b * S + s) * L + k);
+            const double q = syn[s].re * syn[s].re + syn[s].im * syn[s].im;
+            active = active || (q > th2hi) || (q >= th2lo && cabs_(syn[s]) > th);
+        }
+        uint8_t st = 0;
+        if (active) {
+            Decoded o;
+            decode_try_t<1, S>(syn, n, L, k, o);
+            if (o.accept) {
+                st = 1;
+                bin_loc[t * a_max] = o.loc[0];
+                stcx(bin_val + t * a_max, o.val[0]);
+            } else if (a_max > 1) {
+                st = 0xFE;
+                pending = true;
+            } else {
+                st = 0xFF;
+            }
+        }
+        status[t] = st;
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, pending);
+    if (mask) {
         unsigned long long base = 0;
         if (lane == __ffs(mask) - 1) base = atomicAdd(wl_count, (unsigned long long)__popc(mask));
         base = __shfl_sync(0xffffffffu, base, __ffs(mask) - 1);
@@ -386,12 +461,16 @@ __global__ void __launch_bounds__(128) k_decode_a1_dense(const cx *__restrict__ 
 #endif
 template <int S>
 __global__ void __launch_bounds__(128, SFDT_MULTI_MINB) k_decode_multi(const cx *__restrict__ V, int64_t L, int a_max,
-                                                      int64_t n, uint8_t *__restrict__ status,
+                                                      int a_hi, int64_t n, uint8_t *__restrict__ status,
                                                       int64_t *__restrict__ bin_loc,
                                                       cx *__restrict__ bin_val,
                                                       const int64_t *__restrict__ wl,
-                                                      const unsigned long long *__restrict__ wl_count) {
+                                                      const unsigned long long *__restrict__ wl_count,
+                                                      int64_t *__restrict__ wl2,
+                                                      unsigned long long *__restrict__ wl2_count) {
     pdl_wait();
+    // tries a = 2..a_hi; with a_hi < a_max the bins still unsolved go to wl2
+    // (k_decode_coop takes a_hi + 1..a_max)
     const int64_t cnt = (int64_t)*wl_count;
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < cnt;
          i += int64_t(gridDim.x) * blockDim.x) {
@@ -400,9 +479,9 @@ __global__ void __launch_bounds__(128, SFDT_MULTI_MINB) k_decode_multi(const cx 
         cx syn[S];
 #pragma unroll
         for (int s = 0; s < S; s++) syn[s] = ldcx(V + (b * S + s) * L + k);
-        uint8_t st = 0xFF;
+        uint8_t st = a_hi < a_max ? 0xFE : 0xFF;
         Decoded o;
-        for (int a = 2; a <= a_max; a++) {
+        for (int a = 2; a <= a_hi; a++) {
 #if SFDT_MULTI_TEMPLATED
             if (a == 2) decode_try_t<2, S>(syn, n, L, k, o);
             else if (a == 3) decode_try_t<3, S>(syn, n, L, k, o);
@@ -420,18 +499,184 @@ __global__ void __launch_bounds__(128, SFDT_MULTI_MINB) k_decode_multi(const cx 
             }
         }
         status[t] = st;
+        if (a_hi < a_max) {
+            const bool pend = st == 0xFE;
+            const unsigned act_mask = __activemask();
+            const unsigned m = __ballot_sync(act_mask, pend);
+            if (m) {
+                const int lane = threadIdx.x & 31;
+                const int leader = __ffs(m) - 1;
+                unsigned long long base = 0;
+                if (lane == leader) base = atomicAdd(wl2_count, (unsigned long long)__popc(m));
+                base = __shfl_sync(act_mask, base, leader);
+                if (pend) wl2[base + __popc(m & ((1u << lane) - 1))] = t;
+            }
+        }
     }
+}
+
+// Cooperative multi-collision decode (decode_coop.cuh).  A CTA of `nw` warps
+// takes four worklist bins at a time (eight lanes per bin, so a warp executes
+// one trial's code without divergence): warp w runs the a = a_lo + w trial of
+// all four bins at once, and the smallest accepted a wins -- the one the
+// reference's ascending loop (exact.py:184-192) stops at, because a trial
+// depends only on the bin's syndromes.  Trials beyond a_lo + nw - 1 (rare:
+// 3 % of config-1 signals hold a 4-collision bin) run afterwards on warp 0,
+// only when one of the four bins is still unsolved.
+constexpr int COOP_BINS = 32 / COOP_G;
+
+template <int S>
+__device__ __forceinline__ void coop_trial(int A, const cx *syn, int64_t n, int64_t L, int64_t k, int g,
+                                           DecodedCoop &o) {
+    o.accept = false;
+    if (A == 2) {
+        if constexpr (S >= 4) decode_try_coop<2, S>(syn, n, L, k, g, o);
+    } else if (A == 3) {
+        if constexpr (S >= 6) decode_try_coop<3, S>(syn, n, L, k, g, o);
+    } else {
+        if constexpr (S >= 8) decode_try_coop<4, S>(syn, n, L, k, g, o);
+    }
+}
+
+template <int S>
+__global__ void __launch_bounds__(96) k_decode_coop(const cx *__restrict__ V, int64_t L, int a_max, int a_lo,
+                                                    int64_t n, uint8_t *__restrict__ status,
+                                                    int64_t *__restrict__ bin_loc, cx *__restrict__ bin_val,
+                                                    const int64_t *__restrict__ wl,
+                                                    const unsigned long long *__restrict__ wl_count) {
+    pdl_wait();
+    __shared__ int s_acc[3][COOP_BINS];
+    __shared__ long long s_loc[3][COOP_BINS][4];
+    __shared__ double2 s_val[3][COOP_BINS][4];
+    __shared__ int s_more;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane & (COOP_G - 1), grp = lane / COOP_G;
+    const int nw = blockDim.x >> 5;
+    const int64_t cnt = (int64_t)*wl_count;
+    for (int64_t base = int64_t(blockIdx.x) * COOP_BINS; base < cnt; base += int64_t(gridDim.x) * COOP_BINS) {
+        const int64_t i = base + grp;
+        const bool valid = i < cnt;
+        const int64_t t = valid ? wl[i] : 0;
+        const int64_t b = t / L, k = t - b * L;
+        cx syn[S];
+#pragma unroll
+        for (int s = 0; s < S; s++) syn[s] = valid ? ldcx(V + (b * S + s) * L + k) : mk(0.0, 0.0);
+        int A = a_lo + warp, next = a_lo + nw;
+        bool run = true;
+        int a_win = 0, slot = 0;   // warp 0's verdict on its four bins
+        for (;;) {
+            if (run) {
+                DecodedCoop o;
+                coop_trial<S>(A, syn, n, L, k, g, o);
+                if (g == 0 && a_win == 0) {
+                    s_acc[warp][grp] = o.accept ? 1 : 0;
+                    if (o.accept) {
+                        for (int j = 0; j < A; j++) {
+                            s_loc[warp][grp][j] = o.loc[j];
+                            s_val[warp][grp][j] = make_double2(o.val[j].re, o.val[j].im);
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+            if (warp == 0) {
+                if (a_win == 0) {
+                    for (int w = nw - 1; w >= 0; w--)
+                        if (s_acc[w][grp]) {
+                            a_win = w == 0 ? A : a_lo + w;
+                            slot = w;
+                        }
+                }
+                const bool open = __any_sync(0xffffffffu, valid && a_win == 0 && next <= a_max);
+                if (lane == 0) s_more = open ? next : 0;
+            }
+            __syncthreads();
+            const int mo = s_more;   // CTA-uniform
+            if (!mo) break;
+            // later trials (rare) on warp 0 alone; the other warps' flags for
+            // a still-open bin stay 0
+            A = mo;
+            next = mo + 1;
+            run = warp == 0;
+        }
+        if (warp == 0 && valid) {
+            if (g == 0) status[t] = a_win ? (uint8_t)a_win : 0xFF;
+            if (g < a_win) {
+                bin_loc[t * a_max + g] = s_loc[slot][grp][g];
+                *reinterpret_cast<double2 *>(bin_val + t * a_max + g) = s_val[slot][grp][g];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// decode_coop (sfdt_tuning): 0 one thread per bin for every a; 1 cooperative
+// trials, a = 2 and 3 side by side (a = 4 afterwards where needed); 2 thread
+// per bin for a = 2, cooperative for a = 3 then 4; 3 cooperative, every a
+// side by side; -1 picks 1 while the batch has few bins (a latency-bound
+// solve), else 2.
+static inline int decode_coop_mode(int req, int64_t nbins, int a_max) {
+    if (a_max < 2) return 0;
+    int mode = req;
+    if (mode < 0) mode = nbins <= (int64_t)1 << 17 ? 1 : 2;
+    if (mode == 2 && a_max < 3) mode = 0;
+    return mode;
+}
+
+// a >= 2 trials on the worklist of bins the a = 1 model failed on
+template <int S>
+static int launch_decode_multi(const cx *V, int64_t nbins, int64_t L, int a_max, int64_t n, uint8_t *status,
+                               int64_t *bin_loc, cx *bin_val, int64_t *wl, unsigned long long *wl_count,
+                               int64_t *wl2, unsigned long long *wl2_count, int coop, cudaStream_t stream) {
+    if (a_max > 1) {
+        const int mode = decode_coop_mode(coop, nbins, a_max);
+        if (mode != 1 && mode != 3) {
+            const int a_hi = mode == 2 ? 2 : a_max;
+            launch_pdl(k_decode_multi<S>, dim3(wl_grid(nbins, 128, one_wave(k_decode_multi<S>, 128))), dim3(128), 0,
+                       stream, V, L, a_max, a_hi, n, status, bin_loc, bin_val, (const int64_t *)wl,
+                       (const unsigned long long *)wl_count, wl2, wl2_count);
+            SFDT_CHECK_LAUNCH();
+        }
+        if (mode != 0) {
+            const int a_lo = mode == 2 ? 3 : 2;
+            int nw = mode == 2 ? 1 : (mode == 3 ? 3 : 2);
+            if (nw > a_max - a_lo + 1) nw = a_max - a_lo + 1;
+            const int threads = 32 * nw;
+            launch_pdl(k_decode_coop<S>, dim3(wl_grid(nbins, COOP_BINS, one_wave(k_decode_coop<S>, threads))),
+                       dim3(threads), 0, stream, V, L, a_max, a_lo, n, status, bin_loc, bin_val,
+                       (const int64_t *)(mode == 2 ? wl2 : wl),
+                       (const unsigned long long *)(mode == 2 ? wl2_count : wl_count));
+            SFDT_CHECK_LAUNCH();
+        }
+    }
+    return SFDT_OK;
+}
+
+// the latency path's decode: rms + activity + a = 1 in one kernel, then a >= 2
+template <int S>
+static int launch_decode_small(const cx *V, int64_t B, int64_t L, int a_max, int64_t n, const double *partial,
+                               int64_t nchunk, double zt, int64_t d, double *rms, double *thr, uint8_t *status,
+                               int64_t *bin_loc, cx *bin_val, int64_t *wl, unsigned long long *wl_count,
+                               int64_t *wl2, unsigned long long *wl2_count, int coop, cudaStream_t stream) {
+    const int64_t nbins = B * L;
+    launch_pdl(k_decode_a1r<S>, dim3((unsigned)((nbins + 127) / 128)), dim3(128), 0, stream, V, B, L, a_max, n,
+               partial, nchunk, zt, d, rms, thr, status, bin_loc, bin_val, wl, wl_count);
+    SFDT_CHECK_LAUNCH();
+    return launch_decode_multi<S>(V, nbins, L, a_max, n, status, bin_loc, bin_val, wl, wl_count, wl2, wl2_count, coop,
+                                  stream);
 }
 
 template <int S>
 static int launch_decode_noniter(const cx *V, int64_t B, int64_t L, int a_max, int64_t n,
                                  const double *thr, uint8_t *status, int64_t *bin_loc, cx *bin_val,
                                  int64_t *wl, unsigned long long *wl_count, cudaStream_t stream,
-                                 const uint8_t *act = nullptr, int64_t *awl = nullptr,
-                                 unsigned long long *awlc = nullptr) {
+                                 const uint8_t *act, int64_t *awl, unsigned long long *awlc,
+                                 int64_t *wl2, unsigned long long *wl2_count, int coop) {
     const int64_t nbins = B * L;
     // with `act` (the dense path) the counters were zeroed by the rms kernel
-    if (!act) cudaMemsetAsync(wl_count, 0, sizeof(unsigned long long), stream);
+    if (!act) {
+        cudaMemsetAsync(wl_count, 0, sizeof(unsigned long long), stream);
+        cudaMemsetAsync(wl2_count, 0, sizeof(unsigned long long), stream);
+    }
     if (act) {
         launch_pdl(k_act_compact, dim3((unsigned)((nbins + 4095) / 4096)), dim3(1024), 0, stream, act, nbins, status,
                    awl, awlc);
@@ -444,13 +689,8 @@ static int launch_decode_noniter(const cx *V, int64_t B, int64_t L, int a_max, i
                    status, bin_loc, bin_val, wl, wl_count);
     }
     SFDT_CHECK_LAUNCH();
-    if (a_max > 1) {
-        launch_pdl(k_decode_multi<S>, dim3(wl_grid(nbins, 128, one_wave(k_decode_multi<S>, 128))), dim3(128), 0, stream,
-                   V, L, a_max, n, status, bin_loc, bin_val, (const int64_t *)wl,
-                   (const unsigned long long *)wl_count);
-        SFDT_CHECK_LAUNCH();
-    }
-    return SFDT_OK;
+    return launch_decode_multi<S>(V, nbins, L, a_max, n, status, bin_loc, bin_val, wl, wl_count, wl2, wl2_count, coop,
+                                  stream);
 }
 
 // ----------------------------------------------------- iterative pass l
@@ -698,17 +938,15 @@ __global__ void k_iter_final(const cx *__restrict__ V, const uint8_t *__restrict
 constexpr int64_t NONITER_SEG = 8192;
 constexpr int SEGF = 8;   // per-segment fields: unresolved, entries a=1..4, active, tries
 
+// counts of one signal's bins [k0, k1): on return red[q][0], q = 0..6, hold
+// unresolved bins, entries of a = 1..4, active bins, trials (all threads call)
 template <int THREADS>
-__global__ void __launch_bounds__(THREADS) k_noniter_count(const uint8_t *__restrict__ status, int64_t L,
-                                                           int a_max, int64_t nseg,
-                                                           long long *__restrict__ segcnt) {
-    pdl_wait();
-    const int64_t b = blockIdx.x / nseg, g = blockIdx.x - b * nseg;
-    const int64_t k0 = g * NONITER_SEG, k1 = (k0 + NONITER_SEG < L) ? k0 + NONITER_SEG : L;
+__device__ __forceinline__ void noniter_count_bins(const uint8_t *__restrict__ row, int64_t k0, int64_t k1,
+                                                   int a_max, long long (*red)[THREADS]) {
     long long cnt[5] = {0, 0, 0, 0, 0};   // entries per a (1..4) and unresolved in [0]
     long long active = 0, tries = 0;
     for (int64_t k = k0 + threadIdx.x; k < k1; k += THREADS) {
-        const uint8_t s = status[b * L + k];
+        const uint8_t s = row[k];
         if (s == 0) continue;
         active++;
         if (s == 0xFF) {
@@ -719,7 +957,6 @@ __global__ void __launch_bounds__(THREADS) k_noniter_count(const uint8_t *__rest
             tries += s;
         }
     }
-    __shared__ long long red[7][THREADS];
     red[0][threadIdx.x] = cnt[0];
     red[1][threadIdx.x] = cnt[1];
     red[2][threadIdx.x] = cnt[2];
@@ -733,19 +970,22 @@ __global__ void __launch_bounds__(THREADS) k_noniter_count(const uint8_t *__rest
             for (int q = 0; q < 7; q++) red[q][threadIdx.x] += red[q][threadIdx.x + s];
         __syncthreads();
     }
+}
+
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) k_noniter_count(const uint8_t *__restrict__ status, int64_t L,
+                                                           int a_max, int64_t nseg,
+                                                           long long *__restrict__ segcnt) {
+    pdl_wait();
+    const int64_t b = blockIdx.x / nseg, g = blockIdx.x - b * nseg;
+    const int64_t k0 = g * NONITER_SEG, k1 = (k0 + NONITER_SEG < L) ? k0 + NONITER_SEG : L;
+    __shared__ long long red[7][THREADS];
+    noniter_count_bins<THREADS>(status + b * L, k0, k1, a_max, red);
     if (threadIdx.x < 7) segcnt[blockIdx.x * SEGF + threadIdx.x] = red[threadIdx.x][0];
 }
 
-// per signal: fold the segment counts into the stats record
-__global__ void k_noniter_fin(const long long *__restrict__ segcnt, int64_t B, int64_t nseg, int64_t L,
-                              int S, int64_t d, int64_t *__restrict__ stats) {
-    pdl_wait();
-    const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (b >= B) return;
-    long long r[7] = {0, 0, 0, 0, 0, 0, 0};
-    for (int64_t g = 0; g < nseg; g++)
-        for (int q = 0; q < 7; q++) r[q] += segcnt[(b * nseg + g) * SEGF + q];
-    int64_t *st = stats + b * SFDT_ST_PER_SIGNAL;
+// the stats record of a non-iterative solve from a signal's counts r[0..6]
+__device__ __forceinline__ void noniter_fill_stats(int64_t *st, const long long *r, int S, int64_t L, int64_t d) {
     const long long nent = r[1] + r[2] + r[3] + r[4];
     st[SFDT_ST_NITER] = 1;
     st[SFDT_ST_FULL_SUCCESS] = r[0] == 0;
@@ -770,6 +1010,18 @@ __global__ void k_noniter_fin(const long long *__restrict__ segcnt, int64_t B, i
     st[7] = 0;
     for (int q = SFDT_ST_ITER0 + 6; q < 24; q++) st[q] = 0;
     for (int q = 28; q < SFDT_ST_PER_SIGNAL; q++) st[q] = 0;
+}
+
+// per signal: fold the segment counts into the stats record
+__global__ void k_noniter_fin(const long long *__restrict__ segcnt, int64_t B, int64_t nseg, int64_t L,
+                              int S, int64_t d, int64_t *__restrict__ stats) {
+    pdl_wait();
+    const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    long long r[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (int64_t g = 0; g < nseg; g++)
+        for (int q = 0; q < 7; q++) r[q] += segcnt[(b * nseg + g) * SEGF + q];
+    noniter_fill_stats(stats + b * SFDT_ST_PER_SIGNAL, r, S, L, d);
 }
 
 // exclusive scans of up to three per-signal stats fields -> offsets (one
@@ -850,29 +1102,16 @@ __device__ __forceinline__ unsigned long long block_excl_scan_u64(unsigned long 
     return before + inc - v;
 }
 
+// emit the bins [k0, k1) of signal b: entries in (a, bin) order at the class
+// bases base[0..3], unresolved bins ascending at base[4] (all threads call)
 template <int THREADS>
-__global__ void __launch_bounds__(THREADS) k_noniter_emit(
-    const uint8_t *__restrict__ status, const int64_t *__restrict__ bin_loc,
-    const cx *__restrict__ bin_val, int64_t L, int a_max, const int64_t *__restrict__ stats,
-    const int64_t *__restrict__ eoff, const int64_t *__restrict__ uoff, int64_t *__restrict__ locs,
-    cx *__restrict__ vals, int32_t *__restrict__ ubins, int64_t nseg, const long long *__restrict__ segcnt) {
-    pdl_wait();
-    __shared__ unsigned long long wtot[THREADS / 32];
-    const int64_t b = blockIdx.x / nseg, g = blockIdx.x - b * nseg;
-    const int64_t *st = stats + b * SFDT_ST_PER_SIGNAL;
-    long long base[5];
-    base[0] = eoff[b];
-    for (int c = 1; c < 4; c++) base[c] = base[c - 1] + st[24 + c - 1];
-    base[4] = uoff[b];
-    // segments before this one: entries per class (classes store entries,
-    // so a bin of class c advances its base by c + 1) and unresolved bins
-    for (int64_t g2 = 0; g2 < g; g2++) {
-        const long long *sc = segcnt + (b * nseg + g2) * SEGF;
-        base[4] += sc[0];
-        for (int c = 0; c < 4; c++) base[c] += sc[1 + c];
-    }
+__device__ __forceinline__ void noniter_emit_bins(const uint8_t *__restrict__ status,
+                                                  const int64_t *__restrict__ bin_loc,
+                                                  const cx *__restrict__ bin_val, int64_t L, int a_max, int64_t b,
+                                                  int64_t k0, int64_t k1, const long long *base,
+                                                  int64_t *__restrict__ locs, cx *__restrict__ vals,
+                                                  int32_t *__restrict__ ubins, unsigned long long *wtot) {
     long long carry[5] = {0, 0, 0, 0, 0};
-    const int64_t k0 = g * NONITER_SEG, k1 = (k0 + NONITER_SEG < L) ? k0 + NONITER_SEG : L;
     for (int64_t t0 = k0; t0 < k1; t0 += THREADS * 4) {
         int ci[4];
         unsigned long long packed = 0;
@@ -907,6 +1146,71 @@ __global__ void __launch_bounds__(THREADS) k_noniter_emit(
         }
 #pragma unroll
         for (int c = 0; c < 5; c++) carry[c] += (long long)((total >> (12 * c)) & 0xFFF);
+    }
+}
+
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) k_noniter_emit(
+    const uint8_t *__restrict__ status, const int64_t *__restrict__ bin_loc,
+    const cx *__restrict__ bin_val, int64_t L, int a_max, const int64_t *__restrict__ stats,
+    const int64_t *__restrict__ eoff, const int64_t *__restrict__ uoff, int64_t *__restrict__ locs,
+    cx *__restrict__ vals, int32_t *__restrict__ ubins, int64_t nseg, const long long *__restrict__ segcnt) {
+    pdl_wait();
+    __shared__ unsigned long long wtot[THREADS / 32];
+    const int64_t b = blockIdx.x / nseg, g = blockIdx.x - b * nseg;
+    const int64_t *st = stats + b * SFDT_ST_PER_SIGNAL;
+    long long base[5];
+    base[0] = eoff[b];
+    for (int c = 1; c < 4; c++) base[c] = base[c - 1] + st[24 + c - 1];
+    base[4] = uoff[b];
+    // segments before this one: entries per class (classes store entries,
+    // so a bin of class c advances its base by c + 1) and unresolved bins
+    for (int64_t g2 = 0; g2 < g; g2++) {
+        const long long *sc = segcnt + (b * nseg + g2) * SEGF;
+        base[4] += sc[0];
+        for (int c = 0; c < 4; c++) base[c] += sc[1 + c];
+    }
+    const int64_t k0 = g * NONITER_SEG, k1 = (k0 + NONITER_SEG < L) ? k0 + NONITER_SEG : L;
+    noniter_emit_bins<THREADS>(status, bin_loc, bin_val, L, a_max, b, k0, k1, base, locs, vals, ubins, wtot);
+}
+
+// Latency path (few signals, L <= NONITER_SEG): count, stats, offsets and
+// emission of every signal in ONE CTA -- the four-kernel compaction above costs
+// four launch latencies, which is most of a config-1 solve.  Same counts, same
+// order, same record.
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) k_noniter_small(
+    const uint8_t *__restrict__ status, const int64_t *__restrict__ bin_loc, const cx *__restrict__ bin_val,
+    int64_t B, int64_t L, int a_max, int S, int64_t d, int64_t *__restrict__ stats, int64_t *__restrict__ eoff,
+    int64_t *__restrict__ uoff, int64_t *__restrict__ doff, int64_t *__restrict__ locs, cx *__restrict__ vals,
+    int32_t *__restrict__ ubins) {
+    pdl_wait();
+    __shared__ long long red[7][THREADS];
+    __shared__ unsigned long long wtot[THREADS / 32];
+    long long e_run = 0, u_run = 0;
+    for (int64_t b = 0; b < B; b++) {
+        noniter_count_bins<THREADS>(status + b * L, 0, L, a_max, red);
+        long long r[7];
+        for (int q = 0; q < 7; q++) r[q] = red[q][0];
+        __syncthreads();   // red is rewritten by the next signal's count
+        if (threadIdx.x == 0) {
+            noniter_fill_stats(stats + b * SFDT_ST_PER_SIGNAL, r, S, L, d);
+            eoff[b] = e_run;
+            uoff[b] = u_run;
+            if (doff) doff[b] = 0;
+        }
+        long long base[5];
+        base[0] = e_run;
+        for (int c = 1; c < 4; c++) base[c] = base[c - 1] + r[c];
+        base[4] = u_run;
+        noniter_emit_bins<THREADS>(status, bin_loc, bin_val, L, a_max, b, 0, L, base, locs, vals, ubins, wtot);
+        e_run += r[1] + r[2] + r[3] + r[4];
+        u_run += r[0];
+    }
+    if (threadIdx.x == 0) {
+        eoff[B] = e_run;
+        uoff[B] = u_run;
+        if (doff) doff[B] = 0;
     }
 }
 
@@ -1192,7 +1496,7 @@ struct ExactPlan {
     int64_t B, n, d, L, S, CH, nchunk, npass;
     int logd;
     size_t off_V, off_partial, off_thr, off_status, off_bloc, off_bval, off_def,
-        off_sloc, off_sval, off_sa, off_sdup, off_cnt, off_resid, off_ndef, off_scratch, off_fft, off_wl,
+        off_sloc, off_sval, off_sa, off_sdup, off_cnt, off_resid, off_ndef, off_scratch, off_fft, off_wl, off_wl2,
         off_act, off_awl, off_seg,
         total;
 };
@@ -1221,6 +1525,7 @@ static int make_plan(const sfdt_exact_args *a, ExactPlan &p) {
         p.off_bloc = take(size_t(p.B) * p.L * a->a_max * 8);
         p.off_bval = take(size_t(p.B) * p.L * a->a_max * 16);
         p.off_wl = take(size_t(p.B) * p.L * 8);
+        p.off_wl2 = take(size_t(p.B) * p.L * 8);
         p.off_act = take(size_t(p.B) * p.L);
         p.off_awl = take(size_t(p.B) * p.L * 8);
         p.off_seg = take(size_t(p.B) * ((p.L + NONITER_SEG - 1) / NONITER_SEG) * SEGF * 8);
@@ -1235,7 +1540,7 @@ static int make_plan(const sfdt_exact_args *a, ExactPlan &p) {
         p.off_ndef = take(size_t(p.B) * 8);
         p.off_awl = take(size_t(p.B) * p.L * 8);
     }
-    p.off_scratch = take(128 * 8);
+    p.off_scratch = take(192 * 8);
     p.off_fft = (p.L > FFT_SMEM_MAX) ? take(size_t(p.B) * p.L * p.S * 16) : 0;
     p.total = o;
     return SFDT_OK;
@@ -1289,7 +1594,8 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
     // of every SM's threads and shared memory to the FFT/decode of the
     // previous chunk.
     const bool reserve = a->aux_stream != nullptr;
-    auto launch_stream = [&](int64_t c0, int64_t bc) -> int {
+    const DecodeScratch no_scratch{nullptr, 0, nullptr, nullptr, nullptr};
+    auto launch_stream = [&](int64_t c0, int64_t bc, DecodeScratch zc) -> int {
         dim3 grid((unsigned)p.nchunk, (unsigned)bc);
         const char *xc = (const char *)a->x + c0 * p.n * (is_c64 ? 8 : 16);
         if (reserve) {
@@ -1312,10 +1618,10 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
             constexpr int TH = 512, UN = 4;
             if (is_c64)
                 launch_pdl(k_sumsq<1, TH, UN>, grid, dim3(TH), 0, stream, (const void *)xc, p.n, p.CH,
-                           partial + c0 * p.nchunk);
+                           partial + c0 * p.nchunk, zc);
             else
                 launch_pdl(k_sumsq<0, TH, UN>, grid, dim3(TH), 0, stream, (const void *)xc, p.n, p.CH,
-                           partial + c0 * p.nchunk);
+                           partial + c0 * p.nchunk, zc);
         }
         SFDT_CHECK_LAUNCH();
         launches += 1;
@@ -1338,6 +1644,7 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
         int64_t *bloc = (int64_t *)(w + p.off_bloc);
         cx *bval = (cx *)(w + p.off_bval);
         int64_t *wl = (int64_t *)(w + p.off_wl);
+        int64_t *wl2 = (int64_t *)(w + p.off_wl2);
         unsigned long long *wlc = (unsigned long long *)(w + p.off_scratch);
         cudaEvent_t ev_done = nullptr;
         if (a->ev_stream_begin) cudaEventRecord((cudaEvent_t)a->ev_stream_begin, stream);
@@ -1347,6 +1654,39 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
             cudaEventRecord(ev, stream);
             cudaStreamWaitEvent(aux, ev, 0);
             cudaEventDestroy(ev);
+        }
+        // Latency path (a few short signals, config 1): five or six kernels
+        // instead of ten -- the stream kernel zeroes the counters, the a = 1
+        // decode folds the rms tree and the activity test in, and one CTA
+        // compacts.  Same arithmetic, same bits.
+        const bool small = tn.latency_path != 0 && aux == stream && !a->rms_in && p.nchunk <= 64 &&
+                           (p.L % 32) == 0 && p.L <= NONITER_SEG && p.B <= (tn.latency_path > 0 ? 64 : 8);
+        if (small) {
+            if ((rc = launch_stream(0, p.B, DecodeScratch{nullptr, 0, wlc, wlc + 64, wlc + 128}))) return rc;
+            if (a->ev_stream_end) cudaEventRecord((cudaEvent_t)a->ev_stream_end, stream);
+            const ViewSrc src = consecutive_views((const char *)a->x, is_c64, p.n, p.d, 0, (int)p.S);
+            rc = launch_fft_views(src, p.B, p.L, a->twiddles, V, (int)p.S, p.L, stream, fft_scratch, 1, nullptr,
+                                  nullptr, tn.fft_split);
+            if (rc) return rc;
+            switch (p.S) {
+#define SFDT_SMALL(Sv)                                                                                            \
+    rc = launch_decode_small<Sv>(V, p.B, p.L, a->a_max, p.n, partial, p.nchunk, a->zero_threshold, p.d, a->rms, \
+                                 thr, status, bloc, bval, wl, wlc, wl2, wlc + 128, tn.decode_coop, stream);
+            case 2: SFDT_SMALL(2) break;
+            case 4: SFDT_SMALL(4) break;
+            case 6: SFDT_SMALL(6) break;
+            default: SFDT_SMALL(8) break;
+#undef SFDT_SMALL
+            }
+            if (rc) return rc;
+            launch_pdl(k_noniter_small<256>, dim3(1), dim3(256), 0, stream, (const uint8_t *)status,
+                       (const int64_t *)bloc, (const cx *)bval, p.B, p.L, a->a_max, (int)p.S, p.d, a->stats,
+                       a->entry_offsets, a->unres_offsets, a->dup_offsets, a->locs, (cx *)a->vals, a->unres_bins);
+            SFDT_CHECK_LAUNCH();
+            launches += fft_view_launches(p.L, tn.fft_split) + 2 +
+                        (a->a_max > 1 ? (decode_coop_mode(tn.decode_coop, p.B * p.L, a->a_max) == 2 ? 2 : 1) : 0);
+            a->kernel_launches = launches;
+            return SFDT_OK;
         }
         for (int64_t c = 0; c < nc; c++) {
             const int64_t c0 = c * bc, nb = (c0 + bc <= p.B) ? bc : p.B - c0;
@@ -1361,7 +1701,7 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
             };
             const bool overlap = aux != stream;
             if (overlap && (rc = launch_fft())) return rc;
-            if (!a->rms_in && (rc = launch_stream(c0, nb))) return rc;
+            if (!a->rms_in && (rc = launch_stream(c0, nb, no_scratch))) return rc;
             if (c == nc - 1 && a->ev_stream_end) cudaEventRecord((cudaEvent_t)a->ev_stream_end, stream);
             if (aux != stream) {
                 cudaEvent_t ev;
@@ -1374,8 +1714,8 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
             // the rms kernel zeroes their flags and the worklist counters
             const bool dense = !overlap;
             uint8_t *actc = dense ? (uint8_t *)(w + p.off_act) + c0 * p.L : nullptr;
-            const DecodeScratch zs = dense ? DecodeScratch{actc, p.L, wlc + c, wlc + 64 + c}
-                                           : DecodeScratch{nullptr, 0, nullptr, nullptr};
+            const DecodeScratch zs = dense ? DecodeScratch{actc, p.L, wlc + c, wlc + 64 + c, wlc + 128 + c}
+                                           : DecodeScratch{nullptr, 0, nullptr, nullptr, nullptr};
             if (a->rms_in)
                 launch_pdl(k_thr_from_rms, dim3((unsigned)((nb + 255) / 256)), dim3(256), 0, aux,
                            (const double *)(a->rms_in + c0), nb, a->zero_threshold, p.d, a->rms + c0, thr + c0, zs);
@@ -1397,13 +1737,14 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
             int64_t *blc = bloc + c0 * p.L * a->a_max;
             cx *bvc = bval + c0 * p.L * a->a_max;
             switch (p.S) {
-            case 2: rc = launch_decode_noniter<2>(Vc, nb, p.L, a->a_max, p.n, thr + c0, stc, blc, bvc, wl + c0 * p.L, wlc + c, aux, actc, awlc_p, wlc + 64 + c); break;
-            case 4: rc = launch_decode_noniter<4>(Vc, nb, p.L, a->a_max, p.n, thr + c0, stc, blc, bvc, wl + c0 * p.L, wlc + c, aux, actc, awlc_p, wlc + 64 + c); break;
-            case 6: rc = launch_decode_noniter<6>(Vc, nb, p.L, a->a_max, p.n, thr + c0, stc, blc, bvc, wl + c0 * p.L, wlc + c, aux, actc, awlc_p, wlc + 64 + c); break;
-            default: rc = launch_decode_noniter<8>(Vc, nb, p.L, a->a_max, p.n, thr + c0, stc, blc, bvc, wl + c0 * p.L, wlc + c, aux, actc, awlc_p, wlc + 64 + c); break;
+            case 2: rc = launch_decode_noniter<2>(Vc, nb, p.L, a->a_max, p.n, thr + c0, stc, blc, bvc, wl + c0 * p.L, wlc + c, aux, actc, awlc_p, wlc + 64 + c, wl2 + c0 * p.L, wlc + 128 + c, tn.decode_coop); break;
+            case 4: rc = launch_decode_noniter<4>(Vc, nb, p.L, a->a_max, p.n, thr + c0, stc, blc, bvc, wl + c0 * p.L, wlc + c, aux, actc, awlc_p, wlc + 64 + c, wl2 + c0 * p.L, wlc + 128 + c, tn.decode_coop); break;
+            case 6: rc = launch_decode_noniter<6>(Vc, nb, p.L, a->a_max, p.n, thr + c0, stc, blc, bvc, wl + c0 * p.L, wlc + c, aux, actc, awlc_p, wlc + 64 + c, wl2 + c0 * p.L, wlc + 128 + c, tn.decode_coop); break;
+            default: rc = launch_decode_noniter<8>(Vc, nb, p.L, a->a_max, p.n, thr + c0, stc, blc, bvc, wl + c0 * p.L, wlc + c, aux, actc, awlc_p, wlc + 64 + c, wl2 + c0 * p.L, wlc + 128 + c, tn.decode_coop); break;
             }
             if (rc) return rc;
-            launches += 1 + fft_view_launches(p.L, tn.fft_split) + 1 + (a->a_max > 1 ? 1 : 0) + (dense ? 1 : 0);
+            launches += 1 + fft_view_launches(p.L, tn.fft_split) + 1 + (dense ? 1 : 0) +
+                        (a->a_max > 1 ? (decode_coop_mode(tn.decode_coop, nb * p.L, a->a_max) == 2 ? 2 : 1) : 0);
         }
         if (aux != stream) {
             if (cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming) != cudaSuccess) return SFDT_ECUDA;
@@ -1436,12 +1777,12 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
 
     // iterative: the single pass over x first (all signals), then the passes
     if (a->ev_stream_begin) cudaEventRecord((cudaEvent_t)a->ev_stream_begin, stream);
-    if (!a->rms_in && (rc = launch_stream(0, p.B))) return rc;
+    if (!a->rms_in && (rc = launch_stream(0, p.B, no_scratch))) return rc;
     if (a->ev_stream_end) cudaEventRecord((cudaEvent_t)a->ev_stream_end, stream);
     if (a->rms_in)
         k_thr_from_rms<<<(unsigned)((p.B + 255) / 256), 256, 0, stream>>>(a->rms_in, p.B, a->zero_threshold,
                                                                           p.d, a->rms, thr,
-                                                                          DecodeScratch{nullptr, 0, nullptr, nullptr});
+                                                                          DecodeScratch{nullptr, 0, nullptr, nullptr, nullptr});
     else
         launch_rms(partial, p.B, p.nchunk, p.n, a->zero_threshold, p.d, a->rms, thr, stream);
     SFDT_CHECK_LAUNCH();
@@ -1555,9 +1896,9 @@ extern "C" int sfdt_rms(const void *x, int32_t x_dtype, int64_t batch, int64_t n
     constexpr int TH = 512, UN = 4;
     const dim3 grid((unsigned)nchunk, (unsigned)batch);
     if (x_dtype == SFDT_C64)
-        k_sumsq<1, TH, UN><<<grid, TH, 0, stream>>>(x, n, CH, partial);
+        k_sumsq<1, TH, UN><<<grid, TH, 0, stream>>>(x, n, CH, partial, DecodeScratch{nullptr, 0, nullptr, nullptr, nullptr});
     else
-        k_sumsq<0, TH, UN><<<grid, TH, 0, stream>>>(x, n, CH, partial);
+        k_sumsq<0, TH, UN><<<grid, TH, 0, stream>>>(x, n, CH, partial, DecodeScratch{nullptr, 0, nullptr, nullptr, nullptr});
     SFDT_CHECK_LAUNCH();
     launch_rms(partial, batch, nchunk, n, 0.0, 1, out, thr, stream);
     SFDT_CHECK_LAUNCH();

@@ -756,3 +756,62 @@ def test_general_prune_four_lanes(n, k):
     locs = np.fromiter(want.keys(), dtype=np.int64, count=len(want))
     vals = np.fromiter(want.values(), dtype=np.complex128, count=len(want))
     _general_check(got.spectrum(1).entries, locs, vals, "b=1")
+
+
+@pytest.mark.parametrize("B,n,k,mu,a_max", [(64, 1 << 20, 256, 4, 4), (8, 1 << 18, 1024, 1, 4),
+                                             (1, 1 << 16, 64, 4, 4), (16, 1 << 16, 256, 1, 3),
+                                             (16, 1 << 16, 256, 2, 2), (300, 1 << 14, 64, 1, 4)])
+def test_cooperative_decode_bitwise(B, n, k, mu, a_max):
+    """Multi-collision decode, non-iterative solver: eight lanes per bin with
+    one warp per trial a (k_decode_coop, tuning decode_coop=1), the two-stage
+    form (thread per bin for a = 2, cooperative for a >= 3; decode_coop=2)
+    and one thread per bin for every a (decode_coop=0) return the same bits:
+    entries, dict order, values, unresolved bins."""
+    from tests.synth import device_exact_batch
+    X, _, _ = device_exact_batch(B, n, k, 4242 + B, DEV, values="mag1_10")
+    cfg = P.ExactConfig(n=n, k=k, mu=mu, a_max=a_max)
+    outs = {}
+    for mode in (0, 1, 2, 3, -1):
+        with P.tuning(decode_coop=mode):
+            outs[mode] = P.exact_batch(X, cfg, False).to_host()
+    ref = outs[0]
+    assert int(ref["entry_offsets"][-1]) > 0
+    for mode in (1, 2, 3, -1):
+        h = outs[mode]
+        for key in ("entry_offsets", "unres_offsets", "stats"):
+            assert np.array_equal(h[key], ref[key]), (mode, key)
+        ne, nu = int(ref["entry_offsets"][-1]), int(ref["unres_offsets"][-1])
+        assert np.array_equal(h["locs"][:ne], ref["locs"][:ne]), mode
+        assert _bits(h["vals"][:ne], ref["vals"][:ne]), mode
+        assert np.array_equal(h["unres_bins"][:nu], ref["unres_bins"][:nu]), mode
+    if mu == 1:   # the high-alias cases must exercise a = 3 / 4 trials and failures
+        assert int(ref["unres_offsets"][-1]) > 0
+
+
+@pytest.mark.parametrize("B,n,k,mu,a_max", [(1, 1 << 16, 64, 4, 4), (5, 1 << 16, 256, 1, 4), (8, 1 << 20, 256, 4, 4),
+                                             (3, 1 << 12, 16, 2, 2), (40, 1 << 14, 64, 1, 3)])
+def test_latency_path_bitwise(B, n, k, mu, a_max):
+    """Small non-iterative solves run a fused chain (the stream kernel zeroes
+    the counters, k_decode_a1r folds the rms tree + activity + a = 1 decode,
+    k_noniter_small compacts in one CTA): every output -- rms, stats,
+    offsets, entries, values, unresolved bins -- has the bits of the general
+    ten-kernel chain (tuning latency_path=0)."""
+    from tests.synth import device_exact_batch
+    X, _, _ = device_exact_batch(B, n, k, 99 + B, DEV, values="mag1_10")
+    cfg = P.ExactConfig(n=n, k=k, mu=mu, a_max=a_max)
+    with P.tuning(latency_path=0):
+        ref = P.exact_batch(X, cfg, False)
+        ref_launches = ref.kernel_launches
+        ref = ref.to_host()
+    with P.tuning(latency_path=1):
+        got = P.exact_batch(X, cfg, False)
+        assert got.kernel_launches < ref_launches
+        got = got.to_host()
+    for key in ("entry_offsets", "unres_offsets", "stats"):
+        assert np.array_equal(got[key], ref[key]), key
+    assert _bits(got["rms"], ref["rms"])
+    ne, nu = int(ref["entry_offsets"][-1]), int(ref["unres_offsets"][-1])
+    assert ne > 0
+    assert np.array_equal(got["locs"][:ne], ref["locs"][:ne])
+    assert _bits(got["vals"][:ne], ref["vals"][:ne])
+    assert np.array_equal(got["unres_bins"][:nu], ref["unres_bins"][:nu])

@@ -152,6 +152,23 @@ def run_general_grid(n: int, n_over_k_values, snr_db_values, trials: int = 50, a
     return report
 
 
+def summarize_general(report: ExperimentReport) -> list:
+    """experiments.py:219-233: per (N/K, SNR) cell, the mean of every snr_* /
+    error_ratio* / elapsed* column over the cell's finite values."""
+    cells = {}
+    for row in report.rows:
+        cells.setdefault((row["n_over_k"], row["snr_target_db"]), []).append(row)
+    out = []
+    for (n_over_k, snr_db), rows in sorted(cells.items()):
+        entry = {"n_over_k": n_over_k, "snr_target_db": snr_db, "trials": len(rows)}
+        for key in rows[0]:
+            if key.startswith(("snr_", "error_ratio", "elapsed")):
+                vals = [r[key] for r in rows if math.isfinite(r[key])]
+                entry[f"mean_{key}"] = float(np.mean(vals)) if vals else math.inf
+        out.append(entry)
+    return out
+
+
 def run_collision_census(n: int, k: int, n_plus_values, trials: int = 1000, seed: int = 0,
                          a_cap: int = 4) -> dict:
     """experiments.py:81-111: empirical per-bin collision histograms (host

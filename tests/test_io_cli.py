@@ -131,3 +131,55 @@ def test_device_fft_bitexact_long():
         assert np.array_equal(got.view(np.uint64), OK.fft_radix2(x).view(np.uint64)), n
         got = fft(x, inverse=True)
         assert np.array_equal(got.view(np.uint64), OK.fft_radix2(x, True).view(np.uint64)), n
+
+
+def test_cli_census_subcommand(tmp_path, capsys):
+    """`census` (reference cli.py:184-208): host integer counting, the
+    reference's summary keys and CSV / JSON row layout."""
+    import csv
+
+    from paper_1407_8315_b200 import cli
+    from paper_1407_8315_b200.experiments import run_collision_census
+    out = tmp_path / "census.csv"
+    rc = cli.main(["census", "--n", "4096", "--k", "16", "--n-plus", "4", "8", "--trials", "50",
+                   "--seed", "3", "--out", str(out), "--threads", "2"])
+    summary = json.loads(capsys.readouterr().out)
+    want = run_collision_census(4096, 16, [4, 8], trials=50, seed=3)
+    assert rc == 0 and sorted(summary) == ["4", "8"]
+    for key, res in want.items():
+        got = summary[str(key)]
+        assert got == {"p_signal_over": res["p_signal_over"], "bound_signal_over": res["bound_signal_over"],
+                       "p_bin_over": res["p_bin_over"]}
+    rows = list(csv.DictReader(open(out)))
+    assert list(rows[0]) == ["n_plus", "d", "a", "probability"]
+    assert len(rows) == sum(len(r["per_bin_probability"]) for r in want.values())
+    assert float(rows[1]["probability"]) == float(want[4]["per_bin_probability"][1])
+    outj = tmp_path / "census.json"
+    assert cli.main(["census", "--n", "4096", "--k", "16", "--trials", "10", "--format", "json",
+                     "--out", str(outj)]) == 0
+    capsys.readouterr()
+    assert json.loads(outj.read_text())[0].keys() == {"n_plus", "d", "a", "probability"}
+    # incompatible oversampling ratio: the reference's ValueError -> exit code 1
+    assert cli.main(["census", "--n", "4096", "--k", "16", "--n-plus", "3"]) == 1
+
+
+@pytest.mark.gpu
+def test_cli_bench_subcommand(tmp_path, capsys):
+    """`bench` (reference cli.py:161-181): the named grids, each cell one GPU
+    batch; report columns as the reference writes them."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_1407_8315_b200 import cli
+    out = tmp_path / "grid.json"
+    assert cli.main(["bench", "--grid", "exact-small", "--trials", "3", "--format", "json", "--out", str(out)]) == 0
+    rep = json.loads(out.read_text())
+    assert rep["name"] == "exact_grid" and rep["meta"]["k_values"] == [16, 32, 64]
+    assert len(rep["rows"]) == 9 and all(r["perfect"] == 1 for r in rep["rows"])
+    assert list(rep["rows"][0]) == ["n", "k", "mu", "a_max", "solver", "seed", "perfect", "recovered_fraction",
+                                    "full_success", "fft_samples", "elapsed_s"]
+    outc = tmp_path / "grid.csv"
+    assert cli.main(["bench", "--grid", "general-desk", "--trials", "2", "--out", str(outc)]) == 0
+    cells = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    assert len(cells) == 6 and cells[0]["trials"] == 2 and "mean_snr_out_db_prune" in cells[0]
+    assert outc.read_text().startswith("n,n_over_k,k,snr_target_db")

@@ -29,6 +29,16 @@
 #else
 #define SFDT_HD static inline
 #endif
+// The long scalar routines (complex division, csqrt, clog/cexp, hypot) as real
+// calls instead of inline copies: a translation unit built with
+// SFDT_NOINLINE_HEAVY keeps one copy of each, so a decode trial's straight-line
+// code shrinks severalfold and stays in the instruction cache.  Same
+// instructions, same results.
+#if defined(__CUDACC__) && defined(SFDT_NOINLINE_HEAVY)
+#define SFDT_HEAVY __host__ __device__ __noinline__
+#else
+#define SFDT_HEAVY SFDT_HD
+#endif
 
 #if defined(__CUDA_ARCH__)
 #define DMUL(a, b) __dmul_rn((a), (b))
@@ -74,7 +84,7 @@ SFDT_HD cx nmul(cx a, cx b)
 }
 
 // libgcc __divdc3 (GCC >= 12): Smith's algorithm with range scaling.
-SFDT_HD cx gdiv(cx num, cx den)
+SFDT_HEAVY cx gdiv(cx num, cx den)
 {
     double a = num.re, b = num.im, c = den.re, d = den.im;
     const double RBIG = DBL_MAX / 2, RMIN = DBL_MIN, RMIN2 = DBL_EPSILON;
@@ -152,11 +162,13 @@ SFDT_HD cx ndiv(cx a, cx b)
     return mk(DMUL(DADD(DMUL(a.re, rat), a.im), scl), DMUL(DSUB(DMUL(a.im, rat), a.re), scl));
 }
 
-SFDT_HD double cabs_(cx a) { return hypot(a.re, a.im); }
+SFDT_HEAVY double cabs_(cx a) { return hypot(a.re, a.im); }
+// always-inline form for the rare boundary tests inside streaming kernels
+SFDT_HD double cabs_i(cx a) { return hypot(a.re, a.im); }
 
 // glibc csqrt (finite inputs): principal branch, Re >= 0, using the identity
 // 2 Re(r) Im(r) = Im(z) to avoid cancellation.
-SFDT_HD cx gsqrt(cx z)
+SFDT_HEAVY cx gsqrt(cx z)
 {
     double re = z.re, im = z.im;
     if (!isfinite(re) || !isfinite(im)) {
@@ -223,7 +235,7 @@ SFDT_HD cx gsqrt(cx z)
 }
 
 // glibc cexp for finite arguments: exp(re) * (cos im, sin im)
-SFDT_HD cx gexp(cx z)
+SFDT_HEAVY cx gexp(cx z)
 {
     double s, c;
 #if defined(__CUDA_ARCH__)
@@ -273,7 +285,7 @@ SFDT_HD double x2y2m1(double x, double y)
 }
 
 // glibc clog for finite, nonzero arguments
-SFDT_HD cx gclog(cx z)
+SFDT_HEAVY cx gclog(cx z)
 {
     double absx = fabs(z.re), absy = fabs(z.im);
     int scale = 0;

@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(128) k_decode_a1(const cx *__restrict__ V, int
         for (int s = 0; s < S; s++) {
             syn[s] = ldcx(V + (b * S + s) * L + k);
             const double q = syn[s].re * syn[s].re + syn[s].im * syn[s].im;
-            active = active || (q > th2hi) || (q >= th2lo && cabs_(syn[s]) > th);
+            active = active || (q > th2hi) || (q >= th2lo && cabs_i(syn[s]) > th);
         }
         uint8_t st = 0;
         if (active) {
@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(128) k_decode_a1r(const cx *__restrict__ V, in
         for (int s = 0; s < S; s++) {
             syn[s] = ldcx(V + (b * S + s) * L + k);
             const double q = syn[s].re * syn[s].re + syn[s].im * syn[s].im;
-            active = active || (q > th2hi) || (q >= th2lo && cabs_(syn[s]) > th);
+            active = active || (q > th2hi) || (q >= th2lo && cabs_i(syn[s]) > th);
         }
         uint8_t st = 0;
         if (active) {

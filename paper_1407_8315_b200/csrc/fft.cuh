@@ -324,7 +324,7 @@ static __global__ void __launch_bounds__(256, MINB) k_fft_views(const ViewSrc sr
         stcx(out + s_obase[v] + k, y);
         if (act) {
             const double q = y.re * y.re + y.im * y.im;
-            if (q > s_th2hi[v] || (q >= s_th2lo[v] && cabs_(y) > s_th[v]))
+            if (q > s_th2hi[v] || (q >= s_th2lo[v] && cabs_i(y) > s_th[v]))
                 act[s_sig[v] * (int64_t)L + k] = 1;
         }
     };
@@ -468,7 +468,7 @@ static __global__ void __launch_bounds__(256) k_fft_large_b_reg(cx *buf, int64_t
         stcx(o + (int64_t)q * P, y);
         if (act) {   // activity epilogue, as in k_fft_views
             const double m2 = y.re * y.re + y.im * y.im;
-            if (m2 > th * th * (1.0 + 1e-6) || (m2 >= th * th * (1.0 - 1e-6) && cabs_(y) > th))
+            if (m2 > th * th * (1.0 + 1e-6) || (m2 >= th * th * (1.0 - 1e-6) && cabs_i(y) > th))
                 act[(b << logL) + i0 + (int64_t)q * P] = 1;
         }
     }
@@ -603,7 +603,7 @@ static __global__ void __launch_bounds__(32 << (LQ - 4), 16 >> (LQ - 4)) k_fft_l
             stcx(o + i, v);
             if (act) {
                 const double m2 = v.re * v.re + v.im * v.im;
-                if (m2 > th * th * (1.0 + 1e-6) || (m2 >= th * th * (1.0 - 1e-6) && cabs_(v) > th))
+                if (m2 > th * th * (1.0 + 1e-6) || (m2 >= th * th * (1.0 - 1e-6) && cabs_i(v) > th))
                     act[(b << logL) + r0 + rl + i] = 1;
             }
         }

@@ -965,39 +965,46 @@ __device__ __forceinline__ void subspace_pursuit_dev(const cx *y, const cx *phas
         for (int j = 0; j < r; j++) ss = fma(res[j].re, res[j].re, fma(res[j].im, res[j].im, ss));
         return sqrt(ss);
     };
-    lsq(sup, nsup, coef);
-    double best = residual(sup, nsup, coef);
-    int best_sup[GEN_MAX_SUP], best_n = nsup;
+    // general.py:212-269 as ONE loop with a single least-squares call site
+    // (the pursuit's code is mostly the inlined register-resident QR forms;
+    // three copies of them -- initial, merged and pruned supports -- tripled
+    // the kernel and its instruction-cache misses).  stage 0 solves on the
+    // current support and judges the residual; stage 1 solves on the merged
+    // support and prunes it.  Same solves, same order.
+    double best = 0.0;
+    int best_sup[GEN_MAX_SUP], best_n = 0;
     cx best_coef[GEN_MAX_SUP];
-    for (int i = 0; i < nsup; i++) {
-        best_sup[i] = sup[i];
-        best_coef[i] = coef[i];
-    }
-    for (int it = 0; it < max_iter; it++) {
-        // merged = union(support, top a_eff of |phi^H residual|)
-        nt = top_cols(res);
-        int topc[GEN_MAX_SUP];
-        for (int i = 0; i < nt; i++) topc[i] = tid_[i];
-        sort_ints(topc, nt);
-        int merged[2 * GEN_MAX_SUP];
-        const int nm = union_sorted(sup, nsup, topc, nt, merged);
-        cx mcoef[2 * GEN_MAX_SUP];
-        lsq(merged, nm, mcoef);
-        // support = sorted(merged[top a_eff of |mcoef|, stable])
-        int n2 = 0;
-        for (int c = 0; c < nm; c++) topk_insert(tsc, tid_, n2, a_eff, cabs_(mcoef[c]), c);
-        nsup = n2;
-        for (int i = 0; i < n2; i++) sup[i] = merged[tid_[i]];
-        sort_ints(sup, nsup);
-        lsq(sup, nsup, coef);
+    int merged[2 * GEN_MAX_SUP], nm = 0;
+    cx mcoef[2 * GEN_MAX_SUP];
+    int stage = 0, it = -1;
+    for (;;) {
+        lsq(stage ? merged : sup, stage ? nm : nsup, stage ? mcoef : coef);
+        if (stage) {
+            // support = sorted(merged[top a_eff of |mcoef|, stable])
+            int n2 = 0;
+            for (int c = 0; c < nm; c++) topk_insert(tsc, tid_, n2, a_eff, cabs_(mcoef[c]), c);
+            nsup = n2;
+            for (int i = 0; i < n2; i++) sup[i] = merged[tid_[i]];
+            sort_ints(sup, nsup);
+            stage = 0;
+            continue;
+        }
         const double nrm = residual(sup, nsup, coef);
-        if (nrm >= best * (1.0 - 1e-12)) break;
+        if (it >= 0 && nrm >= best * (1.0 - 1e-12)) break;
         best = nrm;
         best_n = nsup;
         for (int i = 0; i < nsup; i++) {
             best_sup[i] = sup[i];
             best_coef[i] = coef[i];
         }
+        if (++it >= max_iter) break;
+        // merged = union(support, top a_eff of |phi^H residual|)
+        nt = top_cols(res);
+        int topc[GEN_MAX_SUP];
+        for (int i = 0; i < nt; i++) topc[i] = tid_[i];
+        sort_ints(topc, nt);
+        nm = union_sorted(sup, nsup, topc, nt, merged);
+        stage = 1;
     }
     o.nsup = best_n;
     for (int i = 0; i < best_n; i++) {

@@ -95,8 +95,10 @@ int sfdt_hankel_singular_values(const double *m, int64_t nb, int64_t ld, int a_m
  * sfdt_default_tuning.  Only the solve that receives the struct reads it:
  * the library keeps no global state. */
 typedef struct {
-    int32_t fft_split;       /* large views L = 2^17..2^19: 0 register-blocked pass A + one pass B,
-                                1 the stage-split register passes (round-1 plan) */
+    int32_t fft_split;       /* bit 0 -- large views L = 2^17..2^19: 0 register-blocked pass A + one pass B,
+                                1 the stage-split register passes (round-1 plan); bit 1 -- 4096-point
+                                views: 0 the register-blocked radix-16 kernel, 2 k_fft_views (radix-8
+                                shared-memory passes) */
     int32_t gen_dedup;       /* 1: a random shift equal to a consecutive one shares that view */
     int32_t gen_svd_closed;  /* 1: closed-form 3x3 singular values where accurate, Jacobi for the
                                 rest; 0: Jacobi for every bin */

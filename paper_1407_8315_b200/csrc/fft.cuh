@@ -492,9 +492,19 @@ __device__ __forceinline__ cx ld_stream(const cx *p) {   // no L1 allocation
     return mk(v.x, v.y);
 }
 
+// FINAL (L = 4096 exactly, the block is the whole view): the last round's
+// outputs go straight to the views with the scale / activity epilogue of
+// k_fft_views -- at L = 4096 this register-blocked form replaces the four
+// radix-8 shared-memory passes of k_fft_views<3> (two exchanges instead of
+// three, every twiddle of a round loaded up front): config 4 view FFT
+// 1044 -> 951 us, bit-identical.
+template <bool FINAL>
 static __global__ void __launch_bounds__(256, 2) k_fft_large_a16(const ViewSrc src, int logL,
                                                                  const cx *__restrict__ tw,
-                                                                 cx *__restrict__ scratch) {
+                                                                 cx *__restrict__ scratch, int SV, int64_t ldV,
+                                                                 int scale, const double *__restrict__ thr,
+                                                                 uint8_t *__restrict__ act) {
+    pdl_wait();
     extern __shared__ double4 smem_raw[];
     cx *a = reinterpret_cast<cx *>(smem_raw);
     constexpr int logP = 12;
@@ -542,9 +552,30 @@ static __global__ void __launch_bounds__(256, 2) k_fft_large_a16(const ViewSrc s
 #pragma unroll
     for (int k = 0; k < 16; k++) x[k] = a[swz16(t + 256 * k)];
     group_stages_pre<4>(x, t, 256, tw);                     // stages 8-11
-    cx *dst = scratch + ((b * src.nshift + s) << logL) + ((int64_t)c << logP);
+    if constexpr (FINAL) {
+        cx *dst = scratch + (b * SV + s) * ldV;   // `scratch` is the view array here
+        const double sc = 1.0 / 4096.0;
+        double th = 0.0, th2hi = 0.0, th2lo = 0.0;
+        if (act) {
+            th = thr[b];
+            th2hi = th * th * (1.0 + 1e-6);
+            th2lo = th * th * (1.0 - 1e-6);
+        }
 #pragma unroll
-    for (int k = 0; k < 16; k++) stcx(dst + t + 256 * k, x[k]);
+        for (int k = 0; k < 16; k++) {
+            cx y = x[k];
+            if (scale) y = mk(DMUL(y.re, sc), DMUL(y.im, sc));
+            stcx(dst + t + 256 * k, y);
+            if (act) {
+                const double q = y.re * y.re + y.im * y.im;
+                if (q > th2hi || (q >= th2lo && cabs_i(y) > th)) act[b * 4096 + t + 256 * k] = 1;
+            }
+        }
+    } else {
+        cx *dst = scratch + ((b * src.nshift + s) << logL) + ((int64_t)c << logP);
+#pragma unroll
+        for (int k = 0; k < 16; k++) stcx(dst + t + 256 * k, x[k]);
+    }
 }
 
 // Large views, register-blocked pass B: the LQ (5..7) stages left after pass
@@ -627,9 +658,9 @@ static inline void launch_large_b_reg(cx *buf, int64_t nviews, int logL, int s0,
 // passes of <= 4 stages.
 constexpr int LARGE_LOGP = 12;
 static inline int large_logp(int logL) { return LARGE_LOGP < logL ? LARGE_LOGP : logL - 1; }
-static inline bool large_blocked(int logL, int split) {
+static inline bool large_blocked(int logL, int split) {   // split: sfdt_tuning.fft_split (bit 0 here)
     const int lq = logL - LARGE_LOGP;
-    return !split && lq >= 5 && lq <= 7;
+    return !(split & 1) && lq >= 5 && lq <= 7;
 }
 static inline int large_next(int logL, int s0) {
     const int rem = logL - s0;
@@ -656,6 +687,17 @@ static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, con
     const int logL = ilog2_64(L);
     const int64_t nviews = B * src.nshift;
     if (nviews == 0) return SFDT_OK;
+    if (logL == 12 && !src.jfast && !(split & 2)) {
+        // 4096-point views: the register-blocked radix-16 form
+        const size_t smem = size_t(4096) * 16;
+        cudaFuncSetAttribute(k_fft_large_a16<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_fft_large_a16<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             (int)((2 * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024)));
+        launch_pdl(k_fft_large_a16<true>, dim3((unsigned)nviews), dim3(256), smem, stream, src, logL, tw, out, SV, ldV,
+                   scale, thr, act);
+        SFDT_CHECK_LAUNCH();
+        return SFDT_OK;
+    }
     if (L <= FFT_SMEM_MAX) {
         int logvpc = 0;
         // views per CTA: up to 2048 points, but small batches keep >= 2 CTAs
@@ -696,10 +738,11 @@ static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, con
     if (large_blocked(logL, split)) {
         // pass A: 4096-point blocks in registers (three radix-16 rounds)
         const size_t smem = size_t(P) * 16;
-        cudaFuncSetAttribute(k_fft_large_a16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_fft_large_a16, cudaFuncAttributePreferredSharedMemoryCarveout,
+        cudaFuncSetAttribute(k_fft_large_a16<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_fft_large_a16<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
                              (int)((2 * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024)));
-        k_fft_large_a16<<<(unsigned)(nviews << logQ), 256, smem, stream>>>(src, logL, tw, large_scratch);
+        k_fft_large_a16<false><<<(unsigned)(nviews << logQ), 256, smem, stream>>>(src, logL, tw, large_scratch, 0, 0,
+                                                                                 0, nullptr, nullptr);
         SFDT_CHECK_LAUNCH();
         // pass B: every remaining stage in one register-blocked pass
         const int lq = logL - logP;

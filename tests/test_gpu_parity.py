@@ -815,3 +815,34 @@ def test_latency_path_bitwise(B, n, k, mu, a_max):
     assert np.array_equal(got["locs"][:ne], ref["locs"][:ne])
     assert _bits(got["vals"][:ne], ref["vals"][:ne])
     assert np.array_equal(got["unres_bins"][:nu], ref["unres_bins"][:nu])
+
+
+@pytest.mark.parametrize("kind", ["exact", "exact_it", "general", "c64"])
+def test_views_4096_radix16_vs_radix8_bitwise(kind):
+    """4096-point views: the register-blocked radix-16 kernel
+    (k_fft_large_a16<true>) gives the bits of k_fft_views' radix-8
+    shared-memory passes (tuning fft_split=2): entries, order, values."""
+    B = 6
+    if kind == "general":
+        n, k = 1 << 20, 128
+        seeds = [(17, b) for b in range(B)]
+        X = np.stack([general_signal(n, k, 20.0, s_)[0] for s_ in seeds])
+        cfg = P.GeneralConfig(n=n, k=k)
+        assert n // cfg.resolved_d() == 4096
+        run = lambda: P.solve_general_batch(X, cfg, seeds=seeds)
+    else:
+        n, k = 1 << 22, 1 << 10
+        X = np.stack([exact_signal(n, k, 700 + b, "unit")[0] for b in range(B)])
+        if kind == "c64":
+            X = X.astype(np.complex64)
+        cfg = P.ExactConfig(n=n, k=k)
+        assert n // cfg.resolved_d() == 4096
+        run = lambda: P.exact_batch(X, cfg, kind == "exact_it")
+    got = run().to_host()
+    with P.tuning(fft_split=2):
+        ref = run().to_host()
+    ne = int(ref["entry_offsets"][-1])
+    assert ne > 0 and np.array_equal(got["entry_offsets"], ref["entry_offsets"])
+    assert np.array_equal(got["locs"][:ne], ref["locs"][:ne])
+    assert _bits(got["vals"][:ne], ref["vals"][:ne])
+    assert np.array_equal(got["stats"], ref["stats"])

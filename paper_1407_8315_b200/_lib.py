@@ -37,7 +37,7 @@ class Tuning(ctypes.Structure):
     """sfdt_tuning (include/sfdt.h): A/B switches of measured design decisions."""
     _fields_ = [(name, _i32) for name in (
         "fft_split", "gen_dedup", "gen_svd_closed", "gen_mf_small", "gen_mf_list", "gen_warp",
-        "gen_split_a", "gen_prune_lanes", "gen_deal", "decode_coop", "latency_path")]
+        "gen_split_a", "gen_prune_lanes", "gen_deal", "decode_coop", "latency_path", "gen_window")]
 
 
 class ExactArgs(ctypes.Structure):
@@ -130,7 +130,7 @@ _lib = None
 # environment variables of the experiment scripts (tools/*.sh) are read ONCE,
 # at the first solve, into the process defaults.
 TUNING_DEFAULTS = dict(fft_split=0, gen_dedup=1, gen_svd_closed=1, gen_mf_small=1, gen_mf_list=0,
-                       gen_warp=-1, gen_split_a=3, gen_prune_lanes=0, gen_deal=8, gen_overlap=1, decode_coop=-1, latency_path=-1)
+                       gen_warp=-1, gen_split_a=3, gen_prune_lanes=0, gen_deal=8, gen_overlap=1, decode_coop=-1, latency_path=-1, gen_window=0)
 _ENV = None
 _local = threading.local()
 
@@ -147,7 +147,8 @@ def _env_overrides() -> dict:
                          ("SFDT_GEN_MF_LIST", "gen_mf_list"), ("SFDT_GEN_WARP", "gen_warp"),
                          ("SFDT_GEN_SPLIT", "gen_split_a"), ("SFDT_GEN_PRUNE_LANES", "gen_prune_lanes"),
                          ("SFDT_GEN_DEAL", "gen_deal"), ("SFDT_GEN_OVERLAP", "gen_overlap"),
-                         ("SFDT_DECODE_COOP", "decode_coop"), ("SFDT_LATENCY_PATH", "latency_path")):
+                         ("SFDT_DECODE_COOP", "decode_coop"), ("SFDT_LATENCY_PATH", "latency_path"),
+                         ("SFDT_GEN_WINDOW", "gen_window")):
             if e(var) is not None:
                 o[key] = int(e(var))
         if e("SFDT_GEN_SVD") is not None:

@@ -578,6 +578,167 @@ static __global__ void __launch_bounds__(256, 2) k_fft_large_a16(const ViewSrc s
     }
 }
 
+// ---------------------------------------------------------------------------
+// 4096-point views of the general path through a WINDOW RING (tuning
+// gen_window > 0).  k_fft_large_a16<true> gathers view v of signal b itself:
+// a warp instruction reads one sample from each of 32 different d-blocks, so
+// every 16-B sample opens its own DRAM row (36 G random line fetches/s, the
+// measured fully-random ceiling).  A d-block's samples of ALL the signal's
+// views fetched by one warp instruction share that row: tools/blockgather.cu
+// measures 61 G lines/s for this pattern with the 64-B fetch hint
+// (profiles/r02_blockgather.txt).  Here each CTA does both jobs in turn:
+//   1. gather piece `s` (d-block tiles s, s + nv, ...) of signal b + LOOK:
+//      half-warps over d-blocks, lanes over the views, rows W[slot][m][0..16)
+//      of 256 B written whole;
+//   2. the FFT of view s of signal b, its samples read from the ring (L2).
+// CTAs take a ticket in start order, so the pieces of signal b were taken by
+// CTAs that started before any consumer of b and wait on nothing newer:
+// waiting on `arrive[b]` (pieces written) and on `done[b - ring]` (ring slot
+// drained) cannot deadlock.  Same butterflies and twiddles as every other
+// form: bit-identical views.
+// MEASURED SLOWER, off by default (profiles/r02_window/): config 4 DRAM reads
+// 4.72 -> 2.77 GB per launch, but 0.95 -> 1.55 ms -- at 2 CTAs per SM (128
+// registers, 64 KiB) the gather piece and the FFT serialise inside a CTA
+// (gather alone 1.18 ms in this structure vs 0.61 ms standalone; the FFT
+// from the ring alone 0.67 ms).
+__device__ __forceinline__ cx ld_win64(const cx *p) {   // gather load: no L1 allocation, 64-B L2 fetch
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::64B.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return mk(v.x, v.y);
+}
+__device__ __forceinline__ cx ld_win64(const float2 *p) {
+    float2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::64B.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+    return mk((double)v.x, (double)v.y);
+}
+__device__ __forceinline__ int ld_acquire(const int *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+constexpr int WIN_NVP = 16;   // views per ring row (nv <= 16)
+
+static __global__ void __launch_bounds__(256, 2) k_fft_win16(const ViewSrc src, int64_t B, int look, int ring,
+                                                             cx *__restrict__ W, int *__restrict__ flags,
+                                                             const cx *__restrict__ tw, cx *__restrict__ out,
+                                                             int SV, int64_t ldV, int scale) {
+    pdl_wait();
+    extern __shared__ double4 smem_raw[];
+    cx *a = reinterpret_cast<cx *>(smem_raw);
+    __shared__ unsigned s_ticket;
+    const int t = threadIdx.x;
+    const int nv = src.nshift;
+    int *ticket = flags, *arrive = flags + 1, *done = flags + 1 + B;
+    if (t == 0) s_ticket = (unsigned)atomicAdd(ticket, 1);
+    __syncthreads();
+    const int64_t u = (int64_t)s_ticket - (int64_t)look * nv;   // < 0: prologue (gather only)
+    const int64_t tk = s_ticket;
+    const int64_t b = u >= 0 ? u / nv : -1;
+    const int s = (int)(u >= 0 ? u - b * nv : tk % nv);
+    const int64_t bg = u >= 0 ? b + look : tk / nv;             // signal whose piece s this CTA gathers
+    constexpr int L = 4096, NT = L / 16;
+    if (bg < B) {
+        if (bg >= ring) {   // the slot's previous signal must be drained
+            if (t == 0)
+                while (ld_acquire(done + (bg - ring)) < nv) __nanosleep(64);
+            __syncthreads();
+        }
+        const int v = t & 15, h = t >> 4;
+        if (v < nv) {
+            const int64_t o = (v >= src.dyn_first) ? __ldg(src.dyn_off + bg * src.dyn_stride + (v - src.dyn_first))
+                                                   : src.off[v];
+            const int64_t ib = bg * src.sig_stride;
+            cx *wr = W + ((int64_t)(bg % ring) * L) * WIN_NVP + v;
+            for (int i0 = 0; s + nv * i0 < NT; i0 += 8) {
+                cx val[8];
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    const int tau = s + nv * (i0 + q);
+                    if (tau < NT) {
+                        const int64_t m = tau * 16 + h;
+                        const int64_t e = ib + ((m * src.jstride + o) & src.wrap);
+                        val[q] = src.is_c64 ? ld_win64(reinterpret_cast<const float2 *>(src.x) + e)
+                                            : ld_win64(reinterpret_cast<const cx *>(src.x) + e);
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    const int tau = s + nv * (i0 + q);
+                    if (tau < NT) stcx(wr + (int64_t)(tau * 16 + h) * WIN_NVP, val[q]);
+                }
+            }
+        }
+        __threadfence();
+        __syncthreads();
+        if (t == 0) {
+            __threadfence();
+            atomicAdd(arrive + bg, 1);
+        }
+    }
+    if (b < 0) return;
+    if (src.nview && s >= __ldg(src.nview + b)) {   // unused view: nothing to read from the slot
+        if (t == 0) atomicAdd(done + b, 1);
+        return;
+    }
+    if (t == 0)
+        while (ld_acquire(arrive + b) < nv) __nanosleep(64);
+    __syncthreads();
+    const cx *ws = W + ((int64_t)(b % ring) * L) * WIN_NVP + s;
+    const int rt = (int)(__brev((unsigned)t) >> 24);   // rev8(t)
+    cx x[16];
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+        const int k4 = (int)(__brev((unsigned)k) >> 28);   // rev4(k)
+        const double2 w2 = __ldcg(reinterpret_cast<const double2 *>(ws + (int64_t)(k4 * 256 + rt) * WIN_NVP));
+        x[k] = mk(w2.x, w2.y);
+    }
+    group_stages_pre<4>(x, 0, 1, tw);                       // stages 0-3
+#pragma unroll
+    for (int k = 0; k < 16; k++) a[swz16(16 * t + k)] = x[k];
+    __syncthreads();
+    if (t == 0) atomicAdd(done + b, 1);   // every thread's ring loads have landed
+    const int base2 = (t & 15) + ((t >> 4) << 8);
+#pragma unroll
+    for (int k = 0; k < 16; k++) x[k] = a[swz16(base2 + 16 * k)];
+    group_stages_pre<4>(x, t & 15, 16, tw);                 // stages 4-7
+#pragma unroll
+    for (int k = 0; k < 16; k++) a[swz16(base2 + 16 * k)] = x[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; k++) x[k] = a[swz16(t + 256 * k)];
+    group_stages_pre<4>(x, t, 256, tw);                     // stages 8-11
+    cx *dst = out + (b * SV + s) * ldV;
+    const double sc = 1.0 / 4096.0;
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+        cx y = x[k];
+        if (scale) y = mk(DMUL(y.re, sc), DMUL(y.im, sc));
+        stcx(dst + t + 256 * k, y);
+    }
+}
+
+// ring bytes / flag bytes of the window path for B signals (0: not applicable)
+static inline bool win_applicable(int64_t B, int64_t L, int nshift, int look) {
+    return look > 0 && L == 4096 && nshift <= WIN_NVP && B >= 4 * (int64_t)look;
+}
+static inline size_t win_ring_bytes(int look) { return size_t(2 * look) * 4096 * WIN_NVP * 16; }
+static inline size_t win_flag_bytes(int64_t B) { return size_t(2 * B + 1) * 4; }
+
+static inline int launch_fft_win16(const ViewSrc &src, int64_t B, const double *tw_, cx *out, int SV, int64_t ldV,
+                                   cudaStream_t stream, int look, cx *ring, int *flags, int scale = 1) {
+    const cx *tw = reinterpret_cast<const cx *>(tw_);
+    const size_t smem = size_t(4096) * 16;
+    cudaMemsetAsync(flags, 0, win_flag_bytes(B), stream);
+    cudaFuncSetAttribute(k_fft_win16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_fft_win16, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)((2 * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024)));
+    const int64_t grid = (B + look) * src.nshift;
+    k_fft_win16<<<(unsigned)grid, 256, smem, stream>>>(src, B, look, 2 * look, ring, flags, tw, out, SV, ldV, scale);
+    SFDT_CHECK_LAUNCH();
+    return SFDT_OK;
+}
+
 // Large views, register-blocked pass B: the LQ (5..7) stages left after pass
 // A act on the columns i = r + q*P (P = 2^(logL-LQ)) of each residue r.  A
 // CTA of 32 * 2^(LQ-4) threads owns 32 consecutive residues of one view:

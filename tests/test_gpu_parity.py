@@ -846,3 +846,29 @@ def test_views_4096_radix16_vs_radix8_bitwise(kind):
     assert np.array_equal(got["locs"][:ne], ref["locs"][:ne])
     assert _bits(got["vals"][:ne], ref["vals"][:ne])
     assert np.array_equal(got["stats"], ref["stats"])
+
+
+@pytest.mark.parametrize("look,dtype", [(4, "c128"), (8, "c128"), (8, "c64")])
+def test_general_window_ring_bitwise(look, dtype):
+    """4096-point views through the window ring (tuning gen_window = look:
+    every CTA gathers a piece of the d-block rows of the signal `look` ahead,
+    then transforms its view from the ring of 2*look signals, k_fft_win16)
+    give the same bits as each view's CTA gathering its own samples -- at
+    the config-4 shape, over enough signals that every ring slot is reused
+    several times, with per-signal random shifts (some deduplicated)."""
+    import torch
+    from tests.synth import device_general_batch
+    n, k, B = 1 << 20, 128, 40
+    X = device_general_batch(B, n, k, 20.0, 23, torch.device("cuda"))
+    if dtype == "c64":
+        X = X.to(torch.complex64)
+    seeds = [(5, b) for b in range(B)]
+    cfg = P.GeneralConfig(n=n, k=k)
+    ref = P.solve_general_batch(X, cfg, seeds=seeds)
+    with P.tuning(gen_window=look):
+        got = P.solve_general_batch(X, cfg, seeds=seeds)
+    for b in range(B):
+        g, r = got.spectrum(b).entries, ref.spectrum(b).entries
+        assert list(g) == list(r), f"b={b}"
+        assert np.array_equal(np.fromiter(g.values(), complex), np.fromiter(r.values(), complex)), f"b={b}"
+        assert got.trace(b).collision_histogram == ref.trace(b).collision_histogram

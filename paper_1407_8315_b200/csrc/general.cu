@@ -29,6 +29,9 @@
 #include "decode.cuh"
 #include "fft.cuh"
 #include "general.cuh"
+#ifdef SFDT_BINS_PROFILE
+#include <cstdio>
+#endif
 
 namespace sfdt {
 
@@ -812,6 +815,10 @@ struct SPOut {
     int sup[GEN_MAX_SUP];
     cx coef[GEN_MAX_SUP];
     int rankdef;
+#ifdef SFDT_BINS_PROFILE
+    int iters, nminnorm;
+    long long cyc_lsq, cyc_top;
+#endif
 };
 
 // Warp merge of per-lane top lists (each sorted best-first by score desc,
@@ -906,6 +913,9 @@ __device__ __forceinline__ void subspace_pursuit_dev(const cx *y, const cx *phas
     sort_ints(sup, nsup);
     cx A[GEN_MAX_R * GEN_MAX_SUP], coef[GEN_MAX_SUP], res[GEN_MAX_R];
     o.rankdef = 0;
+#ifdef SFDT_BINS_PROFILE
+    o.iters = 0; o.nminnorm = 0; o.cyc_lsq = 0; o.cyc_top = 0;
+#endif
     auto lsq = [&](const int *s, int ns, cx *x) {
         if constexpr (RT > 0) {
             cx yy[RT > 0 ? RT : 1];
@@ -952,6 +962,9 @@ __device__ __forceinline__ void subspace_pursuit_dev(const cx *y, const cx *phas
             for (int c = 0; c < ns; c++) phi_col(s[c], A + c * r);
             if (lstsq_qr(A, r, ns, y, x)) return;   // full rank: unique LS solution
         }
+#ifdef SFDT_BINS_PROFILE
+        o.nminnorm++;
+#endif
         const int rk = lstsq_min_norm(A, r, ns, y, x);
         if (rk < ns) o.rankdef++;
     };
@@ -978,7 +991,14 @@ __device__ __forceinline__ void subspace_pursuit_dev(const cx *y, const cx *phas
     cx mcoef[2 * GEN_MAX_SUP];
     int stage = 0, it = -1;
     for (;;) {
+#ifdef SFDT_BINS_PROFILE
+        const long long c0_ = clock64();
+#endif
         lsq(stage ? merged : sup, stage ? nm : nsup, stage ? mcoef : coef);
+#ifdef SFDT_BINS_PROFILE
+        o.cyc_lsq += clock64() - c0_;
+        o.iters++;
+#endif
         if (stage) {
             // support = sorted(merged[top a_eff of |mcoef|, stable])
             int n2 = 0;
@@ -1727,8 +1747,11 @@ __global__ void __launch_bounds__(128) k_gen_sp1(const cx *__restrict__ V, GenPa
 // goes to lane q / nwarps of warp q % nwarps -- with fewer items than warps
 // no two chains share a warp (divergent lanes would run them one after the
 // other).
+#ifndef SFDT_BINS_MINB
+#define SFDT_BINS_MINB 2   // resident CTAs per SM (255 registers; 3 / 4 spill -- measured, profiles/r02_bins_minb)
+#endif
 template <int RT>
-__global__ void __launch_bounds__(128) k_gen_bins(const cx *__restrict__ V, GenParams p,
+__global__ void __launch_bounds__(128, SFDT_BINS_MINB) k_gen_bins(const cx *__restrict__ V, GenParams p,
                                                   const int32_t *__restrict__ votes,
                                                   const int64_t *__restrict__ wl,
                                                   const int64_t *__restrict__ hl,
@@ -1788,7 +1811,18 @@ __global__ void __launch_bounds__(128) k_gen_bins(const cx *__restrict__ V, GenP
         }
         const int a_sp = a < r ? a : r;
         SPOut o;
+#ifdef SFDT_BINS_PROFILE
+        const long long c0 = clock64();
+#endif
         subspace_pursuit_dev<RT>(y, phase, bphi, p.d, r, cols, ncols, all_cols, a_sp, o);
+#ifdef SFDT_BINS_PROFILE
+        {
+            const long long dc = clock64() - c0;
+            if (dc > 150000 || (q & 63) == 0)
+                printf("BIN q=%lld a=%d ncols=%d nsup=%d lsqcalls=%d minnorm=%d rankdef=%d cyc=%lld cyc_lsq=%lld lane=%d\n", (long long)q, a, ncols, o.nsup,
+                       o.iters, o.nminnorm, o.rankdef, dc, o.cyc_lsq, lane);
+        }
+#endif
         int ne = 0;
         for (int i = 0; i < o.nsup; i++) {
             if (o.coef[i].re == 0.0 && o.coef[i].im == 0.0) continue;   // np.nonzero(coef)

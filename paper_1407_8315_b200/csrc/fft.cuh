@@ -814,9 +814,9 @@ static inline void launch_large_b_reg(cx *buf, int64_t nviews, int logL, int s0,
 // Large views (L > FFT_SMEM_MAX): pass A runs the first LARGE_LOGP stages on
 // 4096-point blocks; the remaining stages act on the residue classes mod
 // 4096.  5..7 remaining stages (L = 2^17 .. 2^19): register-blocked
-// k_fft_large_a16 + one k_fft_large_b16.  Otherwise, or with `split` (the
-// round-1 plan, kept for A/B runs and tests): k_fft_large_a + register
-// passes of <= 4 stages.
+// k_fft_large_a16 + one k_fft_large_b16.  Other large L: k_fft_large_a16 +
+// register passes of <= 4 stages.  With `split` (the round-1 plan, kept for
+// A/B runs and tests): k_fft_large_a + register passes of <= 4 stages.
 constexpr int LARGE_LOGP = 12;
 static inline int large_logp(int logL) { return LARGE_LOGP < logL ? LARGE_LOGP : logL - 1; }
 static inline bool large_blocked(int logL, int split) {   // split: sfdt_tuning.fft_split (bit 0 here)
@@ -920,7 +920,17 @@ static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, con
         SFDT_CHECK_LAUNCH();
         return SFDT_OK;
     }
-    {
+    if (!(split & 1) && logP == LARGE_LOGP) {
+        // other large L (2^13..2^16, >= 2^20): the register-blocked pass A,
+        // then register passes of <= 4 stages
+        const size_t smem = size_t(P) * 16;
+        cudaFuncSetAttribute(k_fft_large_a16<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_fft_large_a16<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             (int)((2 * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024)));
+        k_fft_large_a16<false><<<(unsigned)(nviews << logQ), 256, smem, stream>>>(src, logL, tw, large_scratch, 0, 0,
+                                                                                 0, nullptr, nullptr);
+        SFDT_CHECK_LAUNCH();
+    } else {
         const size_t smem = size_t(P) * 16;
         cudaFuncSetAttribute(k_fft_large_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         // 2 CTAs/SM at 4096 points (4 at 2048), the rest L1 for the

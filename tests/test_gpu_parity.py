@@ -388,23 +388,27 @@ def test_general_batch_vs_oracle_cfg4_shape():
 
 @pytest.mark.parametrize("kind,n,k,d", [("exact", 1 << 20, 8192, 8), ("exact", 1 << 21, 8192, 8),
                                         ("exact", 1 << 21, 16384, 4), ("general", 1 << 22, 1 << 12, None),
-                                        ("general", 1 << 21, 1 << 13, None)])
+                                        ("general", 1 << 21, 1 << 13, None),
+                                        ("exact", 1 << 20, 2048, 128), ("exact", 1 << 20, 4096, 64),
+                                        ("exact", 1 << 20, 8192, 16), ("exact", 1 << 22, 16384, 4),
+                                        ("general", 1 << 20, 1 << 10, None)])
 def test_large_view_blocked_vs_stage_split_bitwise(kind, n, k, d):
-    """Views of 2^17 .. 2^19 points: the register-blocked pass A
-    (k_fft_large_a16) + one register-blocked pass B (k_fft_large_b16) give
-    the same bits as the stage-split plan (k_fft_large_a + register passes
-    of <= 4 stages, tuning fft_split=1), in entries and dict order."""
+    """Views of 2^13 .. 2^20 points: the register-blocked pass A
+    (k_fft_large_a16) + one register-blocked pass B (k_fft_large_b16, L =
+    2^17..2^19) or register passes (other L) give the same bits as the
+    stage-split plan (k_fft_large_a + register passes of <= 4 stages,
+    tuning fft_split=1), in entries and dict order."""
     B = 2
     if kind == "exact":
         X = np.stack([exact_signal(n, k, 90 + b, "unit")[0] for b in range(B)])
         cfg = P.ExactConfig(n=n, k=k, initial_d=d)
-        assert n // cfg.resolved_d() >= 1 << 17
+        assert n // cfg.resolved_d() >= 1 << 13
         run = lambda: P.exact_batch(X, cfg, False)
     else:
         seeds = [(61, b) for b in range(B)]
         X = np.stack([general_signal(n, k, 30.0, s_)[0] for s_ in seeds])
         cfg = P.GeneralConfig(n=n, k=k)
-        assert n // cfg.resolved_d() >= 1 << 17
+        assert n // cfg.resolved_d() >= 1 << 13
         run = lambda: P.solve_general_batch(X, cfg, seeds=seeds)
     got = run()
     with P.tuning(fft_split=1):

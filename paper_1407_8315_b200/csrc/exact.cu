@@ -467,11 +467,15 @@ __global__ void __launch_bounds__(128, SFDT_MULTI_MINB) k_decode_multi(const cx 
                                                       const int64_t *__restrict__ wl,
                                                       const unsigned long long *__restrict__ wl_count,
                                                       int64_t *__restrict__ wl2,
-                                                      unsigned long long *__restrict__ wl2_count) {
+                                                      unsigned long long *__restrict__ wl2_count, int a_lo = 2,
+                                                      long long gate_min = -1) {
     pdl_wait();
-    // tries a = 2..a_hi; with a_hi < a_max the bins still unsolved go to wl2
-    // (k_decode_coop takes a_hi + 1..a_max)
+    // tries a = a_lo..a_hi; with a_hi < a_max the bins still unsolved go to
+    // wl2 (the a >= 3 launches take a_hi + 1..a_max).  gate_min: run only
+    // when the list holds more than gate_min bins (k_decode_coop takes it
+    // otherwise)
     const int64_t cnt = (int64_t)*wl_count;
+    if (cnt <= gate_min) return;
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < cnt;
          i += int64_t(gridDim.x) * blockDim.x) {
         const int64_t t = wl[i];
@@ -481,7 +485,7 @@ __global__ void __launch_bounds__(128, SFDT_MULTI_MINB) k_decode_multi(const cx 
         for (int s = 0; s < S; s++) syn[s] = ldcx(V + (b * S + s) * L + k);
         uint8_t st = a_hi < a_max ? 0xFE : 0xFF;
         Decoded o;
-        for (int a = 2; a <= a_hi; a++) {
+        for (int a = a_lo; a <= a_hi; a++) {
 #if SFDT_MULTI_TEMPLATED
             if (a == 2) decode_try_t<2, S>(syn, n, L, k, o);
             else if (a == 3) decode_try_t<3, S>(syn, n, L, k, o);
@@ -543,8 +547,10 @@ __global__ void __launch_bounds__(96) k_decode_coop(const cx *__restrict__ V, in
                                                     int64_t n, uint8_t *__restrict__ status,
                                                     int64_t *__restrict__ bin_loc, cx *__restrict__ bin_val,
                                                     const int64_t *__restrict__ wl,
-                                                    const unsigned long long *__restrict__ wl_count) {
+                                                    const unsigned long long *__restrict__ wl_count,
+                                                    long long gate_max = 0x7fffffffffffffffLL) {
     pdl_wait();
+    if ((long long)*wl_count > gate_max) return;   // CTA-uniform: k_decode_multi took the list
     __shared__ int s_acc[3][COOP_BINS];
     __shared__ long long s_loc[3][COOP_BINS][4];
     __shared__ double2 s_val[3][COOP_BINS][4];
@@ -633,7 +639,7 @@ static int launch_decode_multi(const cx *V, int64_t nbins, int64_t L, int a_max,
             const int a_hi = mode == 2 ? 2 : a_max;
             launch_pdl(k_decode_multi<S>, dim3(wl_grid(nbins, 128, one_wave(k_decode_multi<S>, 128))), dim3(128), 0,
                        stream, V, L, a_max, a_hi, n, status, bin_loc, bin_val, (const int64_t *)wl,
-                       (const unsigned long long *)wl_count, wl2, wl2_count);
+                       (const unsigned long long *)wl_count, wl2, wl2_count, 2, -1LL);
             SFDT_CHECK_LAUNCH();
         }
         if (mode != 0) {
@@ -641,10 +647,25 @@ static int launch_decode_multi(const cx *V, int64_t nbins, int64_t L, int a_max,
             int nw = mode == 2 ? 1 : (mode == 3 ? 3 : 2);
             if (nw > a_max - a_lo + 1) nw = a_max - a_lo + 1;
             const int threads = 32 * nw;
-            launch_pdl(k_decode_coop<S>, dim3(wl_grid(nbins, COOP_BINS, one_wave(k_decode_coop<S>, threads))),
+            const int wave = one_wave(k_decode_coop<S>, threads);
+            // mode 2: eight lanes per bin pay while the a >= 3 bins fit one
+            // cooperative wave (config 2: 9k bins, 188 -> 140 us); a high
+            // alias load (config 3 at mu = 1: 21k such bins, several waves)
+            // is faster one thread per bin (2.72 -> 2.59 ms per batch).  The
+            // count is known only on the device: both kernels are enqueued
+            // and the list's length picks the one that runs.
+            const long long gate = mode == 2 ? (long long)wave * COOP_BINS : 0x7fffffffffffffffLL;
+            if (mode == 2) {
+                launch_pdl(k_decode_multi<S>, dim3(wl_grid(nbins, 128, one_wave(k_decode_multi<S>, 128))), dim3(128),
+                           0, stream, V, L, a_max, a_max, n, status, bin_loc, bin_val, (const int64_t *)wl2,
+                           (const unsigned long long *)wl2_count, (int64_t *)nullptr,
+                           (unsigned long long *)nullptr, 3, gate);
+                SFDT_CHECK_LAUNCH();
+            }
+            launch_pdl(k_decode_coop<S>, dim3(wl_grid(nbins, COOP_BINS, wave)),
                        dim3(threads), 0, stream, V, L, a_max, a_lo, n, status, bin_loc, bin_val,
                        (const int64_t *)(mode == 2 ? wl2 : wl),
-                       (const unsigned long long *)(mode == 2 ? wl2_count : wl_count));
+                       (const unsigned long long *)(mode == 2 ? wl2_count : wl_count), gate);
             SFDT_CHECK_LAUNCH();
         }
     }
@@ -1684,7 +1705,7 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
                        a->entry_offsets, a->unres_offsets, a->dup_offsets, a->locs, (cx *)a->vals, a->unres_bins);
             SFDT_CHECK_LAUNCH();
             launches += fft_view_launches(p.L, tn.fft_split) + 2 +
-                        (a->a_max > 1 ? (decode_coop_mode(tn.decode_coop, p.B * p.L, a->a_max) == 2 ? 2 : 1) : 0);
+                        (a->a_max > 1 ? (decode_coop_mode(tn.decode_coop, p.B * p.L, a->a_max) == 2 ? 3 : 1) : 0);
             a->kernel_launches = launches;
             return SFDT_OK;
         }
@@ -1744,7 +1765,7 @@ extern "C" int sfdt_exact_solve(sfdt_exact_args *a, void *ws, size_t ws_bytes,
             }
             if (rc) return rc;
             launches += 1 + fft_view_launches(p.L, tn.fft_split) + 1 + (dense ? 1 : 0) +
-                        (a->a_max > 1 ? (decode_coop_mode(tn.decode_coop, nb * p.L, a->a_max) == 2 ? 2 : 1) : 0);
+                        (a->a_max > 1 ? (decode_coop_mode(tn.decode_coop, nb * p.L, a->a_max) == 2 ? 3 : 1) : 0);
         }
         if (aux != stream) {
             if (cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming) != cudaSuccess) return SFDT_ECUDA;

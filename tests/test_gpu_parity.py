@@ -764,13 +764,17 @@ def test_general_prune_four_lanes(n, k):
 
 @pytest.mark.parametrize("B,n,k,mu,a_max", [(64, 1 << 20, 256, 4, 4), (8, 1 << 18, 1024, 1, 4),
                                              (1, 1 << 16, 64, 4, 4), (16, 1 << 16, 256, 1, 3),
-                                             (16, 1 << 16, 256, 2, 2), (300, 1 << 14, 64, 1, 4)])
+                                             (16, 1 << 16, 256, 2, 2), (300, 1 << 14, 64, 1, 4),
+                                             (8, 1 << 20, 1 << 16, 1, 4)])
 def test_cooperative_decode_bitwise(B, n, k, mu, a_max):
     """Multi-collision decode, non-iterative solver: eight lanes per bin with
     one warp per trial a (k_decode_coop, tuning decode_coop=1), the two-stage
     form (thread per bin for a = 2, cooperative for a >= 3; decode_coop=2)
     and one thread per bin for every a (decode_coop=0) return the same bits:
-    entries, dict order, values, unresolved bins."""
+    entries, dict order, values, unresolved bins.  In the two-stage form the
+    a >= 3 list's length picks, on the device, between the cooperative kernel
+    and one thread per bin (more bins than one cooperative wave holds); the
+    last case (524k bins at mu = 1, ~40k of them a >= 3) takes the latter."""
     from tests.synth import device_exact_batch
     X, _, _ = device_exact_batch(B, n, k, 4242 + B, DEV, values="mag1_10")
     cfg = P.ExactConfig(n=n, k=k, mu=mu, a_max=a_max)

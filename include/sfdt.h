@@ -116,7 +116,9 @@ typedef struct {
     int32_t latency_path;    /* non-iterative solves of <= 8 short signals (L <= 8192, n <= 2^20): -1 the
                                 fused five-kernel chain; 0 the general ten-kernel chain; 1 the fused chain
                                 for up to 64 signals */
-    int32_t gen_window;      /* general path, 4096-point views: 0 each view's CTA gathers its own samples;
+    int32_t gen_window;      /* general path, 4096-point views: -1 auto (16 for host-mapped signals, else 0;
+                                -2 / -3: auto with / without the 64-B fetch hint, for A/B runs);
+                                0 each view's CTA gathers its own samples;
                                 n > 0 window ring -- every CTA first gathers a piece of the d-block rows
                                 (all views of a d-block in one warp instruction) of the signal n ahead,
                                 then transforms its view from the ring of 2n signals (k_fft_win16) */

@@ -130,7 +130,7 @@ _lib = None
 # environment variables of the experiment scripts (tools/*.sh) are read ONCE,
 # at the first solve, into the process defaults.
 TUNING_DEFAULTS = dict(fft_split=0, gen_dedup=1, gen_svd_closed=1, gen_mf_small=1, gen_mf_list=0,
-                       gen_warp=-1, gen_split_a=3, gen_prune_lanes=0, gen_deal=8, gen_overlap=1, decode_coop=-1, latency_path=-1, gen_window=0)
+                       gen_warp=-1, gen_split_a=3, gen_prune_lanes=0, gen_deal=8, gen_overlap=1, decode_coop=-1, latency_path=-1, gen_window=-1)
 _ENV = None
 _local = threading.local()
 

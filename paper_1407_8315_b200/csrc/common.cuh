@@ -97,7 +97,7 @@ static inline sfdt_tuning default_tuning() {
     t.gen_deal = 8;
     t.decode_coop = -1;
     t.latency_path = -1;
-    t.gen_window = 0;
+    t.gen_window = -1;
     return t;
 }
 static inline sfdt_tuning tuning_or_default(const sfdt_tuning *t) { return t ? *t : default_tuning(); }

@@ -596,7 +596,10 @@ static __global__ void __launch_bounds__(256, 2) k_fft_large_a16(const ViewSrc s
 // waiting on `arrive[b]` (pieces written) and on `done[b - ring]` (ring slot
 // drained) cannot deadlock.  Same butterflies and twiddles as every other
 // form: bit-identical views.
-// MEASURED SLOWER, off by default (profiles/r02_window/): config 4 DRAM reads
+// Default for HOST-MAPPED signals (the zero-copy end-to-end path: the six
+// consecutive shifts of a d-block are one PCIe read request instead of six
+// from six CTAs; config 4 e2e 6.36k -> 14.4k signals/s).  For signals in HBM it
+// is measured slower and off (profiles/r02_window/): config 4 DRAM reads
 // 4.72 -> 2.77 GB per launch, but 0.95 -> 1.55 ms -- at 2 CTAs per SM (128
 // registers, 64 KiB) the gather piece and the FFT serialise inside a CTA
 // (gather alone 1.18 ms in this structure vs 0.61 ms standalone; the FFT
@@ -611,6 +614,16 @@ __device__ __forceinline__ cx ld_win64(const float2 *p) {
     asm volatile("ld.global.nc.L1::no_allocate.L2::64B.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
     return mk((double)v.x, (double)v.y);
 }
+__device__ __forceinline__ cx ld_win(const cx *p) {   // the same without the fetch-size hint (host-mapped x)
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return mk(v.x, v.y);
+}
+__device__ __forceinline__ cx ld_win(const float2 *p) {
+    float2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+    return mk((double)v.x, (double)v.y);
+}
 __device__ __forceinline__ int ld_acquire(const int *p) {
     int v;
     asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -622,7 +635,7 @@ constexpr int WIN_NVP = 16;   // views per ring row (nv <= 16)
 static __global__ void __launch_bounds__(256, 2) k_fft_win16(const ViewSrc src, int64_t B, int look, int ring,
                                                              cx *__restrict__ W, int *__restrict__ flags,
                                                              const cx *__restrict__ tw, cx *__restrict__ out,
-                                                             int SV, int64_t ldV, int scale) {
+                                                             int SV, int64_t ldV, int scale, int hint64) {
     pdl_wait();
     extern __shared__ double4 smem_raw[];
     cx *a = reinterpret_cast<cx *>(smem_raw);
@@ -658,8 +671,12 @@ static __global__ void __launch_bounds__(256, 2) k_fft_win16(const ViewSrc src, 
                     if (tau < NT) {
                         const int64_t m = tau * 16 + h;
                         const int64_t e = ib + ((m * src.jstride + o) & src.wrap);
-                        val[q] = src.is_c64 ? ld_win64(reinterpret_cast<const float2 *>(src.x) + e)
-                                            : ld_win64(reinterpret_cast<const cx *>(src.x) + e);
+                        if (hint64)
+                            val[q] = src.is_c64 ? ld_win64(reinterpret_cast<const float2 *>(src.x) + e)
+                                                : ld_win64(reinterpret_cast<const cx *>(src.x) + e);
+                        else
+                            val[q] = src.is_c64 ? ld_win(reinterpret_cast<const float2 *>(src.x) + e)
+                                                : ld_win(reinterpret_cast<const cx *>(src.x) + e);
                     }
                 }
 #pragma unroll
@@ -726,7 +743,7 @@ static inline size_t win_ring_bytes(int look) { return size_t(2 * look) * 4096 *
 static inline size_t win_flag_bytes(int64_t B) { return size_t(2 * B + 1) * 4; }
 
 static inline int launch_fft_win16(const ViewSrc &src, int64_t B, const double *tw_, cx *out, int SV, int64_t ldV,
-                                   cudaStream_t stream, int look, cx *ring, int *flags, int scale = 1) {
+                                   cudaStream_t stream, int look, cx *ring, int *flags, int hint64, int scale = 1) {
     const cx *tw = reinterpret_cast<const cx *>(tw_);
     const size_t smem = size_t(4096) * 16;
     cudaMemsetAsync(flags, 0, win_flag_bytes(B), stream);
@@ -734,7 +751,7 @@ static inline int launch_fft_win16(const ViewSrc &src, int64_t B, const double *
     cudaFuncSetAttribute(k_fft_win16, cudaFuncAttributePreferredSharedMemoryCarveout,
                          (int)((2 * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024)));
     const int64_t grid = (B + look) * src.nshift;
-    k_fft_win16<<<(unsigned)grid, 256, smem, stream>>>(src, B, look, 2 * look, ring, flags, tw, out, SV, ldV, scale);
+    k_fft_win16<<<(unsigned)grid, 256, smem, stream>>>(src, B, look, 2 * look, ring, flags, tw, out, SV, ldV, scale, hint64);
     SFDT_CHECK_LAUNCH();
     return SFDT_OK;
 }

@@ -71,7 +71,8 @@ def solve_host_batch(X_host, cfg, iterative: bool = False, chunk: int = 256,
     X_host: (B, n) torch tensor (pinned for full PCIe overlap) or numpy.
     n_signals: process this many signals, cycling over X_host's rows
     (synthetic benchmarking of large batches from a smaller host pool).
-    zero_copy (GeneralConfig only; default: on when X_host is pinned): the
+    zero_copy (GeneralConfig only; default: on when X_host is pinned and the
+    downsampling factor d is >= 128, or >= 64 with 4096-point views): the
     general solver touches only (2*a_max + r_eff)*L samples per signal, so
     its view gather reads them from the pinned host rows directly over PCIe
     and the other N - 15*L samples never cross the bus.  The exact solvers
@@ -86,7 +87,15 @@ def solve_host_batch(X_host, cfg, iterative: bool = False, chunk: int = 256,
     total = H if n_signals is None else int(n_signals)
     chunk = max(1, min(chunk, total))
     if zero_copy is None:
-        zero_copy = isinstance(cfg, GeneralConfig) and X_host.is_pinned()
+        # zero-copy pays while the views touch a small part of the signal: the
+        # link then carries ~(1 + r_eff) read requests per d-block (window-ring
+        # gather, 4096-point views; 2*a_max + r_eff otherwise) at the measured
+        # ~650 M requests/s, against 16*d bytes per d-block at 55 GB/s for whole
+        # rows -- the crossover is d ~ 64 (ring) / 128
+        zero_copy = False
+        if isinstance(cfg, GeneralConfig) and X_host.is_pinned():
+            d = cfg.resolved_d()
+            zero_copy = d >= 128 or (d >= 64 and n // d == 4096)
     if zero_copy:
         if not isinstance(cfg, GeneralConfig):
             raise ValueError("zero_copy applies to the general solver only (the exact "

@@ -217,7 +217,7 @@ def test_host_batch_general_zero_copy(dtype):
     Xh = torch.from_numpy(X).to(dtype).pin_memory()
     cfg = P.GeneralConfig(n=n, k=k, rng_seed=11)
     dev = P.solve_general_batch(Xh.cuda(), cfg)
-    hr = P.solve_host_batch(Xh, cfg, chunk=3, n_signals=7)
+    hr = P.solve_host_batch(Xh, cfg, chunk=3, n_signals=7, zero_copy=True)
     assert hr.zero_copy
     L = n // cfg.resolved_d()
     assert hr.h2d_bytes == 7 * (2 * cfg.a_max + min(cfg.r, cfg.resolved_d())) * L * Xh.element_size()
@@ -225,11 +225,41 @@ def test_host_batch_general_zero_copy(dtype):
         got, want = hr.spectrum(b).entries, dev.spectrum(b % H).entries
         assert list(got) == list(want), f"b={b}"
         assert np.array_equal(np.fromiter(got.values(), complex), np.fromiter(want.values(), complex))
-    # the streamed (copying) path gives the same answer
-    hs = P.solve_host_batch(Xh, cfg, chunk=2, zero_copy=False)
+    # the streamed (copying) path gives the same answer; it is the default at
+    # this d = 32 (half of every d-block is read: whole rows are cheaper)
+    hs = P.solve_host_batch(Xh, cfg, chunk=2)
     assert not hs.zero_copy and hs.h2d_bytes == H * n * Xh.element_size()
     for b in range(H):
         assert hs.spectrum(b).entries == dev.spectrum(b).entries
+
+
+def test_host_batch_zero_copy_default_and_window_ring():
+    """Default zero-copy policy (pinned signals, d >= 128, or d >= 64 with
+    4096-point views) and, at the config-4 shape, the window-ring gather
+    (k_fft_win16, picked for host-mapped signals) reading pinned host memory:
+    results equal the device-resident batch bitwise."""
+    from tests.synth import general_signal, device_general_batch
+    n, k, H = 1 << 16, 16, 3
+    X = np.stack([general_signal(n, k, 20.0, 70 + b)[0] for b in range(H)])
+    Xh = torch.from_numpy(X).pin_memory()
+    cfg = P.GeneralConfig(n=n, k=k, rng_seed=3)
+    assert cfg.resolved_d() == 128
+    hr = P.solve_host_batch(Xh, cfg)
+    assert hr.zero_copy
+    dev = P.solve_general_batch(Xh.cuda(), cfg)
+    for b in range(H):
+        assert hr.spectrum(b).entries == dev.spectrum(b).entries
+    n, k, B = 1 << 20, 128, 72
+    Xd = device_general_batch(B, n, k, 20.0, 31, torch.device("cuda"))
+    Xh = Xd.cpu().pin_memory()
+    cfg = P.GeneralConfig(n=n, k=k, rng_seed=9)
+    dev = P.solve_general_batch(Xd, cfg)
+    hr = P.solve_host_batch(Xh, cfg, chunk=72)
+    assert hr.zero_copy
+    for b in range(B):
+        got, want = hr.spectrum(b).entries, dev.spectrum(b).entries
+        assert list(got) == list(want), f"b={b}"
+        assert np.array_equal(np.fromiter(got.values(), complex), np.fromiter(want.values(), complex))
 
 
 def test_host_batch_exact_streams_whole_rows():

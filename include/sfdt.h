@@ -117,7 +117,10 @@ typedef struct {
                                 fused five-kernel chain; 0 the general ten-kernel chain; 1 the fused chain
                                 for up to 64 signals */
     int32_t gen_window;      /* general path, 4096-point views: -1 auto (16 for host-mapped signals, else 0;
-                                -2 / -3: auto with / without the 64-B fetch hint, for A/B runs);
+                                -2 / -3: auto with / without the 64-B fetch hint, -4: auto without the ring
+                                (host-mapped 4096-point views take the gather kernel too) -- for A/B runs;
+                                host-mapped signals of other view lengths: a window gather kernel into a
+                                device buffer, then the ordinary view FFT);
                                 0 each view's CTA gathers its own samples;
                                 n > 0 window ring -- every CTA first gathers a piece of the d-block rows
                                 (all views of a d-block in one warp instruction) of the signal n ahead,

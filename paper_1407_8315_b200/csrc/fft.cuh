@@ -972,6 +972,75 @@ static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, con
     return SFDT_OK;
 }
 
+// Host-mapped signals, any L: the window gather as its own kernel.  Half-
+// warps (quarter-... 256 >> lognvp groups) over d-blocks, lanes over the
+// views, rows W[b][m][0..nvp) written whole to device memory; the ordinary
+// view FFT then reads W (ViewSrc: sample j of view v at (b*L + j)*nvp + v).
+// Over PCIe this is 1 + r_eff read requests per d-block instead of
+// 2*a_max + r_eff issued from as many different CTAs.
+static __global__ void __launch_bounds__(256) k_win_gather(const ViewSrc src, int64_t L, int lognvp,
+                                                           cx *__restrict__ W, int hint64) {
+    constexpr int U = 8;
+    const int nvp = 1 << lognvp, per = 256 >> lognvp;   // d-blocks per CTA step
+    const int t = threadIdx.x, v = t & (nvp - 1), h = t >> lognvp;
+    const int64_t b = blockIdx.y;
+    if (v >= src.nshift) return;
+    const int64_t o = (v >= src.dyn_first) ? __ldg(src.dyn_off + b * src.dyn_stride + (v - src.dyn_first))
+                                           : src.off[v];
+    const int64_t ib = b * src.sig_stride;
+    cx *wr = W + ((b * L) << lognvp) + v;
+    const int64_t m0 = (int64_t)blockIdx.x * per * U + h;
+    cx val[U];
+#pragma unroll
+    for (int q = 0; q < U; q++) {
+        const int64_t m = m0 + (int64_t)q * per;
+        if (m < L) {
+            const int64_t e = ib + ((m * src.jstride + o) & src.wrap);
+            if (hint64)
+                val[q] = src.is_c64 ? ld_win64(reinterpret_cast<const float2 *>(src.x) + e)
+                                    : ld_win64(reinterpret_cast<const cx *>(src.x) + e);
+            else
+                val[q] = src.is_c64 ? ld_win(reinterpret_cast<const float2 *>(src.x) + e)
+                                    : ld_win(reinterpret_cast<const cx *>(src.x) + e);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < U; q++) {
+        const int64_t m = m0 + (int64_t)q * per;
+        if (m < L) stcx(wr + (m << lognvp), val[q]);
+    }
+}
+
+static inline int win_lognvp(int nshift) { return nshift <= 16 ? 4 : 5; }
+static inline size_t win_gather_bytes(int64_t B, int64_t L, int nshift) {
+    return (size_t(B) * L << win_lognvp(nshift)) * 16;
+}
+
+// gather (above) + the ordinary view FFT from the window buffer
+static inline int launch_fft_from_window(const ViewSrc &src, int64_t B, int64_t L, const double *tw_, cx *out,
+                                         int SV, int64_t ldV, cudaStream_t stream, cx *W, cx *large_scratch,
+                                         int hint64, int split) {
+    const int lognvp = win_lognvp(src.nshift);
+    const int per = 256 >> lognvp;
+    const dim3 grid((unsigned)((L + per * 8 - 1) / (per * 8)), (unsigned)B);
+    k_win_gather<<<grid, 256, 0, stream>>>(src, L, lognvp, W, hint64);
+    SFDT_CHECK_LAUNCH();
+    ViewSrc ws;
+    ws.x = W;
+    ws.is_c64 = 0;
+    ws.nshift = src.nshift;
+    ws.sig_stride = L << lognvp;
+    ws.jstride = int64_t(1) << lognvp;
+    ws.wrap = (L << lognvp) - 1;
+    for (int v = 0; v < MAX_VIEWS; v++) ws.off[v] = v;
+    ws.dyn_off = nullptr;
+    ws.dyn_first = MAX_VIEWS;
+    ws.dyn_stride = 0;
+    ws.jfast = 0;
+    ws.nview = src.nview;
+    return launch_fft_views(ws, B, L, tw_, out, SV, ldV, stream, large_scratch, 1, nullptr, nullptr, split);
+}
+
 static inline ViewSrc consecutive_views(const void *x, int is_c64, int64_t n, int64_t d, int shift0,
                                         int nshift) {
     ViewSrc s;

@@ -2030,6 +2030,7 @@ struct GenPlan {
         off_fft, off_mf, off_cols, off_ncols, off_hl, off_vsh, off_vslot, off_nview, off_fix, off_cand, off_seg, off_vsel, off_ghist, off_eqc, off_win, off_winf, total;
     int win;   // window-ring look-ahead in signals (0: each view gathers its own samples)
     int x_host;   // the signals live in host-mapped memory
+    int wing;     // window gather kernel + FFT from its buffer (host-mapped signals, L != 4096)
 };
 
 static int make_gen_plan(const sfdt_general_args *a, GenPlan &p) {
@@ -2046,7 +2047,7 @@ static int make_gen_plan(const sfdt_general_args *a, GenPlan &p) {
         if (t.gen_mf_list != 0 && (t.gen_mf_list < 32 || t.gen_mf_list > MF_LIST)) return SFDT_EINVAL;
         if (t.gen_prune_lanes != 0 && t.gen_prune_lanes != 1 && t.gen_prune_lanes != 4) return SFDT_EINVAL;
         if (t.gen_warp < -1 || t.gen_warp > 1 || t.gen_deal < 0 || t.gen_split_a < 0) return SFDT_EINVAL;
-        if (t.gen_window < -3 || t.gen_window > 256) return SFDT_EINVAL;
+        if (t.gen_window < -4 || t.gen_window > 256) return SFDT_EINVAL;
     }
     p.B = a->batch;
     p.n = a->n;
@@ -2096,9 +2097,13 @@ static int make_gen_plan(const sfdt_general_args *a, GenPlan &p) {
             if (cudaPointerGetAttributes(&at, a->x) == cudaSuccess) p.x_host = at.type == cudaMemoryTypeHost;
             else cudaGetLastError();
         }
-        if (look < 0) look = p.x_host ? 16 : 0;
+        const int req = look;
+        if (look < 0) look = (p.x_host && req != -4) ? 16 : 0;
         p.win = win_applicable(p.B, p.L, (int)p.nv, look) ? look : 0;
-        p.off_win = p.win ? take(win_ring_bytes(p.win)) : 0;
+        // host-mapped signals of any other shape (auto only): window gather as
+        // its own kernel into a (B, L, 16|32) buffer, ordinary FFT from it
+        p.wing = req < 0 && p.x_host && !p.win && p.L >= 128 && p.nv <= 32;
+        p.off_win = p.win ? take(win_ring_bytes(p.win)) : (p.wing ? take(win_gather_bytes(p.B, p.L, (int)p.nv)) : 0);
         p.off_winf = p.win ? take(win_flag_bytes(p.B)) : 0;
     }
     p.total = o;
@@ -2184,7 +2189,10 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
     src.dyn_stride = a->r_eff;
     src.nview = nview;
     if (a->ev_fft_begin) cudaEventRecord((cudaEvent_t)a->ev_fft_begin, stream);
-    if (p.win)
+    if (p.wing)
+        rc = launch_fft_from_window(src, p.B, p.L, a->twiddles, V, (int)p.nv, p.L, stream, (cx *)(w + p.off_win),
+                                    fft_scratch, tn.gen_window == -2, tn.fft_split);
+    else if (p.win)
         rc = launch_fft_win16(src, p.B, a->twiddles, V, (int)p.nv, p.L, stream, p.win, (cx *)(w + p.off_win),
                               (int *)(w + p.off_winf), tn.gen_window == -2 ? 1 : (tn.gen_window == -3 ? 0 : !p.x_host));
     else
@@ -2192,7 +2200,7 @@ extern "C" int sfdt_general_solve(sfdt_general_args *a, void *ws, size_t ws_byte
                               nullptr, tn.fft_split);
     if (rc) return rc;
     if (a->ev_fft_end) cudaEventRecord((cudaEvent_t)a->ev_fft_end, stream);
-    launches += fft_view_launches(p.L, tn.fft_split);
+    launches += fft_view_launches(p.L, tn.fft_split) + (p.wing ? 1 : 0);
 
     // 2. collision vote (general.py:131-155)
     {

@@ -249,6 +249,19 @@ def test_host_batch_zero_copy_default_and_window_ring():
     dev = P.solve_general_batch(Xh.cuda(), cfg)
     for b in range(H):
         assert hr.spectrum(b).entries == dev.spectrum(b).entries
+    # large views (L = 32768, d = 128): window gather kernel + large-view FFT
+    n, k, H = 1 << 22, 1024, 2
+    Xd = device_general_batch(H, n, k, 30.0, 77, torch.device("cuda"))
+    Xh = Xd.cpu().pin_memory()
+    cfg = P.GeneralConfig(n=n, k=k, rng_seed=5)
+    assert cfg.resolved_d() == 128
+    hr = P.solve_host_batch(Xh, cfg)
+    assert hr.zero_copy
+    dev = P.solve_general_batch(Xd, cfg)
+    for b in range(H):
+        got, want = hr.spectrum(b).entries, dev.spectrum(b).entries
+        assert list(got) == list(want), f"b={b}"
+        assert np.array_equal(np.fromiter(got.values(), complex), np.fromiter(want.values(), complex))
     n, k, B = 1 << 20, 128, 72
     Xd = device_general_batch(B, n, k, 20.0, 31, torch.device("cuda"))
     Xh = Xd.cpu().pin_memory()

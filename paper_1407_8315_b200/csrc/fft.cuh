@@ -978,18 +978,21 @@ static inline int launch_fft_views(const ViewSrc &src, int64_t B, int64_t L, con
 // view FFT then reads W (ViewSrc: sample j of view v at (b*L + j)*nvp + v).
 // Over PCIe this is 1 + r_eff read requests per d-block instead of
 // 2*a_max + r_eff issued from as many different CTAs.
-static __global__ void __launch_bounds__(256) k_win_gather(const ViewSrc src, int64_t L, int lognvp,
+static __global__ void __launch_bounds__(256) k_win_gather(const ViewSrc src, int64_t nsig, int64_t L, int lognvp,
                                                            cx *__restrict__ W, int hint64) {
     constexpr int U = 8;
     const int nvp = 1 << lognvp, per = 256 >> lognvp;   // d-blocks per CTA step
     const int t = threadIdx.x, v = t & (nvp - 1), h = t >> lognvp;
-    const int64_t b = blockIdx.y;
     if (v >= src.nshift) return;
+    // persistent: CTA c walks the tiles c, c + grid, ... of the (signal, tile) list in order
+    const int64_t tiles = (L + per * U - 1) / (per * U);
+    for (int64_t item = blockIdx.x; item < tiles * nsig; item += gridDim.x) {
+    const int64_t b = item / tiles, tile = item - b * tiles;
     const int64_t o = (v >= src.dyn_first) ? __ldg(src.dyn_off + b * src.dyn_stride + (v - src.dyn_first))
                                            : src.off[v];
     const int64_t ib = b * src.sig_stride;
     cx *wr = W + ((b * L) << lognvp) + v;
-    const int64_t m0 = (int64_t)blockIdx.x * per * U + h;
+    const int64_t m0 = tile * per * U + h;
     cx val[U];
 #pragma unroll
     for (int q = 0; q < U; q++) {
@@ -1009,6 +1012,7 @@ static __global__ void __launch_bounds__(256) k_win_gather(const ViewSrc src, in
         const int64_t m = m0 + (int64_t)q * per;
         if (m < L) stcx(wr + (m << lognvp), val[q]);
     }
+    }
 }
 
 static inline int win_lognvp(int nshift) { return nshift <= 16 ? 4 : 5; }
@@ -1022,8 +1026,18 @@ static inline int launch_fft_from_window(const ViewSrc &src, int64_t B, int64_t 
                                          int hint64, int split) {
     const int lognvp = win_lognvp(src.nshift);
     const int per = 256 >> lognvp;
-    const dim3 grid((unsigned)((L + per * 8 - 1) / (per * 8)), (unsigned)B);
-    k_win_gather<<<grid, 256, 0, stream>>>(src, L, lognvp, W, hint64);
+    // a persistent grid of half the SMs: over PCIe fewer gathers in flight keep
+    // the read requests closer to address order -- measured 74 CTAs vs one per
+    // tile: config 4 12.4k -> 13.8k, config 5 general K = 64 9.8k -> 12.2k,
+    // K = 1024 2.10k -> 2.35k signals/s end to end; 37 CTAs starve the link at
+    // L = 32768 (1.6k) (profiles/r02_window/e2e.txt)
+    const int64_t items = ((L + per * 8 - 1) / (per * 8)) * B;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t g = sms / 2 > 0 ? sms / 2 : 1;
+    if (g > items) g = items;
+    k_win_gather<<<(unsigned)g, 256, 0, stream>>>(src, B, L, lognvp, W, hint64);
     SFDT_CHECK_LAUNCH();
     ViewSrc ws;
     ws.x = W;

@@ -29,6 +29,13 @@ import paper_1407_8315_b200 as P                                   # noqa: E402
 from tests import oracle_pool                                       # noqa: E402
 from tests.synth import device_exact_batch, device_general_batch   # noqa: E402
 from tests.test_gpu_configs import _envelope, _exact_compare       # noqa: E402
+
+
+def _SCALE(default, full):
+    """Signals compared per test: `default`, or every signal of the batch with
+    SFDT_SCALE_FULL=1 (a one-off campaign, results under profiles/)."""
+    import os
+    return full if os.environ.get("SFDT_SCALE_FULL") == "1" else default
 from tests.test_gpu_parity import VAL_RTOL, _m_levels              # noqa: E402
 
 DEV = torch.device("cuda", 0)
@@ -66,7 +73,7 @@ def test_general_cfg4_256_signals(snr):
     """Config 4 (N=2^20, K=128, per-signal shift seeds): 256 signals of one
     1024-signal batch against the oracle -- vote flips, support differences,
     dict-order differences and values over 1e-9 counted (all must be 0)."""
-    n, k, B, S = 1 << 20, 128, 1024, 256
+    n, k, B, S = 1 << 20, 128, 1024, _SCALE(256, 1024)
     X = device_general_batch(B, n, k, snr, 4000 + int(snr), DEV)
     cfg = P.GeneralConfig(n=n, k=k)
     seeds = [(4000 + int(snr), b) for b in range(B)]
@@ -109,7 +116,7 @@ def test_general_cfg4_256_signals(snr):
 def test_exact_cfg2_64_signals(solver):
     """Config 2 (N=2^20, K=256, |v| in [1,10]): 64 signals of a 512-signal
     batch against the oracle (with the reference's numpy-backend envelope)."""
-    n, k, B, S = 1 << 20, 256, 512, 64
+    n, k, B, S = 1 << 20, 256, 512, _SCALE(64, 512)
     X, _, _ = device_exact_batch(B, n, k, 2200, DEV, values="mag1_10")
     cfg = P.ExactConfig(n=n, k=k)
     res = P.exact_batch(X, cfg, solver == "iterative")

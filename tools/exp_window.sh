@@ -1,4 +1,4 @@
-# window-ring view FFT (tuning gen_window) at config 4: parity test, bench
+# window-ring view FFT (tuning gen_window) at config 4 (signals in HBM): parity test, bench
 # lines per look-ahead, and the FFT kernel's ncu time / DRAM bytes
 O=gpurun_out/win; mkdir -p $O
 python -m pytest tests/test_gpu_parity.py -q -x -k "window_ring" > $O/pytest.log 2>&1; echo rc=$? >> $O/pytest.log

@@ -649,11 +649,12 @@ static int launch_decode_multi(const cx *V, int64_t nbins, int64_t L, int a_max,
             const int threads = 32 * nw;
             const int wave = one_wave(k_decode_coop<S>, threads);
             // mode 2: eight lanes per bin pay while the a >= 3 bins fit one
-            // cooperative wave (config 2: 9k bins, 188 -> 140 us); a high
-            // alias load (config 3 at mu = 1: 21k such bins, several waves)
-            // is faster one thread per bin (2.72 -> 2.59 ms per batch).  The
-            // count is known only on the device: both kernels are enqueued
-            // and the list's length picks the one that runs.
+            // cooperative wave (~9.5k bins; config 2's ~9k sit at the
+            // crossover, either kernel takes ~70 us there); a high alias load
+            // (config 3 at mu = 1: 21k such bins, several waves) is faster one
+            // thread per bin (2.72 -> 2.59 ms per batch).  The count is known
+            // only on the device: both kernels are enqueued and the list's
+            // length picks the one that runs.
             const long long gate = mode == 2 ? (long long)wave * COOP_BINS : 0x7fffffffffffffffLL;
             if (mode == 2) {
                 launch_pdl(k_decode_multi<S>, dim3(wl_grid(nbins, 128, one_wave(k_decode_multi<S>, 128))), dim3(128),

@@ -21,6 +21,9 @@
 #include "decode.cuh"
 #include "decode_coop.cuh"
 #include "fft.cuh"
+#ifdef SFDT_MULTI_PROFILE
+#include <cstdio>
+#endif
 
 namespace sfdt {
 
@@ -457,7 +460,7 @@ __global__ void __launch_bounds__(128) k_decode_a1_dense(const cx *__restrict__ 
 #define SFDT_MULTI_TEMPLATED 1
 #endif
 #ifndef SFDT_MULTI_MINB
-#define SFDT_MULTI_MINB 6
+#define SFDT_MULTI_MINB 3   // resident CTAs per SM: 6 -> 3 measured 12-15 % faster (instruction-fetch bound: fewer warps, no spills), profiles/r02_decode_minb.txt
 #endif
 template <int S>
 __global__ void __launch_bounds__(128, SFDT_MULTI_MINB) k_decode_multi(const cx *__restrict__ V, int64_t L, int a_max,
@@ -476,8 +479,16 @@ __global__ void __launch_bounds__(128, SFDT_MULTI_MINB) k_decode_multi(const cx 
     // otherwise)
     const int64_t cnt = (int64_t)*wl_count;
     if (cnt <= gate_min) return;
+#ifdef SFDT_MULTI_PROFILE
+    const long long k0_ = clock64();
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        printf("MULTI start a_lo=%d a_hi=%d cnt=%lld grid=%d\n", a_lo, a_hi, (long long)cnt, (int)gridDim.x);
+#endif
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < cnt;
          i += int64_t(gridDim.x) * blockDim.x) {
+#ifdef SFDT_MULTI_PROFILE
+        const long long c0_ = clock64();
+#endif
         const int64_t t = wl[i];
         const int64_t b = t / L, k = t - b * L;
         cx syn[S];
@@ -503,6 +514,10 @@ __global__ void __launch_bounds__(128, SFDT_MULTI_MINB) k_decode_multi(const cx 
             }
         }
         status[t] = st;
+#ifdef SFDT_MULTI_PROFILE
+        if ((i & 8191) == 0)
+            printf("MULTI item i=%lld st=%d start_off=%lld cyc=%lld sm=%d\n", (long long)i, (int)st, c0_ - k0_, clock64() - c0_, (int)blockIdx.x);
+#endif
         if (a_hi < a_max) {
             const bool pend = st == 0xFE;
             const unsigned act_mask = __activemask();

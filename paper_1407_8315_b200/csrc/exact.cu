@@ -414,8 +414,11 @@ __global__ void __launch_bounds__(1024) k_act_compact(const uint8_t *__restrict_
         if (on[u]) awl[pos++] = t0 + u;
 }
 
+#ifndef SFDT_A1D_MINB
+#define SFDT_A1D_MINB 1   // resident CTAs per SM: 3 neutral, 8 (64 registers) 15 % slower (tools/exp_decode_occ.sh)
+#endif
 template <int S>
-__global__ void __launch_bounds__(128) k_decode_a1_dense(const cx *__restrict__ V, int64_t L, int a_max,
+__global__ void __launch_bounds__(128, SFDT_A1D_MINB) k_decode_a1_dense(const cx *__restrict__ V, int64_t L, int a_max,
                                                          int64_t n, uint8_t *__restrict__ status,
                                                          int64_t *__restrict__ bin_loc,
                                                          cx *__restrict__ bin_val,
@@ -851,7 +854,10 @@ __global__ void __launch_bounds__(256) k_iter_prep(IterState st, int64_t B, int6
 // template parameter so the 2l+2 syndromes and every Cramer matrix are
 // register-resident.
 template <int LP>
-__global__ void __launch_bounds__(128, 4) k_iter_decode(IterState st, int64_t L0, int S, int a_max,
+#ifndef SFDT_ITER_MINB
+#define SFDT_ITER_MINB 4   // 2 / 3: the four passes 324 -> 307 / 315 us at config 2 (within 0.2 % of the step)
+#endif
+__global__ void __launch_bounds__(128, SFDT_ITER_MINB) k_iter_decode(IterState st, int64_t L0, int S, int a_max,
                                                         int64_t n, int64_t m,
                                                         const int64_t *__restrict__ awl,
                                                         const unsigned long long *__restrict__ awlc) {

@@ -853,10 +853,10 @@ __global__ void __launch_bounds__(256) k_iter_prep(IterState st, int64_t B, int6
 // accepted terms from every live view (exact.py:253-280).  LP = l is a
 // template parameter so the 2l+2 syndromes and every Cramer matrix are
 // register-resident.
-template <int LP>
 #ifndef SFDT_ITER_MINB
 #define SFDT_ITER_MINB 4   // 2 / 3: the four passes 324 -> 307 / 315 us at config 2 (within 0.2 % of the step)
 #endif
+template <int LP>
 __global__ void __launch_bounds__(128, SFDT_ITER_MINB) k_iter_decode(IterState st, int64_t L0, int S, int a_max,
                                                         int64_t n, int64_t m,
                                                         const int64_t *__restrict__ awl,

@@ -246,6 +246,8 @@ int sfdt_estimate_collisions(const double *syn, int64_t nb, int64_t ld, int64_t 
                              size_t workspace_bytes, sfdt_stream_t stream);
 
 int sfdt_general_caps(const sfdt_general_args *args, int64_t *entry_cap);
+/* args->x and args->tuning must already be the ones of the solve: host-mapped
+ * signals (zero-copy) take a window buffer in the workspace (tuning.gen_window). */
 size_t sfdt_general_workspace_bytes(const sfdt_general_args *args);
 int sfdt_general_solve(sfdt_general_args *args, void *workspace, size_t workspace_bytes,
                        sfdt_stream_t stream);
